@@ -1,0 +1,172 @@
+/*
+ * libstw -- B200-native (sm_100a) spatio-temporal memory planner and trace
+ * replay scorer. Plain C ABI: pointers, sizes and a cudaStream_t passed as
+ * void*; no framework types. Every call is synchronous on return and has no
+ * global state (reentrant per stream). There is no CPU fallback: without a
+ * usable CUDA device every call returns STW_ECUDA.
+ *
+ * Each entry point replaces a function of the reference Python package
+ * (/root/reference/pkg/src/memplan); the citation is next to it. The Python
+ * mirror of the reference API (paper_2507_16274_b200/api.py) binds these via
+ * ctypes; INTEGRATION.md shows the binding a memplan maintainer would add.
+ */
+#ifndef STW_H
+#define STW_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes -> memplan exceptions (model.py:18-31) */
+#define STW_OK 0
+#define STW_ETRACE 1 /* TraceError */
+#define STW_EPLAN 2  /* PlanError */
+#define STW_ESIM 3   /* SimulationError */
+#define STW_ECUDA 4  /* CUDA failure / no device */
+#define STW_EARG 5   /* bad argument (ValueError) */
+
+/* A batch of traces in structure-of-arrays form, concatenated. Trace t owns
+ * events [ev_off[t], ev_off[t+1]). ps/pe are positions in the trace's phase
+ * schedule; a value >= n_sched[t] marks a phase missing from the schedule.
+ * horizon[t] = end of the last scheduled phase (model.py:197-199).
+ * on_device: 1 if every pointer is a device pointer, 0 if all are host
+ * pointers (the library then stages them to HBM itself). */
+typedef struct {
+  int32_t n_traces;
+  int32_t on_device;
+  int64_t n_events;
+  const int64_t *ev_off;
+  const int64_t *id;
+  const int64_t *size;
+  const int32_t *t_s;
+  const int32_t *t_e;
+  const int32_t *ps;
+  const int32_t *pe;
+  const uint8_t *dyn;
+  const int32_t *horizon;
+  const int32_t *n_sched;
+} stw_batch;
+
+/* ---- K1: peak live bytes (model.py:261-281) ----------------------------
+ * peak[t] = max over time of the bytes live in trace t (half-open lifespans,
+ * frees before allocs at equal timestamps). static_only=1 restricts to
+ * non-dynamic events (the planner's static_peak, planner.py:465),
+ * static_only=0 is clique_lower_bound. peak is a host pointer [n_traces]. */
+int stw_peak_live(const stw_batch *b, int32_t static_only, int64_t *peak, void *stream,
+                  char *err, size_t errlen);
+
+/* ---- K2: stable LSD radix sort of (u64 key, u32 value) pairs ------------
+ * Device pointers; sorts bits [begin_bit, end_bit) in place. Used by every
+ * sort of the hot path (planner.py:82-83,392,419,455,483; sim.py:158,169). */
+int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begin_bit,
+                         int32_t end_bit, void *stream, char *err, size_t errlen);
+
+/* ---- planner: synthesize_static_plan (planner.py:357-473) ----------------
+ * Plans every trace of the batch under each candidate (fusion, gap_insert)
+ * setting. Unit u = trace * n_cand + cand. */
+#define STW_CAND_FUSION 1
+#define STW_CAND_GAP 2
+#define STW_NSTATS 12 /* events, persistent, phase_groups, local_plans, residual_events,
+                         fusion_attempts, fusion_accepted, gap_insertions, layers,
+                         pool_size, static_peak, persistent_size (planner.py:261-294) */
+typedef struct {
+  int32_t n_cand;
+  int32_t select_best; /* pick argmin (pool_size, cand) per trace */
+  const uint8_t *cand; /* host [n_cand]: STW_CAND_* bits */
+  int64_t alignment;   /* planner.py:362 */
+  void *stream;
+} stw_plan_opts;
+
+/* Output pointers are host pointers unless on_device=1; any may be NULL.
+ * Per-unit event-shaped arrays are laid out [cand][n_events] (the slice of
+ * unit (t,c) is c*n_events + ev_off[t] .. ). Layer tables and accepted-fusion
+ * audit pairs use the same per-unit slices (capacity = events of the trace). */
+typedef struct {
+  int32_t on_device;
+  int32_t *rc;          /* [units] STW_OK / STW_ETRACE / STW_EPLAN */
+  int64_t *err_ids;     /* [units*2] event ids named by the error message */
+  int64_t *stats;       /* [units*STW_NSTATS] */
+  int64_t *addr;        /* [n_cand*n_events] planned address, -1 for dynamic events */
+  int32_t *layer_of;    /* [n_cand*n_events] layer index, -1 persistent/dynamic */
+  int64_t *layer_base;  /* [n_cand*n_events] per-unit layer table (base) */
+  int64_t *layer_size;  /* [n_cand*n_events] per-unit layer table (size) */
+  double *fus_tmp;      /* [n_cand*n_events] PlanStats.accepted_fusions[k][0] */
+  double *fus_avg;      /* [n_cand*n_events] PlanStats.accepted_fusions[k][1] */
+  int32_t *order;       /* [n_events] trace-local index of the k-th event in (t_s,id) order */
+  int32_t *best_cand;   /* [n_traces] (select_best) */
+  int64_t *addr_best;   /* [n_events] addresses of the best candidate (select_best) */
+  int64_t *best_pool;   /* [n_traces] */
+} stw_plan_out;
+
+int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *out, char *err,
+                   size_t errlen);
+
+/* ---- K7: validate_plan (planner.py:476-505) -----------------------------
+ * Decisions (plan order) as SoA host pointers. Reproduces the reference
+ * sweep's report exactly: pairs (i, j) index the decision arrays, in report
+ * order. Returns the pair count in *n_pairs (may exceed cap; only cap pairs
+ * are written). */
+int stw_validate(int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
+                 const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs,
+                 int64_t cap, void *stream, char *err, size_t errlen);
+
+/* ---- K8: derive_reuse_map (reuse.py:54-93) ------------------------------
+ * Static decisions (host SoA) and K key windows [t_lo, t_hi]. Key k's free
+ * intervals are out_lo/out_hi[out_off[k] .. out_off[k+1]). Returns STW_EARG
+ * with *total set when cap is too small. */
+int stw_reuse_map(int64_t n, const int64_t *addr, const int64_t *size, const int32_t *t_s,
+                  const int32_t *t_e, int64_t K, const int64_t *t_lo, const int64_t *t_hi,
+                  int64_t *out_off, int64_t *out_lo, int64_t *out_hi, int64_t cap, int64_t *total,
+                  void *stream, char *err, size_t errlen);
+
+/* ---- K9/K10: simulate (sim.py:143-238) and run_baseline (baseline.py:98-137) */
+typedef struct {
+  int64_t allocated_peak, reserved_peak, pool_size, fallback_count, fallback_bytes_peak,
+      reuse_hits, mismatch_count;
+  double efficiency, fragmentation;
+} stw_report;
+
+/* Columnar replay log; kind 0 init (size=pool), 1 reserve (size=bytes),
+ * 2 alloc, 3 free; space 0 pool / 1 cache; route 0 planned, 1 reuse,
+ * 2 fallback, 3 mismatch, 4 online, -1 n/a. Host pointers, capacity cap. */
+typedef struct {
+  int64_t cap;
+  int64_t len;
+  int8_t *kind;
+  int64_t *t;
+  int64_t *id;
+  int64_t *size;
+  int64_t *addr;
+  int8_t *space;
+  int8_t *route;
+} stw_log;
+
+/* The plan bundle (traceio.py:313-331): decisions in plan order, reuse
+ * spaces per key (sp_off/sp_lo/sp_hi), and key[i] = reuse key of dynamic
+ * event i of the trace (-1 when the bundle has no entry for it). */
+typedef struct {
+  int64_t pool_size;
+  int64_t alignment;
+  int64_t n_dec;
+  const int64_t *d_id, *d_addr, *d_size;
+  const int32_t *d_ts, *d_te;
+  int64_t n_keys;
+  const int64_t *sp_off, *sp_lo, *sp_hi;
+  const int32_t *key;
+  int32_t reuse;
+} stw_bundle;
+
+int stw_simulate(const stw_batch *trace, const stw_bundle *plan, stw_report *rep, stw_log *log,
+                 int64_t *err_id, void *stream, char *err, size_t errlen);
+int stw_baseline(const stw_batch *trace, stw_report *rep, stw_log *log, int64_t *err_id,
+                 void *stream, char *err, size_t errlen);
+
+/* library identification: returns "stw <version> sm_100a" */
+const char *stw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

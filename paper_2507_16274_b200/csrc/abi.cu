@@ -1,0 +1,54 @@
+// C-ABI entry points of libstw (include/stw.h). Each wraps one hot-path
+// stage in an error context + scratch arena and is synchronous on return.
+#include "batch.cuh"
+
+using namespace stw;
+
+#define STW_ENTRY(stream_ptr, err, errlen) \
+  Ctx ctx;                                  \
+  ctx.stream = (cudaStream_t)(stream_ptr);  \
+  ctx.err = (err);                          \
+  ctx.errlen = (errlen);                    \
+  if ((err) && (errlen)) (err)[0] = 0;
+
+static int finish(Ctx &ctx) {
+  cudaError_t e = cudaStreamSynchronize(ctx.stream);
+  if (e != cudaSuccess) ctx.fail(STW_ECUDA, "stream sync: %s", cudaGetErrorString(e));
+  return ctx.rc;
+}
+
+extern "C" {
+
+const char *stw_version(void) { return "stw 0.1.0 sm_100a"; }
+
+int stw_peak_live(const stw_batch *b, int32_t static_only, int64_t *peak, void *stream, char *err,
+                  size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  {
+    Arena ar(&ctx);
+    DevBatch d;
+    if (stage_batch(ctx, ar, b, &d)) {
+      int64_t *dp = ar.take<int64_t>(d.T > 0 ? d.T : 1);
+      peak_live(ctx, ar, d, static_only != 0, dp);
+      if (ctx.ok() && d.T > 0)
+        STW_CUDA(ctx, cudaMemcpyAsync(peak, dp, d.T * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+    }
+  }
+  return finish(ctx);
+}
+
+int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begin_bit, int32_t end_bit,
+                         void *stream, char *err, size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (begin_bit < 0 || end_bit > 64 || n < 0 || n >= (int64_t)UINT32_MAX) {
+    ctx.fail(STW_EARG, "bad sort arguments");
+    return ctx.rc;
+  }
+  {
+    Arena ar(&ctx);
+    radix_sort_pairs(ctx, ar, keys, vals, n, begin_bit, end_bit);
+  }
+  return finish(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+// Host runtime pieces shared by every entry point: error context, scratch
+// arena, device-wide scan and the stable LSD radix sort (K2).
+#include <stdarg.h>
+#include <string.h>
+
+#include "prims.cuh"
+
+namespace stw {
+
+void Ctx::fail(int code, const char *fmt, ...) {
+  if (rc != STW_OK) return;  // keep the first failure
+  rc = code;
+  if (err && errlen) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, errlen, fmt, ap);
+    va_end(ap);
+  }
+}
+
+static void raise_pool_threshold() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
+void *Arena::raw(size_t bytes) {
+  if (!ctx->ok()) return nullptr;
+  if (n == (int)(sizeof(ptrs) / sizeof(ptrs[0]))) {
+    ctx->fail(STW_ECUDA, "scratch arena: too many allocations");
+    return nullptr;
+  }
+  raise_pool_threshold();
+  void *p = nullptr;
+  STW_CUDA(*ctx, cudaMallocAsync(&p, bytes ? bytes : 16, ctx->stream));
+  if (!ctx->ok()) return nullptr;
+  ptrs[n++] = p;
+  return p;
+}
+
+void Arena::release() {
+  for (int i = 0; i < n; i++) cudaFreeAsync(ptrs[i], ctx->stream);
+  n = 0;
+}
+
+template <class T>
+void device_scan(Ctx &ctx, Arena &ar, const T *in, T *out, int64_t n, bool inclusive) {
+  if (n <= 0 || !ctx.ok()) return;
+  int64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb == 1) {
+    k_tile_scan<T><<<1, kScanThreads, 0, ctx.stream>>>(in, out, nullptr, n, inclusive);
+    STW_LAUNCHED(ctx);
+    return;
+  }
+  T *sums = ar.take<T>(nb);
+  if (!sums) return;
+  k_tile_reduce<T><<<(unsigned)nb, kScanThreads, 0, ctx.stream>>>(in, sums, n);
+  STW_LAUNCHED(ctx);
+  device_scan<T>(ctx, ar, sums, sums, nb, false);
+  k_tile_scan<T><<<(unsigned)nb, kScanThreads, 0, ctx.stream>>>(in, out, sums, n, inclusive);
+  STW_LAUNCHED(ctx);
+}
+template void device_scan<uint32_t>(Ctx &, Arena &, const uint32_t *, uint32_t *, int64_t, bool);
+template void device_scan<int64_t>(Ctx &, Arena &, const int64_t *, int64_t *, int64_t, bool);
+template void device_scan<uint64_t>(Ctx &, Arena &, const uint64_t *, uint64_t *, int64_t, bool);
+template void device_scan<int32_t>(Ctx &, Arena &, const int32_t *, int32_t *, int64_t, bool);
+
+// ---------------------------------------------------------------------------
+// K2: LSD radix sort, 8-bit digits.
+// Pass = upsweep (per-tile digit histogram, digit-major) -> exclusive scan ->
+// downsweep (stable rank inside the tile via warp match_any, scatter).
+
+__global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint64_t *__restrict__ keys,
+                                                             uint32_t *__restrict__ counts, int64_t n,
+                                                             int shift, uint32_t mask, int ntiles) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+  for (int j = 0; j < kSortItems; j++) {
+    int64_t i = base + j * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
+    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, const uint32_t *__restrict__ offs, int64_t n, int shift, uint32_t mask,
+    int ntiles) {
+  constexpr int W = kSortThreads / 32;
+  __shared__ uint32_t base[256];
+  __shared__ uint32_t wc[W][256];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  base[tid] = offs[(int64_t)tid * ntiles + blockIdx.x];
+  int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
+  for (int j = 0; j < kSortItems; j++) {
+#pragma unroll
+    for (int w = 0; w < W; w++) wc[w][tid] = 0;
+    __syncthreads();
+    int64_t i = tile0 + j * kSortThreads + tid;
+    bool valid = i < n;
+    uint64_t k = valid ? kin[i] : 0;
+    uint32_t v = valid ? vin[i] : 0;
+    uint32_t d = (uint32_t)(k >> shift) & mask;
+    unsigned vm = __ballot_sync(0xffffffffu, valid);
+    unsigned peers = 0, rank = 0;
+    if (valid) {
+      peers = __match_any_sync(vm, d);
+      rank = __popc(peers & lanemask_lt());
+      if (rank == 0) wc[warp][d] = __popc(peers);
+    }
+    __syncthreads();
+    {  // exclusive prefix over warps for digit tid
+      uint32_t s = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        uint32_t c = wc[w][tid];
+        wc[w][tid] = s;
+        s += c;
+      }
+      __syncthreads();
+      if (valid) {
+        uint32_t pos = base[d] + wc[warp][d] + rank;
+        kout[pos] = k;
+        vout[pos] = v;
+      }
+      __syncthreads();
+      base[tid] += s;
+    }
+    __syncthreads();
+  }
+}
+
+void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64_t n, int begin_bit,
+                      int end_bit) {
+  if (n <= 1 || end_bit <= begin_bit || !ctx.ok()) return;
+  int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+  uint64_t *k2 = ar.take<uint64_t>(n);
+  uint32_t *v2 = ar.take<uint32_t>(n);
+  uint32_t *counts = ar.take<uint32_t>((size_t)256 * ntiles);
+  if (!ctx.ok()) return;
+  uint64_t *ka = keys, *kb = k2;
+  uint32_t *va = vals, *vb = v2;
+  int passes = 0;
+  for (int b = begin_bit; b < end_bit; b += 8) {
+    int w = end_bit - b < 8 ? end_bit - b : 8;
+    uint32_t mask = (1u << w) - 1;
+    k_radix_hist<<<ntiles, kSortThreads, 0, ctx.stream>>>(ka, counts, n, b, mask, ntiles);
+    STW_LAUNCHED(ctx);
+    device_scan<uint32_t>(ctx, ar, counts, counts, (int64_t)256 * ntiles, false);
+    k_radix_scatter<<<ntiles, kSortThreads, 0, ctx.stream>>>(ka, va, kb, vb, counts, n, b, mask, ntiles);
+    STW_LAUNCHED(ctx);
+    uint64_t *tk = ka;
+    ka = kb;
+    kb = tk;
+    uint32_t *tv = va;
+    va = vb;
+    vb = tv;
+    passes++;
+  }
+  if (passes & 1) {
+    STW_CUDA(ctx, cudaMemcpyAsync(keys, ka, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx.stream));
+    STW_CUDA(ctx, cudaMemcpyAsync(vals, va, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx.stream));
+  }
+}
+
+__global__ void k_iota(uint32_t *p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (uint32_t)i;
+}
+
+void sort_perm(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *perm, int64_t n, int bits) {
+  if (!ctx.ok()) return;
+  k_iota<<<grid_for(n, 256), 256, 0, ctx.stream>>>(perm, n);
+  STW_LAUNCHED(ctx);
+  radix_sort_pairs(ctx, ar, keys, perm, n, 0, bits);
+}
+
+}  // namespace stw
