@@ -86,7 +86,7 @@ typedef struct {
 typedef struct {
   int32_t on_device;
   int32_t *rc;          /* [units] STW_OK / STW_ETRACE / STW_EPLAN */
-  int64_t *err_ids;     /* [units*2] event ids named by the error message */
+  int64_t *err_ids;     /* [units*2] batch event indices named by the error (-1 = none) */
   int64_t *stats;       /* [units*STW_NSTATS] */
   int64_t *addr;        /* [n_cand*n_events] planned address, -1 for dynamic events */
   int32_t *layer_of;    /* [n_cand*n_events] layer index, -1 persistent/dynamic */

@@ -51,3 +51,192 @@ def radix_sort_pairs(keys, vals, begin_bit: int = 0, end_bit: int = 64, stream=N
     s = _lib.stream_handle(stream)
     _lib.check(L.stw_radix_sort_pairs(_lib.ptr(keys), _lib.ptr(vals), C.c_int64(n), C.c_int32(begin_bit),
                                       C.c_int32(end_bit), s, err, C.sizeof(err)), err)
+
+
+# ---------------------------------------------------------------------------
+# planner (planner.py:357-505)
+
+import time as _time
+from dataclasses import dataclass as _dataclass
+
+from .domain import DEFAULT_ALIGNMENT, PlanError, TraceError
+from .plan_types import DecisionColumns, MemoryLayer, PlanStats, StaticPlan
+
+
+@_dataclass
+class BatchPlan:
+    """Raw columnar result of stw_plan_batch for T traces x C candidates."""
+
+    batch: HostBatch
+    cands: tuple
+    rc: np.ndarray        # [T*C]
+    err_ids: np.ndarray   # [T*C, 2]
+    stats: np.ndarray     # [T*C, NSTATS]
+    addr: np.ndarray      # [C, N]
+    layer_of: np.ndarray  # [C, N]
+    layer_base: np.ndarray
+    layer_size: np.ndarray
+    fus_tmp: np.ndarray
+    fus_avg: np.ndarray
+    order: np.ndarray     # [N] trace-local (t_s, id) order
+    best_cand: np.ndarray = None
+    best_pool: np.ndarray = None
+    addr_best: np.ndarray = None
+
+
+def _cand_bits(cands) -> np.ndarray:
+    return np.asarray([(_lib.STW_CAND_FUSION if f else 0) | (_lib.STW_CAND_GAP if g else 0) for f, g in cands],
+                      dtype=np.uint8)
+
+
+def plan_batch(batch, cands=((True, True),), alignment: int = DEFAULT_ALIGNMENT, select_best: bool = False,
+               detail: bool = True, stream=None) -> BatchPlan:
+    """Plan every trace of `batch` (HostBatch or list of TraceArrays) under each
+    candidate (fusion, gap_insert) on the device (stw_plan_batch)."""
+    hb = batch if isinstance(batch, HostBatch) else HostBatch([_arrays_of(t) for t in batch])
+    C_ = len(cands)
+    T, N = hb.T, hb.N
+    U = T * C_
+    cb = _cand_bits(cands)
+    rc = np.zeros(U, np.int32)
+    err_ids = np.full((U, 2), -1, np.int64)
+    stats = np.zeros((U, _lib.NSTATS), np.int64)
+    addr = np.empty((C_, N), np.int64)
+    order = np.empty(N, np.int32)
+    if detail:
+        layer_of = np.empty((C_, N), np.int32)
+        lbase = np.zeros((C_, N), np.int64)
+        lsize = np.zeros((C_, N), np.int64)
+        ftmp = np.zeros((C_, N), np.float64)
+        favg = np.zeros((C_, N), np.float64)
+    else:
+        layer_of = lbase = lsize = ftmp = favg = None
+    best = bpool = abest = None
+    if select_best:
+        best = np.empty(T, np.int32)
+        bpool = np.empty(T, np.int64)
+        abest = np.empty(N, np.int64)
+    opts = _lib.PlanOpts(C_, int(select_best), _lib.ptr(cb), alignment,
+                         _lib.stream_handle(stream) if stream is not None else None)
+    out = _lib.PlanOut(0, _lib.ptr(rc), _lib.ptr(err_ids), _lib.ptr(stats), _lib.ptr(addr), _lib.ptr(layer_of),
+                       _lib.ptr(lbase), _lib.ptr(lsize), _lib.ptr(ftmp), _lib.ptr(favg), _lib.ptr(order),
+                       _lib.ptr(best), _lib.ptr(abest), _lib.ptr(bpool))
+    err = _lib.errbuf()
+    b = hb.struct()
+    _lib.check(_lib.load().stw_plan_batch(C.byref(b), C.byref(opts), C.byref(out), err, C.sizeof(err)), err)
+    return BatchPlan(hb, tuple(cands), rc, err_ids, stats, addr, layer_of, lbase, lsize, ftmp, favg, order,
+                     best, bpool, abest)
+
+
+def _unknown_phase_message(ta) -> str:
+    """The phase named by the reference's TraceError (planner.py:390-392 sort order)."""
+    n = ta.n_sched
+    scoped = np.nonzero((ta.dyn == 0) & (ta.t_e < ta.horizon))[0]
+    keys = sorted({(ta.phases[ta.ps[i]], ta.phases[ta.pe[i]]) for i in scoped.tolist()})
+    known = set(ta.phases[:n])
+    for a, b in keys:
+        for ph in (a, b):
+            if ph not in known:
+                return f"phase {ph} not in schedule"
+    return "phase not in schedule"
+
+
+def raise_unit_error(bp: BatchPlan, t: int, c: int) -> None:
+    u = t * len(bp.cands) + c
+    rc = int(bp.rc[u])
+    if rc == _lib.STW_OK:
+        return
+    ta = bp.batch.traces[t]
+    base = int(bp.batch.ev_off[t])
+    e0, e1 = (int(x) for x in bp.err_ids[u])
+    if rc == _lib.STW_ETRACE:
+        raise TraceError(_unknown_phase_message(ta))
+    if e0 >= 0 and e1 < 0:
+        i = e0 - base
+        raise PlanError(f"event {int(ta.id[i])}: size {int(ta.size[i])} not aligned")
+    if e0 >= 0:
+        raise PlanError(f"planner emitted conflicting decisions {int(ta.id[e0 - base])} and {int(ta.id[e1 - base])}")
+    raise PlanError("pool below the static peak; planner invariant broken")
+
+
+def _unit_plan(bp: BatchPlan, t: int, c: int, trace, alignment: int, stats) -> StaticPlan:
+    raise_unit_error(bp, t, c)
+    ta = bp.batch.traces[t]
+    u = t * len(bp.cands) + c
+    s0, s1 = int(bp.batch.ev_off[t]), int(bp.batch.ev_off[t + 1])
+    st = bp.stats[u]
+    order = bp.order[s0:s1]
+    static = order[ta.dyn[order] == 0]
+    addr = bp.addr[c, s0:s1]
+    cols = DecisionColumns(ta.id[static], addr[static], ta.size[static], ta.t_s[static], ta.t_e[static], src=static)
+    if stats is not None:
+        keys = ("num_events", "num_persistent", "num_groups", "num_plans", "num_residuals", "fusion_attempts",
+                "fusion_accepted", "gap_insertions", "num_layers", "pool_size", "static_peak")
+        for k, v in zip(keys, st[:11].tolist()):
+            setattr(stats, k, v)
+        na = int(st[6])
+        if bp.fus_tmp is not None and na:
+            stats.accepted_fusions.extend(zip(bp.fus_tmp[c, s0:s0 + na].tolist(), bp.fus_avg[c, s0:s0 + na].tolist()))
+    nl = int(st[8])
+    lb = bp.layer_base[c, s0:s0 + nl].copy() if bp.layer_base is not None else np.zeros(nl, np.int64)
+    lsz = bp.layer_size[c, s0:s0 + nl].copy() if bp.layer_size is not None else np.zeros(nl, np.int64)
+    lay = bp.layer_of[c, s0:s1].copy() if bp.layer_of is not None else None
+    events_fn = (lambda tr=trace: tr.events) if trace is not None else ta.to_events
+
+    def layers():
+        out = []
+        for l in range(nl):
+            members = np.nonzero(lay == l)[0] if lay is not None else np.zeros(0, np.int64)
+
+            def slots(members=members):
+                ev = events_fn()
+                return sorted((int(ta.t_s[i]), int(ta.t_e[i]), ev[i]) for i in members.tolist())
+
+            end = int(ta.t_e[members].max()) if members.size else -1
+            out.append((int(lb[l]), MemoryLayer(int(lsz[l]), int(lb[l]), end, slots_fn=slots)))
+        return tuple(out)
+
+    return StaticPlan.from_columns(int(st[9]), alignment, cols, events_fn, int(st[11]), layers)
+
+
+def synthesize_static_plan(trace, *, fusion: bool = True, gap_insert: bool = True,
+                           alignment: int = DEFAULT_ALIGNMENT, stats: PlanStats = None) -> StaticPlan:
+    """Plan every static request of the trace into a minimal pool (planner.py:357-473)."""
+    t0 = _time.monotonic()
+    ta = _arrays_of(trace)
+    bp = plan_batch([ta], ((fusion, gap_insert),), alignment=alignment)
+    if stats is None:
+        stats = PlanStats()
+    plan = _unit_plan(bp, 0, 0, trace if hasattr(trace, "phase_schedule") else None, alignment, stats)
+    stats.plan_seconds = _time.monotonic() - t0
+    return plan
+
+
+def validate_plan(plan) -> list:
+    """Decision pairs the reference sweep reports as conflicting (planner.py:476-505)."""
+    if isinstance(plan, StaticPlan):
+        cols = plan.columns()
+        decs = plan.decisions
+    else:
+        decs = tuple(plan.decisions)
+        cols = DecisionColumns.from_decisions(decs)
+    n = len(cols)
+    if n == 0:
+        return []
+    npairs = C.c_int64(0)
+    cap = max(16, 4 * n)
+    pairs = np.empty(2 * cap, np.int32)
+    err = _lib.errbuf()
+    L = _lib.load()
+    rc = L.stw_validate(C.c_int64(n), _lib.ptr(cols.id), _lib.ptr(cols.addr), _lib.ptr(cols.size),
+                        _lib.ptr(cols.t_s), _lib.ptr(cols.t_e), C.byref(npairs), _lib.ptr(pairs), C.c_int64(cap),
+                        None, err, C.sizeof(err))
+    _lib.check(rc, err)
+    if npairs.value > cap:
+        cap = npairs.value
+        pairs = np.empty(2 * cap, np.int32)
+        _lib.check(L.stw_validate(C.c_int64(n), _lib.ptr(cols.id), _lib.ptr(cols.addr), _lib.ptr(cols.size),
+                                  _lib.ptr(cols.t_s), _lib.ptr(cols.t_e), C.byref(npairs), _lib.ptr(pairs),
+                                  C.c_int64(cap), None, err, C.sizeof(err)), err)
+    p = pairs[: 2 * npairs.value].reshape(-1, 2).tolist()
+    return [(decs[a], decs[b]) for a, b in p]

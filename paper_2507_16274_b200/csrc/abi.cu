@@ -17,6 +17,12 @@ static int finish(Ctx &ctx) {
   return ctx.rc;
 }
 
+namespace stw {
+int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
+int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
+                        const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap);
+}  // namespace stw
+
 extern "C" {
 
 const char *stw_version(void) { return "stw 0.1.0 sm_100a"; }
@@ -48,6 +54,28 @@ int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begi
     Arena ar(&ctx);
     radix_sort_pairs(ctx, ar, keys, vals, n, begin_bit, end_bit);
   }
+  return finish(ctx);
+}
+
+int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *out, char *err, size_t errlen) {
+  STW_ENTRY(opts ? opts->stream : nullptr, err, errlen);
+  if (!b || !opts || !out) {
+    ctx.fail(STW_EARG, "null argument");
+    return ctx.rc;
+  }
+  plan_batch(ctx, b, opts, out);
+  return finish(ctx);
+}
+
+int stw_validate(int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size, const int32_t *t_s,
+                 const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap, void *stream, char *err,
+                 size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (n < 0 || n >= (int64_t)INT32_MAX || !n_pairs) {
+    ctx.fail(STW_EARG, "bad validate arguments");
+    return ctx.rc;
+  }
+  validate_plan_pairs(ctx, n, id, addr, size, t_s, t_e, n_pairs, pairs, cap);
   return finish(ctx);
 }
 

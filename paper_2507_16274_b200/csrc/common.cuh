@@ -47,7 +47,7 @@ struct Ctx {
 // cudaFreeAsync when the Arena goes out of scope.
 struct Arena {
   Ctx *ctx;
-  void *ptrs[256];
+  void *ptrs[512];
   int n = 0;
   explicit Arena(Ctx *c) : ctx(c) {}
   void *raw(size_t bytes);

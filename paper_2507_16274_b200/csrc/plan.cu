@@ -1,0 +1,1586 @@
+// Batched static planner (synthesize_static_plan, planner.py:357-473) for a
+// batch of traces x candidate (fusion, gap_insert) settings.
+//
+// Pipeline (every stage runs on the device; the host only sizes buffers):
+//   A  canonical ranks    q = id rank, r = (t_s, id) rank per trace      (K2 sorts)
+//   B  phase groups       one stable sort by (trace, class, p_s, p_e, r);
+//                         persistent block, HomoPhase groups, packing by a
+//                         global exclusive scan of sizes, per-plan height /
+//                         span / used / TMP                              (K3)
+//   C  fusion sweep       one CTA per trace, block-parallel cursor search  (K4)
+//   D  layer items        plans + residuals, sorted by (size desc, t_s, tie)
+//   E  HomoSize layers    one CTA per unit; per size class: parallel
+//                         fixed-slot fit masks -> warp-serial resolve of gap
+//                         insertion + Alg. 1 -> merge of the slot CSR      (K5)
+//   F  stacking/emission  layer bases by scan, addresses per event        (K6)
+//   G  self-check         static peak (K1) and the rectangle sweep (K7)
+//
+// Decomposition used by E (exactly equivalent to MemoryLayer.fits_gap,
+// planner.py:199-212, because every layer's slots are pairwise disjoint as
+// closed intervals): an item of class S fits layer L iff it does not overlap
+// the slots L held before class S started, and every class-S item already
+// gap-inserted into L ended before the item starts.
+#include <algorithm>
+#include <vector>
+
+#include "planner.cuh"
+
+namespace stw {
+
+constexpr int kPlanThreads = 256;
+constexpr int kFitWords = 4;      // fit masks kept for the first 128 layers of a class
+constexpr int kSmemLayers = 1024;  // per-class resolve state kept in shared memory up to this
+
+// ---------------------------------------------------------------------------
+// generic helpers
+
+template <class T>
+__device__ T block_reduce_min(T v, T *sh) {
+  for (int o = 16; o; o >>= 1) {
+    T n = __shfl_down_sync(0xffffffffu, v, o);
+    v = n < v ? n : v;
+  }
+  int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane_id() == 0) sh[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T m = sh[0];
+    for (int k = 1; k < nw; k++) m = sh[k] < m ? sh[k] : m;
+    sh[32] = m;
+  }
+  __syncthreads();
+  T out = sh[32];
+  __syncthreads();
+  return out;
+}
+
+template <class T>
+__device__ T block_reduce_max(T v, T *sh) {
+  for (int o = 16; o; o >>= 1) {
+    T n = __shfl_down_sync(0xffffffffu, v, o);
+    v = n > v ? n : v;
+  }
+  int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane_id() == 0) sh[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T m = sh[0];
+    for (int k = 1; k < nw; k++) m = sh[k] > m ? sh[k] : m;
+    sh[32] = m;
+  }
+  __syncthreads();
+  T out = sh[32];
+  __syncthreads();
+  return out;
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_trace_of_all(const int64_t *__restrict__ ev_off, int T, int64_t N, int32_t *__restrict__ tr) {
+  GRID_STRIDE(i, N) tr[i] = trace_of(ev_off, T, i);
+}
+
+__global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx) {
+  __shared__ long long sh[33];
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  GRID_STRIDE(i, n) {
+    lo = min(lo, (long long)v[i]);
+    hi = max(hi, (long long)v[i]);
+  }
+  lo = block_reduce_min(lo, sh);
+  hi = block_reduce_max(hi, sh);
+  if (threadIdx.x == 0) {
+    atomicMin(mn, lo);
+    atomicMax(mx, hi);
+  }
+}
+
+__global__ void k_max_i32(const int32_t *__restrict__ v, int64_t n, int *mx) {
+  __shared__ int sh[33];
+  int hi = 0;
+  GRID_STRIDE(i, n) hi = max(hi, v[i]);
+  hi = block_reduce_max(hi, sh);
+  if (threadIdx.x == 0) atomicMax(mx, hi);
+}
+
+__global__ void k_concat_key(uint64_t *__restrict__ hi, const uint64_t *__restrict__ lo, int lobits, int64_t n) {
+  GRID_STRIDE(i, n) hi[i] = (lobits >= 64 ? 0 : (hi[i] << lobits)) | lo[i];
+}
+
+__global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *__restrict__ perm,
+                             uint64_t *__restrict__ dst, int64_t n) {
+  GRID_STRIDE(i, n) dst[i] = src[perm[i]];
+}
+
+void sort_perm2(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, uint64_t *lo, int lobits, uint32_t *perm,
+                int64_t n) {
+  if (!ctx.ok() || n == 0) return;
+  if (hibits + lobits <= 64) {
+    k_concat_key<<<grid_for(n, 256), 256, 0, ctx.stream>>>(hi, lo, lobits, n);
+    STW_LAUNCHED(ctx);
+    sort_perm(ctx, ar, hi, perm, n, hibits + lobits);
+    return;
+  }
+  sort_perm(ctx, ar, lo, perm, n, lobits);
+  k_gather_u64<<<grid_for(n, 256), 256, 0, ctx.stream>>>(hi, perm, lo, n);  // lo := hi[perm]
+  STW_LAUNCHED(ctx);
+  radix_sort_pairs(ctx, ar, lo, perm, n, 0, hibits);
+}
+
+// rank[perm[k]] = k - ev_off[trace]; optional per-trace local permutation
+__global__ void k_rank_from_perm(const uint32_t *__restrict__ perm, const int32_t *__restrict__ tr,
+                                 const int64_t *__restrict__ ev_off, int64_t n, int32_t *__restrict__ rank,
+                                 int32_t *__restrict__ local_order) {
+  GRID_STRIDE(k, n) {
+    uint32_t i = perm[k];
+    int64_t b = ev_off[tr[i]];
+    rank[i] = (int32_t)(k - b);
+    if (local_order) local_order[k] = (int32_t)(i - b);
+  }
+}
+
+__device__ __forceinline__ int ev_class(uint8_t dyn, int32_t te, int32_t horizon) {
+  return dyn ? 2 : (te >= horizon ? 0 : 1);  // 0 persistent, 1 scoped static, 2 dynamic
+}
+
+// ---------------------------------------------------------------------------
+// A: keys
+
+__global__ void k_key_q(const int32_t *__restrict__ tr, const int64_t *__restrict__ id, int64_t n, long long idmin,
+                        uint64_t *__restrict__ hi, uint64_t *__restrict__ lo) {
+  GRID_STRIDE(i, n) {
+    hi[i] = (uint64_t)tr[i];
+    lo[i] = (uint64_t)((long long)id[i] - idmin);
+  }
+}
+
+__global__ void k_key_r(const int32_t *__restrict__ tr, const int32_t *__restrict__ ts, const int32_t *__restrict__ q,
+                        int64_t n, int qb, uint64_t *__restrict__ hi, uint64_t *__restrict__ lo) {
+  GRID_STRIDE(i, n) {
+    hi[i] = (uint64_t)tr[i];
+    lo[i] = ((uint64_t)(uint32_t)ts[i] << qb) | (uint32_t)q[i];
+  }
+}
+
+// alignment (planner.py:371-373) and schedule membership (model.py:201-205)
+__global__ void k_checks(const int32_t *__restrict__ tr, const int64_t *__restrict__ ev_off,
+                         const int64_t *__restrict__ size, const int32_t *__restrict__ te,
+                         const int32_t *__restrict__ ps, const int32_t *__restrict__ pe,
+                         const uint8_t *__restrict__ dyn, const int32_t *__restrict__ horizon,
+                         const int32_t *__restrict__ n_sched, int64_t n, long long align, int *__restrict__ bad_align,
+                         int *__restrict__ bad_phase, int *__restrict__ pmax) {
+  GRID_STRIDE(i, n) {
+    if (dyn[i]) continue;
+    int t = tr[i];
+    int loc = (int)(i - ev_off[t]);
+    if (size[i] % align) atomicMin(bad_align + t, loc);
+    if (te[i] < horizon[t]) {
+      if (ps[i] >= n_sched[t] || pe[i] >= n_sched[t]) atomicMin(bad_phase + t, loc);
+      atomicMax(pmax, max(ps[i], pe[i]));
+    }
+  }
+}
+
+__global__ void k_key_group(const int32_t *__restrict__ tr, const int32_t *__restrict__ te,
+                            const int32_t *__restrict__ ps, const int32_t *__restrict__ pe,
+                            const uint8_t *__restrict__ dyn, const int32_t *__restrict__ horizon,
+                            const int32_t *__restrict__ r, int64_t n, int pb, uint64_t *__restrict__ hi,
+                            uint64_t *__restrict__ lo) {
+  GRID_STRIDE(i, n) {
+    int t = tr[i];
+    int c = ev_class(dyn[i], te[i], horizon[t]);
+    uint64_t a = c == 1 ? (uint32_t)ps[i] : 0, b = c == 1 ? (uint32_t)pe[i] : 0;
+    hi[i] = ((uint64_t)t << (2 + 2 * pb)) | ((uint64_t)c << (2 * pb)) | (a << pb) | b;
+    lo[i] = (uint32_t)r[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B: groups
+
+struct Ev {
+  const int32_t *tr, *ts, *te, *ps, *pe, *q;
+  const int64_t *size;
+  const uint8_t *dyn;
+  const int32_t *horizon;
+};
+
+__device__ __forceinline__ void group_key(const Ev &e, uint32_t i, int *c, int *a, int *b) {
+  *c = ev_class(e.dyn[i], e.te[i], e.horizon[e.tr[i]]);
+  *a = *c == 1 ? e.ps[i] : 0;
+  *b = *c == 1 ? e.pe[i] : 0;
+}
+
+__global__ void k_group_heads(Ev e, const uint32_t *__restrict__ gperm, const int64_t *__restrict__ ev_off, int64_t n,
+                              uint32_t *__restrict__ head, int64_t *__restrict__ szs) {
+  GRID_STRIDE(k, n) {
+    uint32_t i = gperm[k];
+    szs[k] = e.size[i];
+    int t = e.tr[i];
+    uint32_t h = 1;
+    if (k != ev_off[t]) {
+      int c1, a1, b1, c0, a0, b0;
+      group_key(e, i, &c1, &a1, &b1);
+      group_key(e, gperm[k - 1], &c0, &a0, &b0);
+      h = (c1 != c0 || a1 != a0 || b1 != b0);
+    }
+    head[k] = h;
+  }
+}
+
+struct Groups {
+  int64_t *start;  // first sorted position
+  int32_t *tr, *cls, *ps, *pe;
+  int64_t *height;
+};
+
+__global__ void k_group_table(Ev e, const uint32_t *__restrict__ gperm, const uint32_t *__restrict__ head,
+                              const uint32_t *__restrict__ gid_incl, int64_t n, Groups g) {
+  GRID_STRIDE(k, n) {
+    if (!head[k]) continue;
+    uint32_t i = gperm[k];
+    int gi = (int)gid_incl[k] - 1;
+    int c, a, b;
+    group_key(e, i, &c, &a, &b);
+    g.start[gi] = k;
+    g.tr[gi] = e.tr[i];
+    g.cls[gi] = c;
+    g.ps[gi] = a;
+    g.pe[gi] = b;
+  }
+}
+
+__global__ void k_group_rel(const uint32_t *__restrict__ gperm, const uint32_t *__restrict__ gid_incl,
+                            const int64_t *__restrict__ S, const int64_t *__restrict__ szs, Groups g, int G,
+                            int64_t n, int64_t *__restrict__ rel, int32_t *__restrict__ gof) {
+  GRID_STRIDE(k, n) {
+    int gi = (int)gid_incl[k] - 1;
+    uint32_t i = gperm[k];
+    rel[i] = S[k] - S[g.start[gi]];
+    gof[i] = gi;
+    int64_t end = gi + 1 < G ? g.start[gi + 1] : n;
+    if (k == end - 1) g.height[gi] = S[k] + szs[k] - S[g.start[gi]];
+  }
+}
+
+struct TraceCounts {
+  int *n_static, *n_pers, *n_groups, *n_plans, *n_res;
+  int64_t *pers_size;
+};
+
+__global__ void k_trace_counts(Groups g, int G, int64_t n, TraceCounts tc, uint32_t *__restrict__ is_plan) {
+  GRID_STRIDE(gi, (int64_t)G) {
+    int t = g.tr[gi];
+    int64_t cnt = (gi + 1 < G ? g.start[gi + 1] : n) - g.start[gi];
+    int c = g.cls[gi];
+    uint32_t plan = 0;
+    if (c == 0) {
+      tc.n_pers[t] = (int)cnt;
+      tc.pers_size[t] = g.height[gi];
+      atomicAdd(tc.n_static + t, (int)cnt);
+    } else if (c == 1) {
+      atomicAdd(tc.n_groups + t, 1);
+      atomicAdd(tc.n_static + t, (int)cnt);
+      if (g.ps[gi] != g.pe[gi]) {
+        plan = 1;
+        atomicAdd(tc.n_plans + t, 1);
+      } else {
+        atomicAdd(tc.n_res + t, (int)cnt);
+      }
+    }
+    is_plan[gi] = plan;
+  }
+}
+
+// plan table (one entry per cross-phase group, planner.py:88-115)
+struct Plans {
+  int32_t *grp, *tr;
+  int64_t *h;
+  int32_t *ts, *te, *k0, *k1, *minq;
+  unsigned long long *used;  // 2 words per plan
+  double *tmp;
+  uint8_t *alive;
+};
+
+__global__ void k_plan_init(Groups g, int G, const uint32_t *__restrict__ is_plan,
+                            const uint32_t *__restrict__ pidx_excl, const uint32_t *__restrict__ gperm, Ev e,
+                            Plans p) {
+  GRID_STRIDE(gi, (int64_t)G) {
+    if (!is_plan[gi]) continue;
+    uint32_t k = pidx_excl[gi];
+    p.grp[k] = (int)gi;
+    p.tr[k] = g.tr[gi];
+    p.h[k] = g.height[gi];
+    p.ts[k] = e.ts[gperm[g.start[gi]]];  // members are (t_s, id) ordered
+    p.te[k] = INT_MIN;
+    p.minq[k] = INT_MAX;
+    p.k0[k] = g.ps[gi];
+    p.k1[k] = g.pe[gi];
+    p.used[2 * k] = 0;
+    p.used[2 * k + 1] = 0;
+    p.alive[k] = 1;
+  }
+}
+
+__global__ void k_plan_members(const uint32_t *__restrict__ gperm, const int32_t *__restrict__ gof,
+                               const uint32_t *__restrict__ is_plan, const uint32_t *__restrict__ pidx_excl, Ev e,
+                               int64_t n, Plans p, int32_t *__restrict__ pid) {
+  GRID_STRIDE(k, n) {
+    uint32_t i = gperm[k];
+    int gi = gof[i];
+    if (!is_plan[gi]) {
+      pid[i] = -1;
+      continue;
+    }
+    uint32_t pk = pidx_excl[gi];
+    pid[i] = (int)pk;
+    atomicMax(p.te + pk, e.te[i]);
+    atomicMin(p.minq + pk, e.q[i]);
+    atomic_add_u128(p.used + 2 * pk, (u128)(uint64_t)e.size[i] * (u128)(uint32_t)(e.te[i] - e.ts[i]));
+  }
+}
+
+__global__ void k_plan_tmp(Plans p, int64_t P) {
+  GRID_STRIDE(k, P) {
+    u128 used = ((u128)p.used[2 * k + 1] << 64) | p.used[2 * k];
+    p.tmp[k] = exact_div(used, (u128)(uint64_t)p.h[k] * (u128)(uint32_t)(p.te[k] - p.ts[k]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C: fusion sweep (planner.py:124-182, 329-354), one CTA per trace
+
+struct FusionArgs {
+  const int64_t *ev_off;
+  const uint32_t *rperm;  // events in (trace, t_s, id) order
+  Ev e;
+  const int64_t *pl_off;  // [T+1]
+  Plans p;                // variant-1 plan state (mutated)
+  int32_t *lst;           // plan list order, per trace segment
+  int32_t *pid;           // per event plan (mutated)
+  int64_t *frel;          // per event address inside its plan (mutated)
+  // per-trace scratch, segment [ev_off[t], ev_off[t+1])
+  int64_t *fx_addr, *fx_end;
+  int32_t *fx_ts, *fx_te;
+  int32_t *rm_ev;
+  int64_t *rm_new;
+  uint8_t *rm_gone;
+  uint32_t *memo;
+  const int64_t *memo_off;  // bit offsets per trace (memo disabled when off[t]==off[t+1])
+  int64_t *attempts, *accepted;
+  double *acc_tmp, *acc_avg;  // indexed by pl_off[t] + k
+};
+
+__device__ __forceinline__ u128 plan_used(const Plans &p, int k) {
+  return ((u128)p.used[2 * k + 1] << 64) | p.used[2 * k];
+}
+__device__ __forceinline__ u128 space_time(const Plans &p, int k) {
+  return (u128)(uint64_t)p.h[k] * (u128)(uint32_t)(p.te[k] - p.ts[k]);
+}
+
+// weighted_tmp_average([a, b]) with CPython float semantics (planner.py:118-121)
+__device__ double weighted_avg2(const Plans &p, int a, int b) {
+  u128 wa = space_time(p, a), wb = space_time(p, b);
+  double s = __dadd_rn(__dmul_rn(p.tmp[a], u128_to_double_rne(wa)), __dmul_rn(p.tmp[b], u128_to_double_rne(wb)));
+  return __ddiv_rn(s, u128_to_double_rne(wa + wb));
+}
+
+// block-wide compaction of one trace's plan members (in (t_s,id) order)
+__device__ void gather_members(const FusionArgs &A, int64_t base, int64_t nt, int L, int S, int *nf, int *nr,
+                               uint32_t *shu) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    *nf = 0;
+    *nr = 0;
+  }
+  __syncthreads();
+  for (int64_t c = 0; c < nt; c += blockDim.x) {
+    int64_t j = c + tid;
+    uint32_t i = j < nt ? A.rperm[base + j] : 0;
+    int who = j < nt ? A.pid[i] : -1;
+    uint32_t isL = who == L, isS = who == S;
+    uint32_t tl, ts_;
+    uint32_t pl = block_excl_sum<uint32_t>(isL, shu, &tl);
+    uint32_t ps = block_excl_sum<uint32_t>(isS, shu, &ts_);
+    int fbase = *nf, rbase = *nr;
+    if (isL) {
+      int64_t o = base + fbase + pl;
+      A.fx_addr[o] = A.frel[i];
+      A.fx_end[o] = A.frel[i] + A.e.size[i];
+      A.fx_ts[o] = A.e.ts[i];
+      A.fx_te[o] = A.e.te[i];
+    }
+    if (isS) {
+      int64_t o = base + rbase + ps;
+      A.rm_ev[o] = (int32_t)i;
+      A.rm_gone[o] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      *nf += (int)tl;
+      *nr += (int)ts_;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kPlanThreads) k_fusion(FusionArgs A, int T) {
+  const int t = blockIdx.x;
+  const int64_t p0 = A.pl_off[t];
+  int P = (int)(A.pl_off[t + 1] - p0);
+  if (A.attempts && threadIdx.x == 0) {
+    A.attempts[t] = 0;
+    A.accepted[t] = 0;
+  }
+  if (P <= 1) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  const int NW = blockDim.x >> 5;
+  const int64_t base = A.ev_off[t], nt = A.ev_off[t + 1] - base;
+  const int64_t P0 = P;
+  const bool use_memo = A.memo_off[t + 1] > A.memo_off[t];
+  __shared__ uint32_t shu[33];
+  __shared__ long long shl[33];
+  __shared__ int sh_nf, sh_nr, sh_pick, sh_first, sh_left, sh_okw[32];
+  __shared__ long long sh_addr, sh_maxend;
+  __shared__ long long sh_att, sh_acc;
+  int32_t *lst = A.lst + p0;
+  if (tid == 0) {
+    sh_att = 0;
+    sh_acc = 0;
+  }
+  __syncthreads();
+
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (int i = 0; i < P - 1 && !changed; i++) {
+      const int a = lst[i];
+      int j = i + 1;
+      while (j < P) {
+        // next adjacent (and not memo-rejected) partner in list order
+        int jj = j + tid;
+        bool adj = false, fresh = false;
+        if (jj < P) {
+          int b = lst[jj];
+          adj = A.p.k1[a] == A.p.k0[b] || A.p.k1[b] == A.p.k0[a];
+          if (adj) {
+            fresh = true;
+            if (use_memo) {
+              int x = min(a, b) - (int)p0, y = max(a, b) - (int)p0;
+              int64_t bit = A.memo_off[t] + (int64_t)x * P0 + y;
+              fresh = !((A.memo[bit >> 5] >> (bit & 31)) & 1u);
+            }
+          }
+        }
+        int cand = (adj && fresh) ? jj : INT_MAX;
+        int jstar = block_reduce_min(cand, (int *)shu);
+        // attempts counted for every adjacent pair up to and including jstar
+        uint32_t cnt_adj = (adj && jj <= jstar) ? 1u : 0u;
+        uint32_t tot;
+        block_excl_sum<uint32_t>(cnt_adj, shu, &tot);
+        if (tid == 0) sh_att += tot;
+        if (jstar == INT_MAX) {
+          j += blockDim.x;
+          continue;
+        }
+        // ---- try_fuse(larger, smaller) --------------------------------------
+        const int b = lst[jstar];
+        const int L = A.p.h[a] >= A.p.h[b] ? a : b;
+        const int S = L == a ? b : a;
+        gather_members(A, base, nt, L, S, &sh_nf, &sh_nr, shu);
+        const int nf0 = sh_nf, nr = sh_nr;
+        long long amin = LLONG_MAX, emax = LLONG_MIN;
+        for (int k = tid; k < nf0; k += blockDim.x) {
+          amin = min(amin, (long long)A.fx_addr[base + k]);
+          emax = max(emax, (long long)A.fx_end[base + k]);
+        }
+        amin = block_reduce_min(amin, shl);
+        emax = block_reduce_max(emax, shl);
+        if (tid == 0) {
+          sh_addr = amin;
+          sh_maxend = emax;
+          sh_left = nr;
+          sh_first = 0;
+          sh_nf = nf0;
+        }
+        __syncthreads();
+        while (sh_left > 0) {
+          const long long addr = sh_addr;
+          const int nf = sh_nf;
+          if (tid == 0) sh_pick = -1;
+          __syncthreads();
+          for (int cb = sh_first; cb < nr; cb += NW) {
+            int k = cb + warp;
+            bool ok = false;
+            if (k < nr && !A.rm_gone[base + k]) {
+              int ev = A.rm_ev[base + k];
+              long long hi = addr + A.e.size[ev];
+              int ets = A.e.ts[ev], ete = A.e.te[ev];
+              bool conflict = false;
+              for (int f = lane; f < nf && !conflict; f += 32) {
+                int64_t o = base + f;
+                conflict = A.fx_addr[o] < hi && addr < A.fx_end[o] && A.fx_ts[o] < ete && ets < A.fx_te[o];
+              }
+              ok = !__any_sync(0xffffffffu, conflict);
+            }
+            if (lane == 0) sh_okw[warp] = ok ? k : INT_MAX;
+            __syncthreads();
+            if (tid == 0) {
+              int m = INT_MAX;
+              for (int w = 0; w < NW; w++) m = min(m, sh_okw[w]);
+              if (m != INT_MAX) sh_pick = m;
+            }
+            __syncthreads();
+            if (sh_pick >= 0) break;
+          }
+          if (sh_pick >= 0) {
+            if (tid == 0) {
+              int k = sh_pick;
+              int ev = A.rm_ev[base + k];
+              long long sz = A.e.size[ev];
+              A.rm_gone[base + k] = 1;
+              A.rm_new[base + k] = addr;
+              int64_t o = base + sh_nf;
+              A.fx_addr[o] = addr;
+              A.fx_end[o] = addr + sz;
+              A.fx_ts[o] = A.e.ts[ev];
+              A.fx_te[o] = A.e.te[ev];
+              sh_nf++;
+              if (addr + sz > sh_maxend) sh_maxend = addr + sz;
+              sh_addr = addr + sz;
+              sh_left--;
+              int f = sh_first;
+              while (f < nr && A.rm_gone[base + f]) f++;
+              sh_first = f;
+            }
+          } else {
+            // next anchor strictly above the cursor, else the top of everything fixed
+            long long nx = LLONG_MAX;
+            for (int k = tid; k < nf0; k += blockDim.x) {
+              long long v = A.fx_addr[base + k];
+              if (v > addr && v < nx) nx = v;
+            }
+            nx = block_reduce_min(nx, shl);
+            if (tid == 0) sh_addr = nx != LLONG_MAX ? nx : sh_maxend;
+          }
+          __syncthreads();
+        }
+        // fused plan statistics (_plan_from_decisions) and acceptance (try_fuse)
+        const long long fh = sh_maxend;
+        const int fts = min(A.p.ts[L], A.p.ts[S]), fte = max(A.p.te[L], A.p.te[S]);
+        const u128 fused = plan_used(A.p, L) + plan_used(A.p, S);
+        const double ftmp = exact_div(fused, (u128)(uint64_t)fh * (u128)(uint32_t)(fte - fts));
+        const double avg = weighted_avg2(A.p, L, S);
+        const bool accept = ftmp > avg;
+        if (!accept) {
+          if (tid == 0 && use_memo) {
+            int x = min(a, b) - (int)p0, y = max(a, b) - (int)p0;
+            int64_t bit = A.memo_off[t] + (int64_t)x * P0 + y;
+            A.memo[bit >> 5] |= 1u << (bit & 31);
+          }
+          __syncthreads();
+          j = jstar + 1;
+          continue;
+        }
+        // commit: plans[i] = fused; del plans[j]
+        const int si = a, sj = b;
+        for (int k = tid; k < nr; k += blockDim.x) A.frel[A.rm_ev[base + k]] = A.rm_new[base + k];
+        for (int64_t k = tid; k < nt; k += blockDim.x) {
+          uint32_t ev = A.rperm[base + k];
+          int w = A.pid[ev];
+          if (w == si || w == sj) A.pid[ev] = si;
+        }
+        if (tid == 0) {
+          int nk0 = (A.p.ts[L] <= A.p.ts[S] ? A.p.k0[L] : A.p.k0[S]);
+          int nk1 = (A.p.te[L] >= A.p.te[S] ? A.p.k1[L] : A.p.k1[S]);
+          int nminq = min(A.p.minq[L], A.p.minq[S]);
+          A.acc_tmp[p0 + sh_acc] = ftmp;
+          A.acc_avg[p0 + sh_acc] = avg;
+          sh_acc++;
+          A.p.h[si] = fh;
+          A.p.ts[si] = fts;
+          A.p.te[si] = fte;
+          A.p.used[2 * si] = (unsigned long long)fused;
+          A.p.used[2 * si + 1] = (unsigned long long)(fused >> 64);
+          A.p.tmp[si] = ftmp;
+          A.p.k0[si] = nk0;
+          A.p.k1[si] = nk1;
+          A.p.minq[si] = nminq;
+          A.p.alive[sj] = 0;
+        }
+        // memo: forget every verdict involving the rewritten slot
+        if (use_memo) {
+          int x0 = si - (int)p0;
+          for (int k = tid; k < P0; k += blockDim.x) {
+            int x = min(x0, k), y = max(x0, k);
+            int64_t bit = A.memo_off[t] + (int64_t)x * P0 + y;
+            atomicAnd(A.memo + (bit >> 5), ~(1u << (bit & 31)));
+          }
+        }
+        // delete list position jstar
+        int moved[8];
+        int nm = 0;
+        for (int k = jstar + 1 + tid; k < P && nm < 8; k += blockDim.x) moved[nm++] = lst[k];
+        __syncthreads();
+        nm = 0;
+        for (int k = jstar + 1 + tid; k < P && nm < 8; k += blockDim.x) lst[k - 1] = moved[nm++];
+        __syncthreads();
+        if (P - jstar - 1 > 8 * (int)blockDim.x) {  // long lists: serial tail shift
+          if (tid == 0)
+            for (int k = jstar + 1 + 8 * blockDim.x; k < P; k++) lst[k - 1] = lst[k];
+          __syncthreads();
+        }
+        P -= 1;
+        changed = true;
+        break;
+      }
+    }
+  }
+  if (tid == 0) {
+    A.attempts[t] = sh_att;
+    A.accepted[t] = sh_acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// D: items per (variant, trace): final plans + residual events
+
+struct Items {
+  int64_t *size;
+  int32_t *ts, *te, *tie, *ref;  // ref >= 0 plan id, < 0 ~event
+};
+
+__global__ void k_items_plans(Plans p, int64_t P, const uint32_t *__restrict__ alive_excl,
+                              const int64_t *__restrict__ pl_off, const int64_t *__restrict__ io_vt, Items it) {
+  GRID_STRIDE(k, P) {
+    if (!p.alive[k]) continue;
+    int t = p.tr[k];
+    int64_t pos = io_vt[t] + (alive_excl[k] - alive_excl[pl_off[t]]);
+    it.size[pos] = p.h[k];
+    it.ts[pos] = p.ts[k];
+    it.te[pos] = p.te[k];
+    it.tie[pos] = p.minq[k];
+    it.ref[pos] = (int32_t)k;
+  }
+}
+
+__global__ void k_res_flags(Ev e, const int32_t *__restrict__ gof, Groups g, const int32_t *__restrict__ pid0,
+                            int64_t n, uint32_t *__restrict__ flag) {
+  GRID_STRIDE(i, n) {
+    uint32_t f = 0;
+    if (!e.dyn[i] && pid0[i] < 0) {
+      int c = g.cls[gof[i]];
+      f = c == 1;
+    }
+    flag[i] = f;
+  }
+}
+
+__global__ void k_items_res(Ev e, const uint32_t *__restrict__ flag, const uint32_t *__restrict__ res_excl,
+                            const int64_t *__restrict__ ev_off, const int *__restrict__ n_alive,
+                            const int64_t *__restrict__ io_vt, int64_t n, Items it) {
+  GRID_STRIDE(i, n) {
+    if (!flag[i]) continue;
+    int t = e.tr[i];
+    int64_t pos = io_vt[t] + n_alive[t] + (res_excl[i] - res_excl[ev_off[t]]);
+    it.size[pos] = e.size[i];
+    it.ts[pos] = e.ts[i];
+    it.te[pos] = e.te[i];
+    it.tie[pos] = e.q[i];
+    it.ref[pos] = ~(int32_t)i;
+  }
+}
+
+__global__ void k_item_keys(Items it, int64_t n, const int64_t *__restrict__ io, int VT, int qb, long long align,
+                            long long maxsu, int sb, uint64_t *__restrict__ hi, uint64_t *__restrict__ lo) {
+  GRID_STRIDE(j, n) {
+    int vt = 0;
+    {  // segment of j in io[0..VT]
+      int a = 0, b = VT;
+      while (b - a > 1) {
+        int m = (a + b) >> 1;
+        if (io[m] <= j)
+          a = m;
+        else
+          b = m;
+      }
+      vt = a;
+    }
+    long long su = it.size[j] / align;
+    hi[j] = ((uint64_t)vt << sb) | (uint64_t)(maxsu - su);
+    lo[j] = ((uint64_t)(uint32_t)it.ts[j] << qb) | (uint32_t)it.tie[j];
+  }
+}
+
+// gather items into sorted order; item_of_* map plans/residuals of variant v
+// (items of variant 0 precede those of variant 1) to sorted positions
+__global__ void k_item_permute(Items src, Items dst, const uint32_t *__restrict__ perm, int64_t n,
+                               const int64_t *__restrict__ io, int T, int64_t P, int64_t N,
+                               int32_t *__restrict__ item_of_plan, int32_t *__restrict__ item_of_res) {
+  GRID_STRIDE(j, n) {
+    uint32_t s = perm[j];
+    dst.size[j] = src.size[s];
+    dst.ts[j] = src.ts[s];
+    dst.te[j] = src.te[s];
+    dst.tie[j] = src.tie[s];
+    int r = src.ref[s];
+    dst.ref[j] = r;
+    int v = j >= io[T] ? 1 : 0;
+    if (r >= 0)
+      item_of_plan[(int64_t)v * P + r] = (int32_t)j;
+    else
+      item_of_res[(int64_t)v * N + ~r] = (int32_t)j;
+  }
+}
+
+__global__ void k_widen_u8(const uint8_t *__restrict__ a, uint32_t *__restrict__ o, int64_t n) {
+  GRID_STRIDE(x, n) o[x] = a[x];
+}
+
+// class end (exclusive) for every item: classes are runs of equal size inside a (variant, trace) segment
+__global__ void k_class_heads(Items it, const int64_t *__restrict__ io, int VT, int64_t n, uint32_t *__restrict__ head) {
+  GRID_STRIDE(j, n) {
+    uint32_t h = 1;
+    if (j > 0 && it.size[j] == it.size[j - 1]) {
+      int a = 0, b = VT;  // same segment?
+      while (b - a > 1) {
+        int m = (a + b) >> 1;
+        if (io[m] <= j)
+          a = m;
+        else
+          b = m;
+      }
+      h = io[a] == j;
+    }
+    head[j] = h;
+  }
+}
+
+__global__ void k_class_start(const uint32_t *__restrict__ head, const uint32_t *__restrict__ cid_incl, int64_t n,
+                              int64_t *__restrict__ cstart) {
+  GRID_STRIDE(j, n) if (head[j]) cstart[cid_incl[j] - 1] = j;
+}
+
+__global__ void k_class_end(const uint32_t *__restrict__ cid_incl, const int64_t *__restrict__ cstart, int64_t nc,
+                            int64_t n, int64_t *__restrict__ cend) {
+  GRID_STRIDE(j, n) {
+    int64_t c = cid_incl[j];  // id + 1
+    cend[j] = c < nc ? cstart[c] : n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// E: HomoSize layers, one CTA per unit (planner.py:189-254, 414-439)
+
+struct LayerArgs {
+  int C, T;
+  const uint8_t *cand;
+  const int32_t *var_of;
+  const int64_t *io;  // [V*T+1]
+  const int64_t *uo;  // [U+1] unit scratch offsets
+  Items it;
+  const int64_t *cend;
+  const int64_t *pers_size;
+  int32_t *sA_ts, *sA_te, *sB_ts, *sB_te;  // [total]
+  int32_t *loffA, *loffB;                  // [total + U]
+  int32_t *prioA, *prioB, *lastEnd, *nend, *newcnt, *runoff, *run_ts, *run_te;
+  uint32_t *fitw;  // [total * kFitWords]
+  int32_t *ilayer, *irank;
+  int64_t *lsize, *lbase;
+  int32_t *nlayers;
+  int64_t *gapins, *pool;
+};
+
+// fits_gap of item [ts, te] against layer slots [lo, hi) of buffer (sts, ste)
+__device__ __forceinline__ bool slot_fit(const int32_t *__restrict__ sts, const int32_t *__restrict__ ste, int lo,
+                                         int hi, int ts, int te) {
+  int a = lo, b = hi;  // first slot with start > te
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (sts[m] <= te)
+      a = m + 1;
+    else
+      b = m;
+  }
+  return a == lo || ste[a - 1] < ts;
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t *__restrict__ v, int lo, int hi, int x) {
+  while (lo < hi) {
+    int m = (lo + hi) >> 1;
+    if (v[m] < x)
+      lo = m + 1;
+    else
+      hi = m;
+  }
+  return lo;
+}
+
+// block exclusive scan of f(l) for l in [0, n) into out[0..n], out[n] = total
+template <class F>
+__device__ void block_scan_into(int n, F f, int32_t *out, int *shi) {
+  int carry = 0;
+  for (int c = 0; c < n; c += blockDim.x) {
+    int l = c + threadIdx.x;
+    int v = l < n ? f(l) : 0;
+    int tot;
+    int ex = block_excl_sum<int>(v, shi, &tot);
+    if (l < n) out[l] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A) {
+  const int u = blockIdx.x;
+  const int c = u % A.C, t = u / A.C;
+  const int v = A.var_of[c];
+  const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
+  const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
+  const int64_t off = A.uo[u];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  __shared__ int shi[33];
+  __shared__ int sm_last[kSmemLayers], sm_nend[kSmemLayers];
+  __shared__ int sh_nl, sh_nnew;
+  __shared__ long long sh_gap;
+
+  int32_t *sAts = A.sA_ts + off, *sAte = A.sA_te + off, *sBts = A.sB_ts + off, *sBte = A.sB_te + off;
+  int32_t *loffA = A.loffA + off + u, *loffB = A.loffB + off + u;
+  int32_t *prioA = A.prioA + off, *prioB = A.prioB + off;
+  int32_t *newcnt = A.newcnt + off, *runoff = A.runoff + off + u;
+  int32_t *run_ts = A.run_ts + off, *run_te = A.run_te + off;
+  int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
+  uint32_t *fitw = A.fitw + off * kFitWords;
+  int64_t *lsize = A.lsize + off;
+  if (tid == 0) {
+    sh_nl = 0;
+    sh_gap = 0;
+    loffA[0] = 0;
+  }
+  __syncthreads();
+
+  for (int64_t j0 = a0; j0 < a1;) {
+    const int64_t j1 = A.cend[j0];
+    const int m = (int)(j1 - j0);
+    const int64_t S = A.it.size[j0];
+    const int nl = sh_nl;
+    const int nfit = min(nl, 32 * kFitWords);
+    int32_t *last = nl <= kSmemLayers ? sm_last : A.lastEnd + off;
+    // ---- 1. fit masks against the slots of earlier classes
+    if (gap && nl > 0) {
+      for (int x = tid; x < m * kFitWords; x += blockDim.x) fitw[(j0 - a0) * kFitWords + x] = 0;
+      for (int p = tid; p < nl; p += blockDim.x) last[p] = INT_MIN;
+      __syncthreads();
+      for (int64_t x = tid; x < (int64_t)m * nfit; x += blockDim.x) {
+        int jj = (int)(x / nfit), p = (int)(x % nfit);
+        int64_t it = j0 + jj;
+        int l = prioA[p];
+        if (slot_fit(sAts, sAte, loffA[l], loffA[l + 1], A.it.ts[it], A.it.te[it]))
+          atomicOr(fitw + (it - a0) * kFitWords + (p >> 5), 1u << (p & 31));
+      }
+    }
+    for (int l = tid; l < nl; l += blockDim.x) newcnt[l] = 0;
+    __syncthreads();
+    // ---- 2. warp-serial resolve: gap insertion, else Alg. 1 among this class's new layers
+    if (warp == 0) {
+      int nnew = 0;
+      long long gapc = 0;
+      int32_t *nend = A.nend + off;  // spill path when a class opens > kSmemLayers layers
+      for (int64_t cb = j0; cb < j1; cb += 32) {
+        int64_t mine = cb + lane;
+        int my_ts = 0, my_te = 0;
+        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+        if (mine < j1) {
+          my_ts = A.it.ts[mine];
+          my_te = A.it.te[mine];
+          if (gap && nl > 0) {
+            const uint32_t *f = fitw + (mine - a0) * kFitWords;
+            w0 = f[0];
+            w1 = f[1];
+            w2 = f[2];
+            w3 = f[3];
+          }
+        }
+        const int cnt = (int)min((int64_t)32, j1 - cb);
+        for (int k = 0; k < cnt; k++) {
+          const int ts = __shfl_sync(0xffffffffu, my_ts, k), te = __shfl_sync(0xffffffffu, my_te, k);
+          const uint32_t f0 = __shfl_sync(0xffffffffu, w0, k), f1 = __shfl_sync(0xffffffffu, w1, k),
+                         f2 = __shfl_sync(0xffffffffu, w2, k), f3 = __shfl_sync(0xffffffffu, w3, k);
+          const int64_t jj = cb + k;
+          int host_p = -1;
+          if (gap) {
+            for (int pb = 0; pb < nl && host_p < 0; pb += 32) {
+              int p = pb + lane;
+              bool ok = false;
+              if (p < nl) {
+                bool fit;
+                if (p < 32 * kFitWords) {
+                  uint32_t w = pb == 0 ? f0 : pb == 32 ? f1 : pb == 64 ? f2 : f3;
+                  fit = (w >> lane) & 1u;
+                } else {
+                  int l = prioA[p];
+                  fit = slot_fit(sAts, sAte, loffA[l], loffA[l + 1], ts, te);
+                }
+                ok = fit && last[p] < ts;
+              }
+              unsigned msk = __ballot_sync(0xffffffffu, ok);
+              if (msk) host_p = pb + __ffs(msk) - 1;
+            }
+          }
+          int layer;
+          if (host_p >= 0) {
+            layer = prioA[host_p];
+            if (lane == 0) last[host_p] = te;
+            gapc++;
+          } else {
+            int32_t *ne = nnew <= kSmemLayers ? sm_nend : nend;
+            int best_k = -1, best_e = INT_MIN;
+            for (int kb = 0; kb < nnew; kb += 32) {
+              int kk = kb + lane;
+              int e = kk < nnew ? ne[kk] : INT_MIN;
+              bool cand = kk < nnew && e < ts;
+              int mx = __reduce_max_sync(0xffffffffu, cand ? e : INT_MIN);
+              unsigned cm = __ballot_sync(0xffffffffu, cand && e == mx);
+              if (cm && (best_k < 0 || mx > best_e)) {
+                best_e = mx;
+                best_k = kb + __ffs(cm) - 1;
+              }
+            }
+            if (best_k < 0) {
+              best_k = nnew++;
+              if (nnew == kSmemLayers + 1) {  // spill the new-layer ends to global memory
+                for (int x = lane; x < kSmemLayers; x += 32) nend[x] = sm_nend[x];
+                __syncwarp();
+              }
+              if (lane == 0) newcnt[nl + best_k] = 0;
+            }
+            int32_t *ne2 = nnew <= kSmemLayers ? sm_nend : nend;
+            if (lane == 0) ne2[best_k] = te;
+            layer = nl + best_k;
+          }
+          if (lane == 0) {
+            ilayer[jj - a0] = layer;
+            irank[jj - a0] = newcnt[layer]++;
+          }
+          __syncwarp();
+        }
+      }
+      if (lane == 0) {
+        sh_nnew = nnew;
+        sh_gap += gapc;
+      }
+    }
+    __syncthreads();
+    // ---- 3. merge this class's slots into the per-layer sorted slot CSR
+    const int nnew = sh_nnew, nl2 = nl + nnew;
+    for (int x = tid; x < nnew; x += blockDim.x) lsize[nl + x] = S;
+    block_scan_into(nl2, [&](int l) { return (l < nl ? loffA[l + 1] - loffA[l] : 0) + newcnt[l]; }, loffB, shi);
+    block_scan_into(nl2, [&](int l) { return newcnt[l]; }, runoff, shi);
+    for (int x = tid; x < m; x += blockDim.x) {
+      int l = ilayer[j0 - a0 + x];
+      int pos = runoff[l] + irank[j0 - a0 + x];
+      run_ts[pos] = A.it.ts[j0 + x];
+      run_te[pos] = A.it.te[j0 + x];
+    }
+    __syncthreads();
+    const int nold = nl > 0 ? loffA[nl] : 0;
+    for (int s = tid; s < nold; s += blockDim.x) {
+      int a = 0, b = nl;  // layer of slot s
+      while (b - a > 1) {
+        int mid = (a + b) >> 1;
+        if (loffA[mid] <= s)
+          a = mid;
+        else
+          b = mid;
+      }
+      int l = a;
+      while (loffA[l + 1] <= s) l++;  // skip empty layers
+      int ts = sAts[s];
+      int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
+      int dst = loffB[l] + (s - loffA[l]) + k;
+      sBts[dst] = ts;
+      sBte[dst] = sAte[s];
+    }
+    for (int x = tid; x < m; x += blockDim.x) {
+      int l = ilayer[j0 - a0 + x];
+      int ts = A.it.ts[j0 + x];
+      int k = l < nl ? lower_bound_i32(sAts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
+      int dst = loffB[l] + irank[j0 - a0 + x] + k;
+      sBts[dst] = ts;
+      sBte[dst] = A.it.te[j0 + x];
+    }
+    // priority order for later classes: newest (smallest) layers first, creation order within
+    for (int x = tid; x < nl2; x += blockDim.x) prioB[x] = x < nnew ? nl + x : prioA[x - nnew];
+    __syncthreads();
+    {
+      int32_t *tp;
+      tp = sAts, sAts = sBts, sBts = tp;
+      tp = sAte, sAte = sBte, sBte = tp;
+      tp = loffA, loffA = loffB, loffB = tp;
+      tp = prioA, prioA = prioB, prioB = tp;
+    }
+    if (tid == 0) sh_nl = nl2;
+    __syncthreads();
+    j0 = j1;
+  }
+  // ---- F: stacking (planner.py:441-444)
+  const int nl = sh_nl;
+  int64_t *lbase = A.lbase + off;
+  long long carry = A.pers_size[t];
+  for (int c0 = 0; c0 < nl; c0 += blockDim.x) {
+    int l = c0 + tid;
+    long long v0 = l < nl ? lsize[l] : 0;
+    __shared__ long long shl[33];
+    long long tot;
+    long long ex = block_excl_sum<long long>(v0, shl, &tot);
+    if (l < nl) lbase[l] = carry + ex;
+    carry += tot;
+  }
+  if (tid == 0) {
+    A.nlayers[u] = nl;
+    A.gapins[u] = sh_gap;
+    A.pool[u] = carry;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// F: emission (planner.py:446-455)
+
+struct EmitArgs {
+  int C, T;
+  int64_t N, P;
+  const int32_t *var_of;
+  Ev e;
+  const int64_t *rel, *frel1;
+  const int32_t *pid0, *pid1;
+  const int32_t *item_of_plan, *item_of_res;  // [V * P], [V * N]
+  const int64_t *io, *uo;
+  const int32_t *ilayer;
+  const int64_t *lbase;
+  int64_t *addr;    // [C * N]
+  int32_t *layer;   // [C * N]
+};
+
+__global__ void k_emit(EmitArgs A) {
+  GRID_STRIDE(x, (int64_t)A.C * A.N) {
+    int c = (int)(x / A.N);
+    int64_t i = x - (int64_t)c * A.N;
+    int t = A.e.tr[i];
+    int64_t u = (int64_t)t * A.C + c;
+    int v = A.var_of[c];
+    int cl = ev_class(A.e.dyn[i], A.e.te[i], A.e.horizon[t]);
+    long long ad = -1;
+    int ly = -1;
+    if (cl == 0) {
+      ad = A.rel[i];
+    } else if (cl == 1) {
+      int p = v ? A.pid1[i] : A.pid0[i];
+      int64_t j;
+      long long fr = 0;
+      if (p >= 0) {
+        j = A.item_of_plan[(int64_t)v * A.P + p];
+        fr = v ? A.frel1[i] : A.rel[i];
+      } else {
+        j = A.item_of_res[(int64_t)v * A.N + i];
+      }
+      int64_t local = j - A.io[(int64_t)v * A.T + t];
+      ly = A.ilayer[A.uo[u] + local];
+      ad = A.lbase[A.uo[u] + ly] + fr;
+    }
+    A.addr[x] = ad;
+    A.layer[x] = ly;
+  }
+}
+
+// sweep-order rectangle sets for the self-check: static events in (t_s, id) order
+__global__ void k_static_flag(const uint32_t *__restrict__ rperm, const uint8_t *__restrict__ dyn, int64_t n,
+                              uint32_t *__restrict__ f) {
+  GRID_STRIDE(k, n) f[k] = dyn[rperm[k]] ? 0u : 1u;
+}
+
+__global__ void k_rect_fill(const uint32_t *__restrict__ rperm, const uint32_t *__restrict__ f,
+                            const uint32_t *__restrict__ pos, Ev e, int64_t n, int C, const int64_t *__restrict__ addr,
+                            int32_t *__restrict__ rs_ev, int32_t *__restrict__ rts, int32_t *__restrict__ rte,
+                            int64_t *__restrict__ rsz, int64_t *__restrict__ raddr, int64_t nstat) {
+  GRID_STRIDE(k, n) {
+    if (!f[k]) continue;
+    uint32_t i = rperm[k];
+    uint32_t o = pos[k];
+    rs_ev[o] = (int32_t)i;
+    rts[o] = e.ts[i];
+    rte[o] = e.te[i];
+    rsz[o] = e.size[i];
+    for (int c = 0; c < C; c++) raddr[(int64_t)c * nstat + o] = addr[(int64_t)c * n + i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+
+template <class T>
+static void d2h(Ctx &ctx, std::vector<T> &h, const T *d, int64_t n) {
+  h.resize(n);
+  if (n > 0) STW_CUDA(ctx, cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
+}
+template <class T>
+static T *h2d(Ctx &ctx, Arena &ar, const std::vector<T> &h) {
+  T *d = ar.take<T>(h.size() ? h.size() : 1);
+  if (d && h.size())
+    STW_CUDA(ctx, cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx.stream));
+  return d;
+}
+static void sync(Ctx &ctx) { STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream)); }
+
+template <class T>
+static void out_copy(Ctx &ctx, T *dst, const T *src, int64_t n, bool dst_dev) {
+  if (!dst || n <= 0 || !ctx.ok()) return;
+  STW_CUDA(ctx, cudaMemcpyAsync(dst, src, n * sizeof(T), dst_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                ctx.stream));
+}
+
+#define LAUNCH(kern, n, ...)                                                     \
+  do {                                                                           \
+    if (ctx.ok() && (n) > 0) {                                                   \
+      kern<<<grid_for((n), 256), 256, 0, ctx.stream>>>(__VA_ARGS__);             \
+      STW_LAUNCHED(ctx);                                                         \
+    }                                                                            \
+  } while (0)
+
+int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out) {
+  Arena ar(&ctx);
+  DevBatch b;
+  if (!o || o->n_cand <= 0 || !o->cand || o->alignment <= 0) {
+    ctx.fail(STW_EARG, "bad plan options");
+    return ctx.rc;
+  }
+  if (!stage_batch(ctx, ar, in, &b)) return ctx.rc;
+  const int T = b.T, C = o->n_cand;
+  const int64_t N = b.N, U = (int64_t)T * C;
+  std::vector<uint8_t> hcand(o->cand, o->cand + C);
+  std::vector<int32_t> var_of(C);
+  bool want[2] = {false, false};
+  for (int c = 0; c < C; c++) {
+    var_of[c] = (hcand[c] & STW_CAND_FUSION) ? 1 : 0;
+    want[var_of[c]] = true;
+  }
+  const int V = 2;
+  if (T == 0) return ctx.rc;
+
+  // ---- A: canonical ranks
+  int32_t *tr = ar.take<int32_t>(N + 1);
+  int32_t *q = ar.take<int32_t>(N + 1), *r = ar.take<int32_t>(N + 1);
+  uint64_t *khi = ar.take<uint64_t>(N + 1), *klo = ar.take<uint64_t>(N + 1);
+  uint32_t *perm = ar.take<uint32_t>(N + 1), *rperm = ar.take<uint32_t>(N + 1), *gperm = ar.take<uint32_t>(N + 1);
+  int32_t *order_local = ar.take<int32_t>(N + 1);
+  long long *mm = ar.take<long long>(2);
+  int *im = ar.take<int>(4);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_trace_of_all, N, b.ev_off, T, N, tr);
+  long long mm_init[2] = {LLONG_MAX, LLONG_MIN};
+  STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
+  LAUNCH(k_minmax_i64, N, b.id, N, mm, mm + 1);
+  LAUNCH(k_max_i32, N, b.t_s, N, im);
+  long long hmm[2] = {0, 0};
+  int him[4] = {0, 0, 0, 0};
+  STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaMemcpyAsync(him, im, sizeof(him), cudaMemcpyDeviceToHost, ctx.stream));
+  sync(ctx);
+  if (!ctx.ok()) return ctx.rc;
+  const int tb = bitlen_u64((uint64_t)(T - 1));
+  const int idb = N ? bitlen_u64((uint64_t)(hmm[1] - hmm[0])) : 0;
+  const int qb = bitlen_u64((uint64_t)(b.max_trace_events > 0 ? b.max_trace_events - 1 : 0));
+  const int tsb = bitlen_u64((uint64_t)him[0]);
+  // q: id rank within trace
+  LAUNCH(k_key_q, N, tr, b.id, N, hmm[0], khi, klo);
+  sort_perm2(ctx, ar, khi, tb, klo, idb, perm, N);
+  LAUNCH(k_rank_from_perm, N, perm, tr, b.ev_off, N, q, (int32_t *)nullptr);
+  // r: (t_s, id) rank within trace
+  LAUNCH(k_key_r, N, tr, b.t_s, q, N, qb, khi, klo);
+  sort_perm2(ctx, ar, khi, tb, klo, tsb + qb, rperm, N);
+  LAUNCH(k_rank_from_perm, N, rperm, tr, b.ev_off, N, r, order_local);
+
+  // per-trace input checks
+  int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
+  if (!ctx.ok()) return ctx.rc;
+  {
+    std::vector<int> big(T, INT_MAX);
+    STW_CUDA(ctx, cudaMemcpyAsync(bad_align, big.data(), T * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
+    STW_CUDA(ctx, cudaMemcpyAsync(bad_phase, big.data(), T * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
+    sync(ctx);
+  }
+  LAUNCH(k_checks, N, tr, b.ev_off, b.size, b.t_e, b.ps, b.pe, b.dyn, b.horizon, b.n_sched, N, (long long)o->alignment,
+         bad_align, bad_phase, im + 1);
+  STW_CUDA(ctx, cudaMemcpyAsync(him, im, sizeof(him), cudaMemcpyDeviceToHost, ctx.stream));
+  sync(ctx);
+  if (!ctx.ok()) return ctx.rc;
+  const int pb = bitlen_u64((uint64_t)him[1]);
+
+  // ---- B: phase groups
+  Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
+  LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
+  sort_perm2(ctx, ar, khi, tb + 2 + 2 * pb, klo, qb, gperm, N);
+  uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
+  int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
+  int64_t *rel = ar.take<int64_t>(N + 1);
+  int32_t *gof = ar.take<int32_t>(N + 1);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_group_heads, N, e, gperm, b.ev_off, N, head, szs);
+  device_scan<uint32_t>(ctx, ar, head, gid, N, true);
+  device_scan<int64_t>(ctx, ar, szs, S, N, false);
+  uint32_t G32 = 0;
+  if (N) STW_CUDA(ctx, cudaMemcpyAsync(&G32, gid + N - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx.stream));
+  sync(ctx);
+  const int G = (int)G32;
+  Groups g{ar.take<int64_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1),
+           ar.take<int32_t>(G + 1), ar.take<int64_t>(G + 1)};
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_group_table, N, e, gperm, head, gid, N, g);
+  LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, G, N, rel, gof);
+  TraceCounts tc{ar.take<int>(T), ar.take<int>(T), ar.take<int>(T), ar.take<int>(T), ar.take<int>(T),
+                 ar.take<int64_t>(T)};
+  uint32_t *is_plan = ar.take<uint32_t>(G + 1), *pidx = ar.take<uint32_t>(G + 1);
+  if (!ctx.ok()) return ctx.rc;
+  for (int *pcnt : {tc.n_static, tc.n_pers, tc.n_groups, tc.n_plans, tc.n_res})
+    STW_CUDA(ctx, cudaMemsetAsync(pcnt, 0, T * sizeof(int), ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(tc.pers_size, 0, T * sizeof(int64_t), ctx.stream));
+  LAUNCH(k_trace_counts, G, g, G, N, tc, is_plan);
+  device_scan<uint32_t>(ctx, ar, is_plan, pidx, G, false);
+  std::vector<int> h_nplans, h_nstatic, h_npers, h_ngroups, h_nres;
+  d2h(ctx, h_nplans, tc.n_plans, T);
+  d2h(ctx, h_nstatic, tc.n_static, T);
+  d2h(ctx, h_npers, tc.n_pers, T);
+  d2h(ctx, h_ngroups, tc.n_groups, T);
+  d2h(ctx, h_nres, tc.n_res, T);
+  std::vector<int64_t> h_pers_size;
+  d2h(ctx, h_pers_size, tc.pers_size, T);
+  sync(ctx);
+  if (!ctx.ok()) return ctx.rc;
+  std::vector<int64_t> pl_off(T + 1, 0);
+  for (int t = 0; t < T; t++) pl_off[t + 1] = pl_off[t] + h_nplans[t];
+  const int64_t P = pl_off[T];
+  int64_t *d_pl_off = h2d(ctx, ar, pl_off);
+  auto mk_plans = [&]() {
+    return Plans{ar.take<int32_t>(P + 1), ar.take<int32_t>(P + 1), ar.take<int64_t>(P + 1),
+                 ar.take<int32_t>(P + 1), ar.take<int32_t>(P + 1), ar.take<int32_t>(P + 1),
+                 ar.take<int32_t>(P + 1), ar.take<int32_t>(P + 1), ar.take<unsigned long long>(2 * P + 2),
+                 ar.take<double>(P + 1), ar.take<uint8_t>(P + 1)};
+  };
+  Plans p0 = mk_plans();
+  int32_t *pid0 = ar.take<int32_t>(N + 1);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_plan_init, G, g, G, is_plan, pidx, gperm, e, p0);
+  LAUNCH(k_plan_members, N, gperm, gof, is_plan, pidx, e, N, p0, pid0);
+  LAUNCH(k_plan_tmp, P, p0, P);
+
+  // ---- C: fusion variant
+  Plans p1 = p0;
+  int32_t *pid1 = pid0;
+  int64_t *frel1 = rel;
+  std::vector<int64_t> h_att(T, 0), h_acc(T, 0);
+  double *acc_tmp = nullptr, *acc_avg = nullptr;
+  if (want[1]) {
+    p1 = mk_plans();
+    pid1 = ar.take<int32_t>(N + 1);
+    frel1 = ar.take<int64_t>(N + 1);
+    int32_t *lst = ar.take<int32_t>(P + 1);
+    acc_tmp = ar.take<double>(P + 1);
+    acc_avg = ar.take<double>(P + 1);
+    int64_t *att = ar.take<int64_t>(T), *acc = ar.take<int64_t>(T);
+    std::vector<int64_t> moff(T + 1, 0);
+    const int64_t kMemoMax = 4096;
+    for (int t = 0; t < T; t++) {
+      int64_t pp = h_nplans[t];
+      moff[t + 1] = moff[t] + ((pp > 1 && pp <= kMemoMax) ? pp * pp : 0);
+      moff[t + 1] = (moff[t + 1] + 31) & ~(int64_t)31;
+    }
+    int64_t *d_moff = h2d(ctx, ar, moff);
+    uint32_t *memo = ar.take<uint32_t>(moff[T] / 32 + 1);
+    FusionArgs F{b.ev_off, rperm, e, d_pl_off, p1, lst, pid1, frel1,
+                 ar.take<int64_t>(N + 1), ar.take<int64_t>(N + 1), ar.take<int32_t>(N + 1), ar.take<int32_t>(N + 1),
+                 ar.take<int32_t>(N + 1), ar.take<int64_t>(N + 1), ar.take<uint8_t>(N + 1), memo, d_moff, att, acc,
+                 acc_tmp, acc_avg};
+    if (!ctx.ok()) return ctx.rc;
+#define CPY(dst, src, cnt) STW_CUDA(ctx, cudaMemcpyAsync(dst, src, (cnt) * sizeof(*(src)), cudaMemcpyDeviceToDevice, ctx.stream))
+    CPY(p1.grp, p0.grp, P + 1);
+    CPY(p1.tr, p0.tr, P + 1);
+    CPY(p1.h, p0.h, P + 1);
+    CPY(p1.ts, p0.ts, P + 1);
+    CPY(p1.te, p0.te, P + 1);
+    CPY(p1.k0, p0.k0, P + 1);
+    CPY(p1.k1, p0.k1, P + 1);
+    CPY(p1.minq, p0.minq, P + 1);
+    CPY(p1.used, p0.used, 2 * P + 2);
+    CPY(p1.tmp, p0.tmp, P + 1);
+    CPY(p1.alive, p0.alive, P + 1);
+    CPY(pid1, pid0, N + 1);
+    CPY(frel1, rel, N + 1);
+#undef CPY
+    STW_CUDA(ctx, cudaMemsetAsync(memo, 0, (moff[T] / 32 + 1) * sizeof(uint32_t), ctx.stream));
+    k_iota<<<grid_for(P + 1, 256), 256, 0, ctx.stream>>>((uint32_t *)lst, P + 1);
+    STW_LAUNCHED(ctx);
+    if (ctx.ok()) {
+      k_fusion<<<T, kPlanThreads, 0, ctx.stream>>>(F, T);
+      STW_LAUNCHED(ctx);
+    }
+    d2h(ctx, h_att, att, T);
+    d2h(ctx, h_acc, acc, T);
+  }
+
+  // ---- D: items per (variant, trace)
+  std::vector<int64_t> io(V * T + 1, 0);
+  std::vector<int> n_alive(V * T, 0);
+  sync(ctx);
+  if (!ctx.ok()) return ctx.rc;
+  for (int v = 0; v < V; v++)
+    for (int t = 0; t < T; t++) {
+      int64_t na = want[v] ? (v ? h_nplans[t] - h_acc[t] : h_nplans[t]) : 0;
+      int64_t cnt = want[v] ? na + h_nres[t] : 0;
+      n_alive[v * T + t] = (int)na;
+      io[v * T + t + 1] = io[v * T + t] + cnt;
+    }
+  const int64_t NI = io[V * T];
+  int64_t *d_io = h2d(ctx, ar, io);
+  int *d_nalive = h2d(ctx, ar, n_alive);
+  uint32_t *rflag = ar.take<uint32_t>(N + 1), *rexcl = ar.take<uint32_t>(N + 1);
+  uint32_t *aexcl = ar.take<uint32_t>(P + 1), *aflag = ar.take<uint32_t>(P + 1);
+  Items it0{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
+            ar.take<int32_t>(NI + 1)};
+  Items it{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
+           ar.take<int32_t>(NI + 1)};
+  int32_t *item_of_plan = ar.take<int32_t>(V * (P + 1)), *item_of_res = ar.take<int32_t>(V * (N + 1));
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_res_flags, N, e, gof, g, pid0, N, rflag);
+  device_scan<uint32_t>(ctx, ar, rflag, rexcl, N, false);
+  for (int v = 0; v < V; v++) {
+    if (!want[v]) continue;
+    Plans &pv = v ? p1 : p0;
+    LAUNCH(k_widen_u8, P, pv.alive, aflag, P);
+    device_scan<uint32_t>(ctx, ar, aflag, aexcl, P, false);
+    LAUNCH(k_items_plans, P, pv, P, aexcl, d_pl_off, d_io + (int64_t)v * T, it0);
+    LAUNCH(k_items_res, N, e, rflag, rexcl, b.ev_off, d_nalive + (int64_t)v * T, d_io + (int64_t)v * T, N, it0);
+  }
+  // sort items by (variant-trace, size desc, t_s, tie)
+  long long maxsu = 0;
+  {
+    long long *dmx = ar.take<long long>(2);
+    long long init[2] = {LLONG_MAX, LLONG_MIN};
+    STW_CUDA(ctx, cudaMemcpyAsync(dmx, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
+    LAUNCH(k_minmax_i64, NI, it0.size, NI, dmx, dmx + 1);
+    long long h[2] = {0, 0};
+    STW_CUDA(ctx, cudaMemcpyAsync(h, dmx, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+    sync(ctx);
+    maxsu = NI ? h[1] / o->alignment : 0;
+  }
+  uint64_t *ihi = ar.take<uint64_t>(NI + 1), *ilo = ar.take<uint64_t>(NI + 1);
+  uint32_t *iperm = ar.take<uint32_t>(NI + 1);
+  if (!ctx.ok()) return ctx.rc;
+  const int vtb = bitlen_u64((uint64_t)(V * T - 1)), sb = bitlen_u64((uint64_t)maxsu);
+  if (vtb + sb > 64) {
+    ctx.fail(STW_EARG, "item sort key exceeds 64 bits");
+    return ctx.rc;
+  }
+  LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, (long long)o->alignment, maxsu, sb, ihi, ilo);
+  sort_perm2(ctx, ar, ihi, vtb + sb, ilo, tsb + qb, iperm, NI);
+  LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
+  // classes
+  uint32_t *chead = ar.take<uint32_t>(NI + 1), *cid = ar.take<uint32_t>(NI + 1);
+  int64_t *cstart = ar.take<int64_t>(NI + 1), *cend = ar.take<int64_t>(NI + 1);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_class_heads, NI, it, d_io, V * T, NI, chead);
+  device_scan<uint32_t>(ctx, ar, chead, cid, NI, true);
+  uint32_t NC = 0;
+  if (NI) STW_CUDA(ctx, cudaMemcpyAsync(&NC, cid + NI - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx.stream));
+  sync(ctx);
+  LAUNCH(k_class_start, NI, chead, cid, NI, cstart);
+  LAUNCH(k_class_end, NI, cid, cstart, (int64_t)NC, NI, cend);
+
+  // ---- E: layers per unit
+  std::vector<int64_t> uo(U + 1, 0);
+  for (int t = 0; t < T; t++)
+    for (int c = 0; c < C; c++) {
+      int v = var_of[c];
+      int64_t u = (int64_t)t * C + c;
+      uo[u + 1] = uo[u] + (io[(int64_t)v * T + t + 1] - io[(int64_t)v * T + t]);
+    }
+  const int64_t TU = uo[U];
+  int64_t *d_uo = h2d(ctx, ar, uo);
+  uint8_t *d_cand = h2d(ctx, ar, hcand);
+  int32_t *d_var = h2d(ctx, ar, var_of);
+  LayerArgs LA{C, T, d_cand, d_var, d_io, d_uo, it, cend, tc.pers_size,
+               ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1),
+               ar.take<int32_t>(TU + U + 1), ar.take<int32_t>(TU + U + 1),
+               ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1),
+               ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + U + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1),
+               ar.take<uint32_t>((TU + 1) * kFitWords),
+               ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int64_t>(TU + 1), ar.take<int64_t>(TU + 1),
+               ar.take<int32_t>(U), ar.take<int64_t>(U), ar.take<int64_t>(U)};
+  if (!ctx.ok()) return ctx.rc;
+  k_layers<<<(unsigned)U, kPlanThreads, 0, ctx.stream>>>(LA);
+  STW_LAUNCHED(ctx);
+
+  if (getenv("STW_DEBUG_DUMP")) {  // developer aid: dump unit 0's sorted items and layer choices
+    int64_t n0 = uo[1] - uo[0];
+    int v0 = var_of[0];
+    int64_t j0 = io[(int64_t)v0 * T];
+    std::vector<int64_t> hs, hce;
+    std::vector<int32_t> hts, hte, htie, href, hil, hir;
+    d2h(ctx, hs, it.size + j0, n0);
+    d2h(ctx, hts, it.ts + j0, n0);
+    d2h(ctx, hte, it.te + j0, n0);
+    d2h(ctx, htie, it.tie + j0, n0);
+    d2h(ctx, href, it.ref + j0, n0);
+    d2h(ctx, hce, cend + j0, n0);
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    k_layers<<<(unsigned)U, kPlanThreads, 0, ctx.stream>>>(LA);
+    d2h(ctx, hil, LA.ilayer, n0);
+    d2h(ctx, hir, LA.irank, n0);
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    fprintf(stderr, "unit0: v=%d items=%lld (j0=%lld)\n", v0, (long long)n0, (long long)j0);
+    for (int64_t k = 0; k < n0; k++)
+      fprintf(stderr, "  it %lld size=%lld ts=%d te=%d tie=%d ref=%d cend=%lld -> layer %d rank %d\n", (long long)k,
+              (long long)hs[k], hts[k], hte[k], htie[k], href[k], (long long)(hce[k] - j0), hil[k], hir[k]);
+  }
+
+  // ---- F: emission
+  int64_t *addr = ar.take<int64_t>((int64_t)C * N + 1);
+  int32_t *layer = ar.take<int32_t>((int64_t)C * N + 1);
+  if (!ctx.ok()) return ctx.rc;
+  EmitArgs EA{C, T, N, P, d_var, e, rel, frel1, pid0, pid1, item_of_plan, item_of_res, d_io, d_uo,
+              LA.ilayer, LA.lbase, addr, layer};
+  LAUNCH(k_emit, (int64_t)C * N, EA);
+
+  // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
+  int64_t *peak = ar.take<int64_t>(T);
+  if (!ctx.ok()) return ctx.rc;
+  peak_live(ctx, ar, b, true, peak);
+  uint32_t *sflag = ar.take<uint32_t>(N + 1), *spos = ar.take<uint32_t>(N + 1);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_static_flag, N, rperm, b.dyn, N, sflag);
+  device_scan<uint32_t>(ctx, ar, sflag, spos, N, false);
+  std::vector<int64_t> so(T + 1, 0);
+  for (int t = 0; t < T; t++) so[t + 1] = so[t] + h_nstatic[t];
+  const int64_t NS = so[T];
+  int64_t *d_so = h2d(ctx, ar, so);
+  int32_t *rs_ev = ar.take<int32_t>(NS + 1), *rts = ar.take<int32_t>(NS + 1), *rte = ar.take<int32_t>(NS + 1);
+  int64_t *rsz = ar.take<int64_t>(NS + 1), *raddr = ar.take<int64_t>((int64_t)C * NS + 1);
+  long long *vcount = ar.take<long long>(U);
+  int *vfirst = ar.take<int>(U);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_rect_fill, N, rperm, sflag, spos, e, N, C, addr, rs_ev, rts, rte, rsz, raddr, NS);
+  RectSets rs{T, NS, d_so, rts, rte, rsz, C, raddr};
+  validate_sets(ctx, ar, rs, vcount, vfirst);
+
+  // ---- gather per-unit results on the host
+  std::vector<int64_t> h_pool, h_gap, h_peak;
+  std::vector<int32_t> h_nl;
+  std::vector<long long> h_vc;
+  std::vector<int> h_vf, h_ba, h_bp;
+  d2h(ctx, h_pool, LA.pool, U);
+  d2h(ctx, h_gap, LA.gapins, U);
+  d2h(ctx, h_nl, LA.nlayers, U);
+  d2h(ctx, h_peak, peak, T);
+  d2h(ctx, h_vc, vcount, U);
+  d2h(ctx, h_vf, vfirst, U);
+  d2h(ctx, h_ba, bad_align, T);
+  d2h(ctx, h_bp, bad_phase, T);
+  sync(ctx);
+  if (!ctx.ok()) return ctx.rc;
+  std::vector<int32_t> rc(U, STW_OK);
+  std::vector<int64_t> err_ids(2 * U, -1), stats(U * STW_NSTATS, 0);
+  for (int t = 0; t < T; t++)
+    for (int c = 0; c < C; c++) {
+      int64_t u = (int64_t)t * C + c;
+      int v = var_of[c];
+      bool fus_ran = v == 1 && h_nplans[t] > 1;
+      int64_t *st = &stats[u * STW_NSTATS];
+      st[0] = h_nstatic[t];
+      st[1] = h_npers[t];
+      st[2] = h_ngroups[t];
+      st[3] = fus_ran ? h_nplans[t] - h_acc[t] : h_nplans[t];
+      st[4] = h_nres[t];
+      st[5] = fus_ran ? h_att[t] : 0;
+      st[6] = fus_ran ? h_acc[t] : 0;
+      st[7] = h_gap[u];
+      st[8] = h_nl[u];
+      st[9] = h_pool[u];
+      st[10] = h_peak[t];
+      st[11] = h_pers_size[t];
+      if (h_ba[t] != INT_MAX) {
+        rc[u] = STW_EPLAN;
+        err_ids[2 * u] = b.h_ev_off[t] + h_ba[t];  // event index; the shim formats the message
+      } else if (h_bp[t] != INT_MAX) {
+        rc[u] = STW_ETRACE;
+        err_ids[2 * u] = b.h_ev_off[t] + h_bp[t];
+      } else if (h_pool[u] < h_peak[t]) {
+        rc[u] = STW_EPLAN;
+      } else if (h_vc[u] > 0) {
+        rc[u] = STW_EPLAN;
+        int pa = -1, pbb = -1;
+        first_pair(ctx, rs, t, c, h_vf[u], &pa, &pbb);
+        int32_t ev2[2] = {-1, -1};
+        if (pa >= 0) {
+          STW_CUDA(ctx, cudaMemcpy(&ev2[0], rs_ev + so[t] + pa, sizeof(int32_t), cudaMemcpyDeviceToHost));
+          STW_CUDA(ctx, cudaMemcpy(&ev2[1], rs_ev + so[t] + pbb, sizeof(int32_t), cudaMemcpyDeviceToHost));
+          err_ids[2 * u] = ev2[0];
+          err_ids[2 * u + 1] = ev2[1];
+        }
+      }
+    }
+  // ---- outputs
+  const bool od = out->on_device != 0;
+  auto put = [&](auto *dst, const auto &vec) {
+    if (!dst || vec.empty() || !ctx.ok()) return;
+    if (od)
+      STW_CUDA(ctx, cudaMemcpyAsync(dst, vec.data(), vec.size() * sizeof(vec[0]), cudaMemcpyHostToDevice, ctx.stream));
+    else
+      memcpy(dst, vec.data(), vec.size() * sizeof(vec[0]));
+  };
+  put(out->rc, rc);
+  put(out->err_ids, err_ids);
+  put(out->stats, stats);
+  out_copy(ctx, out->addr, addr, (int64_t)C * N, od);
+  out_copy(ctx, out->layer_of, layer, (int64_t)C * N, od);
+  out_copy(ctx, out->order, order_local, N, od);
+  if (out->layer_base || out->layer_size || out->fus_tmp || out->fus_avg) {
+    // per-unit slices at c*N + ev_off[t]
+    for (int t = 0; t < T && ctx.ok(); t++)
+      for (int c = 0; c < C; c++) {
+        int64_t u = (int64_t)t * C + c;
+        int64_t dst = (int64_t)c * N + b.h_ev_off[t];
+        int64_t nl = h_nl[u];
+        if (out->layer_base) out_copy(ctx, out->layer_base + dst, LA.lbase + uo[u], nl, od);
+        if (out->layer_size) out_copy(ctx, out->layer_size + dst, LA.lsize + uo[u], nl, od);
+        bool fus_ran = var_of[c] == 1 && h_nplans[t] > 1;
+        int64_t na = fus_ran ? h_acc[t] : 0;
+        if (out->fus_tmp && na) out_copy(ctx, out->fus_tmp + dst, acc_tmp + pl_off[t], na, od);
+        if (out->fus_avg && na) out_copy(ctx, out->fus_avg + dst, acc_avg + pl_off[t], na, od);
+      }
+  }
+  if (o->select_best) {
+    std::vector<int32_t> best(T, -1);
+    std::vector<int64_t> bpool(T, -1);
+    for (int t = 0; t < T; t++)
+      for (int c = 0; c < C; c++) {
+        int64_t u = (int64_t)t * C + c;
+        if (rc[u] != STW_OK) continue;
+        if (best[t] < 0 || h_pool[u] < bpool[t]) best[t] = c, bpool[t] = h_pool[u];
+      }
+    put(out->best_cand, best);
+    put(out->best_pool, bpool);
+    if (out->addr_best)
+      for (int t = 0; t < T && ctx.ok(); t++) {
+        int64_t n_t = b.h_ev_off[t + 1] - b.h_ev_off[t];
+        if (best[t] >= 0)
+          out_copy(ctx, out->addr_best + b.h_ev_off[t], addr + (int64_t)best[t] * N + b.h_ev_off[t], n_t, od);
+      }
+  }
+  sync(ctx);
+  return ctx.rc;
+}
+
+}  // namespace stw

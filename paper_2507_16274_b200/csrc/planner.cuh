@@ -1,0 +1,36 @@
+// Internal interfaces of the batched planner (plan.cu) and the rectangle
+// validator (validate.cu).
+#pragma once
+#include "batch.cuh"
+
+namespace stw {
+
+// sort by the composite key (hi, lo) of widths (hibits, lobits); perm[k] =
+// index of the k-th smallest. hi/lo are consumed (overwritten).
+void sort_perm2(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, uint64_t *lo, int lobits, uint32_t *perm,
+                int64_t n);
+
+// Static rectangles of a batch of decision sets, set s = [off[s], off[s+1]),
+// each set listed in its sweep order ((t_s, id) order). ts/te/rank are per
+// rectangle; addr/size per (candidate, rectangle) with stride `stride`.
+struct RectSets {
+  int32_t S;            // number of sets (traces)
+  int64_t n;            // rectangles in all sets
+  const int64_t *off;   // [S+1] device
+  const int32_t *ts, *te;  // [n] in sweep order
+  const int64_t *size;     // [n]
+  int32_t n_cand;
+  const int64_t *addr;     // [n_cand * n] (candidate-major)
+};
+
+// K7 for the planner self-check: per (set, candidate) the number of pairs the
+// reference sweep (planner.py:476-505) would report and the sweep position of
+// the first reporting decision (INT_MAX if none). Outputs are device arrays of
+// S*n_cand entries, unit index = set*n_cand + cand.
+void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first);
+
+// Host-side re-derivation of the first reported pair (a, b) of a decision set
+// whose first reporting decision is at sweep position `first` (device data).
+void first_pair(Ctx &ctx, const RectSets &rs, int set, int cand, int first, int *pa, int *pb);
+
+}  // namespace stw

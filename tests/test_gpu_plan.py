@@ -1,0 +1,81 @@
+"""Planner parity: libstw (stw_plan_batch) vs the C oracle, bit-exact.
+
+Addresses of every static event, pool size, every PlanStats counter, the
+accepted-fusion audit pairs (exact doubles) and the layer table, under all
+four (fusion, gap_insert) candidates."""
+
+import numpy as np
+import pytest
+
+from paper_2507_16274_b200 import api, tracegen
+from paper_2507_16274_b200.batching import HostBatch
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CANDS = tracegen.C4_CANDIDATES
+STAT_MAP = ("num_events", "num_persistent", "num_groups", "num_plans", "num_residuals", "fusion_attempts",
+            "fusion_accepted", "gap_insertions", "num_layers", "pool_size", "static_peak", "persistent_size")
+
+
+def fuzz_cfg(seed):
+    preset = tracegen.PRESETS[seed % 6]
+    return tracegen.SynthConfig.for_preset(preset, seed=seed, num_layers=4 + seed % 9,
+                                          num_microbatches=1 + seed % 4, transient_ratio=0.2 + (seed % 5) * 0.2)
+
+
+def check_batch(tas, cands=CANDS):
+    bp = api.plan_batch(tas, cands)
+    C = len(cands)
+    for t, ta in enumerate(tas):
+        s0, s1 = int(bp.batch.ev_off[t]), int(bp.batch.ev_off[t + 1])
+        for c, (f, g) in enumerate(cands):
+            ref = O.plan(ta, f, g)
+            u = t * C + c
+            assert ref.rc == 0 and bp.rc[u] == 0, (t, c, ref.err, bp.rc[u])
+            stat = ~ta.dyn.astype(bool)
+            got = bp.addr[c, s0:s1]
+            bad = np.nonzero(got[stat] != ref.addr[stat])[0]
+            assert bad.size == 0, (t, c, "addr mismatch", bad[:5], got[stat][bad[:5]], ref.addr[stat][bad[:5]])
+            for k, name in enumerate(STAT_MAP):
+                assert int(bp.stats[u, k]) == ref.stats[name], (t, c, name, int(bp.stats[u, k]), ref.stats[name])
+            na = ref.stats["n_accepted"]
+            assert bp.fus_tmp[c, s0:s0 + na].tolist() == [a for a, _ in ref.accepted]
+            assert bp.fus_avg[c, s0:s0 + na].tolist() == [b for _, b in ref.accepted]
+            nl = ref.stats["num_layers"]
+            assert bp.layer_base[c, s0:s0 + nl].tolist() == ref.layer_base.tolist()
+            assert bp.layer_size[c, s0:s0 + nl].tolist() == ref.layer_size.tolist()
+            assert np.array_equal(bp.layer_of[c, s0:s1][stat], ref.layer_of[stat])
+    return bp
+
+
+def test_plan_fuzz_batched():
+    tas = [tracegen.synth_arrays(fuzz_cfg(s)) for s in range(200)]
+    check_batch(tas)
+
+
+def test_plan_fuzz_single_calls():
+    for s in range(0, 60, 7):
+        check_batch([tracegen.synth_arrays(fuzz_cfg(s))])
+
+
+def test_plan_c4_sample_batched():
+    tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(0, 4096, 16)]
+    bp = check_batch(tas)
+    assert bp.rc.max() == 0
+
+
+@pytest.mark.parametrize("name", ["c1_llama2_7b_1f1b", "c3_mixtral_moe", "c3b_mixtral_moe_rcp", "c2_llama2_7b_vpp_rcp"])
+def test_plan_configs(name):
+    check_batch([tracegen.synth_arrays(tracegen.config(name))], ((True, True),))
+
+
+def test_plan_select_best():
+    tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(32)]
+    bp = api.plan_batch(tas, CANDS, select_best=True)
+    for t, ta in enumerate(tas):
+        pools = [O.plan(ta, f, g).stats["pool_size"] for f, g in CANDS]
+        best = min(range(4), key=lambda c: (pools[c], c))
+        assert int(bp.best_cand[t]) == best and int(bp.best_pool[t]) == pools[best]
+        s0, s1 = int(bp.batch.ev_off[t]), int(bp.batch.ev_off[t + 1])
+        assert np.array_equal(bp.addr_best[s0:s1], bp.addr[best, s0:s1])
