@@ -166,6 +166,15 @@ int stw_baseline(const stw_batch *trace, stw_report *rep, stw_log *log, int64_t 
 /* library identification: returns "stw <version> sm_100a" */
 const char *stw_version(void);
 
+/* ---- tracing (diagnostics; off by default) ------------------------------
+ * stw_launch_count: kernels launched by this library since load.
+ * stw_prof_enable: bracket every launch with CUDA events on its stream.
+ * stw_prof_collect: per-kernel launch counts and summed device ms (names in
+ * 64-byte slots); returns the number of distinct kernels. */
+long long stw_launch_count(void);
+void stw_prof_enable(int on);
+int stw_prof_collect(char *names, long long *counts, double *ms, int cap, int reset);
+
 #ifdef __cplusplus
 }
 #endif

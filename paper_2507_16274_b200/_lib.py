@@ -92,6 +92,9 @@ def load() -> C.CDLL:
     for name in EXPORTS[1:]:
         if hasattr(L, name):
             getattr(L, name).restype = C.c_int
+    L.stw_launch_count.restype = C.c_longlong
+    L.stw_prof_enable.restype = None
+    L.stw_prof_collect.restype = C.c_int
     _lib = L
     return L
 
@@ -126,3 +129,27 @@ def stream_handle(stream=None):
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(load().stw_launch_count())
+
+
+def profile(on: bool) -> None:
+    load().stw_prof_enable(C.c_int(int(on)))
+
+
+def profile_collect(reset: bool = True) -> dict:
+    """{kernel name: (launches, total device ms)} recorded since the last reset."""
+    L = load()
+    cap = 256
+    names = C.create_string_buffer(64 * cap)
+    counts = np.zeros(cap, np.int64)
+    ms = np.zeros(cap, np.float64)
+    n = L.stw_prof_collect(names, ptr(counts), ptr(ms), C.c_int(cap), C.c_int(int(reset)))
+    raw = names.raw
+    out = {}
+    for i in range(min(n, cap)):
+        nm = raw[64 * i: 64 * i + 64].split(b"\0", 1)[0].decode()
+        out[nm] = (int(counts[i]), float(ms[i]))
+    return out

@@ -41,6 +41,18 @@ struct Ctx {
 
 #define STW_LAUNCHED(ctx) STW_CUDA(ctx, cudaGetLastError())
 
+// Every kernel launch goes through STW_KL: it counts launches and, when the
+// opt-in profiler is on (stw_prof_enable), brackets the launch with CUDA
+// events recorded on the launching stream.
+int prof_pre(cudaStream_t s);
+void prof_post(cudaStream_t s, const char *name, int slot);
+#define STW_KL(kern, grid, block, stream, ...)               \
+  do {                                                       \
+    int _stw_slot = ::stw::prof_pre(stream);                 \
+    kern<<<(grid), (block), 0, (stream)>>>(__VA_ARGS__);     \
+    ::stw::prof_post(stream, #kern, _stw_slot);              \
+  } while (0)
+
 // Stream-ordered scratch: every take() is a cudaMallocAsync on the call's
 // stream (served from the device's default pool, whose release threshold is
 // raised once so repeated calls do not remap); everything is returned with

@@ -65,8 +65,8 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
   int *tmax = ar.take<int>(T);
   int64_t *tl_len = ar.take<int64_t>(T + 1);
   if (!ctx.ok()) return;
-  k_init_len<<<grid_for(T, 256), 256, 0, ctx.stream>>>(b.horizon, tmax, T);
-  k_timeline_len<<<grid_for(b.N, 256), 256, 0, ctx.stream>>>(b.ev_off, T, b.N, b.t_s, b.t_e, b.horizon, tmax);
+  STW_KL(k_init_len, grid_for(T, 256), 256, ctx.stream, b.horizon, tmax, T);
+  STW_KL(k_timeline_len, grid_for(b.N, 256), 256, ctx.stream, b.ev_off, T, b.N, b.t_s, b.t_e, b.horizon, tmax);
   STW_LAUNCHED(ctx);
   std::vector<int> h(T);
   STW_CUDA(ctx, cudaMemcpyAsync(h.data(), tmax, T * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
@@ -80,12 +80,12 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
   if (!ctx.ok()) return;
   STW_CUDA(ctx, cudaMemsetAsync(D, 0, H * sizeof(int64_t), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(d_peak, 0, T * sizeof(int64_t), ctx.stream));
-  k_timeline_scatter<<<grid_for(b.N, 256), 256, 0, ctx.stream>>>(b.ev_off, T, b.N, b.size, b.t_s, b.t_e, b.dyn,
+  STW_KL(k_timeline_scatter, grid_for(b.N, 256), 256, ctx.stream, b.ev_off, T, b.N, b.size, b.t_s, b.t_e, b.dyn,
                                                                  tl_len, (unsigned long long *)D, static_only);
   STW_LAUNCHED(ctx);
   device_scan<int64_t>(ctx, ar, D, D, H, true);
   int64_t nthreads = (H + 7) / 8;
-  k_segmax<<<(unsigned)((nthreads + 255) / 256), 256, 0, ctx.stream>>>(D, H, tl_len, T, (long long *)d_peak);
+  STW_KL(k_segmax, (unsigned)((nthreads + 255) / 256), 256, ctx.stream, D, H, tl_len, T, (long long *)d_peak);
   STW_LAUNCHED(ctx);
 }
 

@@ -119,13 +119,13 @@ void sort_perm2(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, uint64_t *lo, int
                 int64_t n) {
   if (!ctx.ok() || n == 0) return;
   if (hibits + lobits <= 64) {
-    k_concat_key<<<grid_for(n, 256), 256, 0, ctx.stream>>>(hi, lo, lobits, n);
+    STW_KL(k_concat_key, grid_for(n, 256), 256, ctx.stream, hi, lo, lobits, n);
     STW_LAUNCHED(ctx);
     sort_perm(ctx, ar, hi, perm, n, hibits + lobits);
     return;
   }
   sort_perm(ctx, ar, lo, perm, n, lobits);
-  k_gather_u64<<<grid_for(n, 256), 256, 0, ctx.stream>>>(hi, perm, lo, n);  // lo := hi[perm]
+  STW_KL(k_gather_u64, grid_for(n, 256), 256, ctx.stream, hi, perm, lo, n);  // lo := hi[perm]
   STW_LAUNCHED(ctx);
   radix_sort_pairs(ctx, ar, lo, perm, n, 0, hibits);
 }
@@ -835,8 +835,10 @@ __device__ void block_scan_into(int n, F f, int32_t *out, int *shi) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A) {
-  const int u = blockIdx.x;
+__global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A, const int32_t *__restrict__ ulist,
+                                                         const int *__restrict__ ucount) {
+  if (ucount && (int)blockIdx.x >= *ucount) return;
+  const int u = ulist[blockIdx.x];
   const int c = u % A.C, t = u / A.C;
   const int v = A.var_of[c];
   const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
@@ -1047,6 +1049,197 @@ __global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// E (small units): one warp per unit, the unit's slot CSR in shared memory.
+// Same decomposition as k_layers; fit masks are computed per 32-item chunk by
+// the lanes right before the warp resolves the chunk. A unit that opens more
+// than kWL layers is handed to the CTA kernel (appended to `over`).
+
+constexpr int kWL = 64;
+constexpr int kWarpsPerCTA = 4;
+
+__device__ __forceinline__ int warp_excl_scan(int v, int *total) {
+  int inc = warp_incl_sum(v);
+  *total = __shfl_sync(0xffffffffu, inc, 31);
+  return inc - v;
+}
+
+__global__ void __launch_bounds__(kWarpsPerCTA * 32) k_layers_warp(LayerArgs A, const int32_t *__restrict__ ulist,
+                                                                   int nunits, int cap, int32_t *__restrict__ over,
+                                                                   int *__restrict__ nover) {
+  extern __shared__ int32_t smem[];
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  const int ui = blockIdx.x * kWarpsPerCTA + w;
+  if (ui >= nunits) return;
+  const int u = ulist[ui];
+  const int c = u % A.C, t = u / A.C;
+  const int v = A.var_of[c];
+  const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
+  const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
+  const int64_t off = A.uo[u];
+  const int per_warp = 6 * cap + 8 * (kWL + 1);
+  int32_t *sm = smem + w * per_warp;
+  int32_t *sAts = sm, *sAte = sm + cap, *sBts = sm + 2 * cap, *sBte = sm + 3 * cap;
+  int32_t *run_ts = sm + 4 * cap, *run_te = sm + 5 * cap;
+  int32_t *loffA = sm + 6 * cap, *loffB = loffA + (kWL + 1), *prioA = loffB + (kWL + 1), *prioB = prioA + (kWL + 1);
+  int32_t *last = prioB + (kWL + 1), *nend = last + (kWL + 1), *newcnt = nend + (kWL + 1), *runoff = newcnt + (kWL + 1);
+  int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
+  int64_t *lsize = A.lsize + off;
+  if (lane == 0) loffA[0] = 0;
+  int nl = 0;
+  long long gapc = 0;
+  __syncwarp();
+  for (int64_t j0 = a0; j0 < a1;) {
+    const int64_t j1 = A.cend[j0];
+    const int m = (int)(j1 - j0);
+    const int64_t S = A.it.size[j0];
+    for (int p = lane; p < kWL; p += 32) {
+      newcnt[p] = 0;
+      last[p] = INT_MIN;
+    }
+    __syncwarp();
+    int nnew = 0;
+    for (int64_t cb = j0; cb < j1; cb += 32) {
+      const int64_t mine = cb + lane;
+      int my_ts = 0, my_te = 0;
+      unsigned long long fm = 0;
+      if (mine < j1) {
+        my_ts = A.it.ts[mine];
+        my_te = A.it.te[mine];
+        if (gap)
+          for (int p = 0; p < nl; p++) {
+            int l = prioA[p];
+            if (slot_fit(sAts, sAte, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1ull << p;
+          }
+      }
+      const int cnt = (int)min((int64_t)32, j1 - cb);
+      for (int k = 0; k < cnt; k++) {
+        const int ts = __shfl_sync(0xffffffffu, my_ts, k), te = __shfl_sync(0xffffffffu, my_te, k);
+        const unsigned long long f = __shfl_sync(0xffffffffu, fm, k);
+        int host_p = -1;
+        if (gap && nl > 0) {
+          bool ok1 = lane < nl && ((f >> lane) & 1ull) && last[lane] < ts;
+          bool ok2 = lane + 32 < nl && ((f >> (lane + 32)) & 1ull) && last[lane + 32] < ts;
+          unsigned m1 = __ballot_sync(0xffffffffu, ok1), m2 = __ballot_sync(0xffffffffu, ok2);
+          host_p = m1 ? __ffs(m1) - 1 : (m2 ? 32 + __ffs(m2) - 1 : -1);
+        }
+        int layer;
+        if (host_p >= 0) {
+          layer = prioA[host_p];
+          if (lane == 0) last[host_p] = te;
+          gapc++;
+        } else {
+          int best_k = -1, best_e = INT_MIN;
+#pragma unroll
+          for (int kb = 0; kb < kWL; kb += 32) {
+            int kk = kb + lane;
+            int e = kk < nnew ? nend[kk] : INT_MIN;
+            bool cand = kk < nnew && e < ts;
+            int mx = __reduce_max_sync(0xffffffffu, cand ? e : INT_MIN);
+            unsigned cm = __ballot_sync(0xffffffffu, cand && e == mx);
+            if (cm && (best_k < 0 || mx > best_e)) {
+              best_e = mx;
+              best_k = kb + __ffs(cm) - 1;
+            }
+          }
+          if (best_k < 0) {
+            if (nl + nnew == kWL) {  // too many layers for the warp path
+              if (lane == 0) over[atomicAdd(nover, 1)] = u;
+              return;
+            }
+            best_k = nnew++;
+            if (lane == 0) newcnt[nl + best_k] = 0;
+          }
+          if (lane == 0) nend[best_k] = te;
+          layer = nl + best_k;
+        }
+        if (lane == 0) {
+          ilayer[cb + k - a0] = layer;
+          irank[cb + k - a0] = newcnt[layer]++;
+        }
+        __syncwarp();
+      }
+    }
+    // merge the class's slots into the CSR (sA -> sB)
+    const int nl2 = nl + nnew;
+    for (int x = lane; x < nnew; x += 32) lsize[nl + x] = S;
+    {
+      int carry = 0, carry2 = 0;
+      for (int base = 0; base < nl2; base += 32) {
+        int l = base + lane;
+        int cnt_all = l < nl2 ? (l < nl ? loffA[l + 1] - loffA[l] : 0) + newcnt[l] : 0;
+        int cnt_new = l < nl2 ? newcnt[l] : 0;
+        int tot, tot2;
+        int ex = warp_excl_scan(cnt_all, &tot), ex2 = warp_excl_scan(cnt_new, &tot2);
+        if (l < nl2) {
+          loffB[l] = carry + ex;
+          runoff[l] = carry2 + ex2;
+        }
+        carry += tot;
+        carry2 += tot2;
+      }
+      if (lane == 0) {
+        loffB[nl2] = carry;
+        runoff[nl2] = carry2;
+      }
+    }
+    __syncwarp();
+    for (int x = lane; x < m; x += 32) {
+      int l = ilayer[j0 - a0 + x];
+      int pos = runoff[l] + irank[j0 - a0 + x];
+      run_ts[pos] = A.it.ts[j0 + x];
+      run_te[pos] = A.it.te[j0 + x];
+    }
+    __syncwarp();
+    const int nold = nl > 0 ? loffA[nl] : 0;
+    for (int sidx = lane; sidx < nold; sidx += 32) {
+      int l = 0;
+      while (loffA[l + 1] <= sidx) l++;
+      int ts = sAts[sidx];
+      int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
+      int dst = loffB[l] + (sidx - loffA[l]) + k;
+      sBts[dst] = ts;
+      sBte[dst] = sAte[sidx];
+    }
+    for (int x = lane; x < m; x += 32) {
+      int l = ilayer[j0 - a0 + x];
+      int ts = run_ts[runoff[l] + irank[j0 - a0 + x]];
+      int te = run_te[runoff[l] + irank[j0 - a0 + x]];
+      int k = l < nl ? lower_bound_i32(sAts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
+      int dst = loffB[l] + irank[j0 - a0 + x] + k;
+      sBts[dst] = ts;
+      sBte[dst] = te;
+    }
+    for (int x = lane; x < nl2; x += 32) prioB[x] = x < nnew ? nl + x : prioA[x - nnew];
+    __syncwarp();
+    {
+      int32_t *tp;
+      tp = sAts, sAts = sBts, sBts = tp;
+      tp = sAte, sAte = sBte, sBte = tp;
+      tp = loffA, loffA = loffB, loffB = tp;
+      tp = prioA, prioA = prioB, prioB = tp;
+    }
+    nl = nl2;
+    j0 = j1;
+  }
+  // stacking (planner.py:441-444)
+  int64_t *lbase = A.lbase + off;
+  long long carry = A.pers_size[t];
+  for (int base = 0; base < nl; base += 32) {
+    int l = base + lane;
+    long long v0 = l < nl ? lsize[l] : 0;
+    long long inc = warp_incl_sum(v0);
+    if (l < nl) lbase[l] = carry + inc - v0;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) {
+    A.nlayers[u] = nl;
+    A.gapins[u] = gapc;
+    A.pool[u] = carry;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // F: emission (planner.py:446-455)
 
@@ -1119,6 +1312,128 @@ __global__ void k_rect_fill(const uint32_t *__restrict__ rperm, const uint32_t *
 }
 
 // ---------------------------------------------------------------------------
+// finalisation: verdicts (planner.py:371-373, 392, 464-471), stats, best pick
+
+struct FinalArgs {
+  int T, C;
+  const int32_t *var_of;
+  TraceCounts tc;
+  const int64_t *att, *acc;  // per trace (nullptr when no fusion variant ran)
+  const int64_t *gapins;
+  const int32_t *nlayers;
+  const int64_t *pool, *peak;
+  const int *bad_align, *bad_phase;
+  const long long *vcount;
+  const int64_t *ev_off;
+  int32_t *rc;
+  int64_t *err, *stats;
+  int *nconf;
+};
+
+__global__ void k_unit_finalize(FinalArgs A) {
+  GRID_STRIDE(u, (int64_t)A.T * A.C) {
+    int t = (int)(u / A.C), c = (int)(u % A.C);
+    bool fus_ran = A.var_of[c] == 1 && A.tc.n_plans[t] > 1 && A.att;
+    int64_t *st = A.stats + u * STW_NSTATS;
+    int64_t acc = fus_ran ? A.acc[t] : 0;
+    st[0] = A.tc.n_static[t];
+    st[1] = A.tc.n_pers[t];
+    st[2] = A.tc.n_groups[t];
+    st[3] = A.tc.n_plans[t] - acc;
+    st[4] = A.tc.n_res[t];
+    st[5] = fus_ran ? A.att[t] : 0;
+    st[6] = acc;
+    st[7] = A.gapins[u];
+    st[8] = A.nlayers[u];
+    st[9] = A.pool[u];
+    st[10] = A.peak[t];
+    st[11] = A.tc.pers_size[t];
+    int rc = STW_OK;
+    int64_t e0 = -1;
+    if (A.bad_align[t] != INT_MAX) {
+      rc = STW_EPLAN;
+      e0 = A.ev_off[t] + A.bad_align[t];
+    } else if (A.bad_phase[t] != INT_MAX) {
+      rc = STW_ETRACE;
+      e0 = A.ev_off[t] + A.bad_phase[t];
+    } else if (A.pool[u] < A.peak[t]) {
+      rc = STW_EPLAN;
+    } else if (A.vcount[u] > 0) {
+      rc = STW_EPLAN;
+      atomicAdd(A.nconf, 1);
+    }
+    A.rc[u] = rc;
+    A.err[2 * u] = e0;
+    A.err[2 * u + 1] = -1;
+  }
+}
+
+// best candidate per trace: argmin (pool_size, candidate index) over clean units
+__global__ void k_select_best(const int32_t *__restrict__ rc, const int64_t *__restrict__ pool, int T, int C,
+                              int32_t *__restrict__ best, int64_t *__restrict__ bpool) {
+  GRID_STRIDE(t, (int64_t)T) {
+    int b = -1;
+    long long bp = -1;
+    for (int c = 0; c < C; c++) {
+      int64_t u = t * C + c;
+      if (rc[u] != STW_OK) continue;
+      if (b < 0 || pool[u] < bp) b = c, bp = pool[u];
+    }
+    best[t] = b;
+    bpool[t] = bp;
+  }
+}
+
+__global__ void k_gather_best(const int32_t *__restrict__ tr, const int32_t *__restrict__ best,
+                              const int64_t *__restrict__ addr, int64_t N, int64_t *__restrict__ out) {
+  GRID_STRIDE(i, N) {
+    int b = best[tr[i]];
+    out[i] = b >= 0 ? addr[(int64_t)b * N + i] : -1;
+  }
+}
+
+__global__ void k_scatter_layers(const int64_t *__restrict__ uo, int64_t U, int C, const int64_t *__restrict__ ev_off,
+                                 int64_t N, const int32_t *__restrict__ nl, const int64_t *__restrict__ lbase,
+                                 const int64_t *__restrict__ lsize, int64_t *__restrict__ ob, int64_t *__restrict__ os,
+                                 int64_t TU) {
+  GRID_STRIDE(x, TU) {
+    int64_t a = 0, z = U;  // unit owning scratch slot x
+    while (z - a > 1) {
+      int64_t m = (a + z) >> 1;
+      if (uo[m] <= x)
+        a = m;
+      else
+        z = m;
+    }
+    while (uo[a + 1] <= x) a++;
+    int64_t l = x - uo[a];
+    if (l >= nl[a]) continue;
+    int t = (int)(a / C), c = (int)(a % C);
+    int64_t dst = (int64_t)c * N + ev_off[t] + l;
+    ob[dst] = lbase[x];
+    os[dst] = lsize[x];
+  }
+}
+
+__global__ void k_scatter_fusions(const int32_t *__restrict__ ptr, const int64_t *__restrict__ pl_off,
+                                  const int64_t *__restrict__ acc, const int32_t *__restrict__ var_of, int C,
+                                  const int64_t *__restrict__ ev_off, int64_t N, const double *__restrict__ ft,
+                                  const double *__restrict__ fa, double *__restrict__ ot, double *__restrict__ oa,
+                                  int64_t P) {
+  GRID_STRIDE(p, P) {
+    int t = ptr[p];
+    int64_t k = p - pl_off[t];
+    if (k >= acc[t]) continue;
+    for (int c = 0; c < C; c++) {
+      if (var_of[c] != 1) continue;
+      int64_t dst = (int64_t)c * N + ev_off[t] + k;
+      ot[dst] = ft[p];
+      oa[dst] = fa[p];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host orchestration
 
 template <class T>
@@ -1145,12 +1460,33 @@ static void out_copy(Ctx &ctx, T *dst, const T *src, int64_t n, bool dst_dev) {
 #define LAUNCH(kern, n, ...)                                                     \
   do {                                                                           \
     if (ctx.ok() && (n) > 0) {                                                   \
-      kern<<<grid_for((n), 256), 256, 0, ctx.stream>>>(__VA_ARGS__);             \
+      STW_KL(kern, grid_for((n), 256), 256, ctx.stream, __VA_ARGS__);          \
       STW_LAUNCHED(ctx);                                                         \
     }                                                                            \
   } while (0)
 
+// STW_DEBUG_TIMING=1: synchronise at phase boundaries and print host wall time per phase
+struct PhaseTimer {
+  Ctx &ctx;
+  bool on;
+  double t0;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  explicit PhaseTimer(Ctx &c) : ctx(c), on(getenv("STW_DEBUG_TIMING") != nullptr), t0(now()) {}
+  void mark(const char *name) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx.stream);
+    double t = now();
+    fprintf(stderr, "[stw plan] %-24s %8.3f ms\n", name, t - t0);
+    t0 = t;
+  }
+};
+
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out) {
+  PhaseTimer pt(ctx);
   Arena ar(&ctx);
   DevBatch b;
   if (!o || o->n_cand <= 0 || !o->cand || o->alignment <= 0) {
@@ -1170,6 +1506,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   const int V = 2;
   if (T == 0) return ctx.rc;
 
+  pt.mark("stage");
   // ---- A: canonical ranks
   int32_t *tr = ar.take<int32_t>(N + 1);
   int32_t *q = ar.take<int32_t>(N + 1), *r = ar.take<int32_t>(N + 1);
@@ -1204,6 +1541,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   sort_perm2(ctx, ar, khi, tb, klo, tsb + qb, rperm, N);
   LAUNCH(k_rank_from_perm, N, rperm, tr, b.ev_off, N, r, order_local);
 
+  pt.mark("A ranks");
   // per-trace input checks
   int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
   if (!ctx.ok()) return ctx.rc;
@@ -1220,6 +1558,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   const int pb = bitlen_u64((uint64_t)him[1]);
 
+  pt.mark("A checks");
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
   LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
@@ -1250,14 +1589,10 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   STW_CUDA(ctx, cudaMemsetAsync(tc.pers_size, 0, T * sizeof(int64_t), ctx.stream));
   LAUNCH(k_trace_counts, G, g, G, N, tc, is_plan);
   device_scan<uint32_t>(ctx, ar, is_plan, pidx, G, false);
-  std::vector<int> h_nplans, h_nstatic, h_npers, h_ngroups, h_nres;
+  std::vector<int> h_nplans, h_nstatic, h_nres;
   d2h(ctx, h_nplans, tc.n_plans, T);
   d2h(ctx, h_nstatic, tc.n_static, T);
-  d2h(ctx, h_npers, tc.n_pers, T);
-  d2h(ctx, h_ngroups, tc.n_groups, T);
   d2h(ctx, h_nres, tc.n_res, T);
-  std::vector<int64_t> h_pers_size;
-  d2h(ctx, h_pers_size, tc.pers_size, T);
   sync(ctx);
   if (!ctx.ok()) return ctx.rc;
   std::vector<int64_t> pl_off(T + 1, 0);
@@ -1277,12 +1612,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_plan_members, N, gperm, gof, is_plan, pidx, e, N, p0, pid0);
   LAUNCH(k_plan_tmp, P, p0, P);
 
+  pt.mark("B groups");
   // ---- C: fusion variant
   Plans p1 = p0;
   int32_t *pid1 = pid0;
   int64_t *frel1 = rel;
   std::vector<int64_t> h_att(T, 0), h_acc(T, 0);
   double *acc_tmp = nullptr, *acc_avg = nullptr;
+  int64_t *att_dev = nullptr, *acc_dev = nullptr;
   if (want[1]) {
     p1 = mk_plans();
     pid1 = ar.take<int32_t>(N + 1);
@@ -1291,6 +1628,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     acc_tmp = ar.take<double>(P + 1);
     acc_avg = ar.take<double>(P + 1);
     int64_t *att = ar.take<int64_t>(T), *acc = ar.take<int64_t>(T);
+    att_dev = att;
+    acc_dev = acc;
     std::vector<int64_t> moff(T + 1, 0);
     const int64_t kMemoMax = 4096;
     for (int t = 0; t < T; t++) {
@@ -1321,16 +1660,17 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     CPY(frel1, rel, N + 1);
 #undef CPY
     STW_CUDA(ctx, cudaMemsetAsync(memo, 0, (moff[T] / 32 + 1) * sizeof(uint32_t), ctx.stream));
-    k_iota<<<grid_for(P + 1, 256), 256, 0, ctx.stream>>>((uint32_t *)lst, P + 1);
+    STW_KL(k_iota, grid_for(P + 1, 256), 256, ctx.stream, (uint32_t *)lst, P + 1);
     STW_LAUNCHED(ctx);
     if (ctx.ok()) {
-      k_fusion<<<T, kPlanThreads, 0, ctx.stream>>>(F, T);
+      STW_KL(k_fusion, T, kPlanThreads, ctx.stream, F, T);
       STW_LAUNCHED(ctx);
     }
     d2h(ctx, h_att, att, T);
     d2h(ctx, h_acc, acc, T);
   }
 
+  pt.mark("C fusion");
   // ---- D: items per (variant, trace)
   std::vector<int64_t> io(V * T + 1, 0);
   std::vector<int> n_alive(V * T, 0);
@@ -1364,6 +1704,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     LAUNCH(k_items_plans, P, pv, P, aexcl, d_pl_off, d_io + (int64_t)v * T, it0);
     LAUNCH(k_items_res, N, e, rflag, rexcl, b.ev_off, d_nalive + (int64_t)v * T, d_io + (int64_t)v * T, N, it0);
   }
+  pt.mark("D items");
   // sort items by (variant-trace, size desc, t_s, tie)
   long long maxsu = 0;
   {
@@ -1387,6 +1728,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, (long long)o->alignment, maxsu, sb, ihi, ilo);
   sort_perm2(ctx, ar, ihi, vtb + sb, ilo, tsb + qb, iperm, NI);
   LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
+  pt.mark("D sort");
   // classes
   uint32_t *chead = ar.take<uint32_t>(NI + 1), *cid = ar.take<uint32_t>(NI + 1);
   int64_t *cstart = ar.take<int64_t>(NI + 1), *cend = ar.take<int64_t>(NI + 1);
@@ -1399,6 +1741,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_class_start, NI, chead, cid, NI, cstart);
   LAUNCH(k_class_end, NI, cid, cstart, (int64_t)NC, NI, cend);
 
+  pt.mark("D classes");
   // ---- E: layers per unit
   std::vector<int64_t> uo(U + 1, 0);
   for (int t = 0; t < T; t++)
@@ -1420,8 +1763,51 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
                ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int64_t>(TU + 1), ar.take<int64_t>(TU + 1),
                ar.take<int32_t>(U), ar.take<int64_t>(U), ar.take<int64_t>(U)};
   if (!ctx.ok()) return ctx.rc;
-  k_layers<<<(unsigned)U, kPlanThreads, 0, ctx.stream>>>(LA);
-  STW_LAUNCHED(ctx);
+  {
+    // size buckets: warp-per-unit kernels with the CSR in shared memory; the
+    // largest units (and any unit that needs > kWL layers) go to the CTA kernel
+    static const int caps[] = {128, 256, 512, 1024, 2048};
+    const int NBK = 5;
+    std::vector<std::vector<int32_t>> lists(NBK + 1);
+    for (int64_t u = 0; u < U; u++) {
+      int64_t n_u = uo[u + 1] - uo[u];
+      int bk = 0;
+      while (bk < NBK && n_u > caps[bk]) bk++;
+      lists[bk].push_back((int32_t)u);
+    }
+    std::vector<int32_t> flat;
+    std::vector<int64_t> loff(NBK + 2, 0);
+    for (int bk = 0; bk <= NBK; bk++) {
+      flat.insert(flat.end(), lists[bk].begin(), lists[bk].end());
+      loff[bk + 1] = flat.size();
+    }
+    int32_t *d_list = h2d(ctx, ar, flat);
+    int32_t *d_over = ar.take<int32_t>(U + 1);
+    int *d_nover = ar.take<int>(1);
+    if (!ctx.ok()) return ctx.rc;
+    STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, sizeof(int), ctx.stream));
+    const int64_t nsmall = loff[NBK];
+    for (int bk = 0; bk < NBK && ctx.ok(); bk++) {
+      int nb = (int)(loff[bk + 1] - loff[bk]);
+      if (!nb) continue;
+      size_t smem = (size_t)kWarpsPerCTA * (6 * caps[bk] + 8 * (kWL + 1)) * sizeof(int32_t);
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int prof = prof_pre(ctx.stream);
+      k_layers_warp<<<(nb + kWarpsPerCTA - 1) / kWarpsPerCTA, kWarpsPerCTA * 32, smem, ctx.stream>>>(
+          LA, d_list + loff[bk], nb, caps[bk], d_over, d_nover);
+      prof_post(ctx.stream, "k_layers_warp", prof);
+      STW_LAUNCHED(ctx);
+    }
+    int nbig = (int)(loff[NBK + 1] - loff[NBK]);
+    if (nbig) {
+      STW_KL(k_layers, (unsigned)nbig, kPlanThreads, ctx.stream, LA, d_list + loff[NBK], (const int *)nullptr);
+      STW_LAUNCHED(ctx);
+    }
+    if (nsmall) {
+      STW_KL(k_layers, (unsigned)nsmall, kPlanThreads, ctx.stream, LA, d_over, d_nover);
+      STW_LAUNCHED(ctx);
+    }
+  }
 
   if (getenv("STW_DEBUG_DUMP")) {  // developer aid: dump unit 0's sorted items and layer choices
     int64_t n0 = uo[1] - uo[0];
@@ -1436,7 +1822,6 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     d2h(ctx, href, it.ref + j0, n0);
     d2h(ctx, hce, cend + j0, n0);
     STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
-    k_layers<<<(unsigned)U, kPlanThreads, 0, ctx.stream>>>(LA);
     d2h(ctx, hil, LA.ilayer, n0);
     d2h(ctx, hir, LA.irank, n0);
     STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
@@ -1446,6 +1831,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
               (long long)hs[k], hts[k], hte[k], htie[k], href[k], (long long)(hce[k] - j0), hil[k], hir[k]);
   }
 
+  pt.mark("E layers");
   // ---- F: emission
   int64_t *addr = ar.take<int64_t>((int64_t)C * N + 1);
   int32_t *layer = ar.take<int32_t>((int64_t)C * N + 1);
@@ -1454,6 +1840,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
               LA.ilayer, LA.lbase, addr, layer};
   LAUNCH(k_emit, (int64_t)C * N, EA);
 
+  pt.mark("F emit");
   // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
   int64_t *peak = ar.take<int64_t>(T);
   if (!ctx.ok()) return ctx.rc;
@@ -1475,111 +1862,79 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   RectSets rs{T, NS, d_so, rts, rte, rsz, C, raddr};
   validate_sets(ctx, ar, rs, vcount, vfirst);
 
-  // ---- gather per-unit results on the host
-  std::vector<int64_t> h_pool, h_gap, h_peak;
-  std::vector<int32_t> h_nl;
-  std::vector<long long> h_vc;
-  std::vector<int> h_vf, h_ba, h_bp;
-  d2h(ctx, h_pool, LA.pool, U);
-  d2h(ctx, h_gap, LA.gapins, U);
-  d2h(ctx, h_nl, LA.nlayers, U);
-  d2h(ctx, h_peak, peak, T);
-  d2h(ctx, h_vc, vcount, U);
-  d2h(ctx, h_vf, vfirst, U);
-  d2h(ctx, h_ba, bad_align, T);
-  d2h(ctx, h_bp, bad_phase, T);
+  pt.mark("G check");
+  // ---- per-unit verdicts, stats and best-candidate selection on the device
+  int32_t *d_rc = ar.take<int32_t>(U);
+  int64_t *d_err = ar.take<int64_t>(2 * U), *d_stats = ar.take<int64_t>(U * STW_NSTATS);
+  int32_t *d_best = ar.take<int32_t>(T);
+  int64_t *d_bpool = ar.take<int64_t>(T), *d_abest = ar.take<int64_t>(N + 1);
+  int *d_nconf = ar.take<int>(1);
+  int64_t *d_att = att_dev, *d_acc = acc_dev;
+  if (!ctx.ok()) return ctx.rc;
+  STW_CUDA(ctx, cudaMemsetAsync(d_nconf, 0, sizeof(int), ctx.stream));
+  FinalArgs FA{T, C, d_var, tc, d_att, d_acc, LA.gapins, LA.nlayers, LA.pool, peak, bad_align, bad_phase, vcount,
+               b.ev_off, d_rc, d_err, d_stats, d_nconf};
+  LAUNCH(k_unit_finalize, U, FA);
+  LAUNCH(k_select_best, T, d_rc, LA.pool, T, C, d_best, d_bpool);
+  LAUNCH(k_gather_best, N, tr, d_best, addr, N, d_abest);
+  int h_nconf = 0;
+  STW_CUDA(ctx, cudaMemcpyAsync(&h_nconf, d_nconf, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   sync(ctx);
   if (!ctx.ok()) return ctx.rc;
-  std::vector<int32_t> rc(U, STW_OK);
-  std::vector<int64_t> err_ids(2 * U, -1), stats(U * STW_NSTATS, 0);
-  for (int t = 0; t < T; t++)
-    for (int c = 0; c < C; c++) {
-      int64_t u = (int64_t)t * C + c;
-      int v = var_of[c];
-      bool fus_ran = v == 1 && h_nplans[t] > 1;
-      int64_t *st = &stats[u * STW_NSTATS];
-      st[0] = h_nstatic[t];
-      st[1] = h_npers[t];
-      st[2] = h_ngroups[t];
-      st[3] = fus_ran ? h_nplans[t] - h_acc[t] : h_nplans[t];
-      st[4] = h_nres[t];
-      st[5] = fus_ran ? h_att[t] : 0;
-      st[6] = fus_ran ? h_acc[t] : 0;
-      st[7] = h_gap[u];
-      st[8] = h_nl[u];
-      st[9] = h_pool[u];
-      st[10] = h_peak[t];
-      st[11] = h_pers_size[t];
-      if (h_ba[t] != INT_MAX) {
-        rc[u] = STW_EPLAN;
-        err_ids[2 * u] = b.h_ev_off[t] + h_ba[t];  // event index; the shim formats the message
-      } else if (h_bp[t] != INT_MAX) {
-        rc[u] = STW_ETRACE;
-        err_ids[2 * u] = b.h_ev_off[t] + h_bp[t];
-      } else if (h_pool[u] < h_peak[t]) {
-        rc[u] = STW_EPLAN;
-      } else if (h_vc[u] > 0) {
-        rc[u] = STW_EPLAN;
-        int pa = -1, pbb = -1;
-        first_pair(ctx, rs, t, c, h_vf[u], &pa, &pbb);
+  if (h_nconf > 0) {  // error path: name the first reported pair of every conflicting unit
+    std::vector<long long> h_vc;
+    std::vector<int> h_vf;
+    std::vector<int32_t> h_rc2;
+    std::vector<int64_t> h_err2;
+    d2h(ctx, h_vc, vcount, U);
+    d2h(ctx, h_vf, vfirst, U);
+    d2h(ctx, h_rc2, d_rc, U);
+    d2h(ctx, h_err2, d_err, 2 * U);
+    sync(ctx);
+    for (int64_t u = 0; u < U && ctx.ok(); u++) {
+      if (h_vc[u] <= 0 || h_err2[2 * u] >= 0) continue;
+      int t = (int)(u / C), c = (int)(u % C);
+      int pa = -1, pbb = -1;
+      first_pair(ctx, rs, t, c, h_vf[u], &pa, &pbb);
+      if (pa >= 0) {
         int32_t ev2[2] = {-1, -1};
-        if (pa >= 0) {
-          STW_CUDA(ctx, cudaMemcpy(&ev2[0], rs_ev + so[t] + pa, sizeof(int32_t), cudaMemcpyDeviceToHost));
-          STW_CUDA(ctx, cudaMemcpy(&ev2[1], rs_ev + so[t] + pbb, sizeof(int32_t), cudaMemcpyDeviceToHost));
-          err_ids[2 * u] = ev2[0];
-          err_ids[2 * u + 1] = ev2[1];
-        }
+        STW_CUDA(ctx, cudaMemcpy(&ev2[0], rs_ev + so[t] + pa, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        STW_CUDA(ctx, cudaMemcpy(&ev2[1], rs_ev + so[t] + pbb, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        h_err2[2 * u] = ev2[0];
+        h_err2[2 * u + 1] = ev2[1];
       }
     }
+    STW_CUDA(ctx, cudaMemcpyAsync(d_err, h_err2.data(), 2 * U * sizeof(int64_t), cudaMemcpyHostToDevice, ctx.stream));
+    sync(ctx);
+  }
+  pt.mark("finalize");
+
   // ---- outputs
   const bool od = out->on_device != 0;
-  auto put = [&](auto *dst, const auto &vec) {
-    if (!dst || vec.empty() || !ctx.ok()) return;
-    if (od)
-      STW_CUDA(ctx, cudaMemcpyAsync(dst, vec.data(), vec.size() * sizeof(vec[0]), cudaMemcpyHostToDevice, ctx.stream));
-    else
-      memcpy(dst, vec.data(), vec.size() * sizeof(vec[0]));
-  };
-  put(out->rc, rc);
-  put(out->err_ids, err_ids);
-  put(out->stats, stats);
+  out_copy(ctx, out->rc, d_rc, U, od);
+  out_copy(ctx, out->err_ids, d_err, 2 * U, od);
+  out_copy(ctx, out->stats, d_stats, U * STW_NSTATS, od);
   out_copy(ctx, out->addr, addr, (int64_t)C * N, od);
   out_copy(ctx, out->layer_of, layer, (int64_t)C * N, od);
   out_copy(ctx, out->order, order_local, N, od);
   if (out->layer_base || out->layer_size || out->fus_tmp || out->fus_avg) {
-    // per-unit slices at c*N + ev_off[t]
-    for (int t = 0; t < T && ctx.ok(); t++)
-      for (int c = 0; c < C; c++) {
-        int64_t u = (int64_t)t * C + c;
-        int64_t dst = (int64_t)c * N + b.h_ev_off[t];
-        int64_t nl = h_nl[u];
-        if (out->layer_base) out_copy(ctx, out->layer_base + dst, LA.lbase + uo[u], nl, od);
-        if (out->layer_size) out_copy(ctx, out->layer_size + dst, LA.lsize + uo[u], nl, od);
-        bool fus_ran = var_of[c] == 1 && h_nplans[t] > 1;
-        int64_t na = fus_ran ? h_acc[t] : 0;
-        if (out->fus_tmp && na) out_copy(ctx, out->fus_tmp + dst, acc_tmp + pl_off[t], na, od);
-        if (out->fus_avg && na) out_copy(ctx, out->fus_avg + dst, acc_avg + pl_off[t], na, od);
-      }
+    int64_t *lb_out = ar.take<int64_t>((int64_t)C * N + 1), *ls_out = ar.take<int64_t>((int64_t)C * N + 1);
+    double *ft_out = ar.take<double>((int64_t)C * N + 1), *fa_out = ar.take<double>((int64_t)C * N + 1);
+    if (!ctx.ok()) return ctx.rc;
+    LAUNCH(k_scatter_layers, TU, d_uo, (int64_t)U, C, b.ev_off, N, LA.nlayers, LA.lbase, LA.lsize, lb_out, ls_out, TU);
+    if (want[1]) LAUNCH(k_scatter_fusions, P, p0.tr, d_pl_off, d_acc, d_var, C, b.ev_off, N, acc_tmp, acc_avg, ft_out, fa_out, P);
+    out_copy(ctx, out->layer_base, lb_out, (int64_t)C * N, od);
+    out_copy(ctx, out->layer_size, ls_out, (int64_t)C * N, od);
+    out_copy(ctx, out->fus_tmp, ft_out, (int64_t)C * N, od);
+    out_copy(ctx, out->fus_avg, fa_out, (int64_t)C * N, od);
   }
   if (o->select_best) {
-    std::vector<int32_t> best(T, -1);
-    std::vector<int64_t> bpool(T, -1);
-    for (int t = 0; t < T; t++)
-      for (int c = 0; c < C; c++) {
-        int64_t u = (int64_t)t * C + c;
-        if (rc[u] != STW_OK) continue;
-        if (best[t] < 0 || h_pool[u] < bpool[t]) best[t] = c, bpool[t] = h_pool[u];
-      }
-    put(out->best_cand, best);
-    put(out->best_pool, bpool);
-    if (out->addr_best)
-      for (int t = 0; t < T && ctx.ok(); t++) {
-        int64_t n_t = b.h_ev_off[t + 1] - b.h_ev_off[t];
-        if (best[t] >= 0)
-          out_copy(ctx, out->addr_best + b.h_ev_off[t], addr + (int64_t)best[t] * N + b.h_ev_off[t], n_t, od);
-      }
+    out_copy(ctx, out->best_cand, d_best, T, od);
+    out_copy(ctx, out->best_pool, d_bpool, T, od);
+    out_copy(ctx, out->addr_best, d_abest, N, od);
   }
   sync(ctx);
+  pt.mark("outputs");
   return ctx.rc;
 }
 

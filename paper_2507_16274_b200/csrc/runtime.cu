@@ -3,9 +3,61 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
 #include "prims.cuh"
 
 namespace stw {
+
+// ---------------------------------------------------------------------------
+// launch counter + opt-in per-kernel event profiler
+
+static std::atomic<long long> g_launches{0};
+static std::atomic<bool> g_prof_on{false};
+static std::mutex g_prof_mu;
+struct Pending {
+  const char *name;
+  cudaEvent_t a, b;
+};
+static std::vector<Pending> g_pending;
+static std::vector<cudaEvent_t> g_free_events;
+struct Agg {
+  long long count = 0;
+  double ms = 0;
+};
+static std::map<std::string, Agg> g_agg;
+
+static cudaEvent_t get_event() {
+  if (!g_free_events.empty()) {
+    cudaEvent_t e = g_free_events.back();
+    g_free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+int prof_pre(cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof_on.load(std::memory_order_relaxed)) return -1;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  Pending p{nullptr, get_event(), get_event()};
+  cudaEventRecord(p.a, s);
+  g_pending.push_back(p);
+  return (int)g_pending.size() - 1;
+}
+
+void prof_post(cudaStream_t s, const char *name, int slot) {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_pending[slot].name = name;
+  cudaEventRecord(g_pending[slot].b, s);
+}
 
 void Ctx::fail(int code, const char *fmt, ...) {
   if (rc != STW_OK) return;  // keep the first failure
@@ -54,16 +106,16 @@ void device_scan(Ctx &ctx, Arena &ar, const T *in, T *out, int64_t n, bool inclu
   if (n <= 0 || !ctx.ok()) return;
   int64_t nb = (n + kScanTile - 1) / kScanTile;
   if (nb == 1) {
-    k_tile_scan<T><<<1, kScanThreads, 0, ctx.stream>>>(in, out, nullptr, n, inclusive);
+    STW_KL(k_tile_scan<T>, 1, kScanThreads, ctx.stream, in, out, nullptr, n, inclusive);
     STW_LAUNCHED(ctx);
     return;
   }
   T *sums = ar.take<T>(nb);
   if (!sums) return;
-  k_tile_reduce<T><<<(unsigned)nb, kScanThreads, 0, ctx.stream>>>(in, sums, n);
+  STW_KL(k_tile_reduce<T>, (unsigned)nb, kScanThreads, ctx.stream, in, sums, n);
   STW_LAUNCHED(ctx);
   device_scan<T>(ctx, ar, sums, sums, nb, false);
-  k_tile_scan<T><<<(unsigned)nb, kScanThreads, 0, ctx.stream>>>(in, out, sums, n, inclusive);
+  STW_KL(k_tile_scan<T>, (unsigned)nb, kScanThreads, ctx.stream, in, out, sums, n, inclusive);
   STW_LAUNCHED(ctx);
 }
 template void device_scan<uint32_t>(Ctx &, Arena &, const uint32_t *, uint32_t *, int64_t, bool);
@@ -154,10 +206,10 @@ void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64
   for (int b = begin_bit; b < end_bit; b += 8) {
     int w = end_bit - b < 8 ? end_bit - b : 8;
     uint32_t mask = (1u << w) - 1;
-    k_radix_hist<<<ntiles, kSortThreads, 0, ctx.stream>>>(ka, counts, n, b, mask, ntiles);
+    STW_KL(k_radix_hist, ntiles, kSortThreads, ctx.stream, ka, counts, n, b, mask, ntiles);
     STW_LAUNCHED(ctx);
     device_scan<uint32_t>(ctx, ar, counts, counts, (int64_t)256 * ntiles, false);
-    k_radix_scatter<<<ntiles, kSortThreads, 0, ctx.stream>>>(ka, va, kb, vb, counts, n, b, mask, ntiles);
+    STW_KL(k_radix_scatter, ntiles, kSortThreads, ctx.stream, ka, va, kb, vb, counts, n, b, mask, ntiles);
     STW_LAUNCHED(ctx);
     uint64_t *tk = ka;
     ka = kb;
@@ -180,9 +232,47 @@ __global__ void k_iota(uint32_t *p, int64_t n) {
 
 void sort_perm(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *perm, int64_t n, int bits) {
   if (!ctx.ok()) return;
-  k_iota<<<grid_for(n, 256), 256, 0, ctx.stream>>>(perm, n);
+  STW_KL(k_iota, grid_for(n, 256), 256, ctx.stream, perm, n);
   STW_LAUNCHED(ctx);
   radix_sort_pairs(ctx, ar, keys, perm, n, 0, bits);
 }
 
 }  // namespace stw
+
+extern "C" {
+
+long long stw_launch_count(void) { return stw::g_launches.load(); }
+
+void stw_prof_enable(int on) { stw::g_prof_on.store(on != 0); }
+
+// Drain recorded launches into per-kernel aggregates; then copy up to cap
+// entries (name NUL-padded into 64-byte slots, launch count, summed ms).
+int stw_prof_collect(char *names, long long *counts, double *ms, int cap, int reset) {
+  using namespace stw;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto &p : g_pending) {
+    cudaEventSynchronize(p.b);
+    float t = 0;
+    cudaEventElapsedTime(&t, p.a, p.b);
+    Agg &a = g_agg[p.name ? p.name : "?"];
+    a.count++;
+    a.ms += t;
+    g_free_events.push_back(p.a);
+    g_free_events.push_back(p.b);
+  }
+  g_pending.clear();
+  int n = 0;
+  for (auto &kv : g_agg) {
+    if (n < cap) {
+      strncpy(names + 64 * n, kv.first.c_str(), 63);
+      names[64 * n + 63] = 0;
+      counts[n] = kv.second.count;
+      ms[n] = kv.second.ms;
+    }
+    n++;
+  }
+  if (reset) g_agg.clear();
+  return n;
+}
+
+}  // extern "C"

@@ -213,8 +213,8 @@ static void build_tiles(Ctx &ctx, Arena &ar, const RectSets &rs, Tiles *tl) {
   STW_CUDA(ctx, cudaMemcpyAsync(dbo, bo.data(), (rs.S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(diff, 0, (tl->NB + 2) * sizeof(int), ctx.stream));
   if (tl->NB == 0) return;
-  k_tile_meta<<<grid_for(tl->NB, 256), 256, 0, ctx.stream>>>(rs.off, dbo, rs.S, rs.ts, tl->bset, tl->T0, tl->NB);
-  k_live_count<<<grid_for(rs.n, 256), 256, 0, ctx.stream>>>(rs.off, rs.S, rs.n, rs.ts, rs.te, dbo, tl->T0, diff);
+  STW_KL(k_tile_meta, grid_for(tl->NB, 256), 256, ctx.stream, rs.off, dbo, rs.S, rs.ts, tl->bset, tl->T0, tl->NB);
+  STW_KL(k_live_count, grid_for(rs.n, 256), 256, ctx.stream, rs.off, rs.S, rs.n, rs.ts, rs.te, dbo, tl->T0, diff);
   STW_LAUNCHED(ctx);
   device_scan<int>(ctx, ar, diff, cnt, tl->NB + 1, true);  // cnt[b] = live entries of tile b
   if (!ctx.ok()) return;
@@ -231,7 +231,7 @@ static void build_tiles(Ctx &ctx, Arena &ar, const RectSets &rs, Tiles *tl) {
   int *cursor = ar.take<int>(tl->NB + 1);
   if (!ctx.ok()) return;
   STW_CUDA(ctx, cudaMemsetAsync(cursor, 0, (tl->NB + 1) * sizeof(int), ctx.stream));
-  k_live_fill<<<grid_for(rs.n, 256), 256, 0, ctx.stream>>>(rs.off, rs.S, rs.n, rs.te, dbo, tl->T0, tl->loff, cursor,
+  STW_KL(k_live_fill, grid_for(rs.n, 256), 256, ctx.stream, rs.off, rs.S, rs.n, rs.te, dbo, tl->T0, tl->loff, cursor,
                                                           tl->live);
   STW_LAUNCHED(ctx);
 }
@@ -249,7 +249,7 @@ void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, 
     return;
   }
   dim3 grid((unsigned)tl.NB, (unsigned)rs.n_cand);
-  k_validate_tiles<<<grid, kTile, 0, ctx.stream>>>(rs, tl, d_count, d_first, nullptr);
+  STW_KL(k_validate_tiles, grid, kTile, ctx.stream, rs, tl, d_count, d_first, nullptr);
   STW_LAUNCHED(ctx);
   STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
 }
@@ -387,15 +387,15 @@ int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *a
   long long init[2] = {LLONG_MAX, LLONG_MIN};
   STW_CUDA(ctx, cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(mts, 0, sizeof(int), ctx.stream));
-  k_minmax_id<<<grid_for(n, 256), 256, 0, ctx.stream>>>(did, n, mm, mm + 1);
-  k_max_ts<<<grid_for(n, 256), 256, 0, ctx.stream>>>(dts, n, mts);
+  STW_KL(k_minmax_id, grid_for(n, 256), 256, ctx.stream, did, n, mm, mm + 1);
+  STW_KL(k_max_ts, grid_for(n, 256), 256, ctx.stream, dts, n, mts);
   long long h[2];
   int hts = 0;
   STW_CUDA(ctx, cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
   STW_CUDA(ctx, cudaMemcpyAsync(&hts, mts, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
   if (!ctx.ok()) return ctx.rc;
-  k_sweep_keys<<<grid_for(n, 256), 256, 0, ctx.stream>>>(did, dts, n, h[0], hi, lo);
+  STW_KL(k_sweep_keys, grid_for(n, 256), 256, ctx.stream, did, dts, n, h[0], hi, lo);
   sort_perm2(ctx, ar, hi, bitlen_u64((uint64_t)hts), lo, bitlen_u64((uint64_t)(h[1] - h[0])), perm, n);
   int64_t *a2 = ar.take<int64_t>(n), *s2 = ar.take<int64_t>(n);
   int32_t *ts2 = ar.take<int32_t>(n), *te2 = ar.take<int32_t>(n);
@@ -405,7 +405,7 @@ int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *a
   int32_t *per_d = ar.take<int32_t>(n + 1);
   int64_t *pos = ar.take<int64_t>(n + 1);
   if (!ctx.ok()) return ctx.rc;
-  k_gather_rect<<<grid_for(n, 256), 256, 0, ctx.stream>>>(perm, dad, dsz, dts, dte, n, a2, s2, ts2, te2);
+  STW_KL(k_gather_rect, grid_for(n, 256), 256, ctx.stream, perm, dad, dsz, dts, dte, n, a2, s2, ts2, te2);
   int64_t hoff[2] = {0, n};
   STW_CUDA(ctx, cudaMemcpyAsync(off, hoff, sizeof(hoff), cudaMemcpyHostToDevice, ctx.stream));
   RectSets rs{1, n, off, ts2, te2, s2, 1, a2};
@@ -415,7 +415,7 @@ int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *a
   STW_CUDA(ctx, cudaMemsetAsync(first, 0x7f, sizeof(int), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(per_d, 0, (n + 1) * sizeof(int32_t), ctx.stream));
   if (!ctx.ok()) return ctx.rc;
-  k_validate_tiles<<<dim3((unsigned)tl.NB, 1), kTile, 0, ctx.stream>>>(rs, tl, cnt, first, per_d);
+  STW_KL(k_validate_tiles, dim3((unsigned)tl.NB, 1), kTile, ctx.stream, rs, tl, cnt, first, per_d);
   STW_LAUNCHED(ctx);
   // pair slots per decision: exclusive scan of per-decision counts (as int64)
   {
@@ -431,7 +431,7 @@ int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *a
   int64_t wcap = std::min<int64_t>(cap, *n_pairs);
   int32_t *dpairs = ar.take<int32_t>(2 * wcap + 2);
   if (!ctx.ok()) return ctx.rc;
-  k_pairs<<<grid_for(n, 128), 128, 0, ctx.stream>>>(rs, tl, pos, dpairs, wcap, perm);
+  STW_KL(k_pairs, grid_for(n, 128), 128, ctx.stream, rs, tl, pos, dpairs, wcap, perm);
   STW_LAUNCHED(ctx);
   if (wcap > 0)
     STW_CUDA(ctx, cudaMemcpyAsync(pairs, dpairs, 2 * wcap * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.stream));

@@ -79,3 +79,31 @@ def test_plan_select_best():
         assert int(bp.best_cand[t]) == best and int(bp.best_pool[t]) == pools[best]
         s0, s1 = int(bp.batch.ev_off[t]), int(bp.batch.ev_off[t + 1])
         assert np.array_equal(bp.addr_best[s0:s1], bp.addr[best, s0:s1])
+
+
+def _manual_trace(specs, phases):
+    """specs: (id, size_bytes, t_s, t_e, p_s, p_e); phases: [(tag, start, end)]"""
+    from paper_2507_16274_b200 import soa
+    from paper_2507_16274_b200.domain import MemoryRequestEvent, PhaseId, PhaseSpan
+
+    evs = [MemoryRequestEvent(i, s, a, b, PhaseId.parse(x), PhaseId.parse(y)) for i, s, a, b, x, y in specs]
+    sched = [PhaseSpan(PhaseId.parse(t), a, b) for t, a, b in phases]
+    return soa.from_events(evs, sched)
+
+
+def test_plan_many_layers_overflow_paths():
+    rng = np.random.default_rng(7)
+    tas = []
+    # 150 simultaneously live same-size events (one class, 150 layers) + distinct sizes (150 classes)
+    specs = [(i, 512 * 4, i, 400 + i, "F:0", "F:0") for i in range(150)]
+    tas.append(_manual_trace(specs, [("F:0", 0, 1000)]))
+    specs = [(i, 512 * (i + 1), i, 400 + i, "F:0", "F:0") for i in range(150)]
+    tas.append(_manual_trace(specs, [("F:0", 0, 1000)]))
+    # random single-phase soup with a few hundred layers worth of overlap
+    specs = []
+    for i in range(3000):
+        s = int(rng.integers(0, 2000))
+        specs.append((i * 7 + 3, 512 * int(rng.integers(1, 6)), s, s + int(rng.integers(1, 600)), "F:0", "F:0"))
+    tas.append(_manual_trace(specs, [("F:0", 0, 3000)]))
+    check_batch(tas)
+    check_batch(tas[2:])
