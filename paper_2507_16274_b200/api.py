@@ -240,3 +240,232 @@ def validate_plan(plan) -> list:
                                   C.c_int64(cap), None, err, C.sizeof(err)), err)
     p = pairs[: 2 * npairs.value].reshape(-1, 2).tolist()
     return [(decs[a], decs[b]) for a, b in p]
+
+
+# ---------------------------------------------------------------------------
+# dynamic reusable space (reuse.py:42-93)
+
+from .domain import MemplanError as _MemplanError  # noqa: E402
+from .ivset import IntervalSet  # noqa: E402
+from .plan_types import ReuseEntry, ReuseMap  # noqa: E402
+
+
+def group_dynamic(events) -> dict:
+    """Exact partition of dynamic events by (l_s, l_e) (reuse.py:42-51)."""
+    out: dict = {}
+    for ev in events:
+        if not ev.dynamic or ev.l_s is None or ev.l_e is None:
+            raise TraceError(f"event {ev.id}: dynamic event missing layer")
+        out.setdefault((ev.l_s, ev.l_e), []).append(ev)
+    return out
+
+
+def _windows(keys, layer_schedule):
+    spans = {}
+    for s in layer_schedule:
+        spans[s.name] = s  # last span wins, like the dict in reuse.py:66
+    t_lo, t_hi = [], []
+    for key in keys:
+        for name in key:
+            if name not in spans:
+                raise PlanError(f"unknown layer {name!r} in reuse key")
+        a, b = spans[key[0]].start, spans[key[1]].end
+        if b < a:
+            raise PlanError(f"reuse key {key}: free layer ends before alloc layer starts")
+        t_lo.append(a)
+        t_hi.append(b)
+    return np.asarray(t_lo, np.int64), np.asarray(t_hi, np.int64)
+
+
+def _plan_columns(plan):
+    return plan.columns() if isinstance(plan, StaticPlan) else DecisionColumns.from_decisions(tuple(plan.decisions))
+
+
+def reusable_spaces(cols, t_lo, t_hi) -> list:
+    """K8 on the device: idle address intervals of the plan per window."""
+    K = int(t_lo.shape[0])
+    n = len(cols)
+    off = np.zeros(K + 1, np.int64)
+    cap = max(16, 2 * (n + 1) * max(K, 1) if n * K < 4_000_000 else 4 * n + 4 * K)
+    total = C.c_int64(0)
+    err = _lib.errbuf()
+    L = _lib.load()
+    while True:
+        lo = np.empty(cap, np.int64)
+        hi = np.empty(cap, np.int64)
+        rc = L.stw_reuse_map(C.c_int64(n), _lib.ptr(cols.addr), _lib.ptr(cols.size), _lib.ptr(cols.t_s),
+                             _lib.ptr(cols.t_e), C.c_int64(K), _lib.ptr(t_lo), _lib.ptr(t_hi), _lib.ptr(off),
+                             _lib.ptr(lo), _lib.ptr(hi), C.c_int64(cap), C.byref(total), None, err, C.sizeof(err))
+        if rc == _lib.STW_EARG and total.value > cap:
+            cap = total.value
+            continue
+        _lib.check(rc, err)
+        break
+    return [IntervalSet.from_bounds(lo[off[k]:off[k + 1]], hi[off[k]:off[k + 1]]) for k in range(K)]
+
+
+def compute_reusable_space(plan, key, layer_schedule):
+    """((t_lo, t_hi), idle addresses of the plan over the key's window) (reuse.py:54-80)."""
+    t_lo, t_hi = _windows([key], layer_schedule)
+    return (int(t_lo[0]), int(t_hi[0])), reusable_spaces(_plan_columns(plan), t_lo, t_hi)[0]
+
+
+def derive_reuse_map(plan, trace) -> ReuseMap:
+    """One reuse entry per dynamic (l_s, l_e) group, empty spaces kept (reuse.py:83-93)."""
+    ta = getattr(trace, "_arrays", None)
+    if ta is not None:
+        keys, _ = ta.dynamic_keys()
+    else:
+        keys = sorted(group_dynamic(trace.dynamic_events()))
+    if not keys:
+        return ReuseMap({})
+    t_lo, t_hi = _windows(keys, trace.layer_schedule)
+    spaces = reusable_spaces(_plan_columns(plan), t_lo, t_hi)
+    return ReuseMap({k: ReuseEntry(int(a), int(b), s) for k, a, b, s in zip(keys, t_lo, t_hi, spaces)})
+
+
+def plan_trace(trace, *, fusion=True, gap_insert=True, stats=None):
+    """Plan a trace end to end: static plan plus dynamic reuse map (__init__.py:42-47)."""
+    plan = synthesize_static_plan(trace, fusion=fusion, gap_insert=gap_insert, stats=stats)
+    return plan, derive_reuse_map(plan, trace)
+
+
+# ---------------------------------------------------------------------------
+# replay (sim.py:143-238) and the caching-allocator baseline (baseline.py:98-137)
+
+import json as _json  # noqa: E402
+from collections.abc import Sequence as _Sequence  # noqa: E402
+from pathlib import Path as _Path  # noqa: E402
+
+from .plan_types import PlanBundle, SimReport  # noqa: E402
+
+_KINDS = ("init", "reserve", "alloc", "free")
+_ROUTES = ("planned", "reuse", "fallback", "mismatch", "online")
+
+
+class ReplayLog(_Sequence):
+    """The replay log as the reference's list of dicts, materialised on access
+    from the device's columns (sim.py:164, 186, 209-229, 241-253)."""
+
+    def __init__(self, cols: dict, n: int, keys_by_id: dict):
+        self._c = cols
+        self._n = n
+        self._keys = keys_by_id
+        self._cache = None
+
+    def __len__(self) -> int:
+        return self._n
+
+    def _rec(self, k: int) -> dict:
+        c = self._c
+        kind = _KINDS[int(c["kind"][k])]
+        if kind == "init":
+            return {"kind": "init", "pool_size": int(c["size"][k])}
+        if kind == "reserve":
+            return {"kind": "reserve", "t": int(c["t"][k]), "bytes": int(c["size"][k])}
+        rec = {"kind": kind, "t": int(c["t"][k]), "id": int(c["id"][k]), "size": int(c["size"][k]),
+               "space": "pool" if c["space"][k] == 0 else "cache", "addr": int(c["addr"][k])}
+        if kind == "alloc":
+            rec["route"] = _ROUTES[int(c["route"][k])]
+            key = self._keys.get(rec["id"])
+            if key is not None:
+                rec["key"] = list(key)
+        return rec
+
+    def _all(self) -> list:
+        if self._cache is None:
+            self._cache = [self._rec(k) for k in range(self._n)]
+        return self._cache
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return self._all()[i]
+        return self._all()[i] if self._cache is not None else self._rec(range(self._n)[i])
+
+    def __iter__(self):
+        return iter(self._all())
+
+    def __eq__(self, other) -> bool:
+        return list(self) == list(other)
+
+
+def _log_buffers(n: int):
+    cap = 1 + 3 * n
+    cols = dict(kind=np.empty(cap, np.int8), t=np.empty(cap, np.int64), id=np.empty(cap, np.int64),
+                size=np.empty(cap, np.int64), addr=np.empty(cap, np.int64), space=np.empty(cap, np.int8),
+                route=np.empty(cap, np.int8))
+    lg = _lib.Log(cap, 0, *(_lib.ptr(cols[k]) for k in ("kind", "t", "id", "size", "addr", "space", "route")))
+    return lg, cols
+
+
+def _report(rep) -> SimReport:
+    return SimReport(rep.allocated_peak, rep.reserved_peak, rep.efficiency, rep.fragmentation, rep.pool_size,
+                     rep.fallback_count, rep.fallback_bytes_peak, rep.reuse_hits, rep.mismatch_count)
+
+
+def _dyn_keys_by_id(ta) -> dict:
+    d = np.nonzero(ta.dyn)[0]
+    names = ta.layer_names
+    return {int(ta.id[i]): (names[ta.ls[i]], names[ta.le[i]]) for i in d.tolist()}
+
+
+def _write_log(log, path) -> None:
+    with _Path(path).open("w", encoding="utf-8") as fh:
+        for rec in log:
+            fh.write(_json.dumps(rec, sort_keys=True, separators=(",", ":")) + "\n")
+
+
+def simulate(trace, plan, *, reuse: bool = True, log_path=None):
+    """Replay the trace against a PlanBundle on the device; returns (SimReport, log)."""
+    ta = _arrays_of(trace)
+    hb = HostBatch([ta])
+    cols = getattr(plan, "_cols", None)
+    if cols is None:
+        cols = DecisionColumns.from_decisions(tuple(plan.decisions))
+    bkeys = list(plan.reuse)
+    pos = {k: i for i, k in enumerate(bkeys)}
+    names, kidx = ta.dynamic_keys()
+    key = np.full(len(ta), -1, np.int32)
+    if len(names):
+        m = kidx >= 0
+        key[m] = np.asarray([pos.get(names[k], -1) for k in kidx[m].tolist()], np.int32)
+    off = [0]
+    lo, hi = [], []
+    for k in bkeys:
+        for iv in plan.reuse[k]:
+            lo.append(iv.lo)
+            hi.append(iv.hi)
+        off.append(len(lo))
+    sp_off = np.asarray(off, np.int64)
+    sp_lo = np.asarray(lo, np.int64)
+    sp_hi = np.asarray(hi, np.int64)
+    bun = _lib.Bundle(int(plan.pool_size), int(plan.alignment), len(cols), _lib.ptr(cols.id), _lib.ptr(cols.addr),
+                      _lib.ptr(cols.size), _lib.ptr(cols.t_s), _lib.ptr(cols.t_e), len(bkeys), _lib.ptr(sp_off),
+                      _lib.ptr(sp_lo), _lib.ptr(sp_hi), _lib.ptr(key), int(bool(reuse)))
+    rep = _lib.Report()
+    lg, lcols = _log_buffers(len(ta))
+    eid = C.c_int64(0)
+    err = _lib.errbuf()
+    b = hb.struct()
+    rc = _lib.load().stw_simulate(C.byref(b), C.byref(bun), C.byref(rep), C.byref(lg), C.byref(eid), None, err,
+                                  C.sizeof(err))
+    if rc == _lib.STW_EPLAN and err.value.startswith(b"reuse entry"):
+        k = bkeys[eid.value]
+        raise PlanError(f"reuse entry {k} outside pool")
+    _lib.check(rc, err)
+    log = ReplayLog(lcols, int(lg.len), _dyn_keys_by_id(ta))
+    if log_path is not None:
+        _write_log(log, log_path)
+    return _report(rep), log
+
+
+def run_baseline(trace) -> SimReport:
+    """Replay every event online through the caching allocator (baseline.py:98-137)."""
+    ta = _arrays_of(trace)
+    hb = HostBatch([ta])
+    rep = _lib.Report()
+    eid = C.c_int64(0)
+    err = _lib.errbuf()
+    b = hb.struct()
+    _lib.check(_lib.load().stw_baseline(C.byref(b), C.byref(rep), None, C.byref(eid), None, err, C.sizeof(err)), err)
+    return _report(rep)

@@ -39,7 +39,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *sources()]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed building libstw.so")
+        if verbose and (res.stdout or res.stderr):
+            sys.stderr.write(res.stdout + res.stderr)
     return LIB
 
 

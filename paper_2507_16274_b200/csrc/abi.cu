@@ -21,6 +21,10 @@ namespace stw {
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
                         const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap);
+int reuse_map(Ctx &ctx, int64_t n, const int64_t *addr, const int64_t *size, const int32_t *t_s, const int32_t *t_e,
+              int64_t K, const int64_t *t_lo, const int64_t *t_hi, int64_t *out_off, int64_t *out_lo, int64_t *out_hi,
+              int64_t cap, int64_t *total);
+int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep, stw_log *log, int64_t *err_id);
 }  // namespace stw
 
 extern "C" {
@@ -76,6 +80,40 @@ int stw_validate(int64_t n, const int64_t *id, const int64_t *addr, const int64_
     return ctx.rc;
   }
   validate_plan_pairs(ctx, n, id, addr, size, t_s, t_e, n_pairs, pairs, cap);
+  return finish(ctx);
+}
+
+int stw_reuse_map(int64_t n, const int64_t *addr, const int64_t *size, const int32_t *t_s, const int32_t *t_e,
+                  int64_t K, const int64_t *t_lo, const int64_t *t_hi, int64_t *out_off, int64_t *out_lo,
+                  int64_t *out_hi, int64_t cap, int64_t *total, void *stream, char *err, size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (n < 0 || n >= (int64_t)INT32_MAX || K < 0 || !total) {
+    ctx.fail(STW_EARG, "bad reuse_map arguments");
+    return ctx.rc;
+  }
+  reuse_map(ctx, n, addr, size, t_s, t_e, K, t_lo, t_hi, out_off, out_lo, out_hi, cap, total);
+  return finish(ctx);
+}
+
+int stw_simulate(const stw_batch *trace, const stw_bundle *plan, stw_report *rep, stw_log *log, int64_t *err_id,
+                 void *stream, char *err, size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (!trace || !plan || !rep || !err_id) {
+    ctx.fail(STW_EARG, "null argument");
+    return ctx.rc;
+  }
+  replay(ctx, trace, plan, rep, log, err_id);
+  return finish(ctx);
+}
+
+int stw_baseline(const stw_batch *trace, stw_report *rep, stw_log *log, int64_t *err_id, void *stream, char *err,
+                 size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (!trace || !rep || !err_id) {
+    ctx.fail(STW_EARG, "null argument");
+    return ctx.rc;
+  }
+  replay(ctx, trace, nullptr, rep, log, err_id);
   return finish(ctx);
 }
 

@@ -1,0 +1,925 @@
+// K9/K10 -- trace replay against a plan (simulate, sim.py:143-238) and the
+// online caching-allocator baseline (run_baseline, baseline.py:98-137).
+//
+// Parallel preprocessing on the device:
+//   * plan bundle validation (traceio.py:322-331)
+//   * dense id classes (the reference keys its live maps and events_by_id by id)
+//   * static matching: the k-th static alloc (in op order) of key
+//     (p_s, size) receives the k-th decision of that key in (t_s, id) order
+//     (sim.py:156-162, 189-191) -- a joint radix sort of decisions and static
+//     events by (p_s, size, side, order), then ranks inside each key
+//   * op order (t, is_alloc, id), frees first (sim.py:165-169)
+// Sequential residue on one warp: the pool free-interval set, dynamic best-fit
+// inside the reuse space (sim.py:120-140), the caching allocator
+// (baseline.py:49-95), the replay log and the metrics (sim.py:67-117). The
+// warp prefetches 32 ops at a time; interval lists live in shared memory.
+#include <algorithm>
+#include <vector>
+
+#include "planner.cuh"
+
+namespace stw {
+
+#define GS3(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// kernels shared with plan.cu
+__global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx);
+__global__ void k_max_i32(const int32_t *__restrict__ v, int64_t n, int *mx);
+__global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *__restrict__ perm,
+                             uint64_t *__restrict__ dst, int64_t n);
+double exact_div_host(unsigned long long a, unsigned long long b);
+
+constexpr int kFreeSmem = 4096;   // pool free intervals kept in shared memory
+constexpr int kBlockSmem = 6144;  // cache free blocks kept in shared memory
+constexpr size_t kReplaySmem = (size_t)kFreeSmem * 16 + (size_t)kBlockSmem * 20;
+constexpr long long kMinSegment = 2ll * 1024 * 1024;
+
+enum { R_PLANNED = 0, R_REUSE = 1, R_FALLBACK = 2, R_MISMATCH = 3, R_ONLINE = 4 };
+
+// ---------------------------------------------------------------------------
+// preprocessing kernels
+
+__global__ void k_bundle_check(const int64_t *__restrict__ d_addr, const int64_t *__restrict__ d_size, int64_t nd,
+                               long long pool, long long align, int *__restrict__ first_bad,
+                               const int64_t *__restrict__ sp_off, const int64_t *__restrict__ sp_lo,
+                               const int64_t *__restrict__ sp_hi, int64_t K, int *__restrict__ first_bad_key) {
+  GS3(k, nd) {
+    if (d_addr[k] < 0 || d_addr[k] + d_size[k] > pool || d_addr[k] % align) atomicMin(first_bad, (int)k);
+  }
+  GS3(k, K) {
+    for (int64_t j = sp_off[k]; j < sp_off[k + 1]; j++)
+      if (sp_lo[j] < 0 || sp_hi[j] > pool) {
+        atomicMin(first_bad_key, (int)k);
+        break;
+      }
+  }
+}
+
+__global__ void k_id_keys(const int64_t *__restrict__ id, int64_t n, long long idmin, uint64_t *__restrict__ key) {
+  GS3(i, n) key[i] = (uint64_t)((long long)id[i] - idmin);
+}
+
+// did (dense id class) per event, last event index per class, sorted unique ids
+__global__ void k_id_classes(const uint32_t *__restrict__ perm, const uint64_t *__restrict__ skey, int64_t n,
+                             const uint32_t *__restrict__ cls_incl, int32_t *__restrict__ did, int32_t *__restrict__ last_of,
+                             uint64_t *__restrict__ ukey) {
+  GS3(k, n) {
+    uint32_t i = perm[k];
+    int c = (int)cls_incl[k] - 1;
+    did[i] = c;
+    if (k + 1 == n || skey[k + 1] != skey[k]) {
+      last_of[c] = (int32_t)i;  // stable sort: the largest index of the class comes last
+      ukey[c] = skey[k];
+    }
+  }
+}
+
+__global__ void k_heads_u64(const uint64_t *__restrict__ skey, int64_t n, uint32_t *__restrict__ head) {
+  GS3(k, n) head[k] = (k == 0 || skey[k] != skey[k - 1]) ? 1u : 0u;
+}
+
+// op keys, stage 1 (id) and stage 2 (t, is_alloc); ops are (alloc e, free e) = (2e, 2e+1)
+__global__ void k_op_keys_id(const int64_t *__restrict__ id, int64_t n, long long idmin, uint64_t *__restrict__ key) {
+  GS3(o, 2 * n) key[o] = (uint64_t)((long long)id[o >> 1] - idmin);
+}
+__global__ void k_op_keys_t(const uint32_t *__restrict__ perm, const int32_t *__restrict__ ts,
+                            const int32_t *__restrict__ te, int64_t n, uint64_t *__restrict__ key) {
+  GS3(k, 2 * n) {
+    uint32_t o = perm[k];
+    uint32_t e = o >> 1;
+    bool alloc = !(o & 1);
+    key[k] = ((uint64_t)(uint32_t)(alloc ? ts[e] : te[e]) << 1) | (alloc ? 1u : 0u);
+  }
+}
+__global__ void k_op_rank(const uint32_t *__restrict__ operm, int64_t n2, int32_t *__restrict__ apos) {
+  GS3(k, n2) {
+    uint32_t o = operm[k];
+    if (!(o & 1)) apos[o >> 1] = (int32_t)k;
+  }
+}
+
+// decisions: find the event carrying the id (events_by_id keeps the last one)
+__global__ void k_dec_lookup(const int64_t *__restrict__ d_id, int64_t nd, const uint64_t *__restrict__ ukey, int64_t nu,
+                             long long idmin, const int32_t *__restrict__ last_of, const uint8_t *__restrict__ dyn,
+                             int32_t *__restrict__ d_ev) {
+  GS3(k, nd) {
+    long long x = (long long)d_id[k] - idmin;
+    int e = -1;
+    if (x >= 0) {
+      uint64_t ux = (uint64_t)x;
+      int64_t lo = 0, hi = nu;
+      while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (ukey[m] < ux)
+          lo = m + 1;
+        else
+          hi = m;
+      }
+      if (lo < nu && ukey[lo] == ux) e = last_of[lo];
+    }
+    d_ev[k] = (e >= 0 && !dyn[e]) ? e : -1;
+  }
+}
+
+// decision queue order: (t_s, id, plan position)
+__global__ void k_dec_keys(const int32_t *__restrict__ d_ts, const int64_t *__restrict__ d_id, int64_t nd,
+                           long long idmin, uint64_t *__restrict__ hi, uint64_t *__restrict__ lo) {
+  GS3(k, nd) {
+    hi[k] = (uint32_t)d_ts[k];
+    lo[k] = (uint64_t)((long long)d_id[k] - idmin);
+  }
+}
+__global__ void k_scatter_rank(const uint32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ rank) {
+  GS3(k, n) rank[perm[k]] = (int32_t)k;
+}
+
+// joint records for queue matching. record r < nd: decision; else static event
+struct MatchRec {
+  int64_t nd, n;
+  const int32_t *d_ev, *d_rank;
+  const int64_t *d_size;
+  const int32_t *ps;
+  const int64_t *size;
+  const uint8_t *dyn;
+  const int32_t *apos;
+};
+__global__ void k_match_keys(MatchRec M, uint64_t *__restrict__ k_ord, uint64_t *__restrict__ k_size,
+                             uint64_t *__restrict__ k_ps) {
+  GS3(r, M.nd + M.n) {
+    uint64_t side, ord, sz, ph;
+    if (r < M.nd) {
+      int e = M.d_ev[r];
+      side = 0;
+      ord = (uint32_t)M.d_rank[r];
+      sz = (uint64_t)M.d_size[r];
+      ph = e >= 0 ? (uint32_t)M.ps[e] : 0xFFFFFFFFu;  // ineligible decisions sort last, never matched
+    } else {
+      int64_t e = r - M.nd;
+      side = 1;
+      ord = (uint32_t)M.apos[e];
+      sz = (uint64_t)M.size[e];
+      ph = M.dyn[e] ? 0xFFFFFFFFu : (uint32_t)M.ps[e];
+    }
+    k_ord[r] = (side << 32) | ord;
+    k_size[r] = sz;
+    k_ps[r] = ph;
+  }
+}
+
+__global__ void k_match_heads(const uint32_t *__restrict__ perm, MatchRec M, uint32_t *__restrict__ head) {
+  GS3(k, M.nd + M.n) {
+    auto key = [&](uint32_t r, uint64_t *ph, uint64_t *sz) {
+      if (r < M.nd) {
+        int e = M.d_ev[r];
+        *ph = e >= 0 ? (uint32_t)M.ps[e] : 0xFFFFFFFFu;
+        *sz = (uint64_t)M.d_size[r];
+      } else {
+        int64_t e = r - M.nd;
+        *ph = M.dyn[e] ? 0xFFFFFFFFu : (uint32_t)M.ps[e];
+        *sz = (uint64_t)M.size[e];
+      }
+    };
+    uint32_t h = 1;
+    if (k > 0) {
+      uint64_t a, b, c, d;
+      key(perm[k], &a, &b);
+      key(perm[k - 1], &c, &d);
+      h = (a != c || b != d);
+    }
+    head[k] = h;
+  }
+}
+
+__global__ void k_match_groups(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ gid_incl, int64_t nr,
+                               int64_t nd, int64_t *__restrict__ gstart, int32_t *__restrict__ gndec) {
+  GS3(k, nr) {
+    int g = (int)gid_incl[k] - 1;
+    if (k == 0 || gid_incl[k - 1] != gid_incl[k]) gstart[g] = k;
+    if (perm[k] < nd) atomicAdd(gndec + g, 1);
+  }
+}
+
+__global__ void k_match_assign(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ gid_incl, int64_t nr,
+                               MatchRec M, const int64_t *__restrict__ gstart, const int32_t *__restrict__ gndec,
+                               const int64_t *__restrict__ d_addr, int8_t *__restrict__ route,
+                               int64_t *__restrict__ paddr) {
+  GS3(k, nr) {
+    uint32_t r = perm[k];
+    if (r < M.nd) continue;
+    int64_t e = r - M.nd;
+    if (M.dyn[e]) continue;
+    int g = (int)gid_incl[k] - 1;
+    int64_t rank = k - gstart[g] - gndec[g];
+    if (rank < gndec[g]) {
+      route[e] = R_PLANNED;
+      paddr[e] = d_addr[perm[gstart[g] + rank]];
+    } else {
+      route[e] = R_MISMATCH;
+      paddr[e] = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sequential replay warp
+
+struct ReplayArgs {
+  int64_t n;
+  const uint32_t *operm;
+  const int64_t *id, *size;
+  const int32_t *ts, *te;
+  const uint8_t *dyn;
+  const int32_t *did;
+  const int8_t *route0;  // R_PLANNED / R_MISMATCH for static events; baseline: all R_ONLINE
+  const int64_t *paddr;
+  const int32_t *key;
+  const int64_t *sp_off, *sp_lo, *sp_hi;
+  int reuse, baseline;
+  long long pool;
+  // state (global, per dense id class)
+  int64_t *plo, *phi;
+  int8_t *pflag;
+  int64_t *clo, *chi;
+  int32_t *cseg;
+  int8_t *cflag;
+  int64_t *gflo, *gfhi;              // spill storage for the free list (cap n + 2)
+  int64_t *gblo, *gbhi;              // spill storage for cache blocks (cap 2n + 2)
+  int32_t *gbseg;
+  int64_t *sbase;                    // segment bases (cap n + 1)
+  // log (cap 1 + 3n)
+  int8_t *lkind, *lspace, *lroute;
+  int64_t *lt, *lid, *lsize, *laddr;
+  // results
+  long long *res;  // [0] nlog, [1] err code, [2] err id, [3] err addr, metrics [4..]
+};
+
+// warp helpers ---------------------------------------------------------------
+__device__ __forceinline__ void wshift_right(int64_t *a, int64_t *b, int32_t *c, int from, int n, int s) {
+  for (int base = n - 1; base >= from; base -= 32) {
+    int idx = base - (int)lane_id();
+    int64_t va = 0, vb = 0;
+    int32_t vc = 0;
+    bool ok = idx >= from;
+    if (ok) {
+      va = a[idx];
+      vb = b[idx];
+      if (c) vc = c[idx];
+    }
+    __syncwarp();
+    if (ok) {
+      a[idx + s] = va;
+      b[idx + s] = vb;
+      if (c) c[idx + s] = vc;
+    }
+    __syncwarp();
+  }
+}
+__device__ __forceinline__ void wshift_left(int64_t *a, int64_t *b, int32_t *c, int from, int n, int s) {
+  // a[from .. n-s) = a[from+s .. n)
+  for (int base = from; base < n - s; base += 32) {
+    int idx = base + (int)lane_id();
+    int64_t va = 0, vb = 0;
+    int32_t vc = 0;
+    bool ok = idx < n - s;
+    if (ok) {
+      va = a[idx + s];
+      vb = b[idx + s];
+      if (c) vc = c[idx + s];
+    }
+    __syncwarp();
+    if (ok) {
+      a[idx] = va;
+      b[idx] = vb;
+      if (c) c[idx] = vc;
+    }
+    __syncwarp();
+  }
+}
+// last index with lo[i] <= x (-1 if none), lane-0 binary search, broadcast
+__device__ __forceinline__ int wfind_le(const int64_t *lo, int n, long long x) {
+  int r = 0;
+  if (lane_id() == 0) {
+    int a = 0, b = n;
+    while (a < b) {
+      int m = (a + b) >> 1;
+      if (lo[m] <= x)
+        a = m + 1;
+      else
+        b = m;
+    }
+    r = a - 1;
+  }
+  return __shfl_sync(0xffffffffu, r, 0);
+}
+// first index with hi[i] >= x
+__device__ __forceinline__ int wfind_hi_ge(const int64_t *hi, int n, long long x) {
+  int r = 0;
+  if (lane_id() == 0) {
+    int a = 0, b = n;
+    while (a < b) {
+      int m = (a + b) >> 1;
+      if (hi[m] < x)
+        a = m + 1;
+      else
+        b = m;
+    }
+    r = a;
+  }
+  return __shfl_sync(0xffffffffu, r, 0);
+}
+
+__device__ __forceinline__ void warp_min_pair(long long &k1, long long &k2) {
+  for (int o = 16; o; o >>= 1) {
+    long long a = __shfl_xor_sync(0xffffffffu, k1, o), b = __shfl_xor_sync(0xffffffffu, k2, o);
+    if (a < k1 || (a == k1 && b < k2)) k1 = a, k2 = b;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
+  extern __shared__ int64_t dsm[];
+  int64_t *s_flo = dsm, *s_fhi = dsm + kFreeSmem;
+  int64_t *s_blo = dsm + 2 * kFreeSmem, *s_bhi = s_blo + kBlockSmem;
+  int32_t *s_bseg = (int32_t *)(s_bhi + kBlockSmem);
+  const unsigned lane = lane_id();
+  const bool big_free = A.n + 2 > kFreeSmem, big_blk = 2 * A.n + 2 > kBlockSmem;
+  int64_t *flo = big_free ? A.gflo : s_flo, *fhi = big_free ? A.gfhi : s_fhi;
+  int64_t *blo = big_blk ? A.gblo : s_blo, *bhi = big_blk ? A.gbhi : s_bhi;
+  int32_t *bseg = big_blk ? A.gbseg : s_bseg;
+  int nf = 0, nb = 0, ns = 0;
+  long long next_base = A.baseline ? 0 : A.pool;
+  if (!A.baseline && A.pool > 0) {
+    if (lane == 0) {
+      flo[0] = 0;
+      fhi[0] = A.pool;
+    }
+    nf = 1;
+  }
+  long long nlog = 0, live = 0, peak = 0, clive = 0, cpeak = 0, reserved = 0;
+  long long n_fb = 0, n_reuse = 0, n_mm = 0;
+  long long err = 0, err_id = 0, err_addr = 0;
+  auto logrec = [&](int kind, long long t, long long id, long long size, int space, long long addr, int route) {
+    if (lane == 0) {
+      A.lkind[nlog] = (int8_t)kind;
+      A.lt[nlog] = t;
+      A.lid[nlog] = id;
+      A.lsize[nlog] = size;
+      A.lspace[nlog] = (int8_t)space;
+      A.laddr[nlog] = addr;
+      A.lroute[nlog] = (int8_t)route;
+    }
+    nlog++;
+  };
+  logrec(0, 0, 0, A.baseline ? 0 : A.pool, 0, 0, -1);
+
+  // caching allocator malloc (baseline.py:49-77); returns addr, sets *grown; -1 if already live
+  auto cache_malloc = [&](int c, long long size, long long *grown) -> long long {
+    if (A.cflag[c]) return -1;
+    long long bl = LLONG_MAX, bi = LLONG_MAX;
+    for (int i = lane; i < nb; i += 32) {
+      long long len = bhi[i] - blo[i];
+      if (len >= size && (len < bl || (len == bl && i < bi))) bl = len, bi = i;
+    }
+    warp_min_pair(bl, bi);
+    *grown = 0;
+    int i = (int)bi;
+    if (bi == LLONG_MAX) {  // new segment at the end (segments are appended in creation order)
+      long long ss = 1;
+      while (ss < size) ss <<= 1;
+      if (ss < kMinSegment) ss = kMinSegment;
+      if (lane == 0) {
+        A.sbase[ns] = next_base;
+        blo[nb] = next_base;
+        bhi[nb] = next_base + ss;
+        bseg[nb] = ns;
+      }
+      __syncwarp();
+      i = nb++;
+      ns++;
+      next_base += ss;
+      *grown = ss;
+    }
+    long long lo = blo[i], hi = bhi[i];
+    int sg = bseg[i];
+    __syncwarp();
+    if (lo + size < hi) {
+      if (lane == 0) blo[i] = lo + size;
+      __syncwarp();
+    } else {
+      wshift_left(blo, bhi, bseg, i, nb, 1);
+      nb--;
+    }
+    if (lane == 0) {
+      A.clo[c] = lo;
+      A.chi[c] = lo + size;
+      A.cseg[c] = sg;
+      A.cflag[c] = 1;
+    }
+    __syncwarp();
+    return lo;
+  };
+  // caching allocator free (baseline.py:79-95): insort + merge with neighbours
+  auto cache_free = [&](int c, long long *addr, long long *size) {
+    long long lo = A.clo[c], hi = A.chi[c];
+    int sg = A.cseg[c];
+    if (lane == 0) A.cflag[c] = 0;
+    *addr = lo;
+    *size = hi - lo;
+    int p = 0;  // insertion point: first block with (seg, lo) > (sg, lo)
+    if (lane == 0) {
+      int a = 0, b = nb;
+      while (a < b) {
+        int m = (a + b) >> 1;
+        if (bseg[m] < sg || (bseg[m] == sg && blo[m] < lo))
+          a = m + 1;
+        else
+          b = m;
+      }
+      p = a;
+    }
+    p = __shfl_sync(0xffffffffu, p, 0);
+    bool nxt = p < nb && bseg[p] == sg && blo[p] == hi;
+    bool prv = p > 0 && bseg[p - 1] == sg && bhi[p - 1] == lo;
+    __syncwarp();
+    if (nxt && prv) {
+      long long nh = bhi[p];
+      __syncwarp();
+      if (lane == 0) bhi[p - 1] = nh;
+      __syncwarp();
+      wshift_left(blo, bhi, bseg, p, nb, 1);
+      nb--;
+    } else if (nxt) {
+      if (lane == 0) blo[p] = lo;
+      __syncwarp();
+    } else if (prv) {
+      if (lane == 0) bhi[p - 1] = hi;
+      __syncwarp();
+    } else {
+      wshift_right(blo, bhi, bseg, p, nb, 1);
+      if (lane == 0) {
+        blo[p] = lo;
+        bhi[p] = hi;
+        bseg[p] = sg;
+      }
+      __syncwarp();
+      nb++;
+    }
+  };
+  // pool free list: remove [lo, hi) lying inside free interval i
+  auto free_remove = [&](int i, long long lo, long long hi) {
+    long long a = flo[i], b = fhi[i];
+    __syncwarp();
+    bool left = a < lo, right = b > hi;
+    if (left && right) {
+      wshift_right(flo, fhi, nullptr, i + 1, nf, 1);
+      if (lane == 0) {
+        fhi[i] = lo;
+        flo[i + 1] = hi;
+        fhi[i + 1] = b;
+      }
+      nf++;
+    } else if (left) {
+      if (lane == 0) fhi[i] = lo;
+    } else if (right) {
+      if (lane == 0) flo[i] = hi;
+    } else {
+      wshift_left(flo, fhi, nullptr, i, nf, 1);
+      nf--;
+    }
+    __syncwarp();
+  };
+  // IntervalSet.add (intervals.py:100-111)
+  auto free_add = [&](long long lo, long long hi) {
+    int a = wfind_hi_ge(fhi, nf, lo);  // first with hi >= lo
+    int b = a;                         // first (from a) with lo > hi
+    if (lane == 0) {
+      int x = a, y = nf;
+      while (x < y) {
+        int m = (x + y) >> 1;
+        if (flo[m] <= hi)
+          x = m + 1;
+        else
+          y = m;
+      }
+      b = x;
+    }
+    b = __shfl_sync(0xffffffffu, b, 0);
+    long long nlo = lo, nhi = hi;
+    if (b > a) {
+      nlo = min(nlo, (long long)flo[a]);
+      nhi = max(nhi, (long long)fhi[b - 1]);
+    }
+    __syncwarp();
+    int cnt = b - a;
+    if (cnt == 0) {
+      wshift_right(flo, fhi, nullptr, a, nf, 1);
+      nf++;
+    } else if (cnt > 1) {
+      wshift_left(flo, fhi, nullptr, a + 1, nf, cnt - 1);
+      nf -= cnt - 1;
+    }
+    if (lane == 0) {
+      flo[a] = nlo;
+      fhi[a] = nhi;
+    }
+    __syncwarp();
+  };
+
+  const int64_t n2 = 2 * A.n;
+  for (int64_t cb = 0; cb < n2 && !err; cb += 32) {
+    // prefetch 32 ops
+    int64_t mine = cb + lane;
+    uint32_t o = mine < n2 ? A.operm[mine] : 0;
+    int e = (int)(o >> 1);
+    bool is_alloc = !(o & 1);
+    long long my_t = 0, my_id = 0, my_size = 0, my_paddr = -1;
+    int my_did = 0, my_key = -1, my_route = R_ONLINE;
+    bool my_dyn = false;
+    if (mine < n2) {
+      my_t = is_alloc ? A.ts[e] : A.te[e];
+      my_id = A.id[e];
+      my_size = A.size[e];
+      my_did = A.did[e];
+      my_dyn = A.dyn[e] != 0;
+      if (!A.baseline) {
+        my_route = my_dyn ? -1 : A.route0[e];
+        my_paddr = my_dyn ? -1 : A.paddr[e];
+        my_key = my_dyn ? A.key[e] : -1;
+      }
+    }
+    const int cnt = (int)min((int64_t)32, n2 - cb);
+    for (int k = 0; k < cnt && !err; k++) {
+      const bool alloc = __shfl_sync(0xffffffffu, (int)is_alloc, k);
+      const long long t = __shfl_sync(0xffffffffu, my_t, k), id = __shfl_sync(0xffffffffu, my_id, k);
+      const long long size = __shfl_sync(0xffffffffu, my_size, k);
+      const int c = __shfl_sync(0xffffffffu, my_did, k);
+      if (alloc) {
+        const int route = __shfl_sync(0xffffffffu, my_route, k);
+        if (route == R_PLANNED) {
+          const long long a = __shfl_sync(0xffffffffu, my_paddr, k);
+          int i = wfind_le(flo, nf, a);
+          bool ok = i >= 0 && fhi[i] >= a + size;  // contains_interval (intervals.py:95-98)
+          __syncwarp();
+          if (!ok) {
+            err = STW_ESIM;
+            err_id = id;
+            err_addr = a;
+            break;
+          }
+          free_remove(i, a, a + size);
+          if (lane == 0) {
+            A.plo[c] = a;
+            A.phi[c] = a + size;
+            A.pflag[c] = 1;
+          }
+          logrec(2, t, id, size, 0, a, R_PLANNED);
+          live += size;
+          peak = max(peak, live);
+        } else if (route == R_MISMATCH || route == R_ONLINE) {
+          long long grown;
+          long long a = cache_malloc(c, size, &grown);
+          if (a < 0) {
+            err = STW_ESIM + 100;  // already live in cache
+            err_id = id;
+            break;
+          }
+          if (grown) {
+            logrec(1, t, 0, grown, 0, 0, -1);
+            reserved += grown;
+          }
+          logrec(2, t, id, size, 1, a, route);
+          live += size;
+          peak = max(peak, live);
+          clive += size;
+          cpeak = max(cpeak, clive);
+          if (route == R_MISMATCH) n_fb++, n_mm++;
+        } else {  // dynamic: best fit in free ∩ space[key], else fallback
+          const int kk = __shfl_sync(0xffffffffu, my_key, k);
+          long long best_len = LLONG_MAX, best_lo = LLONG_MAX;
+          int best_i = -1;
+          if (A.reuse && kk >= 0 && A.sp_off[kk + 1] > A.sp_off[kk]) {
+            const int64_t s0 = A.sp_off[kk], s1 = A.sp_off[kk + 1];
+            for (int i = lane; i < nf; i += 32) {
+              long long a = flo[i], b = fhi[i];
+              int64_t lo_j = s0, hi_j = s1;  // first space interval with hi > a
+              while (lo_j < hi_j) {
+                int64_t m = (lo_j + hi_j) >> 1;
+                if (A.sp_hi[m] <= a)
+                  lo_j = m + 1;
+                else
+                  hi_j = m;
+              }
+              for (int64_t j = lo_j; j < s1 && A.sp_lo[j] < b; j++) {
+                long long lo = max(a, (long long)A.sp_lo[j]), hi = min(b, (long long)A.sp_hi[j]);
+                long long len = hi - lo;
+                if (len >= size && (len < best_len || (len == best_len && lo < best_lo))) best_len = len, best_lo = lo;
+              }
+            }
+            warp_min_pair(best_len, best_lo);
+            if (best_len != LLONG_MAX) best_i = wfind_le(flo, nf, best_lo);
+          }
+          if (best_i >= 0) {
+            free_remove(best_i, best_lo, best_lo + size);
+            if (lane == 0) {
+              A.plo[c] = best_lo;
+              A.phi[c] = best_lo + size;
+              A.pflag[c] = 1;
+            }
+            logrec(2, t, id, size, 0, best_lo, R_REUSE);
+            live += size;
+            peak = max(peak, live);
+            n_reuse++;
+          } else {
+            long long grown;
+            long long a = cache_malloc(c, size, &grown);
+            if (a < 0) {
+              err = STW_ESIM + 100;
+              err_id = id;
+              break;
+            }
+            if (grown) {
+              logrec(1, t, 0, grown, 0, 0, -1);
+              reserved += grown;
+            }
+            logrec(2, t, id, size, 1, a, R_FALLBACK);
+            live += size;
+            peak = max(peak, live);
+            clive += size;
+            cpeak = max(cpeak, clive);
+            n_fb++;
+          }
+        }
+      } else {
+        if (A.pflag[c]) {
+          long long lo = A.plo[c], hi = A.phi[c];
+          if (lane == 0) A.pflag[c] = 0;
+          __syncwarp();
+          free_add(lo, hi);
+          logrec(3, t, id, hi - lo, 0, lo, -1);
+          live -= hi - lo;
+        } else if (A.cflag[c]) {
+          long long a, s;
+          cache_free(c, &a, &s);
+          logrec(3, t, id, s, 1, a, -1);
+          live -= s;
+          clive -= s;
+        } else {
+          err = STW_ESIM + 200;  // double free / unknown id
+          err_id = id;
+          break;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    A.res[0] = nlog;
+    A.res[1] = err;
+    A.res[2] = err_id;
+    A.res[3] = err_addr;
+    A.res[4] = peak;
+    A.res[5] = reserved;
+    A.res[6] = cpeak;
+    A.res[7] = n_fb;
+    A.res[8] = n_reuse;
+    A.res[9] = n_mm;
+  }
+}
+
+__global__ void k_fill_i8(int8_t *p, int64_t n, int8_t v) { GS3(i, n) p[i] = v; }
+
+// ---------------------------------------------------------------------------
+// host
+
+
+int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep, stw_log *log, int64_t *err_id) {
+  Arena ar(&ctx);
+  DevBatch b;
+  if (!stage_batch(ctx, ar, in, &b)) return ctx.rc;
+  if (b.T != 1) {
+    ctx.fail(STW_EARG, "replay takes exactly one trace");
+    return ctx.rc;
+  }
+  const bool baseline = bun == nullptr;
+  const int64_t n = b.N;
+  const long long pool = baseline ? 0 : bun->pool_size;
+  const int64_t nd = baseline ? 0 : bun->n_dec;
+  const int64_t K = baseline ? 0 : bun->n_keys;
+  *err_id = 0;
+  int64_t by = 0;
+  const int64_t *d_id = nullptr, *d_addr = nullptr, *d_size = nullptr, *sp_off = nullptr, *sp_lo = nullptr,
+                *sp_hi = nullptr;
+  const int32_t *d_ts = nullptr, *key = nullptr;
+  if (!baseline) {
+    d_id = stage(ctx, ar, bun->d_id, nd, false, &by);
+    d_addr = stage(ctx, ar, bun->d_addr, nd, false, &by);
+    d_size = stage(ctx, ar, bun->d_size, nd, false, &by);
+    d_ts = stage(ctx, ar, bun->d_ts, nd, false, &by);
+    std::vector<int64_t> off1(1, 0);
+    sp_off = stage(ctx, ar, K ? bun->sp_off : off1.data(), K + 1, false, &by);
+    int64_t nsp = K ? bun->sp_off[K] : 0;
+    sp_lo = stage(ctx, ar, bun->sp_lo, nsp, false, &by);
+    sp_hi = stage(ctx, ar, bun->sp_hi, nsp, false, &by);
+    key = stage(ctx, ar, bun->key, n, false, &by);
+    // PlanBundle.validate
+    int *bad = ar.take<int>(2);
+    if (!ctx.ok()) return ctx.rc;
+    int init[2] = {INT_MAX, INT_MAX};
+    STW_CUDA(ctx, cudaMemcpyAsync(bad, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
+    int64_t g = std::max<int64_t>(nd, K);
+    if (g > 0)
+      STW_KL(k_bundle_check, grid_for(g, 256), 256, ctx.stream, d_addr, d_size, nd, pool, (long long)bun->alignment,
+             bad, sp_off, sp_lo, sp_hi, K, bad + 1);
+    int hb[2];
+    STW_CUDA(ctx, cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, ctx.stream));
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    if (!ctx.ok()) return ctx.rc;
+    if (hb[0] != INT_MAX) {
+      int64_t k = hb[0];
+      *err_id = bun->d_id[k];
+      if (bun->d_addr[k] < 0 || bun->d_addr[k] + bun->d_size[k] > pool)
+        ctx.fail(STW_EPLAN, "decision %lld out of pool", (long long)bun->d_id[k]);
+      else
+        ctx.fail(STW_EPLAN, "decision %lld misaligned address %lld", (long long)bun->d_id[k],
+                 (long long)bun->d_addr[k]);
+      return ctx.rc;
+    }
+    if (hb[1] != INT_MAX) {
+      *err_id = hb[1];
+      ctx.fail(STW_EPLAN, "reuse entry %d outside pool", hb[1]);
+      return ctx.rc;
+    }
+  }
+  // id classes
+  long long *mm = ar.take<long long>(2);
+  int *mt = ar.take<int>(1);
+  uint64_t *k1 = ar.take<uint64_t>(2 * n + nd + 1), *k2 = ar.take<uint64_t>(2 * n + nd + 1);
+  uint64_t *k3 = ar.take<uint64_t>(2 * n + nd + 1);
+  uint32_t *perm = ar.take<uint32_t>(2 * n + nd + 1), *head = ar.take<uint32_t>(2 * n + nd + 1);
+  uint32_t *cls = ar.take<uint32_t>(2 * n + nd + 1);
+  int32_t *did = ar.take<int32_t>(n + 1), *last_of = ar.take<int32_t>(n + 1);
+  uint64_t *ukey = ar.take<uint64_t>(n + 1);
+  uint32_t *operm = ar.take<uint32_t>(2 * n + 1);
+  int32_t *apos = ar.take<int32_t>(n + 1);
+  if (!ctx.ok()) return ctx.rc;
+  long long init[2] = {LLONG_MAX, LLONG_MIN};
+  STW_CUDA(ctx, cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(mt, 0, sizeof(int), ctx.stream));
+  if (n) STW_KL(k_minmax_i64, grid_for(n, 256), 256, ctx.stream, b.id, n, mm, mm + 1);
+  if (nd) STW_KL(k_minmax_i64, grid_for(nd, 256), 256, ctx.stream, d_id, nd, mm, mm + 1);
+  if (n) STW_KL(k_max_i32, grid_for(n, 256), 256, ctx.stream, b.t_e, n, mt);
+  if (nd) STW_KL(k_max_i32, grid_for(nd, 256), 256, ctx.stream, d_ts, nd, mt);
+  long long hm[2] = {0, 0};
+  int hmt = 0;
+  STW_CUDA(ctx, cudaMemcpyAsync(hm, mm, sizeof(hm), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaMemcpyAsync(&hmt, mt, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (!ctx.ok()) return ctx.rc;
+  const long long idmin = n || nd ? hm[0] : 0;
+  const int idb = n || nd ? bitlen_u64((uint64_t)(hm[1] - hm[0])) : 0;
+  const int tb = bitlen_u64((uint64_t)hmt);
+  int64_t nu = 0;
+  if (n) {
+    STW_KL(k_id_keys, grid_for(n, 256), 256, ctx.stream, b.id, n, idmin, k1);
+    sort_perm(ctx, ar, k1, perm, n, idb);
+    STW_KL(k_heads_u64, grid_for(n, 256), 256, ctx.stream, k1, n, head);
+    device_scan<uint32_t>(ctx, ar, head, cls, n, true);
+    STW_KL(k_id_classes, grid_for(n, 256), 256, ctx.stream, perm, k1, n, cls, did, last_of, ukey);
+    uint32_t hn = 0;
+    STW_CUDA(ctx, cudaMemcpyAsync(&hn, cls + n - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx.stream));
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    nu = hn;
+    // op order: stable by id, then by (t, is_alloc)
+    STW_KL(k_op_keys_id, grid_for(2 * n, 256), 256, ctx.stream, b.id, n, idmin, k1);
+    sort_perm(ctx, ar, k1, operm, 2 * n, idb);
+    STW_KL(k_op_keys_t, grid_for(2 * n, 256), 256, ctx.stream, operm, b.t_s, b.t_e, n, k1);
+    radix_sort_pairs(ctx, ar, k1, operm, 2 * n, 0, tb + 1);
+    STW_KL(k_op_rank, grid_for(2 * n, 256), 256, ctx.stream, operm, 2 * n, apos);
+  }
+  int8_t *route = ar.take<int8_t>(n + 1);
+  int64_t *paddr = ar.take<int64_t>(n + 1);
+  if (!ctx.ok()) return ctx.rc;
+  STW_KL(k_fill_i8, grid_for(n + 1, 256), 256, ctx.stream, route, n + 1, (int8_t)(baseline ? R_ONLINE : R_MISMATCH));
+  if (!baseline && n && nd) {
+    int32_t *d_ev = ar.take<int32_t>(nd), *d_rank = ar.take<int32_t>(nd);
+    if (!ctx.ok()) return ctx.rc;
+    STW_KL(k_dec_lookup, grid_for(nd, 256), 256, ctx.stream, d_id, nd, ukey, nu, idmin, last_of, b.dyn, d_ev);
+    // queue order of decisions: (t_s, id, plan position)
+    STW_KL(k_dec_keys, grid_for(nd, 256), 256, ctx.stream, d_ts, d_id, nd, idmin, k2, k3);
+    sort_perm2(ctx, ar, k2, tb, k3, idb, perm, nd);
+    STW_KL(k_scatter_rank, grid_for(nd, 256), 256, ctx.stream, perm, nd, d_rank);
+    MatchRec M{nd, n, d_ev, d_rank, d_size, b.ps, b.size, b.dyn, apos};
+    const int64_t nr = nd + n;
+    STW_KL(k_match_keys, grid_for(nr, 256), 256, ctx.stream, M, k1, k2, k3);
+    // LSD: (side, order) then size then phase
+    sort_perm(ctx, ar, k1, perm, nr, 33);
+    STW_KL(k_gather_u64, grid_for(nr, 256), 256, ctx.stream, k2, perm, k1, nr);
+    radix_sort_pairs(ctx, ar, k1, perm, nr, 0, 64);
+    STW_KL(k_gather_u64, grid_for(nr, 256), 256, ctx.stream, k3, perm, k1, nr);
+    radix_sort_pairs(ctx, ar, k1, perm, nr, 0, 32);
+    STW_KL(k_match_heads, grid_for(nr, 256), 256, ctx.stream, perm, M, head);
+    device_scan<uint32_t>(ctx, ar, head, cls, nr, true);
+    uint32_t ng = 0;
+    STW_CUDA(ctx, cudaMemcpyAsync(&ng, cls + nr - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx.stream));
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    int64_t *gstart = ar.take<int64_t>(ng + 1);
+    int32_t *gndec = ar.take<int32_t>(ng + 1);
+    if (!ctx.ok()) return ctx.rc;
+    STW_CUDA(ctx, cudaMemsetAsync(gndec, 0, (ng + 1) * sizeof(int32_t), ctx.stream));
+    STW_KL(k_match_groups, grid_for(nr, 256), 256, ctx.stream, perm, cls, nr, nd, gstart, gndec);
+    STW_KL(k_match_assign, grid_for(nr, 256), 256, ctx.stream, perm, cls, nr, M, gstart, gndec, d_addr, route, paddr);
+  }
+  // sequential replay
+  const int64_t cap_log = 1 + 3 * n;
+  ReplayArgs R{};
+  R.n = n;
+  R.operm = operm;
+  R.id = b.id;
+  R.size = b.size;
+  R.ts = b.t_s;
+  R.te = b.t_e;
+  R.dyn = b.dyn;
+  R.did = did;
+  R.route0 = route;
+  R.paddr = paddr;
+  R.key = key;
+  R.sp_off = sp_off;
+  R.sp_lo = sp_lo;
+  R.sp_hi = sp_hi;
+  R.reuse = baseline ? 0 : bun->reuse;
+  R.baseline = baseline;
+  R.pool = pool;
+  R.plo = ar.take<int64_t>(n + 1);
+  R.phi = ar.take<int64_t>(n + 1);
+  R.pflag = ar.take<int8_t>(n + 1);
+  R.clo = ar.take<int64_t>(n + 1);
+  R.chi = ar.take<int64_t>(n + 1);
+  R.cseg = ar.take<int32_t>(n + 1);
+  R.cflag = ar.take<int8_t>(n + 1);
+  R.gflo = ar.take<int64_t>(n + 3);
+  R.gfhi = ar.take<int64_t>(n + 3);
+  R.gblo = ar.take<int64_t>(2 * n + 3);
+  R.gbhi = ar.take<int64_t>(2 * n + 3);
+  R.gbseg = ar.take<int32_t>(2 * n + 3);
+  R.sbase = ar.take<int64_t>(n + 2);
+  R.lkind = ar.take<int8_t>(cap_log);
+  R.lspace = ar.take<int8_t>(cap_log);
+  R.lroute = ar.take<int8_t>(cap_log);
+  R.lt = ar.take<int64_t>(cap_log);
+  R.lid = ar.take<int64_t>(cap_log);
+  R.lsize = ar.take<int64_t>(cap_log);
+  R.laddr = ar.take<int64_t>(cap_log);
+  R.res = ar.take<long long>(16);
+  if (!ctx.ok()) return ctx.rc;
+  STW_CUDA(ctx, cudaMemsetAsync(R.pflag, 0, n + 1, ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(R.cflag, 0, n + 1, ctx.stream));
+  STW_CUDA(ctx, cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReplaySmem));
+  {
+    int slot = prof_pre(ctx.stream);
+    k_replay<<<1, 32, kReplaySmem, ctx.stream>>>(R);
+    prof_post(ctx.stream, "k_replay", slot);
+  }
+  STW_LAUNCHED(ctx);
+  long long res[16];
+  STW_CUDA(ctx, cudaMemcpyAsync(res, R.res, sizeof(res), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (!ctx.ok()) return ctx.rc;
+  const long long nlog = res[0], err = res[1];
+  if (err) {
+    *err_id = res[2];
+    if (err == STW_ESIM)
+      ctx.fail(STW_ESIM, "planned address %lld for event %lld is occupied", res[3], res[2]);
+    else if (err == STW_ESIM + 100)
+      ctx.fail(STW_ESIM, "request %lld already live in cache", res[2]);
+    else
+      ctx.fail(STW_ESIM, baseline ? "free of unknown id %lld in cache" : "double free or free of unknown id %lld",
+               res[2]);
+    return ctx.rc;
+  }
+  // compute_metrics (sim.py:67-117)
+  rep->allocated_peak = res[4];
+  rep->reserved_peak = pool + res[5];
+  rep->pool_size = pool;
+  rep->fallback_count = res[7];
+  rep->fallback_bytes_peak = res[6];
+  rep->reuse_hits = res[8];
+  rep->mismatch_count = res[9];
+  rep->efficiency = rep->reserved_peak ? exact_div_host(rep->allocated_peak, rep->reserved_peak) : 1.0;
+  rep->fragmentation = 1.0 - rep->efficiency;
+  if (log) {
+    log->len = nlog;
+    int64_t m = std::min<int64_t>(nlog, log->cap);
+    if (m > 0) {
+      STW_CUDA(ctx, cudaMemcpyAsync(log->kind, R.lkind, m, cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(log->space, R.lspace, m, cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(log->route, R.lroute, m, cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(log->t, R.lt, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(log->id, R.lid, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(log->size, R.lsize, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(log->addr, R.laddr, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    }
+  }
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  return ctx.rc;
+}
+
+}  // namespace stw

@@ -1,5 +1,6 @@
 // Host runtime pieces shared by every entry point: error context, scratch
 // arena, device-wide scan and the stable LSD radix sort (K2).
+#include <math.h>
 #include <stdarg.h>
 #include <string.h>
 
@@ -57,6 +58,45 @@ void prof_post(cudaStream_t s, const char *name, int slot) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_pending[slot].name = name;
   cudaEventRecord(g_pending[slot].b, s);
+}
+
+// Correctly rounded a / b (Python int true division) on the host.
+double exact_div_host(unsigned long long a, unsigned long long b) {
+  if (a == 0 || b == 0) return 0.0;
+  if (a < (1ull << 53) && b < (1ull << 53)) return (double)a / (double)b;
+  unsigned long long q = a / b, r = a % b;
+  int nq = q ? 64 - __builtin_clzll(q) : 0;
+  unsigned long long mant;
+  int ex;
+  bool sticky;
+  if (nq >= 54) {
+    int sh = nq - 54;
+    mant = q >> sh;
+    sticky = (sh > 0 && (q & ((1ull << sh) - 1))) || r;
+    ex = sh;
+  } else {
+    int have = nq;
+    mant = q;
+    ex = 0;
+    while (have < 54) {
+      bool carry = (r >> 63) != 0;
+      r <<= 1;
+      unsigned long long bit = 0;
+      if (carry || r >= b) {
+        r -= b;
+        bit = 1;
+      }
+      mant = (mant << 1) | bit;
+      ex -= 1;
+      if (have > 0 || bit) have++;
+    }
+    sticky = r != 0;
+  }
+  bool rnd = mant & 1;
+  mant >>= 1;
+  ex += 1;
+  if (rnd && (sticky || (mant & 1))) mant += 1;
+  return ldexp((double)mant, ex);
 }
 
 void Ctx::fail(int code, const char *fmt, ...) {

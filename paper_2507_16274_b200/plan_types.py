@@ -216,3 +216,56 @@ class StaticPlan:
 
     def __repr__(self) -> str:
         return f"StaticPlan(pool_size={self.pool_size}, decisions=<{len(self.columns())}>)"
+
+
+@dataclass(frozen=True)
+class ReuseEntry:
+    """Reusable space of one dynamic (alloc layer, free layer) group (reuse.py:21-25)."""
+
+    t_lo: int
+    t_hi: int
+    space: IntervalSet
+
+
+@dataclass(frozen=True)
+class ReuseMap:
+    """One entry per dynamic reuse key, keys in sorted order (reuse.py:28-39)."""
+
+    entries: dict
+
+    def spaces(self) -> dict:
+        return {key: entry.space for key, entry in self.entries.items()}
+
+    def __contains__(self, key) -> bool:
+        return key in self.entries
+
+    def get(self, key):
+        return self.entries.get(key)
+
+
+@dataclass(frozen=True)
+class SimReport:
+    """Replay outcome (sim.py:39-64)."""
+
+    allocated_peak: int
+    reserved_peak: int
+    efficiency: float
+    fragmentation: float
+    pool_size: int
+    fallback_count: int
+    fallback_bytes_peak: int
+    reuse_hits: int
+    mismatch_count: int
+
+    def to_dict(self) -> dict:
+        return {
+            "allocated_peak": self.allocated_peak,
+            "reserved_peak": self.reserved_peak,
+            "efficiency": self.efficiency,
+            "fragmentation": self.fragmentation,
+            "pool_size": self.pool_size,
+            "fallback_count": self.fallback_count,
+            "fallback_bytes_peak": self.fallback_bytes_peak,
+            "reuse_hits": self.reuse_hits,
+            "mismatch_count": self.mismatch_count,
+        }

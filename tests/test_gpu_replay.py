@@ -1,0 +1,119 @@
+"""Reuse map (K8), replay scorer (K9) and caching-allocator baseline (K10):
+libstw vs the C oracle, bit-exact (reports, every log record, every interval)."""
+
+import numpy as np
+import pytest
+
+from paper_2507_16274_b200 import api, tracegen
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KIND = {0: "init", 1: "reserve", 2: "alloc", 3: "free"}
+
+
+def fuzz_cfg(seed):
+    preset = tracegen.PRESETS[seed % 6]
+    return tracegen.SynthConfig.for_preset(preset, seed=seed, num_layers=4 + seed % 9,
+                                          num_microbatches=1 + seed % 4, transient_ratio=0.2 + (seed % 5) * 0.2)
+
+
+def oracle_inputs(ta, bundle):
+    names, kidx = ta.dynamic_keys()
+    bkeys = list(bundle.reuse)
+    pos = {k: i for i, k in enumerate(bkeys)}
+    key = np.array([pos.get(names[k], -1) if k >= 0 else -1 for k in kidx], np.int32)
+    off, lo, hi = [0], [], []
+    for k in bkeys:
+        for iv in bundle.reuse[k]:
+            lo.append(iv.lo)
+            hi.append(iv.hi)
+        off.append(len(lo))
+    c = bundle._cols
+    return key, (c.id, c.addr, c.size, c.t_s, c.t_e), off, lo, hi
+
+
+def oracle_log_dicts(lg, ta):
+    evkey = {int(ta.id[i]): [ta.layer_names[ta.ls[i]], ta.layer_names[ta.le[i]]] for i in np.nonzero(ta.dyn)[0]}
+    routes = ("planned", "reuse", "fallback", "mismatch", "online")
+    out = []
+    for k in range(len(lg["kind"])):
+        kind = KIND[int(lg["kind"][k])]
+        if kind == "init":
+            out.append({"kind": "init", "pool_size": int(lg["size"][k])})
+        elif kind == "reserve":
+            out.append({"kind": "reserve", "t": int(lg["t"][k]), "bytes": int(lg["size"][k])})
+        else:
+            r = {"kind": kind, "t": int(lg["t"][k]), "id": int(lg["id"][k]), "size": int(lg["size"][k]),
+                 "space": "pool" if lg["space"][k] == 0 else "cache", "addr": int(lg["addr"][k])}
+            if kind == "alloc":
+                r["route"] = routes[int(lg["route"][k])]
+                if r["id"] in evkey:
+                    r["key"] = evkey[r["id"]]
+            out.append(r)
+    return out
+
+
+def check_trace(ta, reuse_flags=(True, False)):
+    tr = api.Trace.from_arrays(ta) if hasattr(api, "Trace") else None
+    from paper_2507_16274_b200.domain import Trace
+
+    tr = Trace.from_arrays(ta)
+    plan, rmap = api.plan_trace(tr)
+    cols = plan.columns()
+    # K8 vs oracle
+    keys = list(rmap.entries)
+    if keys:
+        t_lo = [rmap.entries[k].t_lo for k in keys]
+        t_hi = [rmap.entries[k].t_hi for k in keys]
+        off, lo, hi = O.reuse(cols.addr, cols.size, cols.t_s, cols.t_e, t_lo, t_hi)
+        for i, k in enumerate(keys):
+            got = [(iv.lo, iv.hi) for iv in rmap.entries[k].space]
+            assert got == list(zip(lo[off[i]:off[i + 1]].tolist(), hi[off[i]:off[i + 1]].tolist())), k
+    bundle = plan.to_bundle(rmap)
+    key, dcols, off, lo, hi = oracle_inputs(ta, bundle)
+    for reuse in reuse_flags:
+        rep, log = api.simulate(tr, bundle, reuse=reuse)
+        o = O.simulate(ta, key, bundle.pool_size, bundle.alignment, *dcols, off, lo, hi, reuse)
+        assert o.rc == 0, o.err
+        assert rep.to_dict() == o.report
+        assert list(log) == oracle_log_dicts(o.log, ta)
+    b = api.run_baseline(tr)
+    ob = O.baseline(ta)
+    assert b.to_dict() == ob.report
+    return rep
+
+
+def test_replay_fuzz():
+    for s in range(48):
+        check_trace(tracegen.synth_arrays(fuzz_cfg(s)))
+
+
+@pytest.mark.parametrize("name", ["c1_llama2_7b_1f1b", "c3_mixtral_moe", "c3b_mixtral_moe_rcp"])
+def test_replay_configs(name):
+    check_trace(tracegen.synth_arrays(tracegen.config(name)), (True,))
+
+
+def test_replay_c2():
+    check_trace(tracegen.synth_arrays(tracegen.config("c2_llama2_7b_vpp_rcp")), (True,))
+
+
+def test_replay_mismatch_and_occupied():
+    from paper_2507_16274_b200.domain import MemoryRequestEvent, PhaseId, PhaseSpan, SimulationError, Trace
+    from paper_2507_16274_b200.plan_types import PlanBundle, PlanDecision
+
+    U = 512
+    F, B = PhaseId.parse("F:0"), PhaseId.parse("B:0")
+    sched = (PhaseSpan(F, 0, 3), PhaseSpan(B, 3, 6))
+    base = Trace((MemoryRequestEvent(0, 8 * U, 0, 4, F, B), MemoryRequestEvent(1, 4 * U, 1, 3, F, F)), sched)
+    plan, rmap = api.plan_trace(base)
+    injected = Trace(base.events + (MemoryRequestEvent(2, 16 * U, 2, 5, F, B),), sched)
+    rep, log = api.simulate(injected, plan.to_bundle(rmap))  # test_sim.py:33-52
+    assert rep.mismatch_count == 1 and rep.fallback_count == 1
+    routes = {r["id"]: r["route"] for r in log if r["kind"] == "alloc"}
+    assert routes == {0: "planned", 1: "planned", 2: "mismatch"}
+    tr = Trace((MemoryRequestEvent(0, 8 * U, 0, 2, F, B), MemoryRequestEvent(1, 8 * U, 1, 3, F, B)),
+               (PhaseSpan(F, 0, 2), PhaseSpan(B, 2, 4)))
+    corrupt = PlanBundle(16 * U, U, (PlanDecision(0, 0, 8 * U, 0, 2), PlanDecision(1, 0, 8 * U, 1, 3)), {})
+    with pytest.raises(SimulationError, match="occupied"):  # test_sim.py:92-104
+        api.simulate(tr, corrupt)
