@@ -11,6 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libstw.so")
+ALLOC_LIB = os.path.join(PKG, "libstw_alloc.so")
+ALLOC_SRC = os.path.join(PKG, "csrc_alloc", "stw_alloc.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
@@ -34,7 +36,26 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build failed: {cmd[-1]}")
+
+
+def build_alloc(force: bool = False, verbose: bool = False) -> str:
+    """libstw_alloc.so: the CUDAPluggableAllocator (host C++ + cudart)."""
+    deps = [ALLOC_SRC, os.path.join(ROOT, "include", "stw_alloc.h"), os.path.join(ROOT, "include", "stw.h")]
+    if force or not os.path.exists(ALLOC_LIB) or any(os.path.getmtime(p) > os.path.getmtime(ALLOC_LIB) for p in deps):
+        _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+              "-I" + os.path.join(ROOT, "include"), "-o", ALLOC_LIB, ALLOC_SRC], verbose)
+    return ALLOC_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_alloc(force, verbose)
     if force or stale():
         cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *sources()]
         if verbose:

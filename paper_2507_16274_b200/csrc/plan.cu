@@ -130,6 +130,81 @@ void sort_perm2(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, uint64_t *lo, int
   radix_sort_pairs(ctx, ar, lo, perm, n, 0, hibits);
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-local segmented sort: one CTA per segment (trace or (variant, trace)),
+// bitonic network over (key, index) pairs in shared memory -- a stable sort of
+// the segment in one global read + write. Used whenever every segment fits
+// kSegSortMax elements; otherwise the global LSD radix sort (K2) runs.
+
+constexpr int kSegSortMax = 4096;
+
+__global__ void k_local_key(uint64_t *__restrict__ hi, const uint64_t *__restrict__ lo, uint64_t mask, int lobits,
+                            int64_t n) {
+  GRID_STRIDE(i, n) hi[i] = (lobits >= 64 ? 0 : ((hi[i] & mask) << lobits)) | lo[i];
+}
+
+__global__ void k_seg_bitonic(uint64_t *__restrict__ keys, uint32_t *__restrict__ perm,
+                              const int64_t *__restrict__ seg_off, int pcap) {
+  extern __shared__ uint64_t sk[];
+  const int64_t s0 = seg_off[blockIdx.x];
+  const int n = (int)(seg_off[blockIdx.x + 1] - s0);
+  if (n == 0) return;
+  int P = 1;
+  while (P < n) P <<= 1;
+  uint32_t *sv = (uint32_t *)(sk + pcap);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    sk[i] = i < n ? keys[s0 + i] : ~0ull;
+    sv[i] = i < n ? (uint32_t)(s0 + i) : ~0u;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        int a = 2 * j * (i / j) + (i % j), b = a + j;
+        bool asc = (a & k) == 0;
+        uint64_t ka = sk[a], kb = sk[b];
+        uint32_t va = sv[a], vb = sv[b];
+        bool gt = ka > kb || (ka == kb && va > vb);
+        if (gt == asc) {
+          sk[a] = kb;
+          sk[b] = ka;
+          sv[a] = vb;
+          sv[b] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    keys[s0 + i] = sk[i];
+    perm[s0 + i] = sv[i];
+  }
+}
+
+// Stable sort of n elements by (segment, hi & ~segment bits, lo), segments
+// given by seg_off[nseg+1] (device) and contiguous. hi/lo are consumed.
+static void seg_sort(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, int segbits, uint64_t *lo, int lobits,
+                     uint32_t *perm, int64_t n, const int64_t *seg_off, int64_t nseg, int64_t max_seg) {
+  if (!ctx.ok() || n == 0) return;
+  const int local_hi = hibits - segbits;
+  if (max_seg <= kSegSortMax && local_hi + lobits <= 64) {
+    uint64_t mask = local_hi >= 64 ? ~0ull : ((1ull << local_hi) - 1);
+    STW_KL(k_local_key, grid_for(n, 256), 256, ctx.stream, hi, lo, mask, lobits, n);
+    int P = 1;
+    while (P < max_seg) P <<= 1;
+    int threads = std::max(32, std::min(256, P / 2));
+    size_t smem = (size_t)P * 12;
+    STW_CUDA(ctx, cudaFuncSetAttribute(k_seg_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int slot = prof_pre(ctx.stream);
+    k_seg_bitonic<<<(unsigned)nseg, threads, smem, ctx.stream>>>(hi, perm, seg_off, P);
+    prof_post(ctx.stream, "k_seg_bitonic", slot);
+    STW_LAUNCHED(ctx);
+    return;
+  }
+  sort_perm2(ctx, ar, hi, hibits, lo, lobits, perm, n);
+}
+
 // rank[perm[k]] = k - ev_off[trace]; optional per-trace local permutation
 __global__ void k_rank_from_perm(const uint32_t *__restrict__ perm, const int32_t *__restrict__ tr,
                                  const int64_t *__restrict__ ev_off, int64_t n, int32_t *__restrict__ rank,
@@ -1057,7 +1132,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A, const int3
 // than kWL layers is handed to the CTA kernel (appended to `over`).
 
 constexpr int kWL = 64;
-constexpr int kWarpsPerCTA = 4;
 
 __device__ __forceinline__ int warp_excl_scan(int v, int *total) {
   int inc = warp_incl_sum(v);
@@ -1065,105 +1139,138 @@ __device__ __forceinline__ int warp_excl_scan(int v, int *total) {
   return inc - v;
 }
 
-__global__ void __launch_bounds__(kWarpsPerCTA * 32) k_layers_warp(LayerArgs A, const int32_t *__restrict__ ulist,
-                                                                   int nunits, int cap, int32_t *__restrict__ over,
-                                                                   int *__restrict__ nover) {
+// per-warp shared-memory footprint (ints) of k_layers_warp for a unit capacity
+__host__ __device__ constexpr int warp_smem_ints(int cap) { return 9 * cap + 5 * (kWL + 1); }
+
+// Register-resident resolve state: lane p holds the same-class "last end" of
+// the layer at priority p (and p+32), the end of the class's new layer p (and
+// p+32), and the class insertion counter of layer id p (and p+32). The per-item
+// step is shuffles, ballots and one max-reduction -- no shared memory traffic.
+__global__ void __launch_bounds__(256) k_layers_warp(LayerArgs A, const int32_t *__restrict__ ulist, int nunits,
+                                                     int cap, int32_t *__restrict__ over, int *__restrict__ nover) {
   extern __shared__ int32_t smem[];
   const int w = threadIdx.x >> 5, lane = lane_id();
-  const int ui = blockIdx.x * kWarpsPerCTA + w;
+  const int ui = blockIdx.x * (blockDim.x >> 5) + w;
   if (ui >= nunits) return;
   const int u = ulist[ui];
   const int c = u % A.C, t = u / A.C;
   const int v = A.var_of[c];
   const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
   const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
+  const int n = (int)(a1 - a0);
   const int64_t off = A.uo[u];
-  const int per_warp = 6 * cap + 8 * (kWL + 1);
-  int32_t *sm = smem + w * per_warp;
-  int32_t *sAts = sm, *sAte = sm + cap, *sBts = sm + 2 * cap, *sBte = sm + 3 * cap;
+  int32_t *sm = smem + w * warp_smem_ints(cap);
+  int32_t *sts = sm, *ste = sm + cap, *tts = sm + 2 * cap, *tte = sm + 3 * cap;  // slots + merge temp
   int32_t *run_ts = sm + 4 * cap, *run_te = sm + 5 * cap;
-  int32_t *loffA = sm + 6 * cap, *loffB = loffA + (kWL + 1), *prioA = loffB + (kWL + 1), *prioB = prioA + (kWL + 1);
-  int32_t *last = prioB + (kWL + 1), *nend = last + (kWL + 1), *newcnt = nend + (kWL + 1), *runoff = newcnt + (kWL + 1);
-  int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
+  int32_t *ilayer = sm + 6 * cap, *irank = sm + 7 * cap, *icend = sm + 8 * cap;
+  int32_t *loffA = sm + 9 * cap, *loffB = loffA + (kWL + 1), *prioA = loffB + (kWL + 1), *prioB = prioA + (kWL + 1);
+  int32_t *newcnt = prioB + (kWL + 1);
+  const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
   int64_t *lsize = A.lsize + off;
+  for (int x = lane; x < n; x += 32) icend[x] = (int)(A.cend[a0 + x] - a0);
   if (lane == 0) loffA[0] = 0;
   int nl = 0;
   long long gapc = 0;
   __syncwarp();
-  for (int64_t j0 = a0; j0 < a1;) {
-    const int64_t j1 = A.cend[j0];
-    const int m = (int)(j1 - j0);
-    const int64_t S = A.it.size[j0];
-    for (int p = lane; p < kWL; p += 32) {
-      newcnt[p] = 0;
-      last[p] = INT_MIN;
-    }
-    __syncwarp();
+  for (int j0 = 0; j0 < n;) {
+    const int j1 = icend[j0];
+    const int m = j1 - j0;
+    const int64_t S = A.it.size[a0 + j0];
+    int lastA = INT_MIN, lastB = INT_MIN, neA = INT_MIN, neB = INT_MIN, cntA = 0, cntB = 0;
+    const int prA = lane < nl ? prioA[lane] : 0, prB = lane + 32 < nl ? prioA[lane + 32] : 0;
     int nnew = 0;
-    for (int64_t cb = j0; cb < j1; cb += 32) {
-      const int64_t mine = cb + lane;
-      int my_ts = 0, my_te = 0;
+    for (int cb = j0; cb < j1; cb += 32) {
+      const int mine = cb + lane;
+      int my_ts = 0, my_te = 0, my_layer = 0, my_rank = 0;
       unsigned long long fm = 0;
       if (mine < j1) {
-        my_ts = A.it.ts[mine];
-        my_te = A.it.te[mine];
+        my_ts = gts[mine];
+        my_te = gte[mine];
         if (gap)
           for (int p = 0; p < nl; p++) {
             int l = prioA[p];
-            if (slot_fit(sAts, sAte, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1ull << p;
+            if (slot_fit(sts, ste, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1ull << p;
           }
       }
-      const int cnt = (int)min((int64_t)32, j1 - cb);
+      const int cnt = min(32, j1 - cb);
       for (int k = 0; k < cnt; k++) {
         const int ts = __shfl_sync(0xffffffffu, my_ts, k), te = __shfl_sync(0xffffffffu, my_te, k);
-        const unsigned long long f = __shfl_sync(0xffffffffu, fm, k);
         int host_p = -1;
         if (gap && nl > 0) {
-          bool ok1 = lane < nl && ((f >> lane) & 1ull) && last[lane] < ts;
-          bool ok2 = lane + 32 < nl && ((f >> (lane + 32)) & 1ull) && last[lane + 32] < ts;
-          unsigned m1 = __ballot_sync(0xffffffffu, ok1), m2 = __ballot_sync(0xffffffffu, ok2);
-          host_p = m1 ? __ffs(m1) - 1 : (m2 ? 32 + __ffs(m2) - 1 : -1);
+          const unsigned long long f = __shfl_sync(0xffffffffu, fm, k);
+          unsigned m1 = __ballot_sync(0xffffffffu, lane < nl && ((f >> lane) & 1ull) && lastA < ts);
+          if (m1) {
+            host_p = __ffs(m1) - 1;
+          } else if (nl > 32) {
+            unsigned m2 = __ballot_sync(0xffffffffu, lane + 32 < nl && ((f >> (lane + 32)) & 1ull) && lastB < ts);
+            if (m2) host_p = 32 + __ffs(m2) - 1;
+          }
         }
         int layer;
         if (host_p >= 0) {
-          layer = prioA[host_p];
-          if (lane == 0) last[host_p] = te;
-          gapc++;
-        } else {
-          int best_k = -1, best_e = INT_MIN;
-#pragma unroll
-          for (int kb = 0; kb < kWL; kb += 32) {
-            int kk = kb + lane;
-            int e = kk < nnew ? nend[kk] : INT_MIN;
-            bool cand = kk < nnew && e < ts;
-            int mx = __reduce_max_sync(0xffffffffu, cand ? e : INT_MIN);
-            unsigned cm = __ballot_sync(0xffffffffu, cand && e == mx);
-            if (cm && (best_k < 0 || mx > best_e)) {
-              best_e = mx;
-              best_k = kb + __ffs(cm) - 1;
-            }
+          const int la = __shfl_sync(0xffffffffu, prA, host_p & 31), lb = __shfl_sync(0xffffffffu, prB, host_p & 31);
+          layer = host_p < 32 ? la : lb;
+          if (lane == (host_p & 31)) {
+            if (host_p < 32)
+              lastA = te;
+            else
+              lastB = te;
           }
-          if (best_k < 0) {
-            if (nl + nnew == kWL) {  // too many layers for the warp path
+          gapc++;
+        } else {  // Alg. 1: new layer of this class with the largest end < ts, ties to the oldest
+          const bool ca = lane < nnew && neA < ts;
+          const int mxa = __reduce_max_sync(0xffffffffu, ca ? neA : INT_MIN);
+          const unsigned cma = __ballot_sync(0xffffffffu, ca && neA == mxa);
+          int best = cma ? __ffs(cma) - 1 : -1, best_e = mxa;
+          if (nnew > 32) {
+            const bool cbb = lane + 32 < nnew && neB < ts;
+            const int mxb = __reduce_max_sync(0xffffffffu, cbb ? neB : INT_MIN);
+            const unsigned cmb = __ballot_sync(0xffffffffu, cbb && neB == mxb);
+            if (cmb && (best < 0 || mxb > best_e)) best = 32 + __ffs(cmb) - 1;
+          }
+          if (best < 0) {
+            if (nl + nnew == kWL) {  // too many layers for the warp path: the CTA kernel redoes the unit
               if (lane == 0) over[atomicAdd(nover, 1)] = u;
               return;
             }
-            best_k = nnew++;
-            if (lane == 0) newcnt[nl + best_k] = 0;
+            best = nnew++;
           }
-          if (lane == 0) nend[best_k] = te;
-          layer = nl + best_k;
+          if (lane == (best & 31)) {
+            if (best < 32)
+              neA = te;
+            else
+              neB = te;
+          }
+          layer = nl + best;
         }
-        if (lane == 0) {
-          ilayer[cb + k - a0] = layer;
-          irank[cb + k - a0] = newcnt[layer]++;
+        const int ra = __shfl_sync(0xffffffffu, cntA, layer & 31), rb = __shfl_sync(0xffffffffu, cntB, layer & 31);
+        const int rank = layer < 32 ? ra : rb;
+        if (lane == (layer & 31)) {
+          if (layer < 32)
+            cntA++;
+          else
+            cntB++;
         }
-        __syncwarp();
+        if (lane == k) {
+          my_layer = layer;
+          my_rank = rank;
+        }
+      }
+      if (mine < j1) {
+        ilayer[mine] = my_layer;
+        irank[mine] = my_rank;
       }
     }
-    // merge the class's slots into the CSR (sA -> sB)
+    // ---- merge the class into the layer-major slot CSR
     const int nl2 = nl + nnew;
     for (int x = lane; x < nnew; x += 32) lsize[nl + x] = S;
+    newcnt[lane] = cntA;
+    newcnt[lane + 32] = cntB;
+    __syncwarp();
+    // first old layer that received gap insertions (slots before it keep their place)
+    unsigned tm1 = __ballot_sync(0xffffffffu, lane < nl && cntA > 0);
+    unsigned tm2 = __ballot_sync(0xffffffffu, lane + 32 < nl && cntB > 0);
+    const int first = tm1 ? __ffs(tm1) - 1 : (tm2 ? 32 + __ffs(tm2) - 1 : nl);
     {
       int carry = 0, carry2 = 0;
       for (int base = 0; base < nl2; base += 32) {
@@ -1174,57 +1281,82 @@ __global__ void __launch_bounds__(kWarpsPerCTA * 32) k_layers_warp(LayerArgs A, 
         int ex = warp_excl_scan(cnt_all, &tot), ex2 = warp_excl_scan(cnt_new, &tot2);
         if (l < nl2) {
           loffB[l] = carry + ex;
-          runoff[l] = carry2 + ex2;
+          prioB[l] = carry2 + ex2;  // prioB doubles as run offsets until the priority update below
         }
         carry += tot;
         carry2 += tot2;
       }
-      if (lane == 0) {
-        loffB[nl2] = carry;
-        runoff[nl2] = carry2;
+      if (lane == 0) loffB[nl2] = carry;
+    }
+    __syncwarp();
+    const int32_t *runoff = prioB;
+    const int s0 = loffA[first > nl ? nl : first];
+    const int nold = nl > 0 ? loffA[nl] : 0;
+    if (first < nl) {
+      for (int x = lane; x < m; x += 32) {
+        int l = ilayer[j0 + x];
+        int pos = runoff[l] + irank[j0 + x];
+        run_ts[pos] = gts[j0 + x];
+        run_te[pos] = gte[j0 + x];
+      }
+      __syncwarp();
+      for (int sidx = s0 + lane; sidx < nold; sidx += 32) {
+        int lo = first, hi = nl;  // layer of slot sidx
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (loffA[mid] <= sidx)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        int l = lo;
+        while (loffA[l + 1] <= sidx) l++;
+        int ts = sts[sidx];
+        int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
+        int dst = loffB[l] + (sidx - loffA[l]) + k - s0;
+        tts[dst] = ts;
+        tte[dst] = ste[sidx];
       }
     }
-    __syncwarp();
     for (int x = lane; x < m; x += 32) {
-      int l = ilayer[j0 - a0 + x];
-      int pos = runoff[l] + irank[j0 - a0 + x];
-      run_ts[pos] = A.it.ts[j0 + x];
-      run_te[pos] = A.it.te[j0 + x];
+      int l = ilayer[j0 + x];
+      int ts = gts[j0 + x];
+      int k = l < nl ? lower_bound_i32(sts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
+      int dst = loffB[l] + irank[j0 + x] + k - s0;
+      tts[dst] = ts;
+      tte[dst] = gte[j0 + x];
     }
     __syncwarp();
-    const int nold = nl > 0 ? loffA[nl] : 0;
-    for (int sidx = lane; sidx < nold; sidx += 32) {
-      int l = 0;
-      while (loffA[l + 1] <= sidx) l++;
-      int ts = sAts[sidx];
-      int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
-      int dst = loffB[l] + (sidx - loffA[l]) + k;
-      sBts[dst] = ts;
-      sBte[dst] = sAte[sidx];
+    const int ntail = loffB[nl2] - s0;
+    for (int x = lane; x < ntail; x += 32) {
+      sts[s0 + x] = tts[x];
+      ste[s0 + x] = tte[x];
     }
-    for (int x = lane; x < m; x += 32) {
-      int l = ilayer[j0 - a0 + x];
-      int ts = run_ts[runoff[l] + irank[j0 - a0 + x]];
-      int te = run_te[runoff[l] + irank[j0 - a0 + x]];
-      int k = l < nl ? lower_bound_i32(sAts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
-      int dst = loffB[l] + irank[j0 - a0 + x] + k;
-      sBts[dst] = ts;
-      sBte[dst] = te;
-    }
-    for (int x = lane; x < nl2; x += 32) prioB[x] = x < nnew ? nl + x : prioA[x - nnew];
-    __syncwarp();
+    // priority order for later classes: newest (smallest) layers first, creation order within
     {
-      int32_t *tp;
-      tp = sAts, sAts = sBts, sBts = tp;
-      tp = sAte, sAte = sBte, sBte = tp;
-      tp = loffA, loffA = loffB, loffB = tp;
-      tp = prioA, prioA = prioB, prioB = tp;
+      int pa = lane < nl ? prioA[lane] : 0, pb = lane + 32 < nl ? prioA[lane + 32] : 0;
+      __syncwarp();
+      // write new priorities: first nnew are the new layers, then the old list shifted
+      int old0 = lane - nnew, old1 = lane + 32 - nnew;
+      int v0 = 0, v1 = 0;
+      {
+        int sA = __shfl_sync(0xffffffffu, pa, old0 & 31), sB = __shfl_sync(0xffffffffu, pb, old0 & 31);
+        v0 = lane < nnew ? nl + lane : (old0 < 32 ? sA : sB);
+        int tA = __shfl_sync(0xffffffffu, pa, old1 & 31), tB = __shfl_sync(0xffffffffu, pb, old1 & 31);
+        v1 = lane + 32 < nnew ? nl + lane + 32 : (old1 < 32 ? tA : tB);
+      }
+      if (lane < nl2) prioA[lane] = v0;
+      if (lane + 32 < nl2) prioA[lane + 32] = v1;
     }
+    for (int x = lane; x <= nl2; x += 32) loffA[x] = loffB[x];
+    __syncwarp();
     nl = nl2;
     j0 = j1;
   }
+  for (int x = lane; x < n; x += 32) A.ilayer[off + x] = ilayer[x];
   // stacking (planner.py:441-444)
   int64_t *lbase = A.lbase + off;
+  __syncwarp();
   long long carry = A.pers_size[t];
   for (int base = 0; base < nl; base += 32) {
     int l = base + lane;
@@ -1436,6 +1568,19 @@ __global__ void k_scatter_fusions(const int32_t *__restrict__ ptr, const int64_t
 // ---------------------------------------------------------------------------
 // host orchestration
 
+// Per-thread cache of forked streams/events for concurrent launches inside one
+// call (created once per host thread, reused; the call stays synchronous).
+static cudaStream_t side_stream(int i) {
+  thread_local cudaStream_t s[8] = {};
+  if (!s[i]) cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking);
+  return s[i];
+}
+static cudaEvent_t side_event(int i) {
+  thread_local cudaEvent_t e[8] = {};
+  if (!e[i]) cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming);
+  return e[i];
+}
+
 template <class T>
 static void d2h(Ctx &ctx, std::vector<T> &h, const T *d, int64_t n) {
   h.resize(n);
@@ -1534,11 +1679,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   const int tsb = bitlen_u64((uint64_t)him[0]);
   // q: id rank within trace
   LAUNCH(k_key_q, N, tr, b.id, N, hmm[0], khi, klo);
-  sort_perm2(ctx, ar, khi, tb, klo, idb, perm, N);
+  seg_sort(ctx, ar, khi, tb, tb, klo, idb, perm, N, b.ev_off, T, b.max_trace_events);
   LAUNCH(k_rank_from_perm, N, perm, tr, b.ev_off, N, q, (int32_t *)nullptr);
   // r: (t_s, id) rank within trace
   LAUNCH(k_key_r, N, tr, b.t_s, q, N, qb, khi, klo);
-  sort_perm2(ctx, ar, khi, tb, klo, tsb + qb, rperm, N);
+  seg_sort(ctx, ar, khi, tb, tb, klo, tsb + qb, rperm, N, b.ev_off, T, b.max_trace_events);
   LAUNCH(k_rank_from_perm, N, rperm, tr, b.ev_off, N, r, order_local);
 
   pt.mark("A ranks");
@@ -1562,7 +1707,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
   LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
-  sort_perm2(ctx, ar, khi, tb + 2 + 2 * pb, klo, qb, gperm, N);
+  seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events);
   uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
   int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
   int64_t *rel = ar.take<int64_t>(N + 1);
@@ -1726,7 +1871,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     return ctx.rc;
   }
   LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, (long long)o->alignment, maxsu, sb, ihi, ilo);
-  sort_perm2(ctx, ar, ihi, vtb + sb, ilo, tsb + qb, iperm, NI);
+  {
+    int64_t max_items = 0;
+    for (int64_t x = 0; x < V * T; x++) max_items = std::max(max_items, io[x + 1] - io[x]);
+    seg_sort(ctx, ar, ihi, vtb + sb, vtb, ilo, tsb + qb, iperm, NI, d_io, (int64_t)V * T, max_items);
+  }
   LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
   pt.mark("D sort");
   // classes
@@ -1775,6 +1924,10 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       while (bk < NBK && n_u > caps[bk]) bk++;
       lists[bk].push_back((int32_t)u);
     }
+    // largest units first inside each bucket (shortest tail)
+    for (auto &lst : lists)
+      std::stable_sort(lst.begin(), lst.end(),
+                       [&](int32_t x, int32_t y) { return uo[x + 1] - uo[x] > uo[y + 1] - uo[y]; });
     std::vector<int32_t> flat;
     std::vector<int64_t> loff(NBK + 2, 0);
     for (int bk = 0; bk <= NBK; bk++) {
@@ -1787,17 +1940,28 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     if (!ctx.ok()) return ctx.rc;
     STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, sizeof(int), ctx.stream));
     const int64_t nsmall = loff[NBK];
-    for (int bk = 0; bk < NBK && ctx.ok(); bk++) {
+    // the buckets run concurrently on forked streams (largest buckets first)
+    cudaEvent_t fork_ev = side_event(0), join_ev[NBK];
+    STW_CUDA(ctx, cudaEventRecord(fork_ev, ctx.stream));
+    for (int bk = NBK - 1; bk >= 0 && ctx.ok(); bk--) {
       int nb = (int)(loff[bk + 1] - loff[bk]);
+      join_ev[bk] = nullptr;
       if (!nb) continue;
-      size_t smem = (size_t)kWarpsPerCTA * (6 * caps[bk] + 8 * (kWL + 1)) * sizeof(int32_t);
+      cudaStream_t st = side_stream(bk);
+      STW_CUDA(ctx, cudaStreamWaitEvent(st, fork_ev, 0));
+      size_t per_warp = (size_t)warp_smem_ints(caps[bk]) * sizeof(int32_t);
+      int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp));
+      size_t smem = per_warp * wpc;
       STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int prof = prof_pre(ctx.stream);
-      k_layers_warp<<<(nb + kWarpsPerCTA - 1) / kWarpsPerCTA, kWarpsPerCTA * 32, smem, ctx.stream>>>(
-          LA, d_list + loff[bk], nb, caps[bk], d_over, d_nover);
-      prof_post(ctx.stream, "k_layers_warp", prof);
+      int prof = prof_pre(st);
+      k_layers_warp<<<(nb + wpc - 1) / wpc, wpc * 32, smem, st>>>(LA, d_list + loff[bk], nb, caps[bk], d_over, d_nover);
+      prof_post(st, "k_layers_warp", prof);
       STW_LAUNCHED(ctx);
+      join_ev[bk] = side_event(1 + bk);
+      STW_CUDA(ctx, cudaEventRecord(join_ev[bk], st));
     }
+    for (int bk = 0; bk < NBK; bk++)
+      if (loff[bk + 1] > loff[bk] && join_ev[bk]) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, join_ev[bk], 0));
     int nbig = (int)(loff[NBK + 1] - loff[NBK]);
     if (nbig) {
       STW_KL(k_layers, (unsigned)nbig, kPlanThreads, ctx.stream, LA, d_list + loff[NBK], (const int *)nullptr);
