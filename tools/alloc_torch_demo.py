@@ -40,6 +40,7 @@ for o in np.lexsort((ids, is_alloc, t)).tolist():
         if route == "planned":
             assert v == planned[int(ta.id[e])], (e, v)
             checked += 1
+        del x  # the trace's free must release the last tensor too
     else:
         del live[e]
 torch.cuda.synchronize()
