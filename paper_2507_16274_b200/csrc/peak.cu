@@ -28,10 +28,11 @@ __global__ void k_timeline_scatter(const int64_t *__restrict__ ev_off, int T, in
                                    const int64_t *__restrict__ size, const int32_t *__restrict__ t_s,
                                    const int32_t *__restrict__ t_e, const uint8_t *__restrict__ dyn,
                                    const int64_t *__restrict__ tl_off, unsigned long long *__restrict__ D,
-                                   int static_only) {
+                                   int static_only, const uint8_t *__restrict__ only) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     if (static_only && dyn[i]) continue;
     int t = trace_of(ev_off, T, i);
+    if (!only[t]) continue;
     int64_t o = tl_off[t];
     unsigned long long s = (unsigned long long)size[i];
     atomicAdd(D + o + t_s[i], s);
@@ -39,10 +40,15 @@ __global__ void k_timeline_scatter(const int64_t *__restrict__ ev_off, int T, in
   }
 }
 
+__global__ void k_zero_selected(const uint8_t *__restrict__ only, int T, int64_t *__restrict__ peak) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
+    if (only[t]) peak[t] = 0;
+}
+
 // per-segment max of the scanned timeline; each thread walks 8 consecutive
 // entries and flushes one atomicMax per trace it touched
 __global__ void k_segmax(const int64_t *__restrict__ P, int64_t H, const int64_t *__restrict__ tl_off, int T,
-                         long long *__restrict__ peak) {
+                         long long *__restrict__ peak) {  // peak[t] of the recomputed traces is pre-zeroed
   int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8;
   if (i0 >= H) return;
   int t = trace_of(tl_off, T, i0);
@@ -59,7 +65,107 @@ __global__ void k_segmax(const int64_t *__restrict__ P, int64_t H, const int64_t
   if (best > 0) atomicMax(peak + t, best);
 }
 
+// One CTA per trace whose timeline fits in shared memory (every c4 trace):
+// deltas by shared-memory atomics, then each thread scans a contiguous chunk
+// (local prefix + local max), one block scan of the chunk sums, and the peak
+// is max(excl + local max) -- the timeline never touches HBM, so the kernel
+// reads 17 B per event (t_s, t_e, size, dyn) and writes 8 B per trace.
+// A trace with a timestamp outside [0, kPeakSmem) is flagged for the
+// global-timeline path below.
+constexpr int kPeakThreads = 256;
+constexpr int kPeakSmem = 6016;  // timeline entries (47 KB of static shared memory)
+
+__global__ void __launch_bounds__(kPeakThreads) k_peak_cta(const int64_t *__restrict__ ev_off,
+                                                           const int64_t *__restrict__ size,
+                                                           const int32_t *__restrict__ t_s,
+                                                           const int32_t *__restrict__ t_e,
+                                                           const uint8_t *__restrict__ dyn, int static_only,
+                                                           long long *__restrict__ peak, int *__restrict__ nbig,
+                                                           int32_t *__restrict__ big) {
+  __shared__ unsigned long long D[kPeakSmem];
+  __shared__ long long sh[33];
+  __shared__ int sh_hi;
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
+  if (tid == 0) sh_hi = -1;
+  for (int x = tid; x < kPeakSmem; x += kPeakThreads) D[x] = 0;
+  __syncthreads();
+  int hi = -1;
+  bool bad = false;
+  for (int64_t i = e0 + tid; i < e1; i += kPeakThreads) {
+    if (static_only && dyn[i]) continue;
+    const int a = t_s[i], z = t_e[i];
+    if (a < 0 || z < 0 || a >= kPeakSmem || z >= kPeakSmem) {
+      bad = true;
+      continue;
+    }
+    const unsigned long long sz = (unsigned long long)size[i];
+    atomicAdd(D + a, sz);
+    atomicAdd(D + z, 0ull - sz);
+    hi = max(hi, max(a, z));
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) big[atomicAdd(nbig, 1)] = t;
+    return;
+  }
+  if (hi >= 0) atomicMax(&sh_hi, hi);
+  __syncthreads();
+  const int H = sh_hi + 1;
+  const int per = (H + kPeakThreads - 1) / kPeakThreads;
+  const int x0 = min(H, tid * per), x1 = min(H, x0 + per);
+  long long run = 0, best = LLONG_MIN;
+  for (int x = x0; x < x1; x++) {
+    run += (long long)D[x];
+    best = max(best, run);
+  }
+  long long tot;
+  const long long ex = block_excl_sum<long long>(run, sh, &tot);
+  long long cand = best == LLONG_MIN ? LLONG_MIN : ex + best;
+  // block max
+  for (int o = 16; o; o >>= 1) cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+  if ((tid & 31) == 0) sh[tid >> 5] = cand;
+  __syncthreads();
+  if (tid == 0) {
+    long long m = 0;  // the reference's running maximum starts at 0
+    for (int w = 0; w < kPeakThreads / 32; w++) m = max(m, sh[w]);
+    peak[t] = m;
+  }
+}
+
+__global__ void k_big_offsets(const int32_t *__restrict__ big, const int *__restrict__ nbig, int T,
+                              uint8_t *__restrict__ is_big) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < *nbig; x += gridDim.x * blockDim.x) is_big[big[x]] = 1;
+}
+
+static void peak_live_global(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
+                             const uint8_t *only);
+
 void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak) {
+  if (!ctx.ok() || b.T == 0) return;
+  const int T = b.T;
+  int *nbig = ar.take<int>(1);
+  int32_t *big = ar.take<int32_t>(T);
+  if (!ctx.ok()) return;
+  STW_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(int), ctx.stream));
+  STW_KL(k_peak_cta, (unsigned)T, kPeakThreads, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e, b.dyn,
+         static_only ? 1 : 0, (long long *)d_peak, nbig, big);
+  STW_LAUNCHED(ctx);
+  int h = 0;
+  STW_CUDA(ctx, cudaMemcpyAsync(&h, nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (!ctx.ok() || h == 0) return;
+  uint8_t *is_big = ar.take<uint8_t>(T);
+  if (!ctx.ok()) return;
+  STW_CUDA(ctx, cudaMemsetAsync(is_big, 0, T, ctx.stream));
+  STW_KL(k_big_offsets, grid_for(h, 256), 256, ctx.stream, big, nbig, T, is_big);
+  STW_LAUNCHED(ctx);
+  peak_live_global(ctx, ar, b, static_only, d_peak, is_big);
+}
+
+// Traces with long timelines (e.g. c5, horizon 1,966,792): the timeline lives
+// in HBM; `only` selects the traces to (re)compute.
+static void peak_live_global(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
+                             const uint8_t *only) {
   if (!ctx.ok()) return;
   const int T = b.T;
   int *tmax = ar.take<int>(T);
@@ -79,9 +185,9 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
   int64_t *D = ar.take<int64_t>(H);
   if (!ctx.ok()) return;
   STW_CUDA(ctx, cudaMemsetAsync(D, 0, H * sizeof(int64_t), ctx.stream));
-  STW_CUDA(ctx, cudaMemsetAsync(d_peak, 0, T * sizeof(int64_t), ctx.stream));
+  STW_KL(k_zero_selected, grid_for(T, 256), 256, ctx.stream, only, T, d_peak);
   STW_KL(k_timeline_scatter, grid_for(b.N, 256), 256, ctx.stream, b.ev_off, T, b.N, b.size, b.t_s, b.t_e, b.dyn,
-                                                                 tl_len, (unsigned long long *)D, static_only);
+                                                                 tl_len, (unsigned long long *)D, static_only, only);
   STW_LAUNCHED(ctx);
   device_scan<int64_t>(ctx, ar, D, D, H, true);
   int64_t nthreads = (H + 7) / 8;

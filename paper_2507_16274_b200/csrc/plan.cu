@@ -1372,6 +1372,198 @@ __global__ void __launch_bounds__(256) k_layers_warp(LayerArgs A, const int32_t 
   }
 }
 
+// E (narrow units, <= 32 layers -- every c4 unit): one warp per unit; the
+// per-item greedy is a short dependency chain. Lane p holds the same-class last
+// end of the layer at priority p and lane q the end of the class's new layer q;
+// each item is one ballot (gap host: the lowest fitting priority) raced against
+// one max-reduction + ballot (Alg. 1), both speculative, then a select. Layer
+// ids, insertion ranks (match_any) and the gap count are resolved lane-parallel
+// after each 32-item chunk; ilayer/irank go straight to global scratch so the
+// shared footprint is the slot CSR + merge buffers (6 ints per item). A unit
+// that would open a 33rd layer is handed to the CTA kernel.
+
+constexpr int kWN = 32;
+
+__host__ __device__ constexpr int warpn_smem_ints(int cap) { return 6 * cap + 4 * (kWN + 1) + kWN; }
+
+__global__ void __launch_bounds__(256) k_layers_w32(LayerArgs A, const int32_t *__restrict__ ulist, int nunits,
+                                                    int cap, int32_t *__restrict__ over, int *__restrict__ nover) {
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ int32_t smem[];
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  const int ui = blockIdx.x * (blockDim.x >> 5) + w;
+  if (ui >= nunits) return;
+  const int u = ulist[ui];
+  const int c = u % A.C, t = u / A.C;
+  const int v = A.var_of[c];
+  const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
+  const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
+  const int n = (int)(a1 - a0);
+  const int64_t off = A.uo[u];
+  int32_t *sm = smem + w * warpn_smem_ints(cap);
+  int32_t *sts = sm, *ste = sm + cap, *tts = sm + 2 * cap, *tte = sm + 3 * cap;  // slots + merge temp
+  int32_t *run_ts = sm + 4 * cap, *run_te = sm + 5 * cap;
+  int32_t *loffA = sm + 6 * cap, *loffB = loffA + (kWN + 1), *prio = loffB + (kWN + 1), *runoff = prio + (kWN + 1);
+  int32_t *newcnt = runoff + (kWN + 1);
+  const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
+  const int64_t *gcend = A.cend + a0;
+  int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
+  int64_t *lsize = A.lsize + off;
+  if (lane == 0) loffA[0] = 0;
+  int nl = 0, gapc = 0;
+  __syncwarp();
+  for (int j0 = 0; j0 < n;) {
+    const int j1 = (int)(gcend[j0] - a0);
+    const int m = j1 - j0;
+    const int64_t S = A.it.size[a0 + j0];
+    int last = INT_MIN, ne = INT_MIN, nnew = 0;
+    newcnt[lane] = 0;
+    __syncwarp();
+    for (int cb = j0; cb < j1; cb += 32) {
+      const int mine = cb + lane;
+      const int cnt = min(32, j1 - cb);
+      int my_ts = 0, my_te = 0;
+      unsigned fm = 0;
+      if (mine < j1) {
+        my_ts = gts[mine];
+        my_te = gte[mine];
+        if (gap)
+          for (int p = 0; p < nl; p++) {
+            const int l = prio[p];
+            if (slot_fit(sts, ste, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1u << p;
+          }
+      }
+      int my_code = 0;
+      for (int kg = 0; kg < cnt; kg += 8) {
+#pragma unroll
+        for (int kk = 0; kk < 8; kk++) {
+          const int k = kg + kk;
+          const bool valid = k < cnt;  // warp-uniform
+          const int ts = __shfl_sync(FULL, my_ts, k & 31), te = __shfl_sync(FULL, my_te, k & 31);
+          const unsigned f = __shfl_sync(FULL, fm, k & 31);
+          // gap host (planner.py:420-431): first fitting layer in priority order whose
+          // same-class slots all end before ts
+          const unsigned m1 = __ballot_sync(FULL, ((f >> lane) & 1u) && last < ts);
+          // Alg. 1 (planner.py:244-252): new layer with the largest end < ts, ties to the oldest
+          const bool ca = lane < nnew && ne < ts;
+          const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
+          const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
+          const int host = __ffs(m1) - 1;
+          const int best = cma ? __ffs(cma) - 1 : nnew;
+          const bool newl = valid && !m1 && !cma;
+          if (newl && nl + nnew == kWN) {  // a 33rd layer: the CTA kernel redoes the unit
+            if (lane == 0) over[atomicAdd(nover, 1)] = u;
+            return;
+          }
+          if (valid) {
+            if (m1) {
+              if (lane == host) last = te;
+            } else if (lane == best) {
+              ne = te;
+            }
+          }
+          nnew += newl ? 1 : 0;
+          if (lane == k) my_code = m1 ? host : kWN + best;
+        }
+      }
+      // lane-parallel: layer ids, gap count, insertion ranks
+      const bool act = lane < cnt;
+      const int layer = my_code < kWN ? prio[my_code] : nl + (my_code - kWN);
+      gapc += __popc(__ballot_sync(FULL, act && my_code < kWN));
+      const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
+      const int r = __popc(peers & lanemask_lt());
+      const int base = act ? newcnt[layer] : 0;
+      __syncwarp();
+      if (act) {
+        ilayer[mine] = layer;
+        irank[mine] = base + r;
+        if (r == __popc(peers) - 1) newcnt[layer] = base + __popc(peers);
+      }
+      __syncwarp();
+    }
+    // ---- merge the class into the layer-major slot CSR
+    const int nl2 = nl + nnew;
+    if (lane < nnew) lsize[nl + lane] = S;
+    const int myc = newcnt[lane];
+    const unsigned tm = __ballot_sync(FULL, lane < nl && myc > 0);
+    const int first = tm ? __ffs(tm) - 1 : nl;  // first old layer that received gap insertions
+    {
+      const int cnt_all = lane < nl2 ? (lane < nl ? loffA[lane + 1] - loffA[lane] : 0) + myc : 0;
+      int tot, tot2;
+      const int ex = warp_excl_scan(cnt_all, &tot), ex2 = warp_excl_scan(lane < nl2 ? myc : 0, &tot2);
+      if (lane < nl2) {
+        loffB[lane] = ex;
+        runoff[lane] = ex2;
+      }
+      if (lane == 0) loffB[nl2] = tot;
+    }
+    __syncwarp();
+    const int s0 = loffA[first];
+    const int nold = loffA[nl];
+    if (first < nl) {
+      for (int x = lane; x < m; x += 32) {
+        const int l = ilayer[j0 + x];
+        const int pos = runoff[l] + irank[j0 + x];
+        run_ts[pos] = gts[j0 + x];
+        run_te[pos] = gte[j0 + x];
+      }
+      __syncwarp();
+      for (int sidx = s0 + lane; sidx < nold; sidx += 32) {
+        int lo = first, hi = nl;  // layer of slot sidx
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (loffA[mid] <= sidx)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        int l = lo;
+        while (loffA[l + 1] <= sidx) l++;
+        const int ts = sts[sidx];
+        const int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
+        const int dst = loffB[l] + (sidx - loffA[l]) + k - s0;
+        tts[dst] = ts;
+        tte[dst] = ste[sidx];
+      }
+    }
+    for (int x = lane; x < m; x += 32) {
+      const int l = ilayer[j0 + x];
+      const int ts = gts[j0 + x];
+      const int k = l < nl ? lower_bound_i32(sts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
+      const int dst = loffB[l] + irank[j0 + x] + k - s0;
+      tts[dst] = ts;
+      tte[dst] = gte[j0 + x];
+    }
+    __syncwarp();
+    const int ntail = loffB[nl2] - s0;
+    for (int x = lane; x < ntail; x += 32) {
+      sts[s0 + x] = tts[x];
+      ste[s0 + x] = tte[x];
+    }
+    // priority order for later classes: the class's new layers (creation order), then the old list
+    {
+      const int po = lane < nl ? prio[lane] : 0;
+      const int sv = __shfl_sync(FULL, po, (lane - nnew) & 31);
+      __syncwarp();
+      if (lane < nl2) prio[lane] = lane < nnew ? nl + lane : sv;
+    }
+    for (int x = lane; x <= nl2; x += 32) loffA[x] = loffB[x];
+    __syncwarp();
+    nl = nl2;
+    j0 = j1;
+  }
+  // stacking (planner.py:441-444)
+  const long long sz = lane < nl ? lsize[lane] : 0;
+  const long long inc = warp_incl_sum(sz);
+  const long long base = A.pers_size[t], total = __shfl_sync(FULL, inc, 31);
+  if (lane < nl) A.lbase[off + lane] = base + inc - sz;
+  if (lane == 0) {
+    A.nlayers[u] = nl;
+    A.gapins[u] = gapc;
+    A.pool[u] = base + total;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // F: emission (planner.py:446-455)
 
@@ -1940,6 +2132,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     if (!ctx.ok()) return ctx.rc;
     STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, sizeof(int), ctx.stream));
     const int64_t nsmall = loff[NBK];
+    // units with <= 32 layers take the narrow warp kernel (STW_LAYERS_WIDE=1: the 64-layer one)
+    static const bool wide = getenv("STW_LAYERS_WIDE") != nullptr;
     // the buckets run concurrently on forked streams (largest buckets first)
     cudaEvent_t fork_ev = side_event(0), join_ev[NBK];
     STW_CUDA(ctx, cudaEventRecord(fork_ev, ctx.stream));
@@ -1949,13 +2143,26 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       if (!nb) continue;
       cudaStream_t st = side_stream(bk);
       STW_CUDA(ctx, cudaStreamWaitEvent(st, fork_ev, 0));
-      size_t per_warp = (size_t)warp_smem_ints(caps[bk]) * sizeof(int32_t);
-      int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp));
-      size_t smem = per_warp * wpc;
-      STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int prof = prof_pre(st);
-      k_layers_warp<<<(nb + wpc - 1) / wpc, wpc * 32, smem, st>>>(LA, d_list + loff[bk], nb, caps[bk], d_over, d_nover);
-      prof_post(st, "k_layers_warp", prof);
+      if (wide) {
+        size_t per_warp = (size_t)warp_smem_ints(caps[bk]) * sizeof(int32_t);
+        int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp));
+        size_t smem = per_warp * wpc;
+        STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int prof = prof_pre(st);
+        k_layers_warp<<<(nb + wpc - 1) / wpc, wpc * 32, smem, st>>>(LA, d_list + loff[bk], nb, caps[bk], d_over,
+                                                                   d_nover);
+        prof_post(st, "k_layers_warp", prof);
+      } else {
+        // two CTAs per SM: up to ~112 KB of slot CSR per CTA
+        size_t per_warp = (size_t)warpn_smem_ints(caps[bk]) * sizeof(int32_t);
+        int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (112u << 10) / per_warp));
+        size_t smem = per_warp * wpc;
+        STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_w32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int prof = prof_pre(st);
+        k_layers_w32<<<(nb + wpc - 1) / wpc, wpc * 32, smem, st>>>(LA, d_list + loff[bk], nb, caps[bk], d_over,
+                                                                  d_nover);
+        prof_post(st, "k_layers_w32", prof);
+      }
       STW_LAUNCHED(ctx);
       join_ev[bk] = side_event(1 + bk);
       STW_CUDA(ctx, cudaEventRecord(join_ev[bk], st));
@@ -2024,7 +2231,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   LAUNCH(k_rect_fill, N, rperm, sflag, spos, e, N, C, addr, rs_ev, rts, rte, rsz, raddr, NS);
   RectSets rs{T, NS, d_so, rts, rte, rsz, C, raddr};
-  validate_sets(ctx, ar, rs, vcount, vfirst);
+  validate_sets(ctx, ar, rs, vcount, vfirst, __builtin_ctzll((unsigned long long)o->alignment));
 
   pt.mark("G check");
   // ---- per-unit verdicts, stats and best-candidate selection on the device

@@ -27,7 +27,14 @@ struct RectSets {
 // reference sweep (planner.py:476-505) would report and the sweep position of
 // the first reporting decision (INT_MAX if none). Outputs are device arrays of
 // S*n_cand entries, unit index = set*n_cand + cand.
-void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first);
+// Addresses and sizes are expected to be multiples of 2^shift (the alignment);
+// units that are not fall back to the exact tiled reporter.
+void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first, int shift);
+
+// Fast exact validity test (no report) of every (set, candidate); returns the
+// number of units that need the exact reporter (0 = every unit is valid), -1
+// on a CUDA error.
+int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift);
 
 // Host-side re-derivation of the first reported pair (a, b) of a decision set
 // whose first reporting decision is at sweep position `first` (device data).

@@ -236,10 +236,134 @@ static void build_tiles(Ctx &ctx, Arena &ar, const RectSets &rs, Tiles *tl) {
   STW_LAUNCHED(ctx);
 }
 
-void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first) {
+
+// ---------------------------------------------------------------------------
+// Fast path: exact "does the reference report anything" test, one warp per
+// (set, candidate). The reference reports at least one pair iff some decision
+// overlaps (address x half-open lifespan) a decision allocated before it in
+// sweep order (the first such decision reports its predecessor or a forward
+// neighbour: any other active rectangle it could hit would itself have been a
+// conflict earlier), so a valid plan needs only the overlap test. The warp
+// sweeps 32 decisions at a time: each lane tests its decision against the
+// active list (decisions still live at the tile start) and the tile's earlier
+// decisions, both broadcast from shared memory as int4 (address and end
+// scaled by 2^shift to 32 bits, t_s, t_e); then entries that end before the
+// next tile starts are compacted away. The rectangles stream through once
+// (24 B each, next tile prefetched). A unit that conflicts, does not scale
+// to 32 bits, overflows the active list, or is too long for a serial sweep is
+// flagged and the exact tiled reporter above runs instead.
+constexpr int kOvWarps = 8;
+constexpr int kOvCap = 320;
+constexpr int64_t kOvMaxSerial = 1 << 16;
+
+__global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, int shift, int *__restrict__ nflag) {
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ int4 act[kOvWarps][kOvCap];
+  __shared__ int4 tile[kOvWarps][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * kOvWarps + w;
+  if (u >= (int64_t)rs.S * rs.n_cand) return;
+  const int s = (int)(u / rs.n_cand), c = (int)(u % rs.n_cand);
+  const int64_t s0 = rs.off[s], n = rs.off[s + 1] - s0;
+  if (n > kOvMaxSerial) {
+    if (lane == 0) atomicAdd(nflag, 1);
+    return;
+  }
+  const int64_t *addr = rs.addr + (int64_t)c * rs.n + s0, *size = rs.size + s0;
+  const int32_t *ts = rs.ts + s0, *te = rs.te + s0;
+  int4 *A = act[w], *Tt = tile[w];
+  const long long low = (1ll << shift) - 1;
+  int na = 0;
+  long long pa = 0, psz = 0;
+  int pts = 0, pte = 0;
+  if (lane < n) {
+    pa = addr[lane];
+    psz = size[lane];
+    pts = ts[lane];
+    pte = te[lane];
+  }
+  for (int64_t k0 = 0; k0 < n; k0 += 32) {
+    const bool valid = k0 + lane < n;
+    const long long a = pa, sz = psz;
+    const int dts = pts, dte = pte;
+    const int64_t kn = k0 + 32 + lane;
+    if (kn < n) {
+      pa = addr[kn];
+      psz = size[kn];
+      pts = ts[kn];
+      pte = te[kn];
+    }
+    const int t0n = k0 + 32 < n ? __shfl_sync(FULL, pts, 0) : INT_MAX;  // start of the next tile
+    const long long end = a + sz;
+    const bool ok = !valid || (a >= 0 && sz > 0 && dte > dts && ((a | sz) & low) == 0 && (end >> shift) <= INT_MAX);
+    if (__any_sync(FULL, !ok)) {
+      if (lane == 0) atomicAdd(nflag, 1);
+      return;
+    }
+    const int da = (int)(a >> shift), de = (int)(end >> shift);
+    if (valid) Tt[lane] = make_int4(da, de, dts, dte);
+    __syncwarp();
+    bool hit = false;
+    if (valid) {
+      for (int j = 0; j < na; j++) {
+        const int4 q = A[j];
+        hit |= (q.w > dts) & (q.x < de) & (q.y > da);
+      }
+      for (int j = 0; j < lane; j++) {
+        const int4 q = Tt[j];
+        hit |= (q.w > dts) & (q.x < de) & (q.y > da);
+      }
+    }
+    if (__any_sync(FULL, hit)) {
+      if (lane == 0) atomicAdd(nflag, 1);
+      return;
+    }
+    int nn = 0;
+    for (int cb = 0; cb < na; cb += 32) {
+      const int j = cb + lane;
+      const int4 q = j < na ? A[j] : make_int4(0, 0, 0, 0);
+      const bool keep = j < na && q.w > t0n;
+      const unsigned m = __ballot_sync(FULL, keep);
+      __syncwarp();
+      if (keep) A[nn + __popc(m & lanemask_lt())] = q;
+      nn += __popc(m);
+      __syncwarp();
+    }
+    const bool keep = valid && dte > t0n;
+    const unsigned m = __ballot_sync(FULL, keep);
+    if (nn + __popc(m) > kOvCap) {
+      if (lane == 0) atomicAdd(nflag, 1);
+      return;
+    }
+    if (keep) A[nn + __popc(m & lanemask_lt())] = make_int4(da, de, dts, dte);
+    na = nn + __popc(m);
+    __syncwarp();
+  }
+}
+
+int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift) {
+  if (!ctx.ok()) return -1;
+  const int64_t U = (int64_t)rs.S * rs.n_cand;
+  int *nflag = ar.take<int>(1);
+  if (!ctx.ok()) return -1;
+  STW_CUDA(ctx, cudaMemsetAsync(nflag, 0, sizeof(int), ctx.stream));
+  if (U > 0) {
+    STW_KL(k_overlap_sweep, (unsigned)((U + kOvWarps - 1) / kOvWarps), kOvWarps * 32, ctx.stream, rs, shift, nflag);
+    STW_LAUNCHED(ctx);
+  }
+  int h = 0;
+  STW_CUDA(ctx, cudaMemcpyAsync(&h, nflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  return ctx.ok() ? h : -1;
+}
+
+void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first, int shift) {
   if (!ctx.ok()) return;
   int64_t U = (int64_t)rs.S * rs.n_cand;
   STW_CUDA(ctx, cudaMemsetAsync(d_count, 0, U * sizeof(long long), ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(d_first, 0x7f, U * sizeof(int), ctx.stream));  // 0x7f7f7f7f: no report
+  if (overlap_flags(ctx, ar, rs, shift) == 0) return;  // every unit valid: nothing reported
+  if (!ctx.ok()) return;
   std::vector<int> big(U, INT_MAX);
   STW_CUDA(ctx, cudaMemcpyAsync(d_first, big.data(), U * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
   Tiles tl;
@@ -364,6 +488,14 @@ __global__ void k_minmax_id(const int64_t *__restrict__ v, int64_t n, long long 
   }
 }
 
+__global__ void k_or_bits(const int64_t *__restrict__ a, const int64_t *__restrict__ b, int64_t n,
+                          unsigned long long *out) {
+  unsigned long long v = 0;
+  GS(i, n) v |= (unsigned long long)a[i] | (unsigned long long)b[i];
+  for (int o = 16; o; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicOr(out, v);
+}
+
 __global__ void k_max_ts(const int32_t *__restrict__ v, int64_t n, int *mx) {
   GS(i, n) atomicMax(mx, v[i]);
 }
@@ -409,6 +541,18 @@ int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *a
   int64_t hoff[2] = {0, n};
   STW_CUDA(ctx, cudaMemcpyAsync(off, hoff, sizeof(hoff), cudaMemcpyHostToDevice, ctx.stream));
   RectSets rs{1, n, off, ts2, te2, s2, 1, a2};
+  {  // fast path: a valid plan reports nothing
+    unsigned long long *orv = ar.take<unsigned long long>(1);
+    if (!ctx.ok()) return ctx.rc;
+    STW_CUDA(ctx, cudaMemsetAsync(orv, 0, sizeof(unsigned long long), ctx.stream));
+    STW_KL(k_or_bits, grid_for(n, 256), 256, ctx.stream, a2, s2, n, orv);
+    unsigned long long hor = 0;
+    STW_CUDA(ctx, cudaMemcpyAsync(&hor, orv, sizeof(hor), cudaMemcpyDeviceToHost, ctx.stream));
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    const int shift = hor ? std::min(__builtin_ctzll(hor), 62) : 0;
+    if (overlap_flags(ctx, ar, rs, shift) == 0) return ctx.rc;
+    if (!ctx.ok()) return ctx.rc;
+  }
   Tiles tl;
   build_tiles(ctx, ar, rs, &tl);
   STW_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(long long), ctx.stream));
