@@ -53,6 +53,13 @@ void prof_post(cudaStream_t s, const char *name, int slot);
     ::stw::prof_post(stream, #kern, _stw_slot);              \
   } while (0)
 
+#define STW_KLS(kern, grid, block, smem, stream, ...)         \
+  do {                                                       \
+    int _stw_slot = ::stw::prof_pre(stream);                 \
+    kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__); \
+    ::stw::prof_post(stream, #kern, _stw_slot);              \
+  } while (0)
+
 // Stream-ordered scratch: every take() is a cudaMallocAsync on the call's
 // stream (served from the device's default pool, whose release threshold is
 // raised once so repeated calls do not remap); everything is returned with
@@ -61,6 +68,8 @@ struct Arena {
   Ctx *ctx;
   void *ptrs[512];
   int n = 0;
+  char *cur = nullptr;  // bump pointer inside the newest chunk
+  size_t left = 0;
   explicit Arena(Ctx *c) : ctx(c) {}
   void *raw(size_t bytes);
   template <class T>

@@ -150,6 +150,14 @@ __global__ void k_seg_bitonic(uint64_t *__restrict__ keys, uint32_t *__restrict_
   const int64_t s0 = seg_off[blockIdx.x];
   const int n = (int)(seg_off[blockIdx.x + 1] - s0);
   if (n == 0) return;
+  // already in order (e.g. a trace's events by id or by (t_s, id), as
+  // recorded): the stable result is the identity
+  bool sorted = true;
+  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) sorted &= keys[s0 + i] <= keys[s0 + i + 1];
+  if (__syncthreads_and(sorted)) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[s0 + i] = (uint32_t)(s0 + i);
+    return;
+  }
   int P = 1;
   while (P < n) P <<= 1;
   uint32_t *sv = (uint32_t *)(sk + pcap);
@@ -839,8 +847,9 @@ __global__ void k_class_start(const uint32_t *__restrict__ head, const uint32_t 
   GRID_STRIDE(j, n) if (head[j]) cstart[cid_incl[j] - 1] = j;
 }
 
-__global__ void k_class_end(const uint32_t *__restrict__ cid_incl, const int64_t *__restrict__ cstart, int64_t nc,
-                            int64_t n, int64_t *__restrict__ cend) {
+__global__ void k_class_end(const uint32_t *__restrict__ cid_incl, const int64_t *__restrict__ cstart, int64_t n,
+                            int64_t *__restrict__ cend) {
+  const int64_t nc = cid_incl[n - 1];  // number of classes
   GRID_STRIDE(j, n) {
     int64_t c = cid_incl[j];  // id + 1
     cend[j] = c < nc ? cstart[c] : n;
@@ -910,10 +919,19 @@ __device__ void block_scan_into(int n, F f, int32_t *out, int *shi) {
   __syncthreads();
 }
 
+__device__ void layers_unit(const LayerArgs &A, const int u);
+
+// ulist[0 .. *ucount) (or [0, gridDim.x) without a count), grid-stride
 __global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A, const int32_t *__restrict__ ulist,
                                                          const int *__restrict__ ucount) {
-  if (ucount && (int)blockIdx.x >= *ucount) return;
-  const int u = ulist[blockIdx.x];
+  const int n = ucount ? *ucount : (int)gridDim.x;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    layers_unit(A, ulist[i]);
+    __syncthreads();
+  }
+}
+
+__device__ void layers_unit(const LayerArgs &A, const int u) {
   const int c = u % A.C, t = u / A.C;
   const int v = A.var_of[c];
   const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
@@ -1125,285 +1143,50 @@ __global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A, const int3
 }
 
 
-// ---------------------------------------------------------------------------
-// E (small units): one warp per unit, the unit's slot CSR in shared memory.
-// Same decomposition as k_layers; fit masks are computed per 32-item chunk by
-// the lanes right before the warp resolves the chunk. A unit that opens more
-// than kWL layers is handed to the CTA kernel (appended to `over`).
-
-constexpr int kWL = 64;
-
 __device__ __forceinline__ int warp_excl_scan(int v, int *total) {
   int inc = warp_incl_sum(v);
   *total = __shfl_sync(0xffffffffu, inc, 31);
   return inc - v;
 }
 
-// per-warp shared-memory footprint (ints) of k_layers_warp for a unit capacity
-__host__ __device__ constexpr int warp_smem_ints(int cap) { return 9 * cap + 5 * (kWL + 1); }
-
-// Register-resident resolve state: lane p holds the same-class "last end" of
-// the layer at priority p (and p+32), the end of the class's new layer p (and
-// p+32), and the class insertion counter of layer id p (and p+32). The per-item
-// step is shuffles, ballots and one max-reduction -- no shared memory traffic.
-__global__ void __launch_bounds__(256) k_layers_warp(LayerArgs A, const int32_t *__restrict__ ulist, int nunits,
-                                                     int cap, int32_t *__restrict__ over, int *__restrict__ nover) {
-  extern __shared__ int32_t smem[];
-  const int w = threadIdx.x >> 5, lane = lane_id();
-  const int ui = blockIdx.x * (blockDim.x >> 5) + w;
-  if (ui >= nunits) return;
-  const int u = ulist[ui];
-  const int c = u % A.C, t = u / A.C;
-  const int v = A.var_of[c];
-  const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
-  const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
-  const int n = (int)(a1 - a0);
-  const int64_t off = A.uo[u];
-  int32_t *sm = smem + w * warp_smem_ints(cap);
-  int32_t *sts = sm, *ste = sm + cap, *tts = sm + 2 * cap, *tte = sm + 3 * cap;  // slots + merge temp
-  int32_t *run_ts = sm + 4 * cap, *run_te = sm + 5 * cap;
-  int32_t *ilayer = sm + 6 * cap, *irank = sm + 7 * cap, *icend = sm + 8 * cap;
-  int32_t *loffA = sm + 9 * cap, *loffB = loffA + (kWL + 1), *prioA = loffB + (kWL + 1), *prioB = prioA + (kWL + 1);
-  int32_t *newcnt = prioB + (kWL + 1);
-  const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
-  int64_t *lsize = A.lsize + off;
-  for (int x = lane; x < n; x += 32) icend[x] = (int)(A.cend[a0 + x] - a0);
-  if (lane == 0) loffA[0] = 0;
-  int nl = 0;
-  long long gapc = 0;
-  __syncwarp();
-  for (int j0 = 0; j0 < n;) {
-    const int j1 = icend[j0];
-    const int m = j1 - j0;
-    const int64_t S = A.it.size[a0 + j0];
-    int lastA = INT_MIN, lastB = INT_MIN, neA = INT_MIN, neB = INT_MIN, cntA = 0, cntB = 0;
-    const int prA = lane < nl ? prioA[lane] : 0, prB = lane + 32 < nl ? prioA[lane + 32] : 0;
-    int nnew = 0;
-    for (int cb = j0; cb < j1; cb += 32) {
-      const int mine = cb + lane;
-      int my_ts = 0, my_te = 0, my_layer = 0, my_rank = 0;
-      unsigned long long fm = 0;
-      if (mine < j1) {
-        my_ts = gts[mine];
-        my_te = gte[mine];
-        if (gap)
-          for (int p = 0; p < nl; p++) {
-            int l = prioA[p];
-            if (slot_fit(sts, ste, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1ull << p;
-          }
-      }
-      const int cnt = min(32, j1 - cb);
-      for (int k = 0; k < cnt; k++) {
-        const int ts = __shfl_sync(0xffffffffu, my_ts, k), te = __shfl_sync(0xffffffffu, my_te, k);
-        int host_p = -1;
-        if (gap && nl > 0) {
-          const unsigned long long f = __shfl_sync(0xffffffffu, fm, k);
-          unsigned m1 = __ballot_sync(0xffffffffu, lane < nl && ((f >> lane) & 1ull) && lastA < ts);
-          if (m1) {
-            host_p = __ffs(m1) - 1;
-          } else if (nl > 32) {
-            unsigned m2 = __ballot_sync(0xffffffffu, lane + 32 < nl && ((f >> (lane + 32)) & 1ull) && lastB < ts);
-            if (m2) host_p = 32 + __ffs(m2) - 1;
-          }
-        }
-        int layer;
-        if (host_p >= 0) {
-          const int la = __shfl_sync(0xffffffffu, prA, host_p & 31), lb = __shfl_sync(0xffffffffu, prB, host_p & 31);
-          layer = host_p < 32 ? la : lb;
-          if (lane == (host_p & 31)) {
-            if (host_p < 32)
-              lastA = te;
-            else
-              lastB = te;
-          }
-          gapc++;
-        } else {  // Alg. 1: new layer of this class with the largest end < ts, ties to the oldest
-          const bool ca = lane < nnew && neA < ts;
-          const int mxa = __reduce_max_sync(0xffffffffu, ca ? neA : INT_MIN);
-          const unsigned cma = __ballot_sync(0xffffffffu, ca && neA == mxa);
-          int best = cma ? __ffs(cma) - 1 : -1, best_e = mxa;
-          if (nnew > 32) {
-            const bool cbb = lane + 32 < nnew && neB < ts;
-            const int mxb = __reduce_max_sync(0xffffffffu, cbb ? neB : INT_MIN);
-            const unsigned cmb = __ballot_sync(0xffffffffu, cbb && neB == mxb);
-            if (cmb && (best < 0 || mxb > best_e)) best = 32 + __ffs(cmb) - 1;
-          }
-          if (best < 0) {
-            if (nl + nnew == kWL) {  // too many layers for the warp path: the CTA kernel redoes the unit
-              if (lane == 0) over[atomicAdd(nover, 1)] = u;
-              return;
-            }
-            best = nnew++;
-          }
-          if (lane == (best & 31)) {
-            if (best < 32)
-              neA = te;
-            else
-              neB = te;
-          }
-          layer = nl + best;
-        }
-        const int ra = __shfl_sync(0xffffffffu, cntA, layer & 31), rb = __shfl_sync(0xffffffffu, cntB, layer & 31);
-        const int rank = layer < 32 ? ra : rb;
-        if (lane == (layer & 31)) {
-          if (layer < 32)
-            cntA++;
-          else
-            cntB++;
-        }
-        if (lane == k) {
-          my_layer = layer;
-          my_rank = rank;
-        }
-      }
-      if (mine < j1) {
-        ilayer[mine] = my_layer;
-        irank[mine] = my_rank;
-      }
-    }
-    // ---- merge the class into the layer-major slot CSR
-    const int nl2 = nl + nnew;
-    for (int x = lane; x < nnew; x += 32) lsize[nl + x] = S;
-    newcnt[lane] = cntA;
-    newcnt[lane + 32] = cntB;
-    __syncwarp();
-    // first old layer that received gap insertions (slots before it keep their place)
-    unsigned tm1 = __ballot_sync(0xffffffffu, lane < nl && cntA > 0);
-    unsigned tm2 = __ballot_sync(0xffffffffu, lane + 32 < nl && cntB > 0);
-    const int first = tm1 ? __ffs(tm1) - 1 : (tm2 ? 32 + __ffs(tm2) - 1 : nl);
-    {
-      int carry = 0, carry2 = 0;
-      for (int base = 0; base < nl2; base += 32) {
-        int l = base + lane;
-        int cnt_all = l < nl2 ? (l < nl ? loffA[l + 1] - loffA[l] : 0) + newcnt[l] : 0;
-        int cnt_new = l < nl2 ? newcnt[l] : 0;
-        int tot, tot2;
-        int ex = warp_excl_scan(cnt_all, &tot), ex2 = warp_excl_scan(cnt_new, &tot2);
-        if (l < nl2) {
-          loffB[l] = carry + ex;
-          prioB[l] = carry2 + ex2;  // prioB doubles as run offsets until the priority update below
-        }
-        carry += tot;
-        carry2 += tot2;
-      }
-      if (lane == 0) loffB[nl2] = carry;
-    }
-    __syncwarp();
-    const int32_t *runoff = prioB;
-    const int s0 = loffA[first > nl ? nl : first];
-    const int nold = nl > 0 ? loffA[nl] : 0;
-    if (first < nl) {
-      for (int x = lane; x < m; x += 32) {
-        int l = ilayer[j0 + x];
-        int pos = runoff[l] + irank[j0 + x];
-        run_ts[pos] = gts[j0 + x];
-        run_te[pos] = gte[j0 + x];
-      }
-      __syncwarp();
-      for (int sidx = s0 + lane; sidx < nold; sidx += 32) {
-        int lo = first, hi = nl;  // layer of slot sidx
-        while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
-          if (loffA[mid] <= sidx)
-            lo = mid;
-          else
-            hi = mid;
-        }
-        int l = lo;
-        while (loffA[l + 1] <= sidx) l++;
-        int ts = sts[sidx];
-        int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
-        int dst = loffB[l] + (sidx - loffA[l]) + k - s0;
-        tts[dst] = ts;
-        tte[dst] = ste[sidx];
-      }
-    }
-    for (int x = lane; x < m; x += 32) {
-      int l = ilayer[j0 + x];
-      int ts = gts[j0 + x];
-      int k = l < nl ? lower_bound_i32(sts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
-      int dst = loffB[l] + irank[j0 + x] + k - s0;
-      tts[dst] = ts;
-      tte[dst] = gte[j0 + x];
-    }
-    __syncwarp();
-    const int ntail = loffB[nl2] - s0;
-    for (int x = lane; x < ntail; x += 32) {
-      sts[s0 + x] = tts[x];
-      ste[s0 + x] = tte[x];
-    }
-    // priority order for later classes: newest (smallest) layers first, creation order within
-    {
-      int pa = lane < nl ? prioA[lane] : 0, pb = lane + 32 < nl ? prioA[lane + 32] : 0;
-      __syncwarp();
-      // write new priorities: first nnew are the new layers, then the old list shifted
-      int old0 = lane - nnew, old1 = lane + 32 - nnew;
-      int v0 = 0, v1 = 0;
-      {
-        int sA = __shfl_sync(0xffffffffu, pa, old0 & 31), sB = __shfl_sync(0xffffffffu, pb, old0 & 31);
-        v0 = lane < nnew ? nl + lane : (old0 < 32 ? sA : sB);
-        int tA = __shfl_sync(0xffffffffu, pa, old1 & 31), tB = __shfl_sync(0xffffffffu, pb, old1 & 31);
-        v1 = lane + 32 < nnew ? nl + lane + 32 : (old1 < 32 ? tA : tB);
-      }
-      if (lane < nl2) prioA[lane] = v0;
-      if (lane + 32 < nl2) prioA[lane + 32] = v1;
-    }
-    for (int x = lane; x <= nl2; x += 32) loffA[x] = loffB[x];
-    __syncwarp();
-    nl = nl2;
-    j0 = j1;
-  }
-  for (int x = lane; x < n; x += 32) A.ilayer[off + x] = ilayer[x];
-  // stacking (planner.py:441-444)
-  int64_t *lbase = A.lbase + off;
-  __syncwarp();
-  long long carry = A.pers_size[t];
-  for (int base = 0; base < nl; base += 32) {
-    int l = base + lane;
-    long long v0 = l < nl ? lsize[l] : 0;
-    long long inc = warp_incl_sum(v0);
-    if (l < nl) lbase[l] = carry + inc - v0;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
-  }
-  if (lane == 0) {
-    A.nlayers[u] = nl;
-    A.gapins[u] = gapc;
-    A.pool[u] = carry;
-  }
-}
-
+// ---------------------------------------------------------------------------
 // E (narrow units, <= 32 layers -- every c4 unit): one warp per unit; the
 // per-item greedy is a short dependency chain. Lane p holds the same-class last
 // end of the layer at priority p and lane q the end of the class's new layer q;
 // each item is one ballot (gap host: the lowest fitting priority) raced against
 // one max-reduction + ballot (Alg. 1), both speculative, then a select. Layer
 // ids, insertion ranks (match_any) and the gap count are resolved lane-parallel
-// after each 32-item chunk; ilayer/irank go straight to global scratch so the
-// shared footprint is the slot CSR + merge buffers (6 ints per item). A unit
-// that would open a 33rd layer is handed to the CTA kernel.
+// after each 32-item chunk; ilayer/irank and the merge's output buffer live in
+// global scratch (L2), so the shared footprint is the slot CSR and the class
+// runs (4 ints per item). Units are packed host-side into CTAs of a fixed
+// shared-memory budget, largest first; `wslot` gives each warp its unit and
+// shared-memory offset (unit -1: idle warp). A unit that would open a 33rd
+// layer is handed to the CTA kernel.
 
 constexpr int kWN = 32;
+constexpr int kWarpsPerCta = 8;
+constexpr int kLayerSmemInts = 14336;  // 56 KB per CTA: four CTAs per SM
 
-__host__ __device__ constexpr int warpn_smem_ints(int cap) { return 6 * cap + 4 * (kWN + 1) + kWN; }
+__host__ __device__ constexpr int warpn_smem_ints(int n) { return 4 * n + 4 * (kWN + 1) + kWN; }
 
-__global__ void __launch_bounds__(256) k_layers_w32(LayerArgs A, const int32_t *__restrict__ ulist, int nunits,
-                                                    int cap, int32_t *__restrict__ over, int *__restrict__ nover) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, const int2 *__restrict__ wslot,
+                                                                  int32_t *__restrict__ over, int *__restrict__ nover) {
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ int32_t smem[];
   const int w = threadIdx.x >> 5, lane = lane_id();
-  const int ui = blockIdx.x * (blockDim.x >> 5) + w;
-  if (ui >= nunits) return;
-  const int u = ulist[ui];
+  const int2 slot = wslot[blockIdx.x * kWarpsPerCta + w];
+  if (slot.x < 0) return;
+  const int u = slot.x;
   const int c = u % A.C, t = u / A.C;
   const int v = A.var_of[c];
   const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
   const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
   const int n = (int)(a1 - a0);
   const int64_t off = A.uo[u];
-  int32_t *sm = smem + w * warpn_smem_ints(cap);
-  int32_t *sts = sm, *ste = sm + cap, *tts = sm + 2 * cap, *tte = sm + 3 * cap;  // slots + merge temp
-  int32_t *run_ts = sm + 4 * cap, *run_te = sm + 5 * cap;
-  int32_t *loffA = sm + 6 * cap, *loffB = loffA + (kWN + 1), *prio = loffB + (kWN + 1), *runoff = prio + (kWN + 1);
+  int32_t *sm = smem + slot.y;
+  int32_t *sts = sm, *ste = sm + n, *run_ts = sm + 2 * n, *run_te = sm + 3 * n;  // slots + class runs
+  int32_t *tts = A.sB_ts + off, *tte = A.sB_te + off;                              // merge output (global)
+  int32_t *loffA = sm + 4 * n, *loffB = loffA + (kWN + 1), *prio = loffB + (kWN + 1), *runoff = prio + (kWN + 1);
   int32_t *newcnt = runoff + (kWN + 1);
   const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
   const int64_t *gcend = A.cend + a0;
@@ -2069,21 +1852,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     seg_sort(ctx, ar, ihi, vtb + sb, vtb, ilo, tsb + qb, iperm, NI, d_io, (int64_t)V * T, max_items);
   }
   LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
-  pt.mark("D sort");
-  // classes
-  uint32_t *chead = ar.take<uint32_t>(NI + 1), *cid = ar.take<uint32_t>(NI + 1);
-  int64_t *cstart = ar.take<int64_t>(NI + 1), *cend = ar.take<int64_t>(NI + 1);
-  if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_class_heads, NI, it, d_io, V * T, NI, chead);
-  device_scan<uint32_t>(ctx, ar, chead, cid, NI, true);
-  uint32_t NC = 0;
-  if (NI) STW_CUDA(ctx, cudaMemcpyAsync(&NC, cid + NI - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx.stream));
-  sync(ctx);
-  LAUNCH(k_class_start, NI, chead, cid, NI, cstart);
-  LAUNCH(k_class_end, NI, cid, cstart, (int64_t)NC, NI, cend);
-
-  pt.mark("D classes");
-  // ---- E: layers per unit
+  // host-side preparation of phase E, overlapped with the D kernels: unit
+  // scratch offsets and the warp-per-unit CTA packing
   std::vector<int64_t> uo(U + 1, 0);
   for (int t = 0; t < T; t++)
     for (int c = 0; c < C; c++) {
@@ -2091,6 +1861,56 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       int64_t u = (int64_t)t * C + c;
       uo[u + 1] = uo[u] + (io[(int64_t)v * T + t + 1] - io[(int64_t)v * T + t]);
     }
+  // narrow units: one warp each, packed into fixed-budget CTAs (largest unit
+  // first, then the smallest ones that still fit); units too large for a
+  // CTA's budget, and any unit that needs > 32 layers, go to the CTA kernel
+  std::vector<int32_t> order, bigs;
+  order.reserve(U);
+  for (int64_t u = 0; u < U; u++) {
+    if (warpn_smem_ints((int)std::min<int64_t>(uo[u + 1] - uo[u], INT_MAX / 8)) <= kLayerSmemInts)
+      order.push_back((int32_t)u);
+    else
+      bigs.push_back((int32_t)u);
+  }
+  {  // stable counting sort by item count, descending
+    int64_t mx = 0;
+    for (int32_t u : order) mx = std::max(mx, uo[u + 1] - uo[u]);
+    std::vector<int64_t> pos(mx + 2, 0);
+    for (int32_t u : order) pos[mx - (uo[u + 1] - uo[u]) + 1]++;
+    for (int64_t k = 0; k <= mx; k++) pos[k + 1] += pos[k];
+    std::vector<int32_t> sorted(order.size());
+    for (int32_t u : order) sorted[pos[mx - (uo[u + 1] - uo[u])]++] = u;
+    order.swap(sorted);
+  }
+  std::vector<int2> wslot;
+  wslot.reserve(order.size() + kWarpsPerCta);
+  for (size_t i = 0, j = order.size(); i < j;) {
+    const size_t base = wslot.size();
+    int used = 0, k = 0;
+    auto put = [&](int32_t u) {
+      wslot.push_back(make_int2(u, used));
+      used += warpn_smem_ints((int)(uo[u + 1] - uo[u]));
+      k++;
+    };
+    put(order[i++]);
+    while (k < kWarpsPerCta && i < j && used + warpn_smem_ints((int)(uo[order[i] + 1] - uo[order[i]])) <= kLayerSmemInts)
+      put(order[i++]);
+    while (k < kWarpsPerCta && i < j && used + warpn_smem_ints((int)(uo[order[j - 1] + 1] - uo[order[j - 1]])) <= kLayerSmemInts)
+      put(order[--j]);
+    while (wslot.size() < base + kWarpsPerCta) wslot.push_back(make_int2(-1, 0));
+  }
+  pt.mark("D sort");
+  // classes
+  uint32_t *chead = ar.take<uint32_t>(NI + 1), *cid = ar.take<uint32_t>(NI + 1);
+  int64_t *cstart = ar.take<int64_t>(NI + 1), *cend = ar.take<int64_t>(NI + 1);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_class_heads, NI, it, d_io, V * T, NI, chead);
+  device_scan<uint32_t>(ctx, ar, chead, cid, NI, true);
+  LAUNCH(k_class_start, NI, chead, cid, NI, cstart);
+  LAUNCH(k_class_end, NI, cid, cstart, NI, cend);
+
+  pt.mark("D classes");
+  // ---- E: layers per unit (host-side unit layout and CTA packing were prepared during D)
   const int64_t TU = uo[U];
   int64_t *d_uo = h2d(ctx, ar, uo);
   uint8_t *d_cand = h2d(ctx, ar, hcand);
@@ -2105,77 +1925,27 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
                ar.take<int32_t>(U), ar.take<int64_t>(U), ar.take<int64_t>(U)};
   if (!ctx.ok()) return ctx.rc;
   {
-    // size buckets: warp-per-unit kernels with the CSR in shared memory; the
-    // largest units (and any unit that needs > kWL layers) go to the CTA kernel
-    static const int caps[] = {128, 256, 512, 1024, 2048};
-    const int NBK = 5;
-    std::vector<std::vector<int32_t>> lists(NBK + 1);
-    for (int64_t u = 0; u < U; u++) {
-      int64_t n_u = uo[u + 1] - uo[u];
-      int bk = 0;
-      while (bk < NBK && n_u > caps[bk]) bk++;
-      lists[bk].push_back((int32_t)u);
-    }
-    // largest units first inside each bucket (shortest tail)
-    for (auto &lst : lists)
-      std::stable_sort(lst.begin(), lst.end(),
-                       [&](int32_t x, int32_t y) { return uo[x + 1] - uo[x] > uo[y + 1] - uo[y]; });
-    std::vector<int32_t> flat;
-    std::vector<int64_t> loff(NBK + 2, 0);
-    for (int bk = 0; bk <= NBK; bk++) {
-      flat.insert(flat.end(), lists[bk].begin(), lists[bk].end());
-      loff[bk + 1] = flat.size();
-    }
-    int32_t *d_list = h2d(ctx, ar, flat);
+    const int nctas = (int)(wslot.size() / kWarpsPerCta);
     int32_t *d_over = ar.take<int32_t>(U + 1);
     int *d_nover = ar.take<int>(1);
+    int2 *d_wslot = nctas ? ar.take<int2>(wslot.size()) : nullptr;
+    int32_t *d_bigs = bigs.empty() ? nullptr : h2d(ctx, ar, bigs);
     if (!ctx.ok()) return ctx.rc;
     STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, sizeof(int), ctx.stream));
-    const int64_t nsmall = loff[NBK];
-    // units with <= 32 layers take the narrow warp kernel (STW_LAYERS_WIDE=1: the 64-layer one)
-    static const bool wide = getenv("STW_LAYERS_WIDE") != nullptr;
-    // the buckets run concurrently on forked streams (largest buckets first)
-    cudaEvent_t fork_ev = side_event(0), join_ev[NBK];
-    STW_CUDA(ctx, cudaEventRecord(fork_ev, ctx.stream));
-    for (int bk = NBK - 1; bk >= 0 && ctx.ok(); bk--) {
-      int nb = (int)(loff[bk + 1] - loff[bk]);
-      join_ev[bk] = nullptr;
-      if (!nb) continue;
-      cudaStream_t st = side_stream(bk);
-      STW_CUDA(ctx, cudaStreamWaitEvent(st, fork_ev, 0));
-      if (wide) {
-        size_t per_warp = (size_t)warp_smem_ints(caps[bk]) * sizeof(int32_t);
-        int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp));
-        size_t smem = per_warp * wpc;
-        STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int prof = prof_pre(st);
-        k_layers_warp<<<(nb + wpc - 1) / wpc, wpc * 32, smem, st>>>(LA, d_list + loff[bk], nb, caps[bk], d_over,
-                                                                   d_nover);
-        prof_post(st, "k_layers_warp", prof);
-      } else {
-        // two CTAs per SM: up to ~112 KB of slot CSR per CTA
-        size_t per_warp = (size_t)warpn_smem_ints(caps[bk]) * sizeof(int32_t);
-        int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (112u << 10) / per_warp));
-        size_t smem = per_warp * wpc;
-        STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_w32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int prof = prof_pre(st);
-        k_layers_w32<<<(nb + wpc - 1) / wpc, wpc * 32, smem, st>>>(LA, d_list + loff[bk], nb, caps[bk], d_over,
-                                                                  d_nover);
-        prof_post(st, "k_layers_w32", prof);
-      }
-      STW_LAUNCHED(ctx);
-      join_ev[bk] = side_event(1 + bk);
-      STW_CUDA(ctx, cudaEventRecord(join_ev[bk], st));
-    }
-    for (int bk = 0; bk < NBK; bk++)
-      if (loff[bk + 1] > loff[bk] && join_ev[bk]) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, join_ev[bk], 0));
-    int nbig = (int)(loff[NBK + 1] - loff[NBK]);
-    if (nbig) {
-      STW_KL(k_layers, (unsigned)nbig, kPlanThreads, ctx.stream, LA, d_list + loff[NBK], (const int *)nullptr);
+    if (nctas) {
+      STW_CUDA(ctx, cudaMemcpyAsync(d_wslot, wslot.data(), wslot.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                    ctx.stream));
+      const int smem = kLayerSmemInts * (int)sizeof(int32_t);
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_w32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      STW_KLS(k_layers_w32, (unsigned)nctas, kWarpsPerCta * 32, smem, ctx.stream, LA, d_wslot, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }
-    if (nsmall) {
-      STW_KL(k_layers, (unsigned)nsmall, kPlanThreads, ctx.stream, LA, d_over, d_nover);
+    if (!bigs.empty()) {
+      STW_KL(k_layers, (unsigned)bigs.size(), kPlanThreads, ctx.stream, LA, d_bigs, (const int *)nullptr);
+      STW_LAUNCHED(ctx);
+    }
+    if (nctas) {  // units that overflowed 32 layers (the kernel reads the count on the device)
+      STW_KL(k_layers, 296, kPlanThreads, ctx.stream, LA, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }
   }

@@ -122,23 +122,37 @@ static void raise_pool_threshold() {
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
+// Scratch is bump-allocated (256 B aligned) from stream-ordered chunks of at
+// least 32 MiB, so a planner call costs a handful of cudaMallocAsync calls
+// instead of one per buffer.
 void *Arena::raw(size_t bytes) {
   if (!ctx->ok()) return nullptr;
-  if (n == (int)(sizeof(ptrs) / sizeof(ptrs[0]))) {
-    ctx->fail(STW_ECUDA, "scratch arena: too many allocations");
-    return nullptr;
+  const size_t need = ((bytes ? bytes : 16) + 255) & ~(size_t)255;
+  if (need > left) {
+    if (n == (int)(sizeof(ptrs) / sizeof(ptrs[0]))) {
+      ctx->fail(STW_ECUDA, "scratch arena: too many chunks");
+      return nullptr;
+    }
+    raise_pool_threshold();
+    const size_t chunk = need > (32u << 20) ? need : (32u << 20);
+    void *p = nullptr;
+    STW_CUDA(*ctx, cudaMallocAsync(&p, chunk, ctx->stream));
+    if (!ctx->ok()) return nullptr;
+    ptrs[n++] = p;
+    cur = (char *)p;
+    left = chunk;
   }
-  raise_pool_threshold();
-  void *p = nullptr;
-  STW_CUDA(*ctx, cudaMallocAsync(&p, bytes ? bytes : 16, ctx->stream));
-  if (!ctx->ok()) return nullptr;
-  ptrs[n++] = p;
-  return p;
+  void *out = cur;
+  cur += need;
+  left -= need;
+  return out;
 }
 
 void Arena::release() {
   for (int i = 0; i < n; i++) cudaFreeAsync(ptrs[i], ctx->stream);
   n = 0;
+  cur = nullptr;
+  left = 0;
 }
 
 template <class T>
