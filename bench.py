@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="stw", choices=["stw", "reference"])
     ap.add_argument("--traces", type=int, default=4096, help="traces per rank (c4: 4096)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-sweep", action="store_true", help="skip the K1/K7/K2 >>L2 roofline sweep")
+    ap.add_argument("--sweep-reps", type=int, default=64, help="c4 copies in the K1/K7 sweep")
     ap.add_argument("--profile-print", action="store_true", help="per-kernel table on stderr")
     return ap.parse_args()
 
@@ -176,23 +178,131 @@ def measured_peaks():
 # algorithmic bytes per launch; w = workload counts of one step
 def algo_bytes(kernel: str, w: dict, launches_per_step: float) -> float:
     per_step = {
-        # planner layers: 32 B/event in + 8 B/event out, per unit (K5/K6)
-        "k_layers": 40.0 * w["unit_events"],
-        "k_layers_warp": 40.0 * w["unit_events"],
-        # K2 radix passes: read+write (8 B key + 4 B value) per record per pass
-        "k_radix_scatter": 24.0 * w["sort_records"],
-        "k_radix_hist": 8.0 * w["sort_records"],
-        # K7: 24 B per rectangle per candidate
+        # planner layers (K5/K6): 32 B/item in + 8 B/item out, per unit
+        "k_layers": 40.0 * w["unit_items"],
+        "k_layers_w32": 40.0 * w["unit_items"],
+        # K7 fast path: addr 8 B per (rectangle, candidate) + size/t_s/t_e 16 B per rectangle
+        "k_overlap_sweep": 8.0 * w["unit_events"] + 16.0 * w["events"],
         "k_validate_tiles": 24.0 * w["unit_events"],
         # fusion: the trace's events are read once per attempt at least
         "k_fusion": 32.0 * w["events"],
-        # K1 timeline: 16 B/event read + 16 B/timestep
-        "k_timeline_scatter": 16.0 * w["events"],
+        # K1: 17 B/event (t_s, t_e, size, dyn)
+        "k_peak_cta": 17.0 * w["events"],
+        # segmented sorts: 12 B/record read + written per sort
+        "k_seg_bitonic": 24.0 * w["events"],
         "k_emit": 40.0 * w["unit_events"],
     }.get(kernel)
     if per_step is None:
         return float("nan")
     return per_step / max(launches_per_step, 1.0)
+
+
+# ---------------------------------------------------------------------------
+# HBM roofline sweep of the data-parallel kernels (inputs >> L2)
+
+def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
+    """K1 (peak live bytes), K7 (validate_plan over many plans) and K2 (radix
+    sort) on inputs far larger than the 126 MB L2, each timed on its stream
+    with CUDA events (K1/K7: the library's per-launch events around the
+    kernel; K2: the whole multi-pass call). Returns {kernel: stats}."""
+    import torch
+
+    from paper_2507_16274_b200 import _lib, api
+
+    L = _lib.load()
+    err = _lib.errbuf()
+    stream = torch.cuda.current_stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+    out = {}
+
+    def kernel_ms(fn, name, iters=3):
+        fn()
+        torch.cuda.synchronize(dev)
+        _lib.profile_collect(reset=True)
+        _lib.profile(True)
+        for _ in range(iters):
+            fn()
+        torch.cuda.synchronize(dev)
+        _lib.profile(False)
+        prof = _lib.profile_collect(reset=True)
+        cnt, ms = prof[name]
+        return ms / cnt
+
+    def entry(name, records, unit_bytes, ms, note):
+        gbs = records * unit_bytes / (ms / 1e3) / 1e9
+        out[name] = {"kernel": name, "records": int(records), "algorithmic_bytes_per_record": unit_bytes,
+                     "ms": ms, "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "what": note}
+
+    # K1: R copies of the c4 batch (static_only, as the planner's self-check)
+    T, N = db.T, db.N
+    t = db.t
+    cols = {k: t[k].repeat(reps) for k in ("size", "t_s", "t_e", "dyn")}
+    ev_off = torch.cat([db.ev_off[:-1] + r * N for r in range(reps)] + [db.ev_off[-1:] + (reps - 1) * N])
+    horizon, n_sched = db.horizon.repeat(reps), db.n_sched.repeat(reps)
+    bk1 = _lib.Batch(T * reps, 1, N * reps, _lib.ptr(ev_off), _lib.ptr(t["id"]), _lib.ptr(cols["size"]),
+                     _lib.ptr(cols["t_s"]), _lib.ptr(cols["t_e"]), _lib.ptr(t["ps"]), _lib.ptr(t["pe"]),
+                     _lib.ptr(cols["dyn"]), _lib.ptr(horizon), _lib.ptr(n_sched))
+    peaks = np.zeros(T * reps, np.int64)
+
+    def k1():
+        _lib.check(L.stw_peak_live(C.byref(bk1), 1, _lib.ptr(peaks), sh, err, 1024), err)
+
+    ms = kernel_ms(k1, "k_peak_cta")
+    entry("k_peak_cta", N * reps, 17.0, ms, f"K1 peak live bytes, {reps}x c4 ({N * reps} events); "
+          "17 B/event read (t_s, t_e, size, dyn), timeline in shared memory")
+    del cols, ev_off, horizon, n_sched
+
+    # K7: the c4 plans of all 4 candidates, sweep-ordered, R copies
+    stat = np.concatenate([tr.dyn == 0 for tr in hb.traces])
+    keep = torch.from_numpy(np.flatnonzero(stat)).to(dev)
+    cnt = torch.from_numpy(np.asarray([int((tr.dyn == 0).sum()) for tr in hb.traces], np.int64))
+    off1 = torch.zeros(T + 1, dtype=torch.int64)
+    off1[1:] = torch.cumsum(cnt, 0)
+    n1 = int(off1[-1])
+    off = torch.cat([off1[:-1] + r * n1 for r in range(reps)] + [off1[-1:] + (reps - 1) * n1]).to(dev)
+    ts, te, sz = (t[k].index_select(0, keep).repeat(reps) for k in ("t_s", "t_e", "size"))
+    ad = planned_addr.index_select(1, keep).repeat(1, reps).contiguous()
+    nc = ad.shape[0]
+    count = [None]
+
+    def k7():
+        count[0] = api.validate_sets(off, ts, te, sz, ad, 9)
+
+    ms = kernel_ms(k7, "k_overlap_sweep")
+    assert int(count[0].abs().sum()) == 0, "planner output failed validation"
+    entry("k_overlap_sweep", n1 * reps * nc, (16.0 + 8.0 * nc) / nc, ms,
+          f"K7 validate_plan of {T * reps * nc} plans ({n1 * reps} rectangles x {nc} candidates); "
+          "per (rectangle, candidate): addr 8 B + the shared size/t_s/t_e 16 B over the candidates")
+    del ts, te, sz, ad, off
+
+    # K2: 2^27 (u64 key, u32 value) pairs, 42-bit keys (c5's widest sort: 6 passes)
+    n2 = 1 << 27
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    keys0 = torch.randint(0, 1 << 42, (n2,), dtype=torch.int64, device=dev, generator=g)
+    keys = torch.empty_like(keys0)
+    vals = torch.empty(n2, dtype=torch.int32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot = 0.0
+    for it in range(4):
+        keys.copy_(keys0)
+        torch.arange(n2, dtype=torch.int32, device=dev, out=vals)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        api.radix_sort_pairs(keys, vals, 0, 42, stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if it:
+            tot += e0.elapsed_time(e1)
+    ms = tot / 3
+    assert bool((keys[1:] >= keys[:-1]).all()), "radix sort output not sorted"
+    passes = 6
+    entry("radix_sort_pairs", n2, 24.0 * passes, ms,
+          f"K2 stable LSD radix sort of {n2} (u64, u32) pairs on 42 key bits ({passes} passes); "
+          "24 B/record/pass (key + value read and written)")
+    del keys0, keys, vals
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -238,8 +348,9 @@ def main():
     o_best = torch.empty(T, dtype=torch.int32, device=dev)
     o_bpool = torch.empty(T, dtype=torch.int64, device=dev)
     o_abest = torch.empty(N, dtype=torch.int64, device=dev)
-    dev_out = _lib.PlanOut(1, _lib.ptr(o_rc), _lib.ptr(o_err), _lib.ptr(o_stats), None, None, None, None, None,
-                           None, None, _lib.ptr(o_best), _lib.ptr(o_abest), _lib.ptr(o_bpool))
+    o_addr = torch.empty((Cn, N), dtype=torch.int64, device=dev)  # every candidate's plan (validated in the sweep)
+    dev_out = _lib.PlanOut(1, _lib.ptr(o_rc), _lib.ptr(o_err), _lib.ptr(o_stats), _lib.ptr(o_addr), None, None,
+                           None, None, None, None, _lib.ptr(o_best), _lib.ptr(o_abest), _lib.ptr(o_bpool))
     opts = _lib.PlanOpts(Cn, 1, _lib.ptr(cb), 512, sh)
     dstruct = db.struct()
     err = _lib.errbuf()
@@ -271,7 +382,8 @@ def main():
         raise SystemExit(f"planner reported errors on {int((rc != 0).sum())} units")
     planned = int(stats[:, 0].sum())  # static events given an address, summed over candidates
     events = N
-    w = {"events": events, "unit_events": planned, "sort_records": events}
+    items = int(stats[:, 3].sum() + stats[:, 4].sum() - stats[:, 6].sum())  # plans + residuals - fused away
+    w = {"events": events, "unit_events": planned, "unit_items": items}
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # 256 MiB > 126 MB L2
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -343,6 +455,10 @@ def main():
         for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
             print(f"{k:28s} launches {c:6d}  total {ms:9.3f} ms  avg {ms / c:8.4f} ms", file=sys.stderr)
 
+    sweep = None
+    if not args.no_kernel_sweep:
+        sweep = kernel_sweep(dev, db, hb, o_addr, args.sweep_reps, hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -366,6 +482,7 @@ def main():
                     "d2h_bytes_per_step": int(N * 8 + T * (4 + 8) + T * Cn * (4 + 16 + 8 * _lib.NSTATS))},
             "gpu_launches": int(launches),
             "roofline": roofline,
+            "kernel_roofline": sweep,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

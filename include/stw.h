@@ -58,7 +58,7 @@ int stw_peak_live(const stw_batch *b, int32_t static_only, int64_t *peak, void *
                   char *err, size_t errlen);
 
 /* ---- K2: stable LSD radix sort of (u64 key, u32 value) pairs ------------
- * Device pointers; sorts bits [begin_bit, end_bit) in place. Used by every
+ * Device pointers, n < 2^30; sorts bits [begin_bit, end_bit) in place. Used by every
  * sort of the hot path (planner.py:82-83,392,419,455,483; sim.py:158,169). */
 int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begin_bit,
                          int32_t end_bit, void *stream, char *err, size_t errlen);
@@ -111,6 +111,28 @@ int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *
 int stw_validate(int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
                  const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs,
                  int64_t cap, void *stream, char *err, size_t errlen);
+
+/* ---- K7 over many plans: validate_plan of every (set, candidate) ---------
+ * The batched sweep's self-check as one call: decision set s owns
+ * rectangles [set_off[s], set_off[s+1]) listed in its sweep order ((t_s, id)
+ * order, planner.py:483); t_s/t_e/size are shared by the candidates and addr
+ * is [n_cand][n]. All pointers are device pointers. count[s*n_cand + c] (device)
+ * receives len(validate_plan(...)) of that plan -- 0 for a valid plan. Plans
+ * whose addresses and sizes are multiples of 2^shift take the fast exact
+ * overlap sweep; anything else (and any plan with a conflict) the exact
+ * reporter. */
+typedef struct {
+  int32_t n_sets;
+  int32_t n_cand;
+  int64_t n;
+  const int64_t *set_off;
+  const int32_t *t_s, *t_e;
+  const int64_t *size;
+  const int64_t *addr;
+} stw_rect_sets;
+
+int stw_validate_sets(const stw_rect_sets *rs, int32_t shift, int64_t *count, void *stream, char *err,
+                      size_t errlen);
 
 /* ---- K8: derive_reuse_map (reuse.py:54-93) ------------------------------
  * Static decisions (host SoA) and K key windows [t_lo, t_hi]. Key k's free

@@ -64,9 +64,14 @@ class Bundle(C.Structure):
         ("reuse", C.c_int32)]
 
 
+class RectSets(C.Structure):
+    _fields_ = [("n_sets", C.c_int32), ("n_cand", C.c_int32), ("n", C.c_int64)] + [
+        (n, C.c_void_p) for n in ("set_off", "t_s", "t_e", "size", "addr")]
+
+
 EXPORTS = (
     "stw_version", "stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_validate",
-    "stw_reuse_map", "stw_simulate", "stw_baseline",
+    "stw_validate_sets", "stw_reuse_map", "stw_simulate", "stw_baseline",
 )
 
 _lib = None

@@ -53,6 +53,24 @@ def radix_sort_pairs(keys, vals, begin_bit: int = 0, end_bit: int = 64, stream=N
                                       C.c_int32(end_bit), s, err, C.sizeof(err)), err)
 
 
+def validate_sets(set_off, t_s, t_e, size, addr, shift: int = 9, stream=None):
+    """len(validate_plan(plan)) for every (set, candidate) plan of a batch, on the
+    device (K7 over many plans; planner.py:476-505). Device tensors: set_off
+    int64 [S+1], t_s/t_e int32 [n] and size int64 [n] in each set's sweep
+    order, addr int64 [n_cand, n]. Returns an int64 device tensor [S * n_cand]."""
+    import torch
+
+    n_sets = int(set_off.numel()) - 1
+    n_cand = int(addr.shape[0]) if addr.dim() == 2 else 1
+    count = torch.empty(max(n_sets * n_cand, 1), dtype=torch.int64, device=addr.device)
+    rs = _lib.RectSets(n_sets, n_cand, int(t_s.numel()), _lib.ptr(set_off), _lib.ptr(t_s), _lib.ptr(t_e),
+                       _lib.ptr(size), _lib.ptr(addr))
+    err = _lib.errbuf()
+    _lib.check(_lib.load().stw_validate_sets(C.byref(rs), C.c_int32(shift), _lib.ptr(count),
+                                             _lib.stream_handle(stream), err, C.sizeof(err)), err)
+    return count[: n_sets * n_cand]
+
+
 # ---------------------------------------------------------------------------
 # planner (planner.py:357-505)
 

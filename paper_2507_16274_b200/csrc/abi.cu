@@ -1,6 +1,6 @@
 // C-ABI entry points of libstw (include/stw.h). Each wraps one hot-path
 // stage in an error context + scratch arena and is synchronous on return.
-#include "batch.cuh"
+#include "planner.cuh"
 
 using namespace stw;
 
@@ -50,7 +50,7 @@ int stw_peak_live(const stw_batch *b, int32_t static_only, int64_t *peak, void *
 int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begin_bit, int32_t end_bit,
                          void *stream, char *err, size_t errlen) {
   STW_ENTRY(stream, err, errlen);
-  if (begin_bit < 0 || end_bit > 64 || n < 0 || n >= (int64_t)UINT32_MAX) {
+  if (begin_bit < 0 || end_bit > 64 || n < 0 || n >= (int64_t)1 << 30) {
     ctx.fail(STW_EARG, "bad sort arguments");
     return ctx.rc;
   }
@@ -80,6 +80,22 @@ int stw_validate(int64_t n, const int64_t *id, const int64_t *addr, const int64_
     return ctx.rc;
   }
   validate_plan_pairs(ctx, n, id, addr, size, t_s, t_e, n_pairs, pairs, cap);
+  return finish(ctx);
+}
+
+int stw_validate_sets(const stw_rect_sets *r, int32_t shift, int64_t *count, void *stream, char *err,
+                      size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (!r || !count || r->n_sets < 0 || r->n_cand <= 0 || r->n < 0 || shift < 0 || shift > 62) {
+    ctx.fail(STW_EARG, "bad validate_sets arguments");
+    return ctx.rc;
+  }
+  {
+    Arena ar(&ctx);
+    RectSets rs{r->n_sets, r->n, r->set_off, r->t_s, r->t_e, r->size, r->n_cand, r->addr};
+    int *first = ar.take<int>((int64_t)r->n_sets * r->n_cand + 1);
+    if (ctx.ok() && r->n_sets > 0) validate_sets(ctx, ar, rs, (long long *)count, first, shift);
+  }
   return finish(ctx);
 }
 

@@ -69,48 +69,48 @@ __global__ void k_segmax(const int64_t *__restrict__ P, int64_t H, const int64_t
 // deltas by shared-memory atomics, then each thread scans a contiguous chunk
 // (local prefix + local max), one block scan of the chunk sums, and the peak
 // is max(excl + local max) -- the timeline never touches HBM, so the kernel
-// reads 17 B per event (t_s, t_e, size, dyn) and writes 8 B per trace.
-// A trace with a timestamp outside [0, kPeakSmem) is flagged for the
-// global-timeline path below.
-constexpr int kPeakThreads = 256;
-constexpr int kPeakSmem = 6016;  // timeline entries (47 KB of static shared memory)
+// reads 17 B per event (t_s, t_e, size, dyn) and writes 8 B per trace. The
+// timeline is sized by the batch's largest horizon (dynamic shared memory);
+// a trace with a longer horizon or a timestamp outside [0, horizon] is
+// flagged for the global-timeline path below.
+constexpr int kPeakThreads = 128;
+constexpr int kPeakSmemMax = 12288;  // timeline entries (96 KB)
 
 __global__ void __launch_bounds__(kPeakThreads) k_peak_cta(const int64_t *__restrict__ ev_off,
                                                            const int64_t *__restrict__ size,
                                                            const int32_t *__restrict__ t_s,
                                                            const int32_t *__restrict__ t_e,
-                                                           const uint8_t *__restrict__ dyn, int static_only,
-                                                           long long *__restrict__ peak, int *__restrict__ nbig,
-                                                           int32_t *__restrict__ big) {
-  __shared__ unsigned long long D[kPeakSmem];
+                                                           const uint8_t *__restrict__ dyn,
+                                                           const int32_t *__restrict__ horizon, int hcap,
+                                                           int static_only, long long *__restrict__ peak,
+                                                           int *__restrict__ nbig, int32_t *__restrict__ big) {
+  extern __shared__ unsigned long long D[];
   __shared__ long long sh[33];
-  __shared__ int sh_hi;
   const int t = blockIdx.x, tid = threadIdx.x;
   const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
-  if (tid == 0) sh_hi = -1;
-  for (int x = tid; x < kPeakSmem; x += kPeakThreads) D[x] = 0;
+  const int H = horizon[t] + 1;  // timestamps are in [0, horizon] (model.py:240-241)
+  if (H > hcap || H <= 0) {
+    if (tid == 0) big[atomicAdd(nbig, 1)] = t;
+    return;
+  }
+  for (int x = tid; x < H; x += kPeakThreads) D[x] = 0;
   __syncthreads();
-  int hi = -1;
   bool bad = false;
   for (int64_t i = e0 + tid; i < e1; i += kPeakThreads) {
     if (static_only && dyn[i]) continue;
     const int a = t_s[i], z = t_e[i];
-    if (a < 0 || z < 0 || a >= kPeakSmem || z >= kPeakSmem) {
+    if ((unsigned)a >= (unsigned)H || (unsigned)z >= (unsigned)H) {
       bad = true;
       continue;
     }
     const unsigned long long sz = (unsigned long long)size[i];
     atomicAdd(D + a, sz);
     atomicAdd(D + z, 0ull - sz);
-    hi = max(hi, max(a, z));
   }
   if (__syncthreads_or(bad)) {
     if (tid == 0) big[atomicAdd(nbig, 1)] = t;
     return;
   }
-  if (hi >= 0) atomicMax(&sh_hi, hi);
-  __syncthreads();
-  const int H = sh_hi + 1;
   const int per = (H + kPeakThreads - 1) / kPeakThreads;
   const int x0 = min(H, tid * per), x1 = min(H, x0 + per);
   long long run = 0, best = LLONG_MIN;
@@ -121,7 +121,6 @@ __global__ void __launch_bounds__(kPeakThreads) k_peak_cta(const int64_t *__rest
   long long tot;
   const long long ex = block_excl_sum<long long>(run, sh, &tot);
   long long cand = best == LLONG_MIN ? LLONG_MIN : ex + best;
-  // block max
   for (int o = 16; o; o >>= 1) cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, o));
   if ((tid & 31) == 0) sh[tid >> 5] = cand;
   __syncthreads();
@@ -147,8 +146,13 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
   int32_t *big = ar.take<int32_t>(T);
   if (!ctx.ok()) return;
   STW_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(int), ctx.stream));
-  STW_KL(k_peak_cta, (unsigned)T, kPeakThreads, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e, b.dyn,
-         static_only ? 1 : 0, (long long *)d_peak, nbig, big);
+  int hmax = 0;
+  for (int x : b.h_horizon) hmax = std::max(hmax, x);
+  const int hcap = std::min(hmax + 1, kPeakSmemMax);
+  const int smem = hcap * (int)sizeof(unsigned long long);
+  STW_CUDA(ctx, cudaFuncSetAttribute(k_peak_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  STW_KLS(k_peak_cta, (unsigned)T, kPeakThreads, smem, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e, b.dyn,
+          b.horizon, hcap, static_only ? 1 : 0, (long long *)d_peak, nbig, big);
   STW_LAUNCHED(ctx);
   int h = 0;
   STW_CUDA(ctx, cudaMemcpyAsync(&h, nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));

@@ -51,9 +51,6 @@ void device_scan(Ctx &ctx, Arena &ar, const T *in, T *out, int64_t n, bool inclu
 // ---------------------------------------------------------------------------
 // radix sort
 
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;
 
 void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64_t n, int begin_bit,
                       int end_bit);

@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -178,100 +179,177 @@ template void device_scan<uint64_t>(Ctx &, Arena &, const uint64_t *, uint64_t *
 template void device_scan<int32_t>(Ctx &, Arena &, const int32_t *, int32_t *, int64_t, bool);
 
 // ---------------------------------------------------------------------------
-// K2: LSD radix sort, 8-bit digits.
-// Pass = upsweep (per-tile digit histogram, digit-major) -> exclusive scan ->
-// downsweep (stable rank inside the tile via warp match_any, scatter).
+// K2: stable LSD radix sort, 8-bit digits, one kernel per pass ("onesweep":
+// decoupled look-back instead of a separate upsweep/scan/downsweep).
+//
+//  k_os_hist  one read of the keys -> the digit histograms of every pass
+//  k_os_bins  exclusive scan of each pass's 256 bins
+//  k_os_pass  per 3840-key tile (tile ids handed out in launch order by an
+//             atomic counter): warp-level stable ranking with match_any into
+//             per-warp digit counters, publish the tile's digit counts, look
+//             back over earlier tiles' published counts/prefixes (one thread
+//             per digit), stage the tile in shared memory in digit order and
+//             write it out in digit runs (coalesced).
+// Traffic per pass: 12 B read + 12 B written per (key, value) pair.
 
-__global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint64_t *__restrict__ keys,
-                                                             uint32_t *__restrict__ counts, int64_t n,
-                                                             int shift, uint32_t mask, int ntiles) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
+constexpr int kOsThreads = 256;  // one thread per digit in the look-back
+constexpr int kOsItems = 15;
+constexpr int kOsTile = kOsThreads * kOsItems;
+constexpr int kOsWarps = kOsThreads / 32;
+constexpr uint32_t kOsAgg = 1u << 30, kOsPrefix = 2u << 30, kOsVal = kOsAgg - 1;
+constexpr size_t kOsSmem = (size_t)kOsTile * 12 + (size_t)kOsWarps * 256 * 4 + 256 * 4 + 256 * 8 + 16;
+
+__global__ void __launch_bounds__(256) k_os_hist(const uint64_t *__restrict__ keys, int64_t n, int begin_bit,
+                                                 int end_bit, int passes, uint32_t *__restrict__ hist) {
+  __shared__ uint32_t h[8][256];
+  for (int x = threadIdx.x; x < 8 * 256; x += blockDim.x) (&h[0][0])[x] = 0;
   __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * kSortTile;
-#pragma unroll 4
-  for (int j = 0; j < kSortItems; j++) {
-    int64_t i = base + j * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & mask], 1u);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    for (int p = 0; p < passes; p++) {
+      const int b = begin_bit + 8 * p, w = min(8, end_bit - b);
+      atomicAdd(&h[p][(uint32_t)(k >> b) & ((1u << w) - 1)], 1u);
+    }
   }
   __syncthreads();
-  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  for (int x = threadIdx.x; x < passes * 256; x += blockDim.x) {
+    const uint32_t c = (&h[0][0])[x];
+    if (c) atomicAdd(hist + x, c);
+  }
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
-    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
-    uint32_t *__restrict__ vout, const uint32_t *__restrict__ offs, int64_t n, int shift, uint32_t mask,
-    int ntiles) {
-  constexpr int W = kSortThreads / 32;
-  __shared__ uint32_t base[256];
-  __shared__ uint32_t wc[W][256];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  base[tid] = offs[(int64_t)tid * ntiles + blockIdx.x];
-  int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
-  for (int j = 0; j < kSortItems; j++) {
+__global__ void __launch_bounds__(256) k_os_bins(uint32_t *__restrict__ hist) {
+  __shared__ uint32_t sh[33];
+  uint32_t *hp = hist + blockIdx.x * 256;
+  const uint32_t v = hp[threadIdx.x];
+  hp[threadIdx.x] = block_excl_sum<uint32_t>(v, sh, nullptr);
+}
+
+__global__ void __launch_bounds__(kOsThreads) k_os_pass(const uint64_t *__restrict__ kin,
+                                                        const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+                                                        uint32_t *__restrict__ vout, int64_t n, int shift,
+                                                        uint32_t mask, const uint32_t *__restrict__ bins,
+                                                        uint32_t *__restrict__ status, uint32_t *__restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char os_smem[];
+  uint64_t *sk = (uint64_t *)os_smem;
+  uint32_t *sv = (uint32_t *)(sk + kOsTile);
+  uint32_t *wh = sv + kOsTile;             // [warp][digit] counts, then warp offsets
+  uint32_t *texcl = wh + kOsWarps * 256;   // tile-local exclusive offsets per digit
+  int64_t *gbase = (int64_t *)(texcl + 256);  // global base per digit (minus texcl)
+  uint32_t *stile = (uint32_t *)(gbase + 256);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (tid == 0) *stile = atomicAdd(ctr, 1u);
+  for (int x = tid; x < kOsWarps * 256; x += kOsThreads) wh[x] = 0;
+  __syncthreads();
+  const uint32_t tile = *stile;
+  const int64_t base = (int64_t)tile * kOsTile + (int64_t)w * (kOsItems * 32);
+  uint64_t k[kOsItems];
+  uint32_t v[kOsItems];
 #pragma unroll
-    for (int w = 0; w < W; w++) wc[w][tid] = 0;
-    __syncthreads();
-    int64_t i = tile0 + j * kSortThreads + tid;
-    bool valid = i < n;
-    uint64_t k = valid ? kin[i] : 0;
-    uint32_t v = valid ? vin[i] : 0;
-    uint32_t d = (uint32_t)(k >> shift) & mask;
-    unsigned vm = __ballot_sync(0xffffffffu, valid);
-    unsigned peers = 0, rank = 0;
-    if (valid) {
-      peers = __match_any_sync(vm, d);
-      rank = __popc(peers & lanemask_lt());
-      if (rank == 0) wc[warp][d] = __popc(peers);
-    }
-    __syncthreads();
-    {  // exclusive prefix over warps for digit tid
-      uint32_t s = 0;
+  for (int j = 0; j < kOsItems; j++) {
+    const int64_t i = base + j * 32 + lane;
+    k[j] = i < n ? kin[i] : 0;
+    v[j] = i < n ? vin[i] : 0;
+  }
+  uint16_t rk[kOsItems];
+  uint32_t *myh = wh + w * 256;
 #pragma unroll
-      for (int w = 0; w < W; w++) {
-        uint32_t c = wc[w][tid];
-        wc[w][tid] = s;
-        s += c;
-      }
-      __syncthreads();
-      if (valid) {
-        uint32_t pos = base[d] + wc[warp][d] + rank;
-        kout[pos] = k;
-        vout[pos] = v;
-      }
-      __syncthreads();
-      base[tid] += s;
+  for (int j = 0; j < kOsItems; j++) {
+    const bool valid = base + j * 32 + lane < n;
+    const uint32_t d = valid ? (uint32_t)(k[j] >> shift) & mask : 256u + lane;  // invalid: a group of its own
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t r = __popc(peers & lanemask_lt());
+    const uint32_t before = valid ? myh[d] : 0;
+    __syncwarp();
+    if (valid && r == (uint32_t)__popc(peers) - 1) myh[d] = before + __popc(peers);
+    __syncwarp();
+    rk[j] = (uint16_t)(before + r);
+  }
+  __syncthreads();
+  // digit tid: offsets of each warp inside the tile's run of that digit
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int x = 0; x < kOsWarps; x++) {
+    const uint32_t c = wh[x * 256 + tid];
+    wh[x * 256 + tid] = cnt;
+    cnt += c;
+  }
+  // publish, then look back over the earlier tiles for this digit
+  volatile uint32_t *st = status;
+  if (tile == 0) {
+    atomicExch(status + tid, kOsPrefix | cnt);
+  } else {
+    atomicExch(status + (int64_t)tile * 256 + tid, kOsAgg | cnt);
+  }
+  uint32_t excl = 0;
+  if (tile > 0) {
+    for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+      const uint32_t s = st[t * 256 + tid];
+      if (s == 0) continue;  // not published yet
+      excl += s & kOsVal;
+      if (s & kOsPrefix) break;
+      t--;
     }
-    __syncthreads();
+    atomicExch(status + (int64_t)tile * 256 + tid, kOsPrefix | (excl + cnt));
+  }
+  __shared__ uint32_t shs[33];
+  const uint32_t tx = block_excl_sum<uint32_t>(cnt, shs, nullptr);
+  texcl[tid] = tx;
+  gbase[tid] = (int64_t)bins[tid] + excl - tx;
+  __syncthreads();
+  // stage the tile in digit order
+#pragma unroll
+  for (int j = 0; j < kOsItems; j++) {
+    if (base + j * 32 + lane < n) {
+      const uint32_t d = (uint32_t)(k[j] >> shift) & mask;
+      const uint32_t pos = texcl[d] + wh[w * 256 + d] + rk[j];
+      sk[pos] = k[j];
+      sv[pos] = v[j];
+    }
+  }
+  __syncthreads();
+  const int64_t t0 = (int64_t)tile * kOsTile;
+  const int cnt_tile = (int)(n - t0 < kOsTile ? n - t0 : kOsTile);
+  for (int i = tid; i < cnt_tile; i += kOsThreads) {
+    const uint64_t key = sk[i];
+    const uint32_t d = (uint32_t)(key >> shift) & mask;
+    const int64_t g = gbase[d] + i;
+    kout[g] = key;
+    vout[g] = sv[i];
   }
 }
 
 void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64_t n, int begin_bit,
                       int end_bit) {
   if (n <= 1 || end_bit <= begin_bit || !ctx.ok()) return;
-  int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  const int64_t ntiles = (n + kOsTile - 1) / kOsTile;
   uint64_t *k2 = ar.take<uint64_t>(n);
   uint32_t *v2 = ar.take<uint32_t>(n);
-  uint32_t *counts = ar.take<uint32_t>((size_t)256 * ntiles);
+  uint32_t *hist = ar.take<uint32_t>((size_t)passes * 256);
+  uint32_t *status = ar.take<uint32_t>((size_t)ntiles * 256);
+  uint32_t *ctr = ar.take<uint32_t>(passes);
   if (!ctx.ok()) return;
+  STW_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)passes * 256 * sizeof(uint32_t), ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(ctr, 0, passes * sizeof(uint32_t), ctx.stream));
+  STW_KL(k_os_hist, grid_for(n, 256, 148 * 8), 256, ctx.stream, keys, n, begin_bit, end_bit, passes, hist);
+  STW_KL(k_os_bins, passes, 256, ctx.stream, hist);
+  STW_LAUNCHED(ctx);
+  static bool attr = false;
+  if (!attr) {
+    STW_CUDA(ctx, cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOsSmem));
+    attr = true;
+  }
   uint64_t *ka = keys, *kb = k2;
   uint32_t *va = vals, *vb = v2;
-  int passes = 0;
-  for (int b = begin_bit; b < end_bit; b += 8) {
-    int w = end_bit - b < 8 ? end_bit - b : 8;
-    uint32_t mask = (1u << w) - 1;
-    STW_KL(k_radix_hist, ntiles, kSortThreads, ctx.stream, ka, counts, n, b, mask, ntiles);
+  for (int p = 0; p < passes && ctx.ok(); p++) {
+    const int b = begin_bit + 8 * p, w = end_bit - b < 8 ? end_bit - b : 8;
+    STW_CUDA(ctx, cudaMemsetAsync(status, 0, (size_t)ntiles * 256 * sizeof(uint32_t), ctx.stream));
+    STW_KLS(k_os_pass, (unsigned)ntiles, kOsThreads, kOsSmem, ctx.stream, ka, va, kb, vb, n, b, (1u << w) - 1,
+            hist + p * 256, status, ctr + p);
     STW_LAUNCHED(ctx);
-    device_scan<uint32_t>(ctx, ar, counts, counts, (int64_t)256 * ntiles, false);
-    STW_KL(k_radix_scatter, ntiles, kSortThreads, ctx.stream, ka, va, kb, vb, counts, n, b, mask, ntiles);
-    STW_LAUNCHED(ctx);
-    uint64_t *tk = ka;
-    ka = kb;
-    kb = tk;
-    uint32_t *tv = va;
-    va = vb;
-    vb = tv;
-    passes++;
+    std::swap(ka, kb);
+    std::swap(va, vb);
   }
   if (passes & 1) {
     STW_CUDA(ctx, cudaMemcpyAsync(keys, ka, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx.stream));

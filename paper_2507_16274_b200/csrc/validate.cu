@@ -293,9 +293,8 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
       pts = ts[kn];
       pte = te[kn];
     }
-    const int t0n = k0 + 32 < n ? __shfl_sync(FULL, pts, 0) : INT_MAX;  // start of the next tile
     const long long end = a + sz;
-    const bool ok = !valid || (a >= 0 && sz > 0 && dte > dts && ((a | sz) & low) == 0 && (end >> shift) <= INT_MAX);
+    const bool ok = !valid || (a >= 0 && sz > 0 && dts >= 0 && dte > dts && ((a | sz) & low) == 0 && (end >> shift) <= INT_MAX);
     if (__any_sync(FULL, !ok)) {
       if (lane == 0) atomicAdd(nflag, 1);
       return;
@@ -303,21 +302,25 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
     const int da = (int)(a >> shift), de = (int)(end >> shift);
     if (valid) Tt[lane] = make_int4(da, de, dts, dte);
     __syncwarp();
-    bool hit = false;
+    // overlap <=> (c.addr - d.end) < 0, (d.addr - c.end) < 0 and (d.ts - c.te) < 0: the
+    // sign bit of the AND of the three differences (all operands are in [0, 2^31))
+    int acc = 0;
     if (valid) {
+#pragma unroll 4
       for (int j = 0; j < na; j++) {
         const int4 q = A[j];
-        hit |= (q.w > dts) & (q.x < de) & (q.y > da);
+        acc |= (q.x - de) & (da - q.y) & (dts - q.w);
       }
       for (int j = 0; j < lane; j++) {
         const int4 q = Tt[j];
-        hit |= (q.w > dts) & (q.x < de) & (q.y > da);
+        acc |= (q.x - de) & (da - q.y) & (dts - q.w);
       }
     }
-    if (__any_sync(FULL, hit)) {
+    if (__any_sync(FULL, acc < 0)) {
       if (lane == 0) atomicAdd(nflag, 1);
       return;
     }
+    const int t0n = k0 + 32 < n ? __shfl_sync(FULL, pts, 0) : INT_MAX;  // start of the next tile
     int nn = 0;
     for (int cb = 0; cb < na; cb += 32) {
       const int j = cb + lane;

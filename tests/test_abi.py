@@ -20,7 +20,8 @@ def declared_functions():
 
 def test_header_declares_the_reference_replacements():
     names = declared_functions()
-    for must in ("stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_validate", "stw_reuse_map",
+    for must in ("stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_validate", "stw_validate_sets",
+                 "stw_reuse_map",
                  "stw_simulate", "stw_baseline", "stw_version"):
         assert must in names
 

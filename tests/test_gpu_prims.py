@@ -86,3 +86,46 @@ def test_peak_live_batched(cuda):
     b = hb.struct()
     _lib.check(_lib.load().stw_peak_live(C.byref(b), 1, _lib.ptr(out), None, err, 1024), err)
     assert out.tolist() == [_peak_oracle(t, static_only=True) for t in tas]
+
+
+def _c4_rect_sets(n_traces, cuda):
+    """Sweep-ordered static rectangles of the c4 plans (4 candidates) on the device."""
+    import torch
+
+    tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(n_traces)]
+    bp = api.plan_batch(tas, tracegen.C4_CANDIDATES)
+    off, ts, te, sz, ad = [0], [], [], [], []
+    for t, ta in enumerate(tas):
+        s0 = int(bp.batch.ev_off[t])
+        o = np.lexsort((ta.id, ta.t_s))  # sweep order (t_s, id)
+        o = o[ta.dyn[o] == 0]
+        ts.append(ta.t_s[o])
+        te.append(ta.t_e[o])
+        sz.append(ta.size[o])
+        ad.append(bp.addr[:, s0 + o])
+        off.append(off[-1] + o.size)
+    cat = lambda xs, dt: torch.from_numpy(np.ascontiguousarray(np.concatenate(xs, axis=-1), dtype=dt)).to(cuda)  # noqa
+    return (torch.tensor(off, dtype=torch.int64, device=cuda), cat(ts, np.int32), cat(te, np.int32),
+            cat(sz, np.int64), cat(ad, np.int64))
+
+
+def test_validate_sets_valid_and_conflicting(cuda):
+    """Batched K7 (fast overlap sweep + exact fallback) vs the oracle's validate_plan."""
+    off, ts, te, sz, ad = _c4_rect_sets(48, cuda)
+    assert int(api.validate_sets(off, ts, te, sz, ad).abs().sum()) == 0
+    rng = np.random.default_rng(7)
+    h_ad = ad.cpu().numpy().copy()
+    h_off, h_ts, h_te, h_sz = off.cpu().numpy(), ts.cpu().numpy(), te.cpu().numpy(), sz.cpu().numpy()
+    for _ in range(40):  # move random rectangles onto other addresses (conflicts in most units)
+        c, k = int(rng.integers(0, 4)), int(rng.integers(0, h_ts.size))
+        h_ad[c, k] = h_ad[c, int(rng.integers(0, h_ts.size))]
+    h_ad[1, 5] += 256  # not a multiple of 2^9: that unit takes the exact reporter
+    import torch
+
+    got = api.validate_sets(off, ts, te, sz, torch.from_numpy(h_ad).to(cuda)).cpu().numpy()
+    for s in range(h_off.size - 1):
+        a, b = h_off[s], h_off[s + 1]
+        for c in range(4):
+            ids = np.arange(b - a, dtype=np.int64)
+            n_ref, _ = O.validate(ids, h_ad[c, a:b], h_sz[a:b], h_ts[a:b], h_te[a:b])
+            assert got[s * 4 + c] == n_ref, (s, c)
