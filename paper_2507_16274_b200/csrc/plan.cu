@@ -1545,17 +1545,6 @@ __global__ void k_scatter_fusions(const int32_t *__restrict__ ptr, const int64_t
 
 // Per-thread cache of forked streams/events for concurrent launches inside one
 // call (created once per host thread, reused; the call stays synchronous).
-static cudaStream_t side_stream(int i) {
-  thread_local cudaStream_t s[8] = {};
-  if (!s[i]) cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking);
-  return s[i];
-}
-static cudaEvent_t side_event(int i) {
-  thread_local cudaEvent_t e[8] = {};
-  if (!e[i]) cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming);
-  return e[i];
-}
-
 template <class T>
 static void d2h(Ctx &ctx, std::vector<T> &h, const T *d, int64_t n) {
   h.resize(n);
