@@ -187,7 +187,7 @@ def algo_bytes(kernel: str, w: dict, launches_per_step: float) -> float:
         # fusion: the trace's events are read once per attempt at least
         "k_fusion": 32.0 * w["events"],
         # K1: 17 B/event (t_s, t_e, size, dyn)
-        "k_peak_cta": 17.0 * w["events"],
+        "k_peak_warp": 17.0 * w["events"],
         # segmented sorts: 12 B/record read + written per sort
         "k_seg_bitonic": 24.0 * w["events"],
         "k_emit": 40.0 * w["unit_events"],
@@ -247,8 +247,8 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
     def k1():
         _lib.check(L.stw_peak_live(C.byref(bk1), 1, _lib.ptr(peaks), sh, err, 1024), err)
 
-    ms = kernel_ms(k1, "k_peak_cta")
-    entry("k_peak_cta", N * reps, 17.0, ms, f"K1 peak live bytes, {reps}x c4 ({N * reps} events); "
+    ms = kernel_ms(k1, "k_peak_warp")
+    entry("k_peak_warp", N * reps, 17.0, ms, f"K1 peak live bytes, {reps}x c4 ({N * reps} events); "
           "17 B/event read (t_s, t_e, size, dyn), timeline in shared memory")
     del cols, ev_off, horizon, n_sched
 

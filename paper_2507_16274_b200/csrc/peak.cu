@@ -65,70 +65,80 @@ __global__ void k_segmax(const int64_t *__restrict__ P, int64_t H, const int64_t
   if (best > 0) atomicMax(peak + t, best);
 }
 
-// One CTA per trace whose timeline fits in shared memory (every c4 trace):
-// deltas by shared-memory atomics, then each thread scans a contiguous chunk
-// (local prefix + local max), one block scan of the chunk sums, and the peak
-// is max(excl + local max) -- the timeline never touches HBM, so the kernel
-// reads 17 B per event (t_s, t_e, size, dyn) and writes 8 B per trace. The
-// timeline is sized by the batch's largest horizon (dynamic shared memory);
-// a trace with a longer horizon or a timestamp outside [0, horizon] is
-// flagged for the global-timeline path below.
-constexpr int kPeakThreads = 128;
-constexpr int kPeakSmemMax = 12288;  // timeline entries (96 KB)
+// One warp per trace whose timeline fits in its shared-memory slice (every c4
+// trace): deltas by shared-memory atomics, then each lane scans a contiguous
+// chunk (local prefix + local max), one warp scan of the chunk sums, and the
+// peak is max(excl + local max). The timeline never touches HBM, so the
+// kernel reads 17 B per event (t_s, t_e, size, dyn) and writes 8 B per trace.
+// Traces are packed host-side into CTAs by horizon (slices of 8 B x
+// (horizon + 1), largest first), so there are no block-wide barriers and many
+// traces per SM are in flight. A trace with a timestamp outside [0, horizon]
+// (or too long a horizon) goes to the global-timeline path below.
+constexpr int kPeakWarps = 8;
+constexpr int kPeakSmem = 48 * 1024;  // bytes per CTA: four CTAs per SM
 
-__global__ void __launch_bounds__(kPeakThreads) k_peak_cta(const int64_t *__restrict__ ev_off,
-                                                           const int64_t *__restrict__ size,
-                                                           const int32_t *__restrict__ t_s,
-                                                           const int32_t *__restrict__ t_e,
-                                                           const uint8_t *__restrict__ dyn,
-                                                           const int32_t *__restrict__ horizon, int hcap,
-                                                           int static_only, long long *__restrict__ peak,
-                                                           int *__restrict__ nbig, int32_t *__restrict__ big) {
-  extern __shared__ unsigned long long D[];
-  __shared__ long long sh[33];
-  const int t = blockIdx.x, tid = threadIdx.x;
+__global__ void __launch_bounds__(kPeakWarps * 32) k_peak_warp(const int64_t *__restrict__ ev_off,
+                                                               const int64_t *__restrict__ size,
+                                                               const int32_t *__restrict__ t_s,
+                                                               const int32_t *__restrict__ t_e,
+                                                               const uint8_t *__restrict__ dyn,
+                                                               const int32_t *__restrict__ horizon,
+                                                               int static_only, const int2 *__restrict__ wslot,
+                                                               long long *__restrict__ peak, int *__restrict__ nbig,
+                                                               int32_t *__restrict__ big) {
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ unsigned long long pk_smem[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 slot = wslot[blockIdx.x * kPeakWarps + w];
+  if (slot.x < 0) return;
+  const int t = slot.x;
+  unsigned long long *D = pk_smem + slot.y;
   const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
   const int H = horizon[t] + 1;  // timestamps are in [0, horizon] (model.py:240-241)
-  if (H > hcap || H <= 0) {
-    if (tid == 0) big[atomicAdd(nbig, 1)] = t;
-    return;
-  }
-  for (int x = tid; x < H; x += kPeakThreads) D[x] = 0;
-  __syncthreads();
+  for (int x = lane; x < H; x += 32) D[x] = 0;
+  __syncwarp();
   bool bad = false;
-  for (int64_t i = e0 + tid; i < e1; i += kPeakThreads) {
-    if (static_only && dyn[i]) continue;
-    const int a = t_s[i], z = t_e[i];
-    if ((unsigned)a >= (unsigned)H || (unsigned)z >= (unsigned)H) {
-      bad = true;
-      continue;
+  constexpr int B = 8;  // events per lane loaded together (independent loads in flight)
+  for (int64_t i0 = e0; i0 < e1; i0 += 32 * B) {
+    int a[B], z[B];
+    unsigned long long sz[B];
+    bool use[B];
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      const int64_t i = i0 + q * 32 + lane;
+      use[q] = i < e1;
+      a[q] = use[q] ? t_s[i] : 0;
+      z[q] = use[q] ? t_e[i] : 0;
+      sz[q] = use[q] ? (unsigned long long)size[i] : 0;
+      if (static_only && use[q]) use[q] = dyn[i] == 0;
     }
-    const unsigned long long sz = (unsigned long long)size[i];
-    atomicAdd(D + a, sz);
-    atomicAdd(D + z, 0ull - sz);
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      if (!use[q]) continue;
+      if ((unsigned)a[q] >= (unsigned)H || (unsigned)z[q] >= (unsigned)H) {
+        bad = true;
+        continue;
+      }
+      atomicAdd(D + a[q], sz[q]);
+      atomicAdd(D + z[q], 0ull - sz[q]);
+    }
   }
-  if (__syncthreads_or(bad)) {
-    if (tid == 0) big[atomicAdd(nbig, 1)] = t;
+  if (__any_sync(FULL, bad)) {
+    if (lane == 0) big[atomicAdd(nbig, 1)] = t;
     return;
   }
-  const int per = (H + kPeakThreads - 1) / kPeakThreads;
-  const int x0 = min(H, tid * per), x1 = min(H, x0 + per);
+  __syncwarp();
+  const int per = (H + 31) >> 5;
+  const int x0 = min(H, lane * per), x1 = min(H, x0 + per);
   long long run = 0, best = LLONG_MIN;
   for (int x = x0; x < x1; x++) {
     run += (long long)D[x];
     best = max(best, run);
   }
-  long long tot;
-  const long long ex = block_excl_sum<long long>(run, sh, &tot);
-  long long cand = best == LLONG_MIN ? LLONG_MIN : ex + best;
-  for (int o = 16; o; o >>= 1) cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, o));
-  if ((tid & 31) == 0) sh[tid >> 5] = cand;
-  __syncthreads();
-  if (tid == 0) {
-    long long m = 0;  // the reference's running maximum starts at 0
-    for (int w = 0; w < kPeakThreads / 32; w++) m = max(m, sh[w]);
-    peak[t] = m;
-  }
+  const long long inc = warp_incl_sum(run);
+  long long cand = best == LLONG_MIN ? 0 : inc - run + best;  // the running maximum starts at 0
+  for (int o = 16; o; o >>= 1) cand = max(cand, __shfl_xor_sync(FULL, cand, o));
+  if (lane == 0) peak[t] = cand;
 }
 
 __global__ void k_big_offsets(const int32_t *__restrict__ big, const int *__restrict__ nbig, int T,
@@ -146,13 +156,56 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
   int32_t *big = ar.take<int32_t>(T);
   if (!ctx.ok()) return;
   STW_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(int), ctx.stream));
+  // pack traces into CTAs by timeline size, largest first (counting sort by horizon)
+  std::vector<int32_t> order, longh;
+  order.reserve(T);
   int hmax = 0;
-  for (int x : b.h_horizon) hmax = std::max(hmax, x);
-  const int hcap = std::min(hmax + 1, kPeakSmemMax);
-  const int smem = hcap * (int)sizeof(unsigned long long);
-  STW_CUDA(ctx, cudaFuncSetAttribute(k_peak_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  STW_KLS(k_peak_cta, (unsigned)T, kPeakThreads, smem, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e, b.dyn,
-          b.horizon, hcap, static_only ? 1 : 0, (long long *)d_peak, nbig, big);
+  for (int t = 0; t < T; t++) {
+    const int64_t bytes = 8 * ((int64_t)b.h_horizon[t] + 1);
+    if (b.h_horizon[t] < 0 || bytes > kPeakSmem)
+      longh.push_back(t);
+    else
+      order.push_back(t), hmax = std::max(hmax, b.h_horizon[t]);
+  }
+  {
+    std::vector<int32_t> pos(hmax + 2, 0), sorted(order.size());
+    for (int32_t t : order) pos[hmax - b.h_horizon[t] + 1]++;
+    for (int k = 0; k <= hmax; k++) pos[k + 1] += pos[k];
+    for (int32_t t : order) sorted[pos[hmax - b.h_horizon[t]]++] = t;
+    order.swap(sorted);
+  }
+  std::vector<int2> wslot;
+  wslot.reserve(order.size() + kPeakWarps);
+  const int cap = kPeakSmem / 8;
+  for (size_t i = 0, j = order.size(); i < j;) {
+    const size_t base = wslot.size();
+    int used = 0, k = 0;
+    auto put = [&](int32_t t) {
+      wslot.push_back(make_int2(t, used));
+      used += b.h_horizon[t] + 1;
+      k++;
+    };
+    put(order[i++]);
+    while (k < kPeakWarps && i < j && used + b.h_horizon[order[i]] + 1 <= cap) put(order[i++]);
+    while (k < kPeakWarps && i < j && used + b.h_horizon[order[j - 1]] + 1 <= cap) put(order[--j]);
+    while (wslot.size() < base + kPeakWarps) wslot.push_back(make_int2(-1, 0));
+  }
+  const int nctas = (int)(wslot.size() / kPeakWarps);
+  int2 *d_wslot = nctas ? ar.take<int2>(wslot.size()) : nullptr;
+  if (!ctx.ok()) return;
+  if (!longh.empty()) {  // long horizons go straight to the global path
+    STW_CUDA(ctx, cudaMemcpyAsync(big, longh.data(), longh.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                  ctx.stream));
+    const int nl = (int)longh.size();
+    STW_CUDA(ctx, cudaMemcpyAsync(nbig, &nl, sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
+  }
+  if (nctas) {
+    STW_CUDA(ctx, cudaMemcpyAsync(d_wslot, wslot.data(), wslot.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                  ctx.stream));
+    STW_CUDA(ctx, cudaFuncSetAttribute(k_peak_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kPeakSmem));
+    STW_KLS(k_peak_warp, (unsigned)nctas, kPeakWarps * 32, kPeakSmem, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e,
+            b.dyn, b.horizon, static_only ? 1 : 0, d_wslot, (long long *)d_peak, nbig, big);
+  }
   STW_LAUNCHED(ctx);
   int h = 0;
   STW_CUDA(ctx, cudaMemcpyAsync(&h, nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
