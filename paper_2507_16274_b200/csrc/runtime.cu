@@ -112,9 +112,10 @@ void Ctx::fail(int code, const char *fmt, ...) {
 }
 
 static void raise_pool_threshold() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::once_flag once;
+  bool first = false;
+  std::call_once(once, [&] { first = true; });
+  if (!first) return;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return;
   cudaMemPool_t pool;
@@ -367,11 +368,7 @@ void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64
   STW_KL(k_os_hist, grid_for(n, 256, 148 * 8), 256, ctx.stream, keys, n, begin_bit, end_bit, passes, hist);
   STW_KL(k_os_bins, passes, 256, ctx.stream, hist);
   STW_LAUNCHED(ctx);
-  static bool attr = false;
-  if (!attr) {
-    STW_CUDA(ctx, cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOsSmem));
-    attr = true;
-  }
+  STW_CUDA(ctx, cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOsSmem));
   uint64_t *ka = keys, *kb = k2;
   uint32_t *va = vals, *vb = v2;
   for (int p = 0; p < passes && ctx.ok(); p++) {
