@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-sweep", action="store_true", help="skip the K1/K7/K2 >>L2 roofline sweep")
     ap.add_argument("--sweep-reps", type=int, default=64, help="c4 copies in the K1/K7 sweep")
+    ap.add_argument("--no-configs", action="store_true", help="skip the single-trace c1/c2/c3/c3b/c5 section")
     ap.add_argument("--profile-print", action="store_true", help="per-kernel table on stderr")
     return ap.parse_args()
 
@@ -228,10 +229,13 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
         cnt, ms = prof[name]
         return ms / cnt
 
-    def entry(name, records, unit_bytes, ms, note):
+    def entry(name, records, unit_bytes, ms, note, traffic_key=None, launches=1):
         gbs = records * unit_bytes / (ms / 1e3) / 1e9
+        tr = ncu_traffic(traffic_key) if traffic_key else None
         out[name] = {"kernel": name, "records": int(records), "algorithmic_bytes_per_record": unit_bytes,
-                     "ms": ms, "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "what": note}
+                     "ms": ms, "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                     "traffic": tr["bytes"] * launches if tr else None,
+                     "traffic_source": tr["source"] if tr else None, "what": note}
 
     # K1: R copies of the c4 batch (static_only, as the planner's self-check)
     T, N = db.T, db.N
@@ -249,7 +253,7 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
 
     ms = kernel_ms(k1, "k_peak_warp")
     entry("k_peak_warp", N * reps, 17.0, ms, f"K1 peak live bytes, {reps}x c4 ({N * reps} events); "
-          "17 B/event read (t_s, t_e, size, dyn), timeline in shared memory")
+          "17 B/event read (t_s, t_e, size, dyn), timeline in shared memory", "k_peak_warp@sweep")
     del cols, ev_off, horizon, n_sched
 
     # K7: the c4 plans of all 4 candidates, sweep-ordered, R copies
@@ -272,7 +276,8 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
     assert int(count[0].abs().sum()) == 0, "planner output failed validation"
     entry("k_overlap_sweep", n1 * reps * nc, (16.0 + 8.0 * nc) / nc, ms,
           f"K7 validate_plan of {T * reps * nc} plans ({n1 * reps} rectangles x {nc} candidates); "
-          "per (rectangle, candidate): addr 8 B + the shared size/t_s/t_e 16 B over the candidates")
+          "per (rectangle, candidate): addr 8 B + the shared size/t_s/t_e 16 B over the candidates",
+          "k_overlap_sweep@sweep")
     del ts, te, sz, ad, off
 
     # K2: 2^27 (u64 key, u32 value) pairs, 42-bit keys (c5's widest sort: 6 passes)
@@ -299,10 +304,62 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
     passes = 6
     entry("radix_sort_pairs", n2, 24.0 * passes, ms,
           f"K2 stable LSD radix sort of {n2} (u64, u32) pairs on 42 key bits ({passes} passes); "
-          "24 B/record/pass (key + value read and written)")
+          "24 B/record/pass (key + value read and written); traffic = 6 passes (+ the 8 B/record histogram read)",
+          "k_os_pass@sweep", passes)
     del keys0, keys, vals
     torch.cuda.empty_cache()
     return out
+
+
+# ---------------------------------------------------------------------------
+# single-trace configs: plan / replay / baseline on the device,
+# replay ops/s and the bit-exact fragmentation ratios
+
+def config_sweep(names, reps: int = 3):
+    """Per config: Python Trace in -> StaticPlan out (synthesize_static_plan +
+    derive_reuse_map), simulate (replay scorer) and run_baseline, each timed
+    end to end through the package API (host arrays in, host objects out),
+    best of `reps`; plus the fragmentation ratios they return."""
+    import paper_2507_16274_b200 as M
+    from paper_2507_16274_b200 import tracegen
+
+    out = {}
+    for name in names:
+        ta = tracegen.synth_arrays(tracegen.config(name))
+        tr = M.Trace.from_arrays(ta)
+
+        def best(fn):
+            t, r = float("inf"), None
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                r = fn()
+                t = min(t, time.perf_counter() - t0)
+            return t, r
+
+        t_plan, (plan, rmap) = best(lambda: M.plan_trace(tr))
+        bundle = plan.to_bundle(rmap)
+        t_sim, (rep, _log) = best(lambda: M.simulate(tr, bundle))
+        t_base, base = best(lambda: M.run_baseline(tr))
+        n = len(ta)
+        out[name] = {"events": n, "pool_size": int(plan.pool_size),
+                     "plan_ms": 1e3 * t_plan, "planned_allocs_per_s": int((ta.dyn == 0).sum()) / t_plan,
+                     "replay_ms": 1e3 * t_sim, "replay_ops_per_s": 2 * n / t_sim,
+                     "baseline_ms": 1e3 * t_base,
+                     "fragmentation": rep.fragmentation, "efficiency": rep.efficiency,
+                     "baseline_fragmentation": base.fragmentation,
+                     "fallbacks": int(rep.fallback_count), "reuse_hits": int(rep.reuse_hits)}
+    return out
+
+
+def ncu_traffic(key):
+    """DRAM bytes per launch of `key` from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            e = json.load(fh).get(key)
+    except (OSError, ValueError):
+        return None
+    return None if e is None else {"bytes": e["dram_bytes_per_launch"], "source": e["capture"]}
 
 
 def main():
@@ -447,8 +504,11 @@ def main():
     abytes = algo_bytes(kname, w, lps)
     achieved = abytes / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else float("nan")
     prof_total = sum(v[1] for v in prof.values())
+    tr = ncu_traffic(kname)
     roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "avg_launch_ms": avg_ms,
+                "frac": achieved / hbm, "traffic": tr["bytes"] if tr else None,
+                "algorithmic_bytes_per_launch": abytes, "traffic_source": tr["source"] if tr else None,
+                "avg_launch_ms": avg_ms,
                 "share_of_kernel_time": kms / prof_total if prof_total else None,
                 "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
     if args.profile_print and rank == 0:
@@ -458,6 +518,10 @@ def main():
     sweep = None
     if not args.no_kernel_sweep:
         sweep = kernel_sweep(dev, db, hb, o_addr, args.sweep_reps, hbm)
+    configs = None
+    if rank == 0 and not args.no_configs:
+        configs = config_sweep(["c1_llama2_7b_1f1b", "c2_llama2_7b_vpp_rcp", "c3_mixtral_moe", "c3b_mixtral_moe_rcp",
+                                "c5_llama3_70b"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -483,6 +547,7 @@ def main():
             "gpu_launches": int(launches),
             "roofline": roofline,
             "kernel_roofline": sweep,
+            "configs": configs,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

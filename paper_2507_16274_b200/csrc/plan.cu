@@ -1574,23 +1574,53 @@ static void out_copy(Ctx &ctx, T *dst, const T *src, int64_t n, bool dst_dev) {
     }                                                                            \
   } while (0)
 
-// STW_DEBUG_TIMING=1: synchronise at phase boundaries and print host wall time per phase
+// STW_DEBUG_TIMING=1: synchronise at phase boundaries and print host wall time per phase.
+// STW_DEBUG_TIMING=2: no extra syncs; print, per phase, the host time at which
+// the phase's last work was enqueued and the GPU time (events) at which it ended.
 struct PhaseTimer {
   Ctx &ctx;
-  bool on;
-  double t0;
+  int mode;
+  double t0, tstart;
+  std::vector<std::pair<const char *, double>> host;
+  std::vector<cudaEvent_t> ev;
   static double now() {
     timespec ts;
     clock_gettime(CLOCK_MONOTONIC, &ts);
     return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
   }
-  explicit PhaseTimer(Ctx &c) : ctx(c), on(getenv("STW_DEBUG_TIMING") != nullptr), t0(now()) {}
+  explicit PhaseTimer(Ctx &c) : ctx(c), mode(0), t0(now()), tstart(t0) {
+    if (const char *e = getenv("STW_DEBUG_TIMING")) mode = atoi(e) == 2 ? 2 : 1;
+    if (mode == 2) mark0();
+  }
+  void mark0() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ctx.stream);
+    ev.push_back(e);
+  }
   void mark(const char *name) {
-    if (!on) return;
+    if (!mode) return;
+    if (mode == 2) {
+      mark0();
+      host.push_back({name, now() - tstart});
+      return;
+    }
     cudaStreamSynchronize(ctx.stream);
     double t = now();
     fprintf(stderr, "[stw plan] %-24s %8.3f ms\n", name, t - t0);
     t0 = t;
+  }
+  ~PhaseTimer() {
+    if (mode != 2) return;
+    cudaStreamSynchronize(ctx.stream);
+    for (size_t i = 0; i < host.size(); i++) {
+      float g = 0, d = 0;
+      cudaEventElapsedTime(&g, ev[0], ev[i + 1]);
+      cudaEventElapsedTime(&d, ev[i], ev[i + 1]);
+      fprintf(stderr, "[stw plan] %-24s host enq %8.3f ms   gpu end %8.3f ms  (phase %7.3f)\n", host[i].first,
+              host[i].second, g, d);
+    }
+    for (auto e : ev) cudaEventDestroy(e);
   }
 };
 

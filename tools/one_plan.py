@@ -6,5 +6,6 @@ from paper_2507_16274_b200.batching import HostBatch
 
 tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(4096)]
 hb = HostBatch(tas)
-bp = api.plan_batch(hb, tracegen.C4_CANDIDATES, select_best=True, detail=False)
+for _ in range(2):
+    bp = api.plan_batch(hb, tracegen.C4_CANDIDATES, select_best=True, detail=False)
 print("rc max", bp.rc.max())
