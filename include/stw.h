@@ -103,6 +103,14 @@ typedef struct {
 int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *out, char *err,
                    size_t errlen);
 
+/* The same planner over a sequence of n host batches (host inputs, host
+ * outputs out[k] for batch k; every out[k] requests the same fields). HBM
+ * staging is double-buffered on a copy stream: batch k+1's host->device copy
+ * and batch k-1's results overlap batch k's planning. Results are identical to
+ * n stw_plan_batch calls. */
+int stw_plan_batches(int32_t n, const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *out, char *err,
+                     size_t errlen);
+
 /* ---- K7: validate_plan (planner.py:476-505) -----------------------------
  * Decisions (plan order) as SoA host pointers. Reproduces the reference
  * sweep's report exactly: pairs (i, j) index the decision arrays, in report

@@ -70,7 +70,7 @@ class RectSets(C.Structure):
 
 
 EXPORTS = (
-    "stw_version", "stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_validate",
+    "stw_version", "stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_plan_batches", "stw_validate",
     "stw_validate_sets", "stw_reuse_map", "stw_simulate", "stw_baseline",
 )
 

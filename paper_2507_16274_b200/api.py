@@ -107,11 +107,8 @@ def _cand_bits(cands) -> np.ndarray:
                       dtype=np.uint8)
 
 
-def plan_batch(batch, cands=((True, True),), alignment: int = DEFAULT_ALIGNMENT, select_best: bool = False,
-               detail: bool = True, stream=None) -> BatchPlan:
-    """Plan every trace of `batch` (HostBatch or list of TraceArrays) under each
-    candidate (fusion, gap_insert) on the device (stw_plan_batch)."""
-    hb = batch if isinstance(batch, HostBatch) else HostBatch([_arrays_of(t) for t in batch])
+def _plan_buffers(hb, cands, alignment, select_best, detail, stream):
+    """Host output buffers + the stw_plan_opts/stw_plan_out structs for one batch."""
     C_ = len(cands)
     T, N = hb.T, hb.N
     U = T * C_
@@ -139,11 +136,38 @@ def plan_batch(batch, cands=((True, True),), alignment: int = DEFAULT_ALIGNMENT,
     out = _lib.PlanOut(0, _lib.ptr(rc), _lib.ptr(err_ids), _lib.ptr(stats), _lib.ptr(addr), _lib.ptr(layer_of),
                        _lib.ptr(lbase), _lib.ptr(lsize), _lib.ptr(ftmp), _lib.ptr(favg), _lib.ptr(order),
                        _lib.ptr(best), _lib.ptr(abest), _lib.ptr(bpool))
+    bp = BatchPlan(hb, tuple(cands), rc, err_ids, stats, addr, layer_of, lbase, lsize, ftmp, favg, order,
+                   best, bpool, abest)
+    return bp, opts, out, cb
+
+
+def plan_batch(batch, cands=((True, True),), alignment: int = DEFAULT_ALIGNMENT, select_best: bool = False,
+               detail: bool = True, stream=None) -> BatchPlan:
+    """Plan every trace of `batch` (HostBatch or list of TraceArrays) under each
+    candidate (fusion, gap_insert) on the device (stw_plan_batch)."""
+    hb = batch if isinstance(batch, HostBatch) else HostBatch([_arrays_of(t) for t in batch])
+    bp, opts, out, _cb = _plan_buffers(hb, cands, alignment, select_best, detail, stream)
     err = _lib.errbuf()
     b = hb.struct()
     _lib.check(_lib.load().stw_plan_batch(C.byref(b), C.byref(opts), C.byref(out), err, C.sizeof(err)), err)
-    return BatchPlan(hb, tuple(cands), rc, err_ids, stats, addr, layer_of, lbase, lsize, ftmp, favg, order,
-                     best, bpool, abest)
+    return bp
+
+
+def plan_batches(batches, cands=((True, True),), alignment: int = DEFAULT_ALIGNMENT, select_best: bool = False,
+                 detail: bool = True, stream=None) -> list:
+    """plan_batch over a sequence of batches in one pipelined device call
+    (stw_plan_batches: uploads, planning and downloads of neighbouring batches
+    overlap). Returns one BatchPlan per batch."""
+    hbs = [b if isinstance(b, HostBatch) else HostBatch([_arrays_of(t) for t in b]) for b in batches]
+    if not hbs:
+        return []
+    parts = [_plan_buffers(hb, cands, alignment, select_best, detail, stream) for hb in hbs]
+    k = len(hbs)
+    bs = (_lib.Batch * k)(*[hb.struct() for hb in hbs])
+    outs = (_lib.PlanOut * k)(*[p[2] for p in parts])
+    err = _lib.errbuf()
+    _lib.check(_lib.load().stw_plan_batches(k, bs, C.byref(parts[0][1]), outs, err, C.sizeof(err)), err)
+    return [p[0] for p in parts]
 
 
 def _unknown_phase_message(ta) -> str:

@@ -19,6 +19,7 @@ static int finish(Ctx &ctx) {
 
 namespace stw {
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
+int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
                         const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap);
 int reuse_map(Ctx &ctx, int64_t n, const int64_t *addr, const int64_t *size, const int32_t *t_s, const int32_t *t_e,
@@ -68,6 +69,17 @@ int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *
     return ctx.rc;
   }
   plan_batch(ctx, b, opts, out);
+  return finish(ctx);
+}
+
+int stw_plan_batches(int32_t n, const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *out, char *err,
+                     size_t errlen) {
+  STW_ENTRY(opts ? opts->stream : nullptr, err, errlen);
+  if (n < 0 || (n > 0 && (!b || !opts || !out))) {
+    ctx.fail(STW_EARG, "null argument");
+    return ctx.rc;
+  }
+  plan_batches(ctx, n, b, opts, out);
   return finish(ctx);
 }
 

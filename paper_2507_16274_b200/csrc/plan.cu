@@ -2081,6 +2081,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     int64_t *lb_out = ar.take<int64_t>((int64_t)C * N + 1), *ls_out = ar.take<int64_t>((int64_t)C * N + 1);
     double *ft_out = ar.take<double>((int64_t)C * N + 1), *fa_out = ar.take<double>((int64_t)C * N + 1);
     if (!ctx.ok()) return ctx.rc;
+    for (void *p : {(void *)lb_out, (void *)ls_out, (void *)ft_out, (void *)fa_out})  // unused slots read as 0
+      STW_CUDA(ctx, cudaMemsetAsync(p, 0, ((int64_t)C * N + 1) * 8, ctx.stream));
     LAUNCH(k_scatter_layers, TU, d_uo, (int64_t)U, C, b.ev_off, N, LA.nlayers, LA.lbase, LA.lsize, lb_out, ls_out, TU);
     if (want[1]) LAUNCH(k_scatter_fusions, P, p0.tr, d_pl_off, d_acc, d_var, C, b.ev_off, N, acc_tmp, acc_avg, ft_out, fa_out, P);
     out_copy(ctx, out->layer_base, lb_out, (int64_t)C * N, od);

@@ -107,3 +107,16 @@ def test_plan_many_layers_overflow_paths():
     tas.append(_manual_trace(specs, [("F:0", 0, 3000)]))
     check_batch(tas)
     check_batch(tas[2:])
+
+
+def test_plan_batches_pipeline_matches_single_calls():
+    """stw_plan_batches (double-buffered staging across batches) == stw_plan_batch per batch."""
+    groups = [[tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(a, b)] for a, b in
+              ((0, 40), (40, 47), (100, 164), (7, 8))]
+    many = api.plan_batches(groups, tracegen.C4_CANDIDATES, select_best=True)
+    for g, got in zip(groups, many):
+        want = api.plan_batch(g, tracegen.C4_CANDIDATES, select_best=True)
+        for f in ("rc", "err_ids", "stats", "addr", "layer_of", "layer_base", "layer_size", "order", "best_cand",
+                  "best_pool", "addr_best"):
+            assert np.array_equal(getattr(got, f), getattr(want, f)), f
+        assert np.array_equal(got.fus_tmp.view(np.int64), want.fus_tmp.view(np.int64))
