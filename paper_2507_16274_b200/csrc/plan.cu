@@ -169,7 +169,7 @@ __global__ void k_seg_bitonic(uint64_t *__restrict__ keys, uint32_t *__restrict_
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
-        int a = 2 * j * (i / j) + (i % j), b = a + j;
+        int a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a + j;  // j is a power of two
         bool asc = (a & k) == 0;
         uint64_t ka = sk[a], kb = sk[b];
         uint32_t va = sv[a], vb = sv[b];
