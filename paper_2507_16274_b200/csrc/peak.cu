@@ -74,6 +74,17 @@ __global__ void k_segmax(const int64_t *__restrict__ P, int64_t H, const int64_t
 // (horizon + 1), largest first), so there are no block-wide barriers and many
 // traces per SM are in flight. A trace with a timestamp outside [0, horizon]
 // (or too long a horizon) goes to the global-timeline path below.
+// 64-bit shared-memory add from two native 32-bit atomics (a 64-bit shared
+// atomicAdd compiles to a CAS loop): add the low word, carry into the high word.
+__device__ __forceinline__ void add64_shared(unsigned long long *p, unsigned long long v) {
+  unsigned *q = reinterpret_cast<unsigned *>(p);
+  const unsigned lo = (unsigned)v;
+  unsigned hi = (unsigned)(v >> 32);
+  const unsigned old = atomicAdd(q, lo);
+  if (old + lo < old) hi += 1u;
+  if (hi) atomicAdd(q + 1, hi);
+}
+
 constexpr int kPeakWarps = 8;
 constexpr int kPeakSmem = 48 * 1024;  // bytes per CTA: four CTAs per SM
 
@@ -119,8 +130,8 @@ __global__ void __launch_bounds__(kPeakWarps * 32) k_peak_warp(const int64_t *__
         bad = true;
         continue;
       }
-      atomicAdd(D + a[q], sz[q]);
-      atomicAdd(D + z[q], 0ull - sz[q]);
+      add64_shared(D + a[q], sz[q]);
+      add64_shared(D + z[q], 0ull - sz[q]);
     }
   }
   if (__any_sync(FULL, bad)) {

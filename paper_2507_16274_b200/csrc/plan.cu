@@ -79,8 +79,12 @@ __device__ T block_reduce_max(T v, T *sh) {
 #define GRID_STRIDE(i, n) \
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
+// trace index of every event: one warp per trace writes its run (coalesced)
 __global__ void k_trace_of_all(const int64_t *__restrict__ ev_off, int T, int64_t N, int32_t *__restrict__ tr) {
-  GRID_STRIDE(i, N) tr[i] = trace_of(ev_off, T, i);
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  for (int t = w; t < T; t += nw)
+    for (int64_t i = ev_off[t] + lane; i < ev_off[t + 1]; i += 32) tr[i] = t;
 }
 
 __global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx) {
@@ -255,6 +259,7 @@ __global__ void k_checks(const int32_t *__restrict__ tr, const int64_t *__restri
                          const uint8_t *__restrict__ dyn, const int32_t *__restrict__ horizon,
                          const int32_t *__restrict__ n_sched, int64_t n, long long align, int *__restrict__ bad_align,
                          int *__restrict__ bad_phase, int *__restrict__ pmax) {
+  int pm = 0;  // warp-aggregated max phase index (one global atomic per warp)
   GRID_STRIDE(i, n) {
     if (dyn[i]) continue;
     int t = tr[i];
@@ -262,9 +267,11 @@ __global__ void k_checks(const int32_t *__restrict__ tr, const int64_t *__restri
     if (size[i] % align) atomicMin(bad_align + t, loc);
     if (te[i] < horizon[t]) {
       if (ps[i] >= n_sched[t] || pe[i] >= n_sched[t]) atomicMin(bad_phase + t, loc);
-      atomicMax(pmax, max(ps[i], pe[i]));
+      pm = max(pm, max(ps[i], pe[i]));
     }
   }
+  pm = __reduce_max_sync(0xffffffffu, pm);
+  if ((threadIdx.x & 31) == 0 && pm > 0) atomicMax(pmax, pm);
 }
 
 __global__ void k_key_group(const int32_t *__restrict__ tr, const int32_t *__restrict__ te,
@@ -1574,6 +1581,15 @@ static void out_copy(Ctx &ctx, T *dst, const T *src, int64_t n, bool dst_dev) {
     }                                                                            \
   } while (0)
 
+// grid-stride reductions: a few CTAs per SM, many elements per thread
+#define LAUNCH_RED(kern, n, ...)                                                 \
+  do {                                                                           \
+    if (ctx.ok() && (n) > 0) {                                                   \
+      STW_KL(kern, grid_for((n), 256, 148 * 4), 256, ctx.stream, __VA_ARGS__);   \
+      STW_LAUNCHED(ctx);                                                         \
+    }                                                                            \
+  } while (0)
+
 // STW_DEBUG_TIMING=1: synchronise at phase boundaries and print host wall time per phase.
 // STW_DEBUG_TIMING=2: no extra syncs; print, per phase, the host time at which
 // the phase's last work was enqueued and the GPU time (events) at which it ended.
@@ -1655,12 +1671,15 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   long long *mm = ar.take<long long>(2);
   int *im = ar.take<int>(4);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_trace_of_all, N, b.ev_off, T, N, tr);
+  if (T > 0) {
+    STW_KL(k_trace_of_all, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, N, tr);
+    STW_LAUNCHED(ctx);
+  }
   long long mm_init[2] = {LLONG_MAX, LLONG_MIN};
   STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
-  LAUNCH(k_minmax_i64, N, b.id, N, mm, mm + 1);
-  LAUNCH(k_max_i32, N, b.t_s, N, im);
+  LAUNCH_RED(k_minmax_i64, N, b.id, N, mm, mm + 1);
+  LAUNCH_RED(k_max_i32, N, b.t_s, N, im);
   long long hmm[2] = {0, 0};
   int him[4] = {0, 0, 0, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
@@ -1850,7 +1869,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     long long *dmx = ar.take<long long>(2);
     long long init[2] = {LLONG_MAX, LLONG_MIN};
     STW_CUDA(ctx, cudaMemcpyAsync(dmx, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
-    LAUNCH(k_minmax_i64, NI, it0.size, NI, dmx, dmx + 1);
+    LAUNCH_RED(k_minmax_i64, NI, it0.size, NI, dmx, dmx + 1);
     long long h[2] = {0, 0};
     STW_CUDA(ctx, cudaMemcpyAsync(h, dmx, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
     sync(ctx);
