@@ -688,6 +688,82 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
 __global__ void k_fill_i8(int8_t *p, int64_t n, int8_t v) { GS3(i, n) p[i] = v; }
 
 // ---------------------------------------------------------------------------
+// Parallel replay of a fully planned static trace. When every event is static
+// with a unique id and the queue matching gave every allocation a planned
+// address, the replay's only state is the pool's free set, and a planned
+// allocation lands iff its interval is free -- i.e. iff no earlier live planned
+// rectangle overlaps it (the K7 test on the (lifespan x planned interval)
+// rectangles in op order). Then the log is a function of the op order and the
+// metrics are a prefix sum: allocated_peak = max over op order of live bytes,
+// reserved = pool, no fallbacks/reuse. Any conflict falls back to the
+// sequential warp, which reports the reference's exact error.
+
+__global__ void k_fast_flags(const int8_t *__restrict__ route, const uint8_t *__restrict__ dyn, int64_t n,
+                             int *__restrict__ bad) {
+  int b = 0;
+  GS3(e, n) b |= (dyn[e] != 0 || route[e] != R_PLANNED) ? 1 : 0;
+  b = __reduce_or_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0 && b) atomicOr(bad, 1);
+}
+
+// rectangles in op order of the allocations (= (t_s, id) order), and the
+// signed size delta of every op
+__global__ void k_fast_rects(const uint32_t *__restrict__ operm, int64_t n,
+                             const int32_t *__restrict__ ts, const int32_t *__restrict__ te,
+                             const int64_t *__restrict__ size, const int64_t *__restrict__ paddr,
+                             const int32_t *__restrict__ arank, int32_t *__restrict__ rts, int32_t *__restrict__ rte,
+                             int64_t *__restrict__ rsz, int64_t *__restrict__ raddr, int64_t *__restrict__ delta) {
+  GS3(k, 2 * n) {
+    const uint32_t o = operm[k];
+    const uint32_t e = o >> 1;
+    const bool alloc = !(o & 1);
+    delta[k] = alloc ? size[e] : -size[e];
+    if (alloc) {
+      const int32_t r = arank[k];
+      rts[r] = ts[e];
+      rte[r] = te[e];
+      rsz[r] = size[e];
+      raddr[r] = paddr[e];
+    }
+  }
+}
+
+__global__ void k_alloc_flag(const uint32_t *__restrict__ operm, int64_t n2, uint32_t *__restrict__ f) {
+  GS3(k, n2) f[k] = (operm[k] & 1) ? 0u : 1u;
+}
+
+__global__ void k_fast_log(const uint32_t *__restrict__ operm, int64_t n, const int32_t *__restrict__ ts,
+                           const int32_t *__restrict__ te, const int64_t *__restrict__ id,
+                           const int64_t *__restrict__ size, const int64_t *__restrict__ paddr, long long pool,
+                           int8_t *__restrict__ lkind, int8_t *__restrict__ lspace, int8_t *__restrict__ lroute,
+                           int64_t *__restrict__ lt, int64_t *__restrict__ lid, int64_t *__restrict__ lsize,
+                           int64_t *__restrict__ laddr) {
+  GS3(k, 2 * n + 1) {
+    if (k == 0) {  // init record (sim.py:153)
+      lkind[0] = 0, lspace[0] = 0, lroute[0] = -1, lt[0] = 0, lid[0] = 0, lsize[0] = pool, laddr[0] = 0;
+      continue;
+    }
+    const uint32_t o = operm[k - 1];
+    const uint32_t e = o >> 1;
+    const bool alloc = !(o & 1);
+    lkind[k] = alloc ? 2 : 3;
+    lspace[k] = 0;
+    lroute[k] = alloc ? R_PLANNED : -1;
+    lt[k] = alloc ? ts[e] : te[e];
+    lid[k] = id[e];
+    lsize[k] = size[e];
+    laddr[k] = paddr[e];
+  }
+}
+
+__global__ void k_max_scan(const int64_t *__restrict__ v, int64_t n, long long *__restrict__ mx) {
+  long long m = 0;
+  GS3(i, n) m = max(m, (long long)v[i]);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(mx, m);
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 
@@ -828,8 +904,81 @@ int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep
     STW_KL(k_match_groups, grid_for(nr, 256), 256, ctx.stream, perm, cls, nr, nd, gstart, gndec);
     STW_KL(k_match_assign, grid_for(nr, 256), 256, ctx.stream, perm, cls, nr, M, gstart, gndec, d_addr, route, paddr);
   }
-  // sequential replay
   const int64_t cap_log = 1 + 3 * n;
+  // parallel fast path (static-only, every allocation planned, unique ids)
+  if (!baseline && n > 0 && nu == n && nd > 0) {
+    int *bad = ar.take<int>(1);
+    if (!ctx.ok()) return ctx.rc;
+    STW_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx.stream));
+    STW_KL(k_fast_flags, grid_for(n, 256, 148 * 4), 256, ctx.stream, route, b.dyn, n, bad);
+    int hbad = 1;
+    STW_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    if (!ctx.ok()) return ctx.rc;
+    if (!hbad) {
+      int32_t *rts = ar.take<int32_t>(n), *rte = ar.take<int32_t>(n), *arank = ar.take<int32_t>(2 * n);
+      int64_t *rsz = ar.take<int64_t>(n), *raddr = ar.take<int64_t>(n), *delta = ar.take<int64_t>(2 * n);
+      uint32_t *af = ar.take<uint32_t>(2 * n);
+      int64_t *roff = ar.take<int64_t>(2);
+      long long *cnt = ar.take<long long>(1), *pk = ar.take<long long>(1);
+      int *first = ar.take<int>(1);
+      if (!ctx.ok()) return ctx.rc;
+      STW_KL(k_alloc_flag, grid_for(2 * n, 256), 256, ctx.stream, operm, 2 * n, af);
+      device_scan<uint32_t>(ctx, ar, af, (uint32_t *)arank, 2 * n, false);
+      STW_KL(k_fast_rects, grid_for(2 * n, 256), 256, ctx.stream, operm, n, b.t_s, b.t_e, b.size, paddr,
+             arank, rts, rte, rsz, raddr, delta);
+      int64_t hoff[2] = {0, n};
+      STW_CUDA(ctx, cudaMemcpyAsync(roff, hoff, sizeof(hoff), cudaMemcpyHostToDevice, ctx.stream));
+      RectSets rs{1, n, roff, rts, rte, rsz, 1, raddr};
+      const long long al = bun->alignment > 0 ? bun->alignment : 1;
+      validate_sets(ctx, ar, rs, cnt, first, __builtin_ctzll((unsigned long long)al));
+      long long hcnt = -1;
+      STW_CUDA(ctx, cudaMemcpyAsync(&hcnt, cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, ctx.stream));
+      STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+      if (!ctx.ok()) return ctx.rc;
+      if (hcnt == 0) {
+        device_scan<int64_t>(ctx, ar, delta, delta, 2 * n, true);
+        STW_CUDA(ctx, cudaMemsetAsync(pk, 0, sizeof(long long), ctx.stream));
+        STW_KL(k_max_scan, grid_for(2 * n, 256, 148 * 4), 256, ctx.stream, delta, 2 * n, pk);
+        const int64_t nlog = 1 + 2 * n;
+        int8_t *lkind = ar.take<int8_t>(nlog), *lspace = ar.take<int8_t>(nlog), *lroute = ar.take<int8_t>(nlog);
+        int64_t *lt = ar.take<int64_t>(nlog), *lid = ar.take<int64_t>(nlog), *lsize = ar.take<int64_t>(nlog),
+                *laddr = ar.take<int64_t>(nlog);
+        if (!ctx.ok()) return ctx.rc;
+        if (log)
+          STW_KL(k_fast_log, grid_for(nlog, 256), 256, ctx.stream, operm, n, b.t_s, b.t_e, b.id, b.size, paddr, pool,
+                 lkind, lspace, lroute, lt, lid, lsize, laddr);
+        long long hpk = 0;
+        STW_CUDA(ctx, cudaMemcpyAsync(&hpk, pk, sizeof(hpk), cudaMemcpyDeviceToHost, ctx.stream));
+        if (log) {
+          log->len = nlog;
+          const int64_t m = std::min<int64_t>(nlog, log->cap);
+          if (m > 0) {
+            STW_CUDA(ctx, cudaMemcpyAsync(log->kind, lkind, m, cudaMemcpyDeviceToHost, ctx.stream));
+            STW_CUDA(ctx, cudaMemcpyAsync(log->space, lspace, m, cudaMemcpyDeviceToHost, ctx.stream));
+            STW_CUDA(ctx, cudaMemcpyAsync(log->route, lroute, m, cudaMemcpyDeviceToHost, ctx.stream));
+            STW_CUDA(ctx, cudaMemcpyAsync(log->t, lt, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            STW_CUDA(ctx, cudaMemcpyAsync(log->id, lid, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            STW_CUDA(ctx, cudaMemcpyAsync(log->size, lsize, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            STW_CUDA(ctx, cudaMemcpyAsync(log->addr, laddr, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
+          }
+        }
+        STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+        if (!ctx.ok()) return ctx.rc;
+        rep->allocated_peak = hpk;
+        rep->reserved_peak = pool;
+        rep->pool_size = pool;
+        rep->fallback_count = 0;
+        rep->fallback_bytes_peak = 0;
+        rep->reuse_hits = 0;
+        rep->mismatch_count = 0;
+        rep->efficiency = rep->reserved_peak ? exact_div_host(rep->allocated_peak, rep->reserved_peak) : 1.0;
+        rep->fragmentation = 1.0 - rep->efficiency;
+        return ctx.rc;
+      }
+    }
+  }
+  // sequential replay
   ReplayArgs R{};
   R.n = n;
   R.operm = operm;

@@ -117,3 +117,35 @@ def test_replay_mismatch_and_occupied():
     corrupt = PlanBundle(16 * U, U, (PlanDecision(0, 0, 8 * U, 0, 2), PlanDecision(1, 0, 8 * U, 1, 3)), {})
     with pytest.raises(SimulationError, match="occupied"):  # test_sim.py:92-104
         api.simulate(tr, corrupt)
+
+
+def test_replay_fast_path_conflicts_fuzz():
+    """Static-only traces take the parallel replay (K7 overlap test + prefix sums);
+    corrupted plans must fall back and raise exactly like the oracle's sequential replay."""
+    from paper_2507_16274_b200.domain import SimulationError, Trace
+    from paper_2507_16274_b200.plan_types import PlanBundle, PlanDecision
+
+    rng = np.random.default_rng(11)
+    for s in range(24):
+        ta = tracegen.synth_arrays(tracegen.c4_config(s))
+        tr = Trace.from_arrays(ta)
+        plan, rmap = api.plan_trace(tr)
+        c = plan.columns()
+        addr = c.addr.copy()
+        if s % 3:  # move a few decisions onto other decisions' addresses (mostly conflicts)
+            for _ in range(1 + s % 4):
+                i, j = rng.integers(0, addr.size, 2)
+                addr[i] = min(addr[j], plan.pool_size - int(c.size[i]))
+        decs = tuple(PlanDecision(int(a), int(b), int(z), int(x), int(y))
+                     for a, b, z, x, y in zip(c.id, addr, c.size, c.t_s, c.t_e))
+        bundle = PlanBundle(plan.pool_size, plan.alignment, decs, {})
+        key, dcols, off, lo, hi = oracle_inputs(ta, plan.to_bundle(rmap))
+        o = O.simulate(ta, key, bundle.pool_size, bundle.alignment, dcols[0], addr, *dcols[2:], [0], [], [], True)
+        if o.rc == 0:
+            rep, log = api.simulate(tr, bundle)
+            assert rep.to_dict() == o.report
+            assert list(log) == oracle_log_dicts(o.log, ta)
+        else:
+            with pytest.raises(SimulationError) as ei:
+                api.simulate(tr, bundle)
+            assert str(o.err_id) in str(ei.value), (str(ei.value), o.err)
