@@ -205,12 +205,29 @@ __global__ void __launch_bounds__(256) k_os_hist(const uint64_t *__restrict__ ke
   __shared__ uint32_t h[8][256];
   for (int x = threadIdx.x; x < 8 * 256; x += blockDim.x) (&h[0][0])[x] = 0;
   __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
+  // 16-byte loads, four in flight per thread (two keys each)
+  const int64_t n2 = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(keys);
+  const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+  auto count = [&](uint64_t k) {
     for (int p = 0; p < passes; p++) {
       const int b = begin_bit + 8 * p, w = min(8, end_bit - b);
       atomicAdd(&h[p][(uint32_t)(k >> b) & ((1u << w) - 1)], 1u);
     }
+  };
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (vec) {
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+      const ulonglong2 a = k2[i], b = k2[i + stride], c = k2[i + 2 * stride], d = k2[i + 3 * stride];
+      count(a.x), count(a.y), count(b.x), count(b.y), count(c.x), count(c.y), count(d.x), count(d.y);
+    }
+    for (; i < n2; i += stride) {
+      const ulonglong2 a = k2[i];
+      count(a.x), count(a.y);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) count(keys[n - 1]);
+  } else {
+    for (; i < n; i += stride) count(keys[i]);
   }
   __syncthreads();
   for (int x = threadIdx.x; x < passes * 256; x += blockDim.x) {
