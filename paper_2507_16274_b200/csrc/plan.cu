@@ -1176,21 +1176,23 @@ constexpr int kLayerSmemInts = 14336;  // 56 KB per CTA: four CTAs per SM
 
 __host__ __device__ constexpr int warpn_smem_ints(int n) { return 4 * n + 4 * (kWN + 1) + kWN; }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, const int2 *__restrict__ wslot,
-                                                                  int32_t *__restrict__ over, int *__restrict__ nover) {
+// GAP = the unit's candidate inserts into gaps of earlier classes' layers.
+// Without gap insertion a class only ever fills its own new layers (Alg. 1),
+// so the slot CSR, the fit masks, the insertion ranks and the per-class merge
+// are not needed at all: such a unit uses no shared memory and its per-item
+// step is the Alg. 1 max-reduce + ballot alone.
+template <bool GAP>
+__device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__restrict__ smem, const int2 slot,
+                                                int32_t *__restrict__ over, int *__restrict__ nover) {
   constexpr unsigned FULL = 0xffffffffu;
-  extern __shared__ int32_t smem[];
-  const int w = threadIdx.x >> 5, lane = lane_id();
-  const int2 slot = wslot[blockIdx.x * kWarpsPerCta + w];
-  if (slot.x < 0) return;
+  const int lane = lane_id();
   const int u = slot.x;
   const int c = u % A.C, t = u / A.C;
   const int v = A.var_of[c];
-  const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
   const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
   const int n = (int)(a1 - a0);
   const int64_t off = A.uo[u];
-  int32_t *sm = smem + slot.y;
+  int32_t *sm = smem;
   int32_t *sts = sm, *ste = sm + n, *run_ts = sm + 2 * n, *run_te = sm + 3 * n;  // slots + class runs
   int32_t *tts = A.sB_ts + off, *tte = A.sB_te + off;                              // merge output (global)
   int32_t *loffA = sm + 4 * n, *loffB = loffA + (kWN + 1), *prio = loffB + (kWN + 1), *runoff = prio + (kWN + 1);
@@ -1199,7 +1201,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
   const int64_t *gcend = A.cend + a0;
   int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
   int64_t *lsize = A.lsize + off;
-  if (lane == 0) loffA[0] = 0;
+  if (GAP && lane == 0) loffA[0] = 0;
   int nl = 0, gapc = 0;
   __syncwarp();
   for (int j0 = 0; j0 < n;) {
@@ -1207,7 +1209,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
     const int m = j1 - j0;
     const int64_t S = A.it.size[a0 + j0];
     int last = INT_MIN, ne = INT_MIN, nnew = 0;
-    newcnt[lane] = 0;
+    if (GAP) newcnt[lane] = 0;
     __syncwarp();
     for (int cb = j0; cb < j1; cb += 32) {
       const int mine = cb + lane;
@@ -1217,7 +1219,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
       if (mine < j1) {
         my_ts = gts[mine];
         my_te = gte[mine];
-        if (gap)
+        if (GAP)
           for (int p = 0; p < nl; p++) {
             const int l = prio[p];
             if (slot_fit(sts, ste, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1u << p;
@@ -1230,10 +1232,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
           const int k = kg + kk;
           const bool valid = k < cnt;  // warp-uniform
           const int ts = __shfl_sync(FULL, my_ts, k & 31), te = __shfl_sync(FULL, my_te, k & 31);
-          const unsigned f = __shfl_sync(FULL, fm, k & 31);
           // gap host (planner.py:420-431): first fitting layer in priority order whose
           // same-class slots all end before ts
-          const unsigned m1 = __ballot_sync(FULL, ((f >> lane) & 1u) && last < ts);
+          unsigned m1 = 0;
+          if (GAP) {
+            const unsigned f = __shfl_sync(FULL, fm, k & 31);
+            m1 = __ballot_sync(FULL, ((f >> lane) & 1u) && last < ts);
+          }
           // Alg. 1 (planner.py:244-252): new layer with the largest end < ts, ties to the oldest
           const bool ca = lane < nnew && ne < ts;
           const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
@@ -1259,6 +1264,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
       // lane-parallel: layer ids, gap count, insertion ranks
       const bool act = lane < cnt;
       const int layer = my_code < kWN ? prio[my_code] : nl + (my_code - kWN);
+      if (!GAP) {
+        if (act) ilayer[mine] = layer;
+        continue;
+      }
       gapc += __popc(__ballot_sync(FULL, act && my_code < kWN));
       const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
       const int r = __popc(peers & lanemask_lt());
@@ -1274,6 +1283,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
     // ---- merge the class into the layer-major slot CSR
     const int nl2 = nl + nnew;
     if (lane < nnew) lsize[nl + lane] = S;
+    if (!GAP) {
+      nl = nl2;
+      j0 = j1;
+      continue;
+    }
     const int myc = newcnt[lane];
     const unsigned tm = __ballot_sync(FULL, lane < nl && myc > 0);
     const int first = tm ? __ffs(tm) - 1 : nl;  // first old layer that received gap insertions
@@ -1352,6 +1366,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, c
     A.gapins[u] = gapc;
     A.pool[u] = base + total;
   }
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, const int2 *__restrict__ wslot,
+                                                                  int32_t *__restrict__ over, int *__restrict__ nover) {
+  extern __shared__ int32_t smem[];
+  const int2 slot = wslot[blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5)];
+  if (slot.x < 0) return;
+  const int c = slot.x % A.C;
+  if (A.cand[c] & STW_CAND_GAP)
+    layers_w32_unit<true>(A, smem + slot.y, slot, over, nover);
+  else
+    layers_w32_unit<false>(A, smem, slot, over, nover);
 }
 
 // ---------------------------------------------------------------------------
@@ -1904,8 +1930,13 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // CTA's budget, and any unit that needs > 32 layers, go to the CTA kernel
   std::vector<int32_t> order, bigs;
   order.reserve(U);
+  // shared-memory need per unit: units without gap insertion use none
+  auto need = [&](int32_t u) {
+    return (hcand[u % C] & STW_CAND_GAP) ? warpn_smem_ints((int)std::min<int64_t>(uo[u + 1] - uo[u], INT_MAX / 8))
+                                         : 0;
+  };
   for (int64_t u = 0; u < U; u++) {
-    if (warpn_smem_ints((int)std::min<int64_t>(uo[u + 1] - uo[u], INT_MAX / 8)) <= kLayerSmemInts)
+    if (need((int32_t)u) <= kLayerSmemInts && uo[u + 1] - uo[u] < INT_MAX / 8)
       order.push_back((int32_t)u);
     else
       bigs.push_back((int32_t)u);
@@ -1927,14 +1958,12 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     int used = 0, k = 0;
     auto put = [&](int32_t u) {
       wslot.push_back(make_int2(u, used));
-      used += warpn_smem_ints((int)(uo[u + 1] - uo[u]));
+      used += need(u);
       k++;
     };
     put(order[i++]);
-    while (k < kWarpsPerCta && i < j && used + warpn_smem_ints((int)(uo[order[i] + 1] - uo[order[i]])) <= kLayerSmemInts)
-      put(order[i++]);
-    while (k < kWarpsPerCta && i < j && used + warpn_smem_ints((int)(uo[order[j - 1] + 1] - uo[order[j - 1]])) <= kLayerSmemInts)
-      put(order[--j]);
+    while (k < kWarpsPerCta && i < j && used + need(order[i]) <= kLayerSmemInts) put(order[i++]);
+    while (k < kWarpsPerCta && i < j && used + need(order[j - 1]) <= kLayerSmemInts) put(order[--j]);
     while (wslot.size() < base + kWarpsPerCta) wslot.push_back(make_int2(-1, 0));
   }
   pt.mark("D sort");
