@@ -987,8 +987,87 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
     }
     for (int l = tid; l < nl; l += blockDim.x) newcnt[l] = 0;
     __syncthreads();
-    // ---- 2. warp-serial resolve: gap insertion, else Alg. 1 among this class's new layers
+    // ---- 2. warp-serial resolve: gap insertion, else Alg. 1 among this class's new layers.
+    // Narrow case (<= 32 layers): the register-resident chain of k_layers_w32;
+    // if the class would open a 33rd layer it is redone by the general loop.
+    __shared__ int sh_cnt[32], sh_fast;
     if (warp == 0) {
+      constexpr unsigned FULL = 0xffffffffu;
+      bool fast = nl <= 32;
+      int nnew = 0, gapc = 0;
+      if (fast) {
+        int lastp = INT_MIN, ne = INT_MIN;
+        sh_cnt[lane] = 0;
+        __syncwarp();
+        for (int64_t cb = j0; cb < j1 && fast; cb += 32) {
+          const int64_t mine = cb + lane;
+          const int cnt = (int)min((int64_t)32, j1 - cb);
+          int my_ts = 0, my_te = 0;
+          unsigned fm = 0;
+          if (mine < j1) {
+            my_ts = A.it.ts[mine];
+            my_te = A.it.te[mine];
+            if (gap && nl > 0) fm = fitw[(mine - a0) * kFitWords];
+          }
+          int my_code = 0;
+          for (int kg = 0; kg < cnt && fast; kg += 8) {
+#pragma unroll
+            for (int kk = 0; kk < 8; kk++) {
+              const int k = kg + kk;
+              const bool valid = k < cnt;
+              const int ts = __shfl_sync(FULL, my_ts, k & 31), te = __shfl_sync(FULL, my_te, k & 31);
+              const unsigned f = __shfl_sync(FULL, fm, k & 31);
+              const unsigned m1 = gap ? __ballot_sync(FULL, ((f >> lane) & 1u) && lastp < ts) : 0u;
+              const bool ca = lane < nnew && ne < ts;
+              const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
+              const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
+              const int host = __ffs(m1) - 1;
+              const int best = cma ? __ffs(cma) - 1 : nnew;
+              const bool newl = valid && !m1 && !cma;
+              if (newl && nl + nnew == 32) fast = false;
+              if (valid && fast) {
+                if (m1) {
+                  if (lane == host) lastp = te;
+                } else if (lane == best) {
+                  ne = te;
+                }
+              }
+              nnew += (newl && fast) ? 1 : 0;
+              if (lane == k) my_code = m1 ? host : 32 + best;
+            }
+          }
+          if (!fast) break;
+          const bool act = lane < cnt;
+          const int layer = my_code < 32 ? prioA[my_code] : nl + (my_code - 32);
+          gapc += __popc(__ballot_sync(FULL, act && my_code < 32));
+          const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
+          const int r = __popc(peers & lanemask_lt());
+          const int base = act ? sh_cnt[layer] : 0;
+          __syncwarp();
+          if (act) {
+            ilayer[mine - a0] = layer;
+            irank[mine - a0] = base + r;
+            if (r == __popc(peers) - 1) sh_cnt[layer] = base + __popc(peers);
+          }
+          __syncwarp();
+        }
+        if (fast) {
+          for (int l = lane; l < nl + nnew; l += 32) newcnt[l] = sh_cnt[l];
+          if (lane == 0) {
+            sh_nnew = nnew;
+            sh_gap += gapc;
+          }
+        } else {  // restart the class on the general path
+          nnew = 0;
+          for (int p = lane; p < nl; p += 32) last[p] = INT_MIN;
+          for (int l = lane; l < nl; l += 32) newcnt[l] = 0;
+          __syncwarp();
+        }
+      }
+      if (lane == 0) sh_fast = fast;
+    }
+    __syncthreads();
+    if (!sh_fast && warp == 0) {
       int nnew = 0;
       long long gapc = 0;
       int32_t *nend = A.nend + off;  // spill path when a class opens > kSmemLayers layers
