@@ -218,6 +218,31 @@ static void seg_sort(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, int segbits,
 }
 
 // rank[perm[k]] = k - ev_off[trace]; optional per-trace local permutation
+// 1 into *flag unless every trace's ids increase strictly and its t_s never
+// decrease (then its id order and its (t_s, id) order are both the listing order)
+__global__ void k_presorted(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
+                            const int32_t *__restrict__ ts, int *__restrict__ flag) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  bool bad = false;
+  for (int t = w; t < T; t += nw)
+    for (int64_t i = ev_off[t] + 1 + lane; i < ev_off[t + 1]; i += 32)
+      bad |= !(id[i - 1] < id[i] && ts[i - 1] <= ts[i]);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_identity_ranks(const int32_t *__restrict__ tr, const int64_t *__restrict__ ev_off, int64_t n,
+                                 int32_t *__restrict__ q, int32_t *__restrict__ r, uint32_t *__restrict__ rperm,
+                                 int32_t *__restrict__ local_order) {
+  GRID_STRIDE(i, n) {
+    const int32_t k = (int32_t)(i - ev_off[tr[i]]);
+    q[i] = k;
+    r[i] = k;
+    rperm[i] = (uint32_t)i;
+    local_order[i] = k;
+  }
+}
+
 __global__ void k_rank_from_perm(const uint32_t *__restrict__ perm, const int32_t *__restrict__ tr,
                                  const int64_t *__restrict__ ev_off, int64_t n, int32_t *__restrict__ rank,
                                  int32_t *__restrict__ local_order) {
@@ -1785,6 +1810,10 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
   LAUNCH_RED(k_minmax_i64, N, b.id, N, mm, mm + 1);
   LAUNCH_RED(k_max_i32, N, b.t_s, N, im);
+  if (T > 0) {  // im[2] = 1 unless every trace lists its events in id order and (t_s, id) order
+    STW_KL(k_presorted, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, im + 2);
+    STW_LAUNCHED(ctx);
+  }
   long long hmm[2] = {0, 0};
   int him[4] = {0, 0, 0, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
@@ -1795,14 +1824,18 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   const int idb = N ? bitlen_u64((uint64_t)(hmm[1] - hmm[0])) : 0;
   const int qb = bitlen_u64((uint64_t)(b.max_trace_events > 0 ? b.max_trace_events - 1 : 0));
   const int tsb = bitlen_u64((uint64_t)him[0]);
-  // q: id rank within trace
-  LAUNCH(k_key_q, N, tr, b.id, N, hmm[0], khi, klo);
-  seg_sort(ctx, ar, khi, tb, tb, klo, idb, perm, N, b.ev_off, T, b.max_trace_events);
-  LAUNCH(k_rank_from_perm, N, perm, tr, b.ev_off, N, q, (int32_t *)nullptr);
-  // r: (t_s, id) rank within trace
-  LAUNCH(k_key_r, N, tr, b.t_s, q, N, qb, khi, klo);
-  seg_sort(ctx, ar, khi, tb, tb, klo, tsb + qb, rperm, N, b.ev_off, T, b.max_trace_events);
-  LAUNCH(k_rank_from_perm, N, rperm, tr, b.ev_off, N, r, order_local);
+  if (him[2] == 0) {  // recorded order: both ranks are the position in the trace
+    LAUNCH(k_identity_ranks, N, tr, b.ev_off, N, q, r, rperm, order_local);
+  } else {
+    // q: id rank within trace
+    LAUNCH(k_key_q, N, tr, b.id, N, hmm[0], khi, klo);
+    seg_sort(ctx, ar, khi, tb, tb, klo, idb, perm, N, b.ev_off, T, b.max_trace_events);
+    LAUNCH(k_rank_from_perm, N, perm, tr, b.ev_off, N, q, (int32_t *)nullptr);
+    // r: (t_s, id) rank within trace
+    LAUNCH(k_key_r, N, tr, b.t_s, q, N, qb, khi, klo);
+    seg_sort(ctx, ar, khi, tb, tb, klo, tsb + qb, rperm, N, b.ev_off, T, b.max_trace_events);
+    LAUNCH(k_rank_from_perm, N, rperm, tr, b.ev_off, N, r, order_local);
+  }
 
   pt.mark("A ranks");
   // per-trace input checks
