@@ -157,21 +157,92 @@ void Arena::release() {
   left = 0;
 }
 
+// Single-pass scan with decoupled look-back: tiles of kScanTile claimed in
+// order by an atomic counter; each tile publishes its aggregate, then a warp
+// looks back over up to 32 predecessors at a time (flag + value arrays, the
+// value written before its flag behind a fence) for the nearest inclusive
+// prefix; one launch and one read + one write of the data.
+template <class T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ in, T *__restrict__ out, int64_t n,
+                                                          int inclusive, uint32_t *__restrict__ flag,
+                                                          T *__restrict__ agg, T *__restrict__ pre,
+                                                          uint32_t *__restrict__ ctr) {
+  __shared__ T sh[33];
+  __shared__ uint32_t s_tile;
+  __shared__ T s_excl;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanTile + (int64_t)tid * kScanItems;
+  T v[kScanItems];
+  T acc = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    v[k] = base + k < n ? in[base + k] : T(0);
+    acc += v[k];
+  }
+  T total;
+  const T ex = block_excl_sum<T>(acc, sh, &total);
+  volatile uint32_t *vf = flag;
+  if (tid == 0) {
+    if (tile == 0) {
+      pre[0] = total;
+      __threadfence();
+      atomicExch(flag, 2u);
+    } else {
+      agg[tile] = total;
+      __threadfence();
+      atomicExch(flag + tile, 1u);
+    }
+  }
+  if (tid < 32) {
+    T excl = 0;
+    if (tile > 0) {
+      for (int64_t t0 = (int64_t)tile - 1;; t0 -= 32) {
+        const int64_t t = t0 - lane;
+        uint32_t f = 2;
+        T val = 0;
+        if (t >= 0) {
+          while ((f = vf[t]) == 0) {
+          }
+          __threadfence();
+          val = f == 2 ? *(volatile T *)(pre + t) : *(volatile T *)(agg + t);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest inclusive prefix in this window
+        T part = lane <= stop ? val : T(0);
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (pm) break;
+      }
+      if (lane == 0) {
+        pre[tile] = excl + total;
+        __threadfence();
+        atomicExch(flag + tile, 2u);
+      }
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  T run = ex + s_excl;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    if (base + k < n) out[base + k] = inclusive ? run + v[k] : run;
+    run += v[k];
+  }
+}
+
 template <class T>
 void device_scan(Ctx &ctx, Arena &ar, const T *in, T *out, int64_t n, bool inclusive) {
   if (n <= 0 || !ctx.ok()) return;
-  int64_t nb = (n + kScanTile - 1) / kScanTile;
-  if (nb == 1) {
-    STW_KL(k_tile_scan<T>, 1, kScanThreads, ctx.stream, in, out, nullptr, n, inclusive);
-    STW_LAUNCHED(ctx);
-    return;
-  }
-  T *sums = ar.take<T>(nb);
-  if (!sums) return;
-  STW_KL(k_tile_reduce<T>, (unsigned)nb, kScanThreads, ctx.stream, in, sums, n);
-  STW_LAUNCHED(ctx);
-  device_scan<T>(ctx, ar, sums, sums, nb, false);
-  STW_KL(k_tile_scan<T>, (unsigned)nb, kScanThreads, ctx.stream, in, out, sums, n, inclusive);
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  uint32_t *flag = ar.take<uint32_t>(nb + 1);
+  T *agg = ar.take<T>(nb), *pre = ar.take<T>(nb);
+  if (!ctx.ok()) return;
+  STW_CUDA(ctx, cudaMemsetAsync(flag, 0, (nb + 1) * sizeof(uint32_t), ctx.stream));
+  STW_KL(k_scan_lb<T>, (unsigned)nb, kScanThreads, ctx.stream, in, out, n, inclusive ? 1 : 0, flag, agg, pre,
+         flag + nb);
   STW_LAUNCHED(ctx);
 }
 template void device_scan<uint32_t>(Ctx &, Arena &, const uint32_t *, uint32_t *, int64_t, bool);
