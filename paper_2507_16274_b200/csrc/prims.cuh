@@ -8,7 +8,7 @@ namespace stw {
 // scan: single pass with decoupled look-back, 2048 elements per block (256 threads x 8)
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 struct Arena;
