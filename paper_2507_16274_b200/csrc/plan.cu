@@ -542,7 +542,7 @@ __device__ void gather_members(const FusionArgs &A, int64_t base, int64_t nt, in
   }
 }
 
-__global__ void __launch_bounds__(kPlanThreads) k_fusion(FusionArgs A, int T) {
+__global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T) {
   const int t = blockIdx.x;
   const int64_t p0 = A.pl_off[t];
   int P = (int)(A.pl_off[t + 1] - p0);
