@@ -1367,11 +1367,11 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
       }
       // lane-parallel: layer ids, gap count, insertion ranks
       const bool act = lane < cnt;
-      const int layer = my_code < kWN ? prio[my_code] : nl + (my_code - kWN);
-      if (!GAP) {
-        if (act) ilayer[mine] = layer;
+      if (!GAP) {  // no shared memory here: every code is a new layer of the class
+        if (act) ilayer[mine] = nl + (my_code - kWN);
         continue;
       }
+      const int layer = my_code < kWN ? prio[my_code] : nl + (my_code - kWN);
       gapc += __popc(__ballot_sync(FULL, act && my_code < kWN));
       const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
       const int r = __popc(peers & lanemask_lt());
@@ -1682,6 +1682,19 @@ __global__ void k_scatter_fusions(const int32_t *__restrict__ ptr, const int64_t
 
 // Per-thread cache of forked streams/events for concurrent launches inside one
 // call (created once per host thread, reused; the call stays synchronous).
+// per-thread side stream and fork/join events (a call's work is joined back
+// into its own stream before the call returns)
+static cudaStream_t side_stream() {
+  thread_local cudaStream_t s = nullptr;
+  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  return s;
+}
+static cudaEvent_t side_event(int i) {
+  thread_local cudaEvent_t e[2] = {};
+  if (!e[i]) cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming);
+  return e[i];
+}
+
 template <class T>
 static void d2h(Ctx &ctx, std::vector<T> &h, const T *d, int64_t n) {
   h.resize(n);
@@ -2063,20 +2076,34 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     for (int32_t u : order) sorted[pos[mx - (uo[u + 1] - uo[u])]++] = u;
     order.swap(sorted);
   }
-  std::vector<int2> wslot;
-  wslot.reserve(order.size() + kWarpsPerCta);
-  for (size_t i = 0, j = order.size(); i < j;) {
-    const size_t base = wslot.size();
-    int used = 0, k = 0;
-    auto put = [&](int32_t u) {
-      wslot.push_back(make_int2(u, used));
-      used += need(u);
-      k++;
-    };
-    put(order[i++]);
-    while (k < kWarpsPerCta && i < j && used + need(order[i]) <= kLayerSmemInts) put(order[i++]);
-    while (k < kWarpsPerCta && i < j && used + need(order[j - 1]) <= kLayerSmemInts) put(order[--j]);
-    while (wslot.size() < base + kWarpsPerCta) wslot.push_back(make_int2(-1, 0));
+  // gap units: CTAs packed to the shared-memory budget; non-gap units need no
+  // shared memory and go eight to a CTA in a second launch (dynamic smem 0),
+  // which runs concurrently on a side stream
+  std::vector<int2> wslot, wslot_ng;
+  {
+    std::vector<int32_t> og;
+    og.reserve(order.size());
+    for (int32_t u : order) {
+      if (need(u) > 0)
+        og.push_back(u);
+      else
+        wslot_ng.push_back(make_int2(u, 0));
+    }
+    while (wslot_ng.size() % kWarpsPerCta) wslot_ng.push_back(make_int2(-1, 0));
+    wslot.reserve(og.size() + kWarpsPerCta);
+    for (size_t i = 0, j = og.size(); i < j;) {
+      const size_t base = wslot.size();
+      int used = 0, k = 0;
+      auto put = [&](int32_t u) {
+        wslot.push_back(make_int2(u, used));
+        used += need(u);
+        k++;
+      };
+      put(og[i++]);
+      while (k < kWarpsPerCta && i < j && used + need(og[i]) <= kLayerSmemInts) put(og[i++]);
+      while (k < kWarpsPerCta && i < j && used + need(og[j - 1]) <= kLayerSmemInts) put(og[--j]);
+      while (wslot.size() < base + kWarpsPerCta) wslot.push_back(make_int2(-1, 0));
+    }
   }
   pt.mark("D sort");
   // classes
@@ -2104,21 +2131,30 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
                ar.take<int32_t>(U), ar.take<int64_t>(U), ar.take<int64_t>(U)};
   if (!ctx.ok()) return ctx.rc;
   {
-    const int nctas = (int)(wslot.size() / kWarpsPerCta);
+    const int nctas = (int)(wslot.size() / kWarpsPerCta), nctas_ng = (int)(wslot_ng.size() / kWarpsPerCta);
     int32_t *d_over = ar.take<int32_t>(U + 1);
     int *d_nover = ar.take<int>(1);
-    int2 *d_wslot = nctas ? ar.take<int2>(wslot.size()) : nullptr;
+    int2 *d_wslot = nctas ? h2d(ctx, ar, wslot) : nullptr;
+    int2 *d_wslot_ng = nctas_ng ? h2d(ctx, ar, wslot_ng) : nullptr;
     int32_t *d_bigs = bigs.empty() ? nullptr : h2d(ctx, ar, bigs);
     if (!ctx.ok()) return ctx.rc;
     STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, sizeof(int), ctx.stream));
+    cudaStream_t side = nullptr;
+    if (nctas_ng) {  // fork: non-gap units on the side stream
+      side = side_stream();
+      STW_CUDA(ctx, cudaEventRecord(side_event(0), ctx.stream));
+      STW_CUDA(ctx, cudaStreamWaitEvent(side, side_event(0), 0));
+      STW_KLS(k_layers_w32, (unsigned)nctas_ng, kWarpsPerCta * 32, 0, side, LA, d_wslot_ng, d_over, d_nover);
+      STW_LAUNCHED(ctx);
+      STW_CUDA(ctx, cudaEventRecord(side_event(1), side));
+    }
     if (nctas) {
-      STW_CUDA(ctx, cudaMemcpyAsync(d_wslot, wslot.data(), wslot.size() * sizeof(int2), cudaMemcpyHostToDevice,
-                                    ctx.stream));
       const int smem = kLayerSmemInts * (int)sizeof(int32_t);
       STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_w32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       STW_KLS(k_layers_w32, (unsigned)nctas, kWarpsPerCta * 32, smem, ctx.stream, LA, d_wslot, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }
+    if (side) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, side_event(1), 0));  // join
     if (!bigs.empty()) {
       STW_KL(k_layers, (unsigned)bigs.size(), kPlanThreads, ctx.stream, LA, d_bigs, (const int *)nullptr);
       STW_LAUNCHED(ctx);
