@@ -99,5 +99,14 @@ __device__ __forceinline__ int trace_of(const int64_t *__restrict__ ev_off, int 
 }
 
 void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak);
+// split form for callers that fold the check into a later host round trip:
+// launch, then finish (runs the global-timeline path for flagged traces)
+struct PeakPending {
+  int *nbig;     // device: traces that need the global-timeline path
+  int32_t *big;  // device list of those traces
+};
+PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak);
+void peak_live_finish(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
+                      const PeakPending &pp);
 
 }  // namespace stw

@@ -161,11 +161,35 @@ static void peak_live_global(Ctx &ctx, Arena &ar, const DevBatch &b, bool static
                              const uint8_t *only);
 
 void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak) {
-  if (!ctx.ok() || b.T == 0) return;
+  PeakPending pp = peak_live_launch(ctx, ar, b, static_only, d_peak);
+  peak_live_finish(ctx, ar, b, static_only, d_peak, pp);
+}
+
+void peak_live_finish(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
+                      const PeakPending &pp) {
+  if (!ctx.ok() || !pp.nbig) return;
+  int h = 0;
+  STW_CUDA(ctx, cudaMemcpyAsync(&h, pp.nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (!ctx.ok() || h == 0) return;
+  const int T = b.T;
+  uint8_t *is_big = ar.take<uint8_t>(T);
+  if (!ctx.ok()) return;
+  STW_CUDA(ctx, cudaMemsetAsync(is_big, 0, T, ctx.stream));
+  STW_KL(k_big_offsets, grid_for(h, 256), 256, ctx.stream, pp.big, pp.nbig, T, is_big);
+  STW_LAUNCHED(ctx);
+  peak_live_global(ctx, ar, b, static_only, d_peak, is_big);
+}
+
+PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak) {
+  PeakPending pp{};
+  if (!ctx.ok() || b.T == 0) return pp;
   const int T = b.T;
   int *nbig = ar.take<int>(1);
   int32_t *big = ar.take<int32_t>(T);
-  if (!ctx.ok()) return;
+  if (!ctx.ok()) return pp;
+  pp.nbig = nbig;
+  pp.big = big;
   STW_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(int), ctx.stream));
   // pack traces into CTAs by timeline size, largest first (counting sort by horizon)
   std::vector<int32_t> order, longh;
@@ -203,7 +227,7 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
   }
   const int nctas = (int)(wslot.size() / kPeakWarps);
   int2 *d_wslot = nctas ? ar.take<int2>(wslot.size()) : nullptr;
-  if (!ctx.ok()) return;
+  if (!ctx.ok()) return pp;
   if (!longh.empty()) {  // long horizons go straight to the global path
     STW_CUDA(ctx, cudaMemcpyAsync(big, longh.data(), longh.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                                   ctx.stream));
@@ -218,16 +242,7 @@ void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t
             b.dyn, b.horizon, static_only ? 1 : 0, d_wslot, (long long *)d_peak, nbig, big);
   }
   STW_LAUNCHED(ctx);
-  int h = 0;
-  STW_CUDA(ctx, cudaMemcpyAsync(&h, nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
-  if (!ctx.ok() || h == 0) return;
-  uint8_t *is_big = ar.take<uint8_t>(T);
-  if (!ctx.ok()) return;
-  STW_CUDA(ctx, cudaMemsetAsync(is_big, 0, T, ctx.stream));
-  STW_KL(k_big_offsets, grid_for(h, 256), 256, ctx.stream, big, nbig, T, is_big);
-  STW_LAUNCHED(ctx);
-  peak_live_global(ctx, ar, b, static_only, d_peak, is_big);
+  return pp;
 }
 
 // Traces with long timelines (e.g. c5, horizon 1,966,792): the timeline lives

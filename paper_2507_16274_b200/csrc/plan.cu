@@ -80,6 +80,10 @@ __device__ T block_reduce_max(T v, T *sh) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // trace index of every event: one warp per trace writes its run (coalesced)
+__global__ void k_fill_i32(int *__restrict__ p, int64_t n, int v) {
+  GRID_STRIDE(i, n) p[i] = v;
+}
+
 __global__ void k_trace_of_all(const int64_t *__restrict__ ev_off, int T, int64_t N, int32_t *__restrict__ tr) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
@@ -220,15 +224,26 @@ static void seg_sort(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, int segbits,
 // rank[perm[k]] = k - ev_off[trace]; optional per-trace local permutation
 // 1 into *flag unless every trace's ids increase strictly and its t_s never
 // decrease (then its id order and its (t_s, id) order are both the listing order)
+// Also the largest per-trace byte total (an upper bound of every plan height
+// and event size, which sizes the item sort key).
 __global__ void k_presorted(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
-                            const int32_t *__restrict__ ts, int *__restrict__ flag) {
+                            const int32_t *__restrict__ ts, const int64_t *__restrict__ size, int *__restrict__ flag,
+                            long long *__restrict__ max_total) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   bool bad = false;
-  for (int t = w; t < T; t += nw)
-    for (int64_t i = ev_off[t] + 1 + lane; i < ev_off[t + 1]; i += 32)
-      bad |= !(id[i - 1] < id[i] && ts[i - 1] <= ts[i]);
+  long long mt = 0;
+  for (int t = w; t < T; t += nw) {
+    long long tot = 0;
+    for (int64_t i = ev_off[t] + lane; i < ev_off[t + 1]; i += 32) {
+      tot += size[i] > 0 ? size[i] : 0;
+      if (i > ev_off[t]) bad |= !(id[i - 1] < id[i] && ts[i - 1] <= ts[i]);
+    }
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    mt = max(mt, tot);
+  }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+  if (lane == 0 && mt > 0) atomicMax(max_total, mt);
 }
 
 __global__ void k_identity_ranks(const int32_t *__restrict__ tr, const int64_t *__restrict__ ev_off, int64_t n,
@@ -1811,23 +1826,31 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   uint64_t *khi = ar.take<uint64_t>(N + 1), *klo = ar.take<uint64_t>(N + 1);
   uint32_t *perm = ar.take<uint32_t>(N + 1), *rperm = ar.take<uint32_t>(N + 1), *gperm = ar.take<uint32_t>(N + 1);
   int32_t *order_local = ar.take<int32_t>(N + 1);
-  long long *mm = ar.take<long long>(2);
+  long long *mm = ar.take<long long>(3);
   int *im = ar.take<int>(4);
   if (!ctx.ok()) return ctx.rc;
   if (T > 0) {
     STW_KL(k_trace_of_all, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, N, tr);
     STW_LAUNCHED(ctx);
   }
-  long long mm_init[2] = {LLONG_MAX, LLONG_MIN};
+  long long mm_init[3] = {LLONG_MAX, LLONG_MIN, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
+  // per-trace input checks (alignment, schedule membership; im[1] = max phase index)
+  int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
+  if (!ctx.ok()) return ctx.rc;
+  LAUNCH(k_fill_i32, T, bad_align, T, INT_MAX);
+  LAUNCH(k_fill_i32, T, bad_phase, T, INT_MAX);
+  LAUNCH(k_checks, N, tr, b.ev_off, b.size, b.t_e, b.ps, b.pe, b.dyn, b.horizon, b.n_sched, N, (long long)o->alignment,
+         bad_align, bad_phase, im + 1);
   LAUNCH_RED(k_minmax_i64, N, b.id, N, mm, mm + 1);
   LAUNCH_RED(k_max_i32, N, b.t_s, N, im);
   if (T > 0) {  // im[2] = 1 unless every trace lists its events in id order and (t_s, id) order
-    STW_KL(k_presorted, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, im + 2);
+    STW_KL(k_presorted, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, b.size, im + 2,
+           mm + 2);
     STW_LAUNCHED(ctx);
   }
-  long long hmm[2] = {0, 0};
+  long long hmm[3] = {0, 0, 0};
   int him[4] = {0, 0, 0, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
   STW_CUDA(ctx, cudaMemcpyAsync(him, im, sizeof(him), cudaMemcpyDeviceToHost, ctx.stream));
@@ -1851,20 +1874,6 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
 
   pt.mark("A ranks");
-  // per-trace input checks
-  int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
-  if (!ctx.ok()) return ctx.rc;
-  {
-    std::vector<int> big(T, INT_MAX);
-    STW_CUDA(ctx, cudaMemcpyAsync(bad_align, big.data(), T * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
-    STW_CUDA(ctx, cudaMemcpyAsync(bad_phase, big.data(), T * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
-    sync(ctx);
-  }
-  LAUNCH(k_checks, N, tr, b.ev_off, b.size, b.t_e, b.ps, b.pe, b.dyn, b.horizon, b.n_sched, N, (long long)o->alignment,
-         bad_align, bad_phase, im + 1);
-  STW_CUDA(ctx, cudaMemcpyAsync(him, im, sizeof(him), cudaMemcpyDeviceToHost, ctx.stream));
-  sync(ctx);
-  if (!ctx.ok()) return ctx.rc;
   const int pb = bitlen_u64((uint64_t)him[1]);
 
   pt.mark("A checks");
@@ -2014,18 +2023,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     LAUNCH(k_items_res, N, e, rflag, rexcl, b.ev_off, d_nalive + (int64_t)v * T, d_io + (int64_t)v * T, N, it0);
   }
   pt.mark("D items");
-  // sort items by (variant-trace, size desc, t_s, tie)
-  long long maxsu = 0;
-  {
-    long long *dmx = ar.take<long long>(2);
-    long long init[2] = {LLONG_MAX, LLONG_MIN};
-    STW_CUDA(ctx, cudaMemcpyAsync(dmx, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
-    LAUNCH_RED(k_minmax_i64, NI, it0.size, NI, dmx, dmx + 1);
-    long long h[2] = {0, 0};
-    STW_CUDA(ctx, cudaMemcpyAsync(h, dmx, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
-    sync(ctx);
-    maxsu = NI ? h[1] / o->alignment : 0;
-  }
+  // sort items by (variant-trace, size desc, t_s, tie); every item size (event
+  // size or plan height) is at most its trace's byte total
+  const long long maxsu = NI ? hmm[2] / o->alignment : 0;
   uint64_t *ihi = ar.take<uint64_t>(NI + 1), *ilo = ar.take<uint64_t>(NI + 1);
   uint32_t *iperm = ar.take<uint32_t>(NI + 1);
   if (!ctx.ok()) return ctx.rc;
@@ -2200,7 +2200,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
   int64_t *peak = ar.take<int64_t>(T);
   if (!ctx.ok()) return ctx.rc;
-  peak_live(ctx, ar, b, true, peak);
+  const PeakPending ppk = peak_live_launch(ctx, ar, b, true, peak);  // finished at the finalize round trip
   uint32_t *sflag = ar.take<uint32_t>(N + 1), *spos = ar.take<uint32_t>(N + 1);
   if (!ctx.ok()) return ctx.rc;
   LAUNCH(k_static_flag, N, rperm, b.dyn, N, sflag);
@@ -2216,7 +2216,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   LAUNCH(k_rect_fill, N, rperm, sflag, spos, e, N, C, addr, rs_ev, rts, rte, rsz, raddr, NS);
   RectSets rs{T, NS, d_so, rts, rte, rsz, C, raddr};
-  validate_sets(ctx, ar, rs, vcount, vfirst, __builtin_ctzll((unsigned long long)o->alignment));
+  // fast validity test now; its verdict is read at the finalize round trip
+  STW_CUDA(ctx, cudaMemsetAsync(vcount, 0, U * sizeof(long long), ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(vfirst, 0x7f, U * sizeof(int), ctx.stream));
+  int *d_nflag = overlap_launch(ctx, ar, rs, __builtin_ctzll((unsigned long long)o->alignment));
+  if (!ctx.ok()) return ctx.rc;
 
   pt.mark("G check");
   // ---- per-unit verdicts, stats and best-candidate selection on the device
@@ -2227,16 +2231,32 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   int *d_nconf = ar.take<int>(1);
   int64_t *d_att = att_dev, *d_acc = acc_dev;
   if (!ctx.ok()) return ctx.rc;
-  STW_CUDA(ctx, cudaMemsetAsync(d_nconf, 0, sizeof(int), ctx.stream));
   FinalArgs FA{T, C, d_var, tc, d_att, d_acc, LA.gapins, LA.nlayers, LA.pool, peak, bad_align, bad_phase, vcount,
                b.ev_off, d_rc, d_err, d_stats, d_nconf};
-  LAUNCH(k_unit_finalize, U, FA);
-  LAUNCH(k_select_best, T, d_rc, LA.pool, T, C, d_best, d_bpool);
-  LAUNCH(k_gather_best, N, tr, d_best, addr, N, d_abest);
-  int h_nconf = 0;
-  STW_CUDA(ctx, cudaMemcpyAsync(&h_nconf, d_nconf, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  auto finalize = [&]() {
+    STW_CUDA(ctx, cudaMemsetAsync(d_nconf, 0, sizeof(int), ctx.stream));
+    LAUNCH(k_unit_finalize, U, FA);
+    LAUNCH(k_select_best, T, d_rc, LA.pool, T, C, d_best, d_bpool);
+    LAUNCH(k_gather_best, N, tr, d_best, addr, N, d_abest);
+  };
+  finalize();
+  // one host round trip for the deferred checks: conflicts, units the fast
+  // validity test could not decide, traces whose peak needs the global timeline
+  int hq[3] = {0, 0, 0};
+  STW_CUDA(ctx, cudaMemcpyAsync(hq, d_nconf, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  if (d_nflag) STW_CUDA(ctx, cudaMemcpyAsync(hq + 1, d_nflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  if (ppk.nbig) STW_CUDA(ctx, cudaMemcpyAsync(hq + 2, ppk.nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   sync(ctx);
   if (!ctx.ok()) return ctx.rc;
+  if (hq[1] > 0 || hq[2] > 0) {  // rare: redo the verdicts with the exact validator / global peaks
+    if (hq[2] > 0) peak_live_finish(ctx, ar, b, true, peak, ppk);
+    if (hq[1] > 0) validate_exact(ctx, ar, rs, vcount, vfirst);
+    finalize();
+    STW_CUDA(ctx, cudaMemcpyAsync(hq, d_nconf, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    sync(ctx);
+    if (!ctx.ok()) return ctx.rc;
+  }
+  const int h_nconf = hq[0];
   if (h_nconf > 0) {  // error path: name the first reported pair of every conflicting unit
     std::vector<long long> h_vc;
     std::vector<int> h_vf;

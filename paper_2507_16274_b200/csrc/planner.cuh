@@ -35,6 +35,10 @@ void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, 
 // number of units that need the exact reporter (0 = every unit is valid), -1
 // on a CUDA error.
 int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift);
+// the same test without the host round trip: returns the device counter
+int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift);
+// the exact reporter for every unit (fills d_count / d_first)
+void validate_exact(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first);
 
 // Host-side re-derivation of the first reported pair (a, b) of a decision set
 // whose first reporting decision is at sweep position `first` (device data).

@@ -344,16 +344,24 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
   }
 }
 
-int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift) {
-  if (!ctx.ok()) return -1;
+// launches the fast test; returns the device counter of units that need the
+// exact reporter (valid after the stream reaches it)
+int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift) {
+  if (!ctx.ok()) return nullptr;
   const int64_t U = (int64_t)rs.S * rs.n_cand;
   int *nflag = ar.take<int>(1);
-  if (!ctx.ok()) return -1;
+  if (!ctx.ok()) return nullptr;
   STW_CUDA(ctx, cudaMemsetAsync(nflag, 0, sizeof(int), ctx.stream));
   if (U > 0) {
     STW_KL(k_overlap_sweep, (unsigned)((U + kOvWarps - 1) / kOvWarps), kOvWarps * 32, ctx.stream, rs, shift, nflag);
     STW_LAUNCHED(ctx);
   }
+  return nflag;
+}
+
+int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift) {
+  int *nflag = overlap_launch(ctx, ar, rs, shift);
+  if (!nflag) return -1;
   int h = 0;
   STW_CUDA(ctx, cudaMemcpyAsync(&h, nflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
@@ -366,7 +374,14 @@ void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, 
   STW_CUDA(ctx, cudaMemsetAsync(d_count, 0, U * sizeof(long long), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(d_first, 0x7f, U * sizeof(int), ctx.stream));  // 0x7f7f7f7f: no report
   if (overlap_flags(ctx, ar, rs, shift) == 0) return;  // every unit valid: nothing reported
+  validate_exact(ctx, ar, rs, d_count, d_first);
+}
+
+// the exact tiled reporter over every unit (counts and first reporting position)
+void validate_exact(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first) {
   if (!ctx.ok()) return;
+  int64_t U = (int64_t)rs.S * rs.n_cand;
+  STW_CUDA(ctx, cudaMemsetAsync(d_count, 0, U * sizeof(long long), ctx.stream));
   std::vector<int> big(U, INT_MAX);
   STW_CUDA(ctx, cudaMemcpyAsync(d_first, big.data(), U * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
   Tiles tl;
