@@ -384,8 +384,9 @@ __global__ void k_group_table(Ev e, const uint32_t *__restrict__ gperm, const ui
 }
 
 __global__ void k_group_rel(const uint32_t *__restrict__ gperm, const uint32_t *__restrict__ gid_incl,
-                            const int64_t *__restrict__ S, const int64_t *__restrict__ szs, Groups g, int G,
+                            const int64_t *__restrict__ S, const int64_t *__restrict__ szs, Groups g,
                             int64_t n, int64_t *__restrict__ rel, int32_t *__restrict__ gof) {
+  const int G = (int)gid_incl[n - 1];  // number of groups
   GRID_STRIDE(k, n) {
     int gi = (int)gid_incl[k] - 1;
     uint32_t i = gperm[k];
@@ -401,7 +402,9 @@ struct TraceCounts {
   int64_t *pers_size;
 };
 
-__global__ void k_trace_counts(Groups g, int G, int64_t n, TraceCounts tc, uint32_t *__restrict__ is_plan) {
+__global__ void k_trace_counts(Groups g, const uint32_t *__restrict__ Gp, int64_t n, TraceCounts tc,
+                               uint32_t *__restrict__ is_plan) {
+  const int G = (int)*Gp;  // launched over an upper bound (n); groups past G idle
   GRID_STRIDE(gi, (int64_t)G) {
     int t = g.tr[gi];
     int64_t cnt = (gi + 1 < G ? g.start[gi + 1] : n) - g.start[gi];
@@ -435,9 +438,10 @@ struct Plans {
   uint8_t *alive;
 };
 
-__global__ void k_plan_init(Groups g, int G, const uint32_t *__restrict__ is_plan,
+__global__ void k_plan_init(Groups g, const uint32_t *__restrict__ Gp, const uint32_t *__restrict__ is_plan,
                             const uint32_t *__restrict__ pidx_excl, const uint32_t *__restrict__ gperm, Ev e,
                             Plans p) {
+  const int G = (int)*Gp;
   GRID_STRIDE(gi, (int64_t)G) {
     if (!is_plan[gi]) continue;
     uint32_t k = pidx_excl[gi];
@@ -1889,15 +1893,15 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_group_heads, N, e, gperm, b.ev_off, N, head, szs);
   device_scan<uint32_t>(ctx, ar, head, gid, N, true);
   device_scan<int64_t>(ctx, ar, szs, S, N, false);
-  uint32_t G32 = 0;
-  if (N) STW_CUDA(ctx, cudaMemcpyAsync(&G32, gid + N - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx.stream));
-  sync(ctx);
-  const int G = (int)G32;
+  // the group count stays on the device (G <= N): tables are sized by N and
+  // the group kernels read G = gid[N-1] themselves
+  const int G = (int)N;  // capacity
+  const uint32_t *d_G = gid + (N > 0 ? N - 1 : 0);
   Groups g{ar.take<int64_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1),
            ar.take<int32_t>(G + 1), ar.take<int64_t>(G + 1)};
   if (!ctx.ok()) return ctx.rc;
   LAUNCH(k_group_table, N, e, gperm, head, gid, N, g);
-  LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, G, N, rel, gof);
+  LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, N, rel, gof);
   TraceCounts tc{ar.take<int>(T), ar.take<int>(T), ar.take<int>(T), ar.take<int>(T), ar.take<int>(T),
                  ar.take<int64_t>(T)};
   uint32_t *is_plan = ar.take<uint32_t>(G + 1), *pidx = ar.take<uint32_t>(G + 1);
@@ -1905,7 +1909,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   for (int *pcnt : {tc.n_static, tc.n_pers, tc.n_groups, tc.n_plans, tc.n_res})
     STW_CUDA(ctx, cudaMemsetAsync(pcnt, 0, T * sizeof(int), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(tc.pers_size, 0, T * sizeof(int64_t), ctx.stream));
-  LAUNCH(k_trace_counts, G, g, G, N, tc, is_plan);
+  STW_CUDA(ctx, cudaMemsetAsync(is_plan, 0, (G + 1) * sizeof(uint32_t), ctx.stream));
+  LAUNCH(k_trace_counts, G, g, d_G, N, tc, is_plan);
   device_scan<uint32_t>(ctx, ar, is_plan, pidx, G, false);
   std::vector<int> h_nplans, h_nstatic, h_nres;
   d2h(ctx, h_nplans, tc.n_plans, T);
@@ -1926,7 +1931,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   Plans p0 = mk_plans();
   int32_t *pid0 = ar.take<int32_t>(N + 1);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_plan_init, G, g, G, is_plan, pidx, gperm, e, p0);
+  LAUNCH(k_plan_init, G, g, d_G, is_plan, pidx, gperm, e, p0);
   LAUNCH(k_plan_members, N, gperm, gof, is_plan, pidx, e, N, p0, pid0);
   LAUNCH(k_plan_tmp, P, p0, P);
 
