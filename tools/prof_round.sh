@@ -10,15 +10,15 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --csv --log-file gpurun_out/${tag}_launches.csv $B --no-kernel-sweep > gpurun_out/${tag}_launches.log 2>&1
 full() {  # name regex skip cmd...
   local name=$1 rx=$2 skip=$3; shift 3
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c ${NCU_COUNT:-1} \
       -o gpurun_out/${tag}_${name} "$@" > gpurun_out/${tag}_${name}.log 2>&1
   tail -1 gpurun_out/${tag}_${name}.log
 }
-full k_layers_w32 k_layers_w32 1 python tools/one_plan.py
+NCU_COUNT=2 full k_layers_w32 k_layers_w32 2 python tools/one_plan.py
 full k_fusion k_fusion 1 python tools/one_plan.py
-full k_seg_bitonic k_seg_bitonic 6 python tools/one_plan.py
+NCU_COUNT=2 full k_seg_bitonic k_seg_bitonic 2 python tools/one_plan.py
 full k_overlap_sweep_c4 k_overlap_sweep 1 python tools/one_plan.py
-full k_overlap_sweep_big k_overlap_sweep 4 $B
-full k_peak_warp_big k_peak_warp 4 $B
+full k_overlap_sweep_big k_overlap_sweep 7 $B
+full k_peak_warp_big k_peak_warp 7 $B
 full k_os_pass_big k_os_pass 6 $B
 ls -la gpurun_out | tail -30
