@@ -84,11 +84,44 @@ __global__ void k_fill_i32(int *__restrict__ p, int64_t n, int v) {
   GRID_STRIDE(i, n) p[i] = v;
 }
 
-__global__ void k_trace_of_all(const int64_t *__restrict__ ev_off, int T, int64_t N, int32_t *__restrict__ tr) {
+// One warp per trace: the trace index of every event (coalesced runs), and
+// *flag = 1 unless every trace's ids increase strictly and its t_s never
+// decrease (then its id order and its (t_s, id) order are both the listing
+// order), and the largest per-trace byte total (an upper bound of every plan
+// height and event size, which sizes the item sort key).
+__global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
+                             const int32_t *__restrict__ ts, const int64_t *__restrict__ size,
+                             int32_t *__restrict__ tr, int *__restrict__ flag, long long *__restrict__ max_total) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  for (int t = w; t < T; t += nw)
-    for (int64_t i = ev_off[t] + lane; i < ev_off[t + 1]; i += 32) tr[i] = t;
+  bool bad = false;
+  long long mt = 0;
+  for (int t = w; t < T; t += nw) {
+    const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
+    long long tot = 0;
+    int64_t pid = 0;  // last id / t_s of the previous chunk
+    int pts = 0;
+    for (int64_t c = e0; c < e1; c += 32) {
+      const int64_t i = c + lane;
+      const bool in = i < e1;
+      const int64_t my_id = in ? id[i] : 0;
+      const int my_ts = in ? ts[i] : 0;
+      if (in) {
+        tr[i] = t;
+        tot += size[i] > 0 ? size[i] : 0;
+      }
+      int64_t prev_id = __shfl_up_sync(0xffffffffu, my_id, 1);
+      int prev_ts = __shfl_up_sync(0xffffffffu, my_ts, 1);
+      if (lane == 0) prev_id = pid, prev_ts = pts;
+      if (in && i > e0) bad |= !(prev_id < my_id && prev_ts <= my_ts);
+      pid = __shfl_sync(0xffffffffu, my_id, 31);
+      pts = __shfl_sync(0xffffffffu, my_ts, 31);
+    }
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    mt = max(mt, tot);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+  if (lane == 0 && mt > 0) atomicMax(max_total, mt);
 }
 
 __global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx) {
@@ -221,31 +254,7 @@ static void seg_sort(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, int segbits,
   sort_perm2(ctx, ar, hi, hibits, lo, lobits, perm, n);
 }
 
-// rank[perm[k]] = k - ev_off[trace]; optional per-trace local permutation
-// 1 into *flag unless every trace's ids increase strictly and its t_s never
-// decrease (then its id order and its (t_s, id) order are both the listing order)
-// Also the largest per-trace byte total (an upper bound of every plan height
-// and event size, which sizes the item sort key).
-__global__ void k_presorted(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
-                            const int32_t *__restrict__ ts, const int64_t *__restrict__ size, int *__restrict__ flag,
-                            long long *__restrict__ max_total) {
-  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  bool bad = false;
-  long long mt = 0;
-  for (int t = w; t < T; t += nw) {
-    long long tot = 0;
-    for (int64_t i = ev_off[t] + lane; i < ev_off[t + 1]; i += 32) {
-      tot += size[i] > 0 ? size[i] : 0;
-      if (i > ev_off[t]) bad |= !(id[i - 1] < id[i] && ts[i - 1] <= ts[i]);
-    }
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    mt = max(mt, tot);
-  }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
-  if (lane == 0 && mt > 0) atomicMax(max_total, mt);
-}
-
+// traces in recorded order: both canonical ranks are the position in the trace
 __global__ void k_identity_ranks(const int32_t *__restrict__ tr, const int64_t *__restrict__ ev_off, int64_t n,
                                  int32_t *__restrict__ q, int32_t *__restrict__ r, uint32_t *__restrict__ rperm,
                                  int32_t *__restrict__ local_order) {
@@ -258,6 +267,7 @@ __global__ void k_identity_ranks(const int32_t *__restrict__ tr, const int64_t *
   }
 }
 
+// rank[perm[k]] = k - ev_off[trace]; optional per-trace local permutation
 __global__ void k_rank_from_perm(const uint32_t *__restrict__ perm, const int32_t *__restrict__ tr,
                                  const int64_t *__restrict__ ev_off, int64_t n, int32_t *__restrict__ rank,
                                  int32_t *__restrict__ local_order) {
@@ -1833,13 +1843,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   long long *mm = ar.take<long long>(3);
   int *im = ar.take<int>(4);
   if (!ctx.ok()) return ctx.rc;
-  if (T > 0) {
-    STW_KL(k_trace_of_all, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, N, tr);
-    STW_LAUNCHED(ctx);
-  }
   long long mm_init[3] = {LLONG_MAX, LLONG_MIN, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
+  if (T > 0) {  // tr, presortedness (im[2]) and the largest trace byte total (mm[2])
+    STW_KL(k_trace_scan, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, b.size, tr,
+           im + 2, mm + 2);
+    STW_LAUNCHED(ctx);
+  }
   // per-trace input checks (alignment, schedule membership; im[1] = max phase index)
   int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
   if (!ctx.ok()) return ctx.rc;
@@ -1849,11 +1860,6 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
          bad_align, bad_phase, im + 1);
   LAUNCH_RED(k_minmax_i64, N, b.id, N, mm, mm + 1);
   LAUNCH_RED(k_max_i32, N, b.t_s, N, im);
-  if (T > 0) {  // im[2] = 1 unless every trace lists its events in id order and (t_s, id) order
-    STW_KL(k_presorted, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, b.size, im + 2,
-           mm + 2);
-    STW_LAUNCHED(ctx);
-  }
   long long hmm[3] = {0, 0, 0};
   int him[4] = {0, 0, 0, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
