@@ -174,7 +174,7 @@ void sort_perm2(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, uint64_t *lo, int
 
 // ---------------------------------------------------------------------------
 // CTA-local segmented sort: one CTA per segment (trace or (variant, trace)),
-// bitonic network over (key, index) pairs in shared memory -- a stable sort of
+// an LSD radix sort of (key, index) pairs in shared memory -- a stable sort of
 // the segment in one global read + write. Used whenever every segment fits
 // kSegSortMax elements; otherwise the global LSD radix sort (K2) runs.
 
@@ -185,69 +185,127 @@ __global__ void k_local_key(uint64_t *__restrict__ hi, const uint64_t *__restric
   GRID_STRIDE(i, n) hi[i] = (lobits >= 64 ? 0 : ((hi[i] & mask) << lobits)) | lo[i];
 }
 
-__global__ void k_seg_bitonic(uint64_t *__restrict__ keys, uint32_t *__restrict__ perm,
-                              const int64_t *__restrict__ seg_off, int pcap) {
-  extern __shared__ uint64_t sk[];
+// Segmented LSD radix sort in shared memory: one CTA per segment, 8-bit
+// digits, only the key bits [bit0, bits) (a caller whose elements are already
+// ordered by the lower bits starts above them). Per pass each warp ranks its
+// contiguous block of the segment row by row -- peers from one ballot per
+// digit bit, the highest peer bumps the warp's digit counter with one shared
+// atomic -- then one thread per digit turns the (digit, warp) counts into
+// offsets and the elements are scattered to the other shared buffer. Stable;
+// ~40 instructions per element per pass instead of the bitonic network's
+// ~log2(P)^2/2 compare-exchanges.
+template <int IPT>
+__global__ void __launch_bounds__(256) k_seg_radix(uint64_t *__restrict__ keys, uint32_t *__restrict__ perm,
+                                                   const int64_t *__restrict__ seg_off, int bit0, int bits) {
+  constexpr int P = 256 * IPT;
+  extern __shared__ __align__(16) unsigned char srx[];
+  uint64_t *kA = (uint64_t *)srx;  // one buffer: a pass holds its elements in registers
+  uint32_t *vA = (uint32_t *)(kA + P);
+  uint32_t *wh = vA + P;  // [8 warps][256 digits]
+  __shared__ uint32_t sh[33];
   const int64_t s0 = seg_off[blockIdx.x];
   const int n = (int)(seg_off[blockIdx.x + 1] - s0);
-  if (n == 0) return;
-  // already in order (e.g. a trace's events by id or by (t_s, id), as
-  // recorded): the stable result is the identity
-  bool sorted = true;
-  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) sorted &= keys[s0 + i] <= keys[s0 + i + 1];
-  if (__syncthreads_and(sorted)) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[s0 + i] = (uint32_t)(s0 + i);
-    return;
-  }
-  int P = 1;
-  while (P < n) P <<= 1;
-  uint32_t *sv = (uint32_t *)(sk + pcap);
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    sk[i] = i < n ? keys[s0 + i] : ~0ull;
-    sv[i] = i < n ? (uint32_t)(s0 + i) : ~0u;
-  }
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
-        int a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a + j;  // j is a power of two
-        bool asc = (a & k) == 0;
-        uint64_t ka = sk[a], kb = sk[b];
-        uint32_t va = sv[a], vb = sv[b];
-        bool gt = ka > kb || (ka == kb && va > vb);
-        if (gt == asc) {
-          sk[a] = kb;
-          sk[b] = ka;
-          sv[a] = vb;
-          sv[b] = va;
-        }
-      }
-      __syncthreads();
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  {
+    bool all = true;  // no bits to sort, or already in order: the stable result is the identity
+    if (bit0 < bits)
+      for (int i = tid; i + 1 < n; i += 256) all &= keys[s0 + i] <= keys[s0 + i + 1];
+    if (__syncthreads_and(all)) {
+      for (int i = tid; i < n; i += 256) perm[s0 + i] = (uint32_t)(s0 + i);
+      return;
     }
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    keys[s0 + i] = sk[i];
-    perm[s0 + i] = sv[i];
+  for (int i = tid; i < n; i += 256) {
+    kA[i] = keys[s0 + i];
+    vA[i] = (uint32_t)(s0 + i);
+  }
+  __syncthreads();
+  const unsigned lt = lanemask_lt();
+  const int R = (n + 255) >> 8;  // rows of 32 per warp actually used (<= IPT)
+  const int run = 32 * R;        // each warp owns a contiguous block of the segment
+  for (int b = bit0; b < bits; b += 8) {
+    const int width = min(8, bits - b);
+    const uint32_t mask = (1u << width) - 1;
+    for (int x = tid; x < 8 * 256; x += 256) wh[x] = 0;
+    __syncthreads();
+    uint64_t k[IPT];
+    uint32_t v[IPT];
+    uint16_t rk[IPT];
+    uint32_t *myh = wh + w * 256;
+#pragma unroll
+    for (int j = 0; j < IPT; j++) {
+      if (j >= R) break;
+      const int e = w * run + j * 32 + lane;
+      const bool valid = e < n;
+      k[j] = valid ? kA[e] : 0;
+      v[j] = valid ? vA[e] : 0;
+      const uint32_t d = (uint32_t)(k[j] >> b) & mask;
+      unsigned peers = __ballot_sync(0xffffffffu, valid);
+      for (int q = 0; q < width; q++) {
+        const bool bit = (d >> q) & 1u;
+        const unsigned bb = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bb : ~bb;
+      }
+      const int leader = 31 - __clz(peers | 1u);
+      uint32_t old = 0;
+      if (valid && lane == leader) old = atomicAdd(myh + d, (uint32_t)__popc(peers));
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rk[j] = (uint16_t)(old + __popc(peers & lt));
+    }
+    __syncthreads();
+    {  // digit tid: offsets of (digit, warp) blocks in digit-major order
+      uint32_t run = 0;
+#pragma unroll
+      for (int x = 0; x < 8; x++) {
+        const uint32_t c = wh[x * 256 + tid];
+        wh[x * 256 + tid] = run;
+        run += c;
+      }
+      const uint32_t base = block_excl_sum<uint32_t>(run, sh, nullptr);
+#pragma unroll
+      for (int x = 0; x < 8; x++) wh[x * 256 + tid] += base;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < IPT; j++) {
+      if (j >= R) break;
+      const int e = w * run + j * 32 + lane;
+      if (e < n) {
+        const uint32_t d = (uint32_t)(k[j] >> b) & mask;
+        const uint32_t pos = myh[d] + rk[j];
+        kA[pos] = k[j];
+        vA[pos] = v[j];
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += 256) {
+    keys[s0 + i] = kA[i];
+    perm[s0 + i] = vA[i];
   }
 }
 
 // Stable sort of n elements by (segment, hi & ~segment bits, lo), segments
 // given by seg_off[nseg+1] (device) and contiguous. hi/lo are consumed.
 static void seg_sort(Ctx &ctx, Arena &ar, uint64_t *hi, int hibits, int segbits, uint64_t *lo, int lobits,
-                     uint32_t *perm, int64_t n, const int64_t *seg_off, int64_t nseg, int64_t max_seg) {
+                     uint32_t *perm, int64_t n, const int64_t *seg_off, int64_t nseg, int64_t max_seg,
+                     bool lo_in_order = false) {
   if (!ctx.ok() || n == 0) return;
   const int local_hi = hibits - segbits;
   if (max_seg <= kSegSortMax && local_hi + lobits <= 64) {
     uint64_t mask = local_hi >= 64 ? ~0ull : ((1ull << local_hi) - 1);
     STW_KL(k_local_key, grid_for(n, 256), 256, ctx.stream, hi, lo, mask, lobits, n);
-    int P = 1;
-    while (P < max_seg) P <<= 1;
-    int threads = std::max(32, std::min(256, P / 2));
-    size_t smem = (size_t)P * 12;
-    STW_CUDA(ctx, cudaFuncSetAttribute(k_seg_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int slot = prof_pre(ctx.stream);
-    k_seg_bitonic<<<(unsigned)nseg, threads, smem, ctx.stream>>>(hi, perm, seg_off, P);
-    prof_post(ctx.stream, "k_seg_bitonic", slot);
+    // lo_in_order: every segment already lists its elements by the low key bits,
+    // so a stable sort on the high bits alone is the full sort
+    const int bit0 = lo_in_order ? lobits : 0, bits = local_hi + lobits;
+    if (max_seg <= 2048) {
+      constexpr int smem = 2048 * 12 + 8 * 256 * 4;
+      STW_KLS(k_seg_radix<8>, (unsigned)nseg, 256, smem, ctx.stream, hi, perm, seg_off, bit0, bits);
+    } else {
+      constexpr int smem = 4096 * 12 + 8 * 256 * 4;
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_seg_radix<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      STW_KLS(k_seg_radix<16>, (unsigned)nseg, 256, smem, ctx.stream, hi, perm, seg_off, bit0, bits);
+    }
     STW_LAUNCHED(ctx);
     return;
   }
@@ -1890,7 +1948,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
   LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
-  seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events);
+  seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events,
+           /*lo_in_order=*/him[2] == 0);
   uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
   int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
   int64_t *rel = ar.take<int64_t>(N + 1);
