@@ -87,18 +87,14 @@ __global__ void k_fill_i32(int *__restrict__ p, int64_t n, int v) {
 // One warp per trace: the trace index of every event (coalesced runs), and
 // *flag = 1 unless every trace's ids increase strictly and its t_s never
 // decrease (then its id order and its (t_s, id) order are both the listing
-// order), and the largest per-trace byte total (an upper bound of every plan
-// height and event size, which sizes the item sort key).
+// order).
 __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
-                             const int32_t *__restrict__ ts, const int64_t *__restrict__ size,
-                             int32_t *__restrict__ tr, int *__restrict__ flag, long long *__restrict__ max_total) {
+                             const int32_t *__restrict__ ts, int32_t *__restrict__ tr, int *__restrict__ flag) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   bool bad = false;
-  long long mt = 0;
   for (int t = w; t < T; t += nw) {
     const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
-    long long tot = 0;
     int64_t pid = 0;  // last id / t_s of the previous chunk
     int pts = 0;
     for (int64_t c = e0; c < e1; c += 32) {
@@ -106,10 +102,7 @@ __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const in
       const bool in = i < e1;
       const int64_t my_id = in ? id[i] : 0;
       const int my_ts = in ? ts[i] : 0;
-      if (in) {
-        tr[i] = t;
-        tot += size[i] > 0 ? size[i] : 0;
-      }
+      if (in) tr[i] = t;
       int64_t prev_id = __shfl_up_sync(0xffffffffu, my_id, 1);
       int prev_ts = __shfl_up_sync(0xffffffffu, my_ts, 1);
       if (lane == 0) prev_id = pid, prev_ts = pts;
@@ -117,11 +110,8 @@ __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const in
       pid = __shfl_sync(0xffffffffu, my_id, 31);
       pts = __shfl_sync(0xffffffffu, my_ts, 31);
     }
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    mt = max(mt, tot);
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
-  if (lane == 0 && mt > 0) atomicMax(max_total, mt);
 }
 
 __global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx) {
@@ -1898,15 +1888,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   uint64_t *khi = ar.take<uint64_t>(N + 1), *klo = ar.take<uint64_t>(N + 1);
   uint32_t *perm = ar.take<uint32_t>(N + 1), *rperm = ar.take<uint32_t>(N + 1), *gperm = ar.take<uint32_t>(N + 1);
   int32_t *order_local = ar.take<int32_t>(N + 1);
-  long long *mm = ar.take<long long>(3);
+  long long *mm = ar.take<long long>(2);
   int *im = ar.take<int>(4);
   if (!ctx.ok()) return ctx.rc;
-  long long mm_init[3] = {LLONG_MAX, LLONG_MIN, 0};
+  long long mm_init[2] = {LLONG_MAX, LLONG_MIN};
   STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
-  if (T > 0) {  // tr, presortedness (im[2]) and the largest trace byte total (mm[2])
-    STW_KL(k_trace_scan, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, b.size, tr,
-           im + 2, mm + 2);
+  if (T > 0) {  // tr and presortedness (im[2])
+    STW_KL(k_trace_scan, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, tr, im + 2);
     STW_LAUNCHED(ctx);
   }
   // per-trace input checks (alignment, schedule membership; im[1] = max phase index)
@@ -1918,7 +1907,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
          bad_align, bad_phase, im + 1);
   LAUNCH_RED(k_minmax_i64, N, b.id, N, mm, mm + 1);
   LAUNCH_RED(k_max_i32, N, b.t_s, N, im);
-  long long hmm[3] = {0, 0, 0};
+  long long hmm[2] = {0, 0};
   int him[4] = {0, 0, 0, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
   STW_CUDA(ctx, cudaMemcpyAsync(him, im, sizeof(him), cudaMemcpyDeviceToHost, ctx.stream));
@@ -2058,6 +2047,17 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     d2h(ctx, h_acc, acc, T);
   }
 
+  // largest item size (plan heights of both variants, event sizes): sizes the
+  // item sort key, read with the fusion counts
+  long long *d_imax = ar.take<long long>(2);
+  long long h_imax[2] = {LLONG_MAX, 0};
+  if (!ctx.ok()) return ctx.rc;
+  STW_CUDA(ctx, cudaMemcpyAsync(d_imax, h_imax, sizeof(h_imax), cudaMemcpyHostToDevice, ctx.stream));
+  LAUNCH_RED(k_minmax_i64, P, p0.h, P, d_imax, d_imax + 1);
+  if (want[1]) LAUNCH_RED(k_minmax_i64, P, p1.h, P, d_imax, d_imax + 1);
+  LAUNCH_RED(k_minmax_i64, N, b.size, N, d_imax, d_imax + 1);
+  STW_CUDA(ctx, cudaMemcpyAsync(h_imax, d_imax, sizeof(h_imax), cudaMemcpyDeviceToHost, ctx.stream));
+
   pt.mark("C fusion");
   // ---- D: items per (variant, trace)
   std::vector<int64_t> io(V * T + 1, 0);
@@ -2093,9 +2093,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     LAUNCH(k_items_res, N, e, rflag, rexcl, b.ev_off, d_nalive + (int64_t)v * T, d_io + (int64_t)v * T, N, it0);
   }
   pt.mark("D items");
-  // sort items by (variant-trace, size desc, t_s, tie); every item size (event
-  // size or plan height) is at most its trace's byte total
-  const long long maxsu = NI ? hmm[2] / o->alignment : 0;
+  // sort items by (variant-trace, size desc, t_s, tie)
+  const long long maxsu = NI ? std::max(0ll, h_imax[1]) / o->alignment : 0;
   uint64_t *ihi = ar.take<uint64_t>(NI + 1), *ilo = ar.take<uint64_t>(NI + 1);
   uint32_t *iperm = ar.take<uint32_t>(NI + 1);
   if (!ctx.ok()) return ctx.rc;
