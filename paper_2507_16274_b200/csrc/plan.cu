@@ -1450,6 +1450,10 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
       }
       const int layer = my_code < kWN ? prio[my_code] : nl + (my_code - kWN);
       gapc += __popc(__ballot_sync(FULL, act && my_code < kWN));
+      if (j1 >= n) {  // last class: no merge follows, so no insertion ranks
+        if (act) ilayer[mine] = layer;
+        continue;
+      }
       const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
       const int r = __popc(peers & lanemask_lt());
       const int base = act ? newcnt[layer] : 0;
@@ -1461,10 +1465,11 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
       }
       __syncwarp();
     }
-    // ---- merge the class into the layer-major slot CSR
+    // ---- merge the class into the layer-major slot CSR (not after the last class:
+    // nothing reads the CSR any more)
     const int nl2 = nl + nnew;
     if (lane < nnew) lsize[nl + lane] = S;
-    if (!GAP) {
+    if (!GAP || j1 >= n) {
       nl = nl2;
       j0 = j1;
       continue;
