@@ -619,6 +619,8 @@ __device__ void gather_members(const FusionArgs &A, int64_t base, int64_t nt, in
   }
 }
 
+constexpr int kFuseCap = 384;  // rectangles of one try staged in shared memory
+
 __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T) {
   const int t = blockIdx.x;
   const int64_t p0 = A.pl_off[t];
@@ -637,6 +639,9 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T)
   __shared__ long long shl[33];
   __shared__ int sh_nf, sh_nr, sh_pick, sh_first, sh_left, sh_okw[32];
   __shared__ long long sh_addr, sh_maxend;
+  __shared__ long long s_fa[kFuseCap], s_fe[kFuseCap], s_csz[kFuseCap], s_new[kFuseCap];
+  __shared__ int s_fts[kFuseCap], s_fte[kFuseCap], s_cts[kFuseCap], s_cte[kFuseCap];
+  __shared__ uint8_t s_gone[kFuseCap];
   __shared__ long long sh_att, sh_acc;
   int32_t *lst = A.lst + p0;
   if (tid == 0) {
@@ -699,7 +704,84 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T)
           sh_nf = nf0;
         }
         __syncthreads();
-        while (sh_left > 0) {
+        if (nf0 + nr <= kFuseCap) {
+          // Shared-memory cursor walk (every c4 try): the fixed rectangles and the
+          // candidates' sizes / lifespans are staged once, so each placement step
+          // is shared-memory loads and barriers instead of L2 round trips.
+          for (int k = tid; k < nf0; k += blockDim.x) {
+            s_fa[k] = A.fx_addr[base + k];
+            s_fe[k] = A.fx_end[base + k];
+            s_fts[k] = A.fx_ts[base + k];
+            s_fte[k] = A.fx_te[base + k];
+          }
+          for (int k = tid; k < nr; k += blockDim.x) {
+            const int ev = A.rm_ev[base + k];
+            s_csz[k] = A.e.size[ev];
+            s_cts[k] = A.e.ts[ev];
+            s_cte[k] = A.e.te[ev];
+            s_gone[k] = 0;
+          }
+          __syncthreads();
+          while (sh_left > 0) {
+            const long long addr = sh_addr;
+            const int nf = sh_nf;
+            if (tid == 0) sh_pick = -1;
+            __syncthreads();
+            for (int cb = sh_first; cb < nr; cb += NW) {
+              const int k = cb + warp;
+              bool ok = false;
+              if (k < nr && !s_gone[k]) {
+                const long long hi = addr + s_csz[k];
+                const int ets = s_cts[k], ete = s_cte[k];
+                bool conflict = false;
+                for (int f = lane; f < nf && !conflict; f += 32)
+                  conflict = s_fa[f] < hi && addr < s_fe[f] && s_fts[f] < ete && ets < s_fte[f];
+                ok = !__any_sync(0xffffffffu, conflict);
+              }
+              if (lane == 0) sh_okw[warp] = ok ? k : INT_MAX;
+              __syncthreads();
+              if (tid == 0) {
+                int mk = INT_MAX;
+                for (int w = 0; w < NW; w++) mk = min(mk, sh_okw[w]);
+                if (mk != INT_MAX) sh_pick = mk;
+              }
+              __syncthreads();
+              if (sh_pick >= 0) break;
+            }
+            if (sh_pick >= 0) {
+              if (tid == 0) {
+                const int k = sh_pick;
+                const long long sz = s_csz[k];
+                s_gone[k] = 1;
+                s_new[k] = addr;
+                s_fa[nf] = addr;
+                s_fe[nf] = addr + sz;
+                s_fts[nf] = s_cts[k];
+                s_fte[nf] = s_cte[k];
+                sh_nf = nf + 1;
+                if (addr + sz > sh_maxend) sh_maxend = addr + sz;
+                sh_addr = addr + sz;
+                sh_left--;
+                int f = sh_first;
+                while (f < nr && s_gone[f]) f++;
+                sh_first = f;
+              }
+            } else {
+              // next anchor strictly above the cursor, else the top of everything fixed
+              long long nx = LLONG_MAX;
+              for (int k = tid; k < nf0; k += blockDim.x) {
+                const long long v = s_fa[k];
+                if (v > addr && v < nx) nx = v;
+              }
+              nx = block_reduce_min(nx, shl);
+              if (tid == 0) sh_addr = nx != LLONG_MAX ? nx : sh_maxend;
+            }
+            __syncthreads();
+          }
+          for (int k = tid; k < nr; k += blockDim.x) A.rm_new[base + k] = s_new[k];
+          __syncthreads();
+        }
+        while (sh_left > 0) {  // large tries: the same walk over global scratch
           const long long addr = sh_addr;
           const int nf = sh_nf;
           if (tid == 0) sh_pick = -1;
