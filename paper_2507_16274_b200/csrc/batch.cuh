@@ -105,7 +105,9 @@ struct PeakPending {
   int *nbig;     // device: traces that need the global-timeline path
   int32_t *big;  // device list of those traces
 };
-PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak);
+// shift: timeline entries count bytes in units of 2^shift (traces whose sizes
+// are not multiples fall back to the global-timeline path)
+PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak, int shift);
 void peak_live_finish(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
                       const PeakPending &pp);
 

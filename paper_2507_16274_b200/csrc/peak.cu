@@ -74,45 +74,43 @@ __global__ void k_segmax(const int64_t *__restrict__ P, int64_t H, const int64_t
 // (horizon + 1), largest first), so there are no block-wide barriers and many
 // traces per SM are in flight. A trace with a timestamp outside [0, horizon]
 // (or too long a horizon) goes to the global-timeline path below.
-// 64-bit shared-memory add from two native 32-bit atomics (a 64-bit shared
-// atomicAdd compiles to a CAS loop): add the low word, carry into the high word.
-__device__ __forceinline__ void add64_shared(unsigned long long *p, unsigned long long v) {
-  unsigned *q = reinterpret_cast<unsigned *>(p);
-  const unsigned lo = (unsigned)v;
-  unsigned hi = (unsigned)(v >> 32);
-  const unsigned old = atomicAdd(q, lo);
-  if (old + lo < old) hi += 1u;
-  if (hi) atomicAdd(q + 1, hi);
-}
-
 constexpr int kPeakWarps = 8;
-constexpr int kPeakSmem = 48 * 1024;  // bytes per CTA: four CTAs per SM
+constexpr int kPeakSmem = 28 * 1024;  // bytes per CTA: eight CTAs per SM
 
+// The timeline holds 32-bit deltas in units of 2^shift bytes (the alignment):
+// half the shared memory of 64-bit deltas, so twice the traces in flight per
+// SM, and native 32-bit shared atomics. A trace whose sizes are not multiples
+// of 2^shift, or whose byte total in those units does not fit 31 bits (so a
+// timeline entry could overflow), or with a timestamp outside [0, horizon],
+// is flagged for the global-timeline path below.
 __global__ void __launch_bounds__(kPeakWarps * 32) k_peak_warp(const int64_t *__restrict__ ev_off,
                                                                const int64_t *__restrict__ size,
                                                                const int32_t *__restrict__ t_s,
                                                                const int32_t *__restrict__ t_e,
                                                                const uint8_t *__restrict__ dyn,
                                                                const int32_t *__restrict__ horizon,
-                                                               int static_only, const int2 *__restrict__ wslot,
+                                                               int static_only, int shift,
+                                                               const int2 *__restrict__ wslot,
                                                                long long *__restrict__ peak, int *__restrict__ nbig,
                                                                int32_t *__restrict__ big) {
   constexpr unsigned FULL = 0xffffffffu;
-  extern __shared__ unsigned long long pk_smem[];
+  extern __shared__ int pk_smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 slot = wslot[blockIdx.x * kPeakWarps + w];
   if (slot.x < 0) return;
   const int t = slot.x;
-  unsigned long long *D = pk_smem + slot.y;
+  int *D = pk_smem + slot.y;
   const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
   const int H = horizon[t] + 1;  // timestamps are in [0, horizon] (model.py:240-241)
   for (int x = lane; x < H; x += 32) D[x] = 0;
   __syncwarp();
   bool bad = false;
-  constexpr int B = 8;  // events per lane loaded together (independent loads in flight)
+  long long units = 0;
+  const long long low = (1ll << shift) - 1;
+  constexpr int B = 4;  // events per lane loaded together (independent loads in flight)
   for (int64_t i0 = e0; i0 < e1; i0 += 32 * B) {
     int a[B], z[B];
-    unsigned long long sz[B];
+    long long sz[B];
     bool use[B];
 #pragma unroll
     for (int q = 0; q < B; q++) {
@@ -120,21 +118,24 @@ __global__ void __launch_bounds__(kPeakWarps * 32) k_peak_warp(const int64_t *__
       use[q] = i < e1;
       a[q] = use[q] ? t_s[i] : 0;
       z[q] = use[q] ? t_e[i] : 0;
-      sz[q] = use[q] ? (unsigned long long)size[i] : 0;
+      sz[q] = use[q] ? (long long)size[i] : 0;
       if (static_only && use[q]) use[q] = dyn[i] == 0;
     }
 #pragma unroll
     for (int q = 0; q < B; q++) {
       if (!use[q]) continue;
-      if ((unsigned)a[q] >= (unsigned)H || (unsigned)z[q] >= (unsigned)H) {
+      if ((unsigned)a[q] >= (unsigned)H || (unsigned)z[q] >= (unsigned)H || sz[q] < 0 || (sz[q] & low)) {
         bad = true;
         continue;
       }
-      add64_shared(D + a[q], sz[q]);
-      add64_shared(D + z[q], 0ull - sz[q]);
+      const int u = (int)min(sz[q] >> shift, (long long)INT_MAX);
+      units += sz[q] >> shift;
+      atomicAdd(D + a[q], u);
+      atomicAdd(D + z[q], -u);
     }
   }
-  if (__any_sync(FULL, bad)) {
+  for (int o = 16; o; o >>= 1) units += __shfl_xor_sync(FULL, units, o);
+  if (__any_sync(FULL, bad) || units > INT_MAX) {
     if (lane == 0) big[atomicAdd(nbig, 1)] = t;
     return;
   }
@@ -143,13 +144,13 @@ __global__ void __launch_bounds__(kPeakWarps * 32) k_peak_warp(const int64_t *__
   const int x0 = min(H, lane * per), x1 = min(H, x0 + per);
   long long run = 0, best = LLONG_MIN;
   for (int x = x0; x < x1; x++) {
-    run += (long long)D[x];
+    run += D[x];
     best = max(best, run);
   }
   const long long inc = warp_incl_sum(run);
   long long cand = best == LLONG_MIN ? 0 : inc - run + best;  // the running maximum starts at 0
   for (int o = 16; o; o >>= 1) cand = max(cand, __shfl_xor_sync(FULL, cand, o));
-  if (lane == 0) peak[t] = cand;
+  if (lane == 0) peak[t] = cand << shift;
 }
 
 __global__ void k_big_offsets(const int32_t *__restrict__ big, const int *__restrict__ nbig, int T,
@@ -161,7 +162,7 @@ static void peak_live_global(Ctx &ctx, Arena &ar, const DevBatch &b, bool static
                              const uint8_t *only);
 
 void peak_live(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak) {
-  PeakPending pp = peak_live_launch(ctx, ar, b, static_only, d_peak);
+  PeakPending pp = peak_live_launch(ctx, ar, b, static_only, d_peak, 9);
   peak_live_finish(ctx, ar, b, static_only, d_peak, pp);
 }
 
@@ -181,7 +182,8 @@ void peak_live_finish(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, 
   peak_live_global(ctx, ar, b, static_only, d_peak, is_big);
 }
 
-PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak) {
+PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
+                             int shift) {
   PeakPending pp{};
   if (!ctx.ok() || b.T == 0) return pp;
   const int T = b.T;
@@ -196,7 +198,7 @@ PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static
   order.reserve(T);
   int hmax = 0;
   for (int t = 0; t < T; t++) {
-    const int64_t bytes = 8 * ((int64_t)b.h_horizon[t] + 1);
+    const int64_t bytes = 4 * ((int64_t)b.h_horizon[t] + 1);
     if (b.h_horizon[t] < 0 || bytes > kPeakSmem)
       longh.push_back(t);
     else
@@ -211,7 +213,7 @@ PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static
   }
   std::vector<int2> wslot;
   wslot.reserve(order.size() + kPeakWarps);
-  const int cap = kPeakSmem / 8;
+  const int cap = kPeakSmem / 4;
   for (size_t i = 0, j = order.size(); i < j;) {
     const size_t base = wslot.size();
     int used = 0, k = 0;
@@ -239,7 +241,7 @@ PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static
                                   ctx.stream));
     STW_CUDA(ctx, cudaFuncSetAttribute(k_peak_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kPeakSmem));
     STW_KLS(k_peak_warp, (unsigned)nctas, kPeakWarps * 32, kPeakSmem, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e,
-            b.dyn, b.horizon, static_only ? 1 : 0, d_wslot, (long long *)d_peak, nbig, big);
+            b.dyn, b.horizon, static_only ? 1 : 0, shift, d_wslot, (long long *)d_peak, nbig, big);
   }
   STW_LAUNCHED(ctx);
   return pp;
