@@ -182,8 +182,8 @@ def algo_bytes(kernel: str, w: dict, launches_per_step: float) -> float:
         # planner layers (K5/K6): 32 B/item in + 8 B/item out, per unit
         "k_layers": 40.0 * w["unit_items"],
         "k_layers_w32": 40.0 * w["unit_items"],
-        # K7 fast path: addr 8 B per (rectangle, candidate) + size/t_s/t_e 16 B per rectangle
-        "k_overlap_sweep": 8.0 * w["unit_events"] + 16.0 * w["events"],
+        # K7 fast path: 24 B per rectangle of each candidate plan
+        "k_overlap_sweep": 24.0 * w["unit_events"],
         "k_validate_tiles": 24.0 * w["unit_events"],
         # fusion: the trace's events are read once per attempt at least
         "k_fusion": 32.0 * w["events"],
@@ -274,9 +274,10 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
 
     ms = kernel_ms(k7, "k_overlap_sweep")
     assert int(count[0].abs().sum()) == 0, "planner output failed validation"
-    entry("k_overlap_sweep", n1 * reps * nc, (16.0 + 8.0 * nc) / nc, ms,
+    entry("k_overlap_sweep", n1 * reps * nc, 24.0, ms,
           f"K7 validate_plan of {T * reps * nc} plans ({n1 * reps} rectangles x {nc} candidates); "
-          "per (rectangle, candidate): addr 8 B + the shared size/t_s/t_e 16 B over the candidates",
+          "SURVEY §8(d4): 24 B per rectangle of each plan (addr, size, t_s, t_e); the kernel reads the shared "
+          "size/t_s/t_e once per set, so DRAM traffic is ~12 B per (rectangle, candidate)",
           "k_overlap_sweep@sweep")
     del ts, te, sz, ad, off
 
