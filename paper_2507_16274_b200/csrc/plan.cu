@@ -80,21 +80,32 @@ __device__ T block_reduce_max(T v, T *sh) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // trace index of every event: one warp per trace writes its run (coalesced)
-__global__ void k_fill_i32(int *__restrict__ p, int64_t n, int v) {
-  GRID_STRIDE(i, n) p[i] = v;
-}
-
-// One warp per trace: the trace index of every event (coalesced runs), and
-// *flag = 1 unless every trace's ids increase strictly and its t_s never
-// decrease (then its id order and its (t_s, id) order are both the listing
-// order).
+// Phase A in one pass, one warp per trace: the trace index of every event
+// (coalesced runs); flags[0] = 1 unless every trace's ids increase strictly
+// and its t_s never decrease (then its id order and its (t_s, id) order are
+// both the listing order); id range (mm[0], mm[1]) and max t_s (flags[1]) for
+// the sort key widths; the input checks -- bad_align[t] / bad_phase[t] = the
+// first static event (trace-local index) whose size is not aligned
+// (planner.py:371-373) / whose scoped phases are missing from the schedule
+// (model.py:201-205), INT_MAX if none -- and flags[2] = the largest phase
+// index of a scoped static event.
 __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
-                             const int32_t *__restrict__ ts, int32_t *__restrict__ tr, int *__restrict__ flag) {
+                             const int32_t *__restrict__ ts, const int32_t *__restrict__ te,
+                             const int64_t *__restrict__ size, const int32_t *__restrict__ ps,
+                             const int32_t *__restrict__ pe, const uint8_t *__restrict__ dyn,
+                             const int32_t *__restrict__ horizon, const int32_t *__restrict__ n_sched,
+                             long long align, int32_t *__restrict__ tr, int *__restrict__ bad_align,
+                             int *__restrict__ bad_phase, int *__restrict__ flags, long long *__restrict__ mm) {
+  constexpr unsigned FULL = 0xffffffffu;
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   bool bad = false;
+  long long idmin = LLONG_MAX, idmax = LLONG_MIN;
+  int tsmax = 0, pmax = 0;
   for (int t = w; t < T; t += nw) {
     const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
+    const int hz = horizon[t], ns = n_sched[t];
+    int ba = INT_MAX, bp = INT_MAX;
     int64_t pid = 0;  // last id / t_s of the previous chunk
     int pts = 0;
     for (int64_t c = e0; c < e1; c += 32) {
@@ -102,16 +113,51 @@ __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const in
       const bool in = i < e1;
       const int64_t my_id = in ? id[i] : 0;
       const int my_ts = in ? ts[i] : 0;
-      if (in) tr[i] = t;
-      int64_t prev_id = __shfl_up_sync(0xffffffffu, my_id, 1);
-      int prev_ts = __shfl_up_sync(0xffffffffu, my_ts, 1);
+      if (in) {
+        tr[i] = t;
+        idmin = min(idmin, (long long)my_id);
+        idmax = max(idmax, (long long)my_id);
+        tsmax = max(tsmax, my_ts);
+        if (!dyn[i]) {
+          const int loc = (int)(i - e0);
+          if (size[i] % align) ba = min(ba, loc);
+          if (te[i] < hz) {
+            const int a = ps[i], z = pe[i];
+            if (a >= ns || z >= ns) bp = min(bp, loc);
+            pmax = max(pmax, max(a, z));
+          }
+        }
+      }
+      int64_t prev_id = __shfl_up_sync(FULL, my_id, 1);
+      int prev_ts = __shfl_up_sync(FULL, my_ts, 1);
       if (lane == 0) prev_id = pid, prev_ts = pts;
       if (in && i > e0) bad |= !(prev_id < my_id && prev_ts <= my_ts);
-      pid = __shfl_sync(0xffffffffu, my_id, 31);
-      pts = __shfl_sync(0xffffffffu, my_ts, 31);
+      pid = __shfl_sync(FULL, my_id, 31);
+      pts = __shfl_sync(FULL, my_ts, 31);
+    }
+    ba = __reduce_min_sync(FULL, ba);
+    bp = __reduce_min_sync(FULL, bp);
+    if (lane == 0) {
+      bad_align[t] = ba;
+      bad_phase[t] = bp;
     }
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+  for (int o = 16; o; o >>= 1) {
+    idmin = min(idmin, __shfl_xor_sync(FULL, idmin, o));
+    idmax = max(idmax, __shfl_xor_sync(FULL, idmax, o));
+  }
+  tsmax = __reduce_max_sync(FULL, tsmax);
+  pmax = __reduce_max_sync(FULL, pmax);
+  const bool anybad = __any_sync(FULL, bad);
+  if (lane == 0) {
+    if (anybad) atomicOr(flags, 1);
+    if (tsmax > 0) atomicMax(flags + 1, tsmax);
+    if (pmax > 0) atomicMax(flags + 2, pmax);
+    if (idmin != LLONG_MAX) {
+      atomicMin(mm, idmin);
+      atomicMax(mm + 1, idmax);
+    }
+  }
 }
 
 __global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx) {
@@ -348,28 +394,6 @@ __global__ void k_key_r(const int32_t *__restrict__ tr, const int32_t *__restric
     hi[i] = (uint64_t)tr[i];
     lo[i] = ((uint64_t)(uint32_t)ts[i] << qb) | (uint32_t)q[i];
   }
-}
-
-// alignment (planner.py:371-373) and schedule membership (model.py:201-205)
-__global__ void k_checks(const int32_t *__restrict__ tr, const int64_t *__restrict__ ev_off,
-                         const int64_t *__restrict__ size, const int32_t *__restrict__ te,
-                         const int32_t *__restrict__ ps, const int32_t *__restrict__ pe,
-                         const uint8_t *__restrict__ dyn, const int32_t *__restrict__ horizon,
-                         const int32_t *__restrict__ n_sched, int64_t n, long long align, int *__restrict__ bad_align,
-                         int *__restrict__ bad_phase, int *__restrict__ pmax) {
-  int pm = 0;  // warp-aggregated max phase index (one global atomic per warp)
-  GRID_STRIDE(i, n) {
-    if (dyn[i]) continue;
-    int t = tr[i];
-    int loc = (int)(i - ev_off[t]);
-    if (size[i] % align) atomicMin(bad_align + t, loc);
-    if (te[i] < horizon[t]) {
-      if (ps[i] >= n_sched[t] || pe[i] >= n_sched[t]) atomicMin(bad_phase + t, loc);
-      pm = max(pm, max(ps[i], pe[i]));
-    }
-  }
-  pm = __reduce_max_sync(0xffffffffu, pm);
-  if ((threadIdx.x & 31) == 0 && pm > 0) atomicMax(pmax, pm);
 }
 
 __global__ void k_key_group(const int32_t *__restrict__ tr, const int32_t *__restrict__ te,
@@ -1981,19 +2005,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   long long mm_init[2] = {LLONG_MAX, LLONG_MIN};
   STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
-  if (T > 0) {  // tr and presortedness (im[2])
-    STW_KL(k_trace_scan, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, tr, im + 2);
-    STW_LAUNCHED(ctx);
-  }
-  // per-trace input checks (alignment, schedule membership; im[1] = max phase index)
+  // one warp-per-trace pass: tr, presortedness, key widths and the input checks
   int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_fill_i32, T, bad_align, T, INT_MAX);
-  LAUNCH(k_fill_i32, T, bad_phase, T, INT_MAX);
-  LAUNCH(k_checks, N, tr, b.ev_off, b.size, b.t_e, b.ps, b.pe, b.dyn, b.horizon, b.n_sched, N, (long long)o->alignment,
-         bad_align, bad_phase, im + 1);
-  LAUNCH_RED(k_minmax_i64, N, b.id, N, mm, mm + 1);
-  LAUNCH_RED(k_max_i32, N, b.t_s, N, im);
+  if (T > 0) {
+    STW_KL(k_trace_scan, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, b.t_e, b.size,
+           b.ps, b.pe, b.dyn, b.horizon, b.n_sched, (long long)o->alignment, tr, bad_align, bad_phase, im, mm);
+    STW_LAUNCHED(ctx);
+  }
   long long hmm[2] = {0, 0};
   int him[4] = {0, 0, 0, 0};
   STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
@@ -2003,8 +2022,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   const int tb = bitlen_u64((uint64_t)(T - 1));
   const int idb = N ? bitlen_u64((uint64_t)(hmm[1] - hmm[0])) : 0;
   const int qb = bitlen_u64((uint64_t)(b.max_trace_events > 0 ? b.max_trace_events - 1 : 0));
-  const int tsb = bitlen_u64((uint64_t)him[0]);
-  if (him[2] == 0) {  // recorded order: both ranks are the position in the trace
+  const int tsb = bitlen_u64((uint64_t)him[1]);
+  if (him[0] == 0) {  // recorded order: both ranks are the position in the trace
     LAUNCH(k_identity_ranks, N, tr, b.ev_off, N, q, r, rperm, order_local);
   } else {
     // q: id rank within trace
@@ -2018,14 +2037,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
 
   pt.mark("A ranks");
-  const int pb = bitlen_u64((uint64_t)him[1]);
+  const int pb = bitlen_u64((uint64_t)him[2]);
 
   pt.mark("A checks");
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
   LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
   seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events,
-           /*lo_in_order=*/him[2] == 0);
+           /*lo_in_order=*/him[0] == 0);
   uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
   int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
   int64_t *rel = ar.take<int64_t>(N + 1);
