@@ -643,6 +643,33 @@ __device__ void gather_members(const FusionArgs &A, int64_t base, int64_t nt, in
   }
 }
 
+__global__ void k_fusion_prep(Plans p0, Plans p1, int64_t np, const int32_t *__restrict__ pid0,
+                              int32_t *__restrict__ pid1, const int64_t *__restrict__ rel, int64_t *__restrict__ frel1,
+                              int64_t ne, int32_t *__restrict__ lst, uint32_t *__restrict__ memo, int64_t nmemo) {
+  GRID_STRIDE(i, max(max(np, ne), nmemo)) {
+    if (i < np) {
+      p1.grp[i] = p0.grp[i];
+      p1.tr[i] = p0.tr[i];
+      p1.h[i] = p0.h[i];
+      p1.ts[i] = p0.ts[i];
+      p1.te[i] = p0.te[i];
+      p1.k0[i] = p0.k0[i];
+      p1.k1[i] = p0.k1[i];
+      p1.minq[i] = p0.minq[i];
+      p1.used[2 * i] = p0.used[2 * i];
+      p1.used[2 * i + 1] = p0.used[2 * i + 1];
+      p1.tmp[i] = p0.tmp[i];
+      p1.alive[i] = p0.alive[i];
+      lst[i] = (int32_t)i;
+    }
+    if (i < ne) {
+      pid1[i] = pid0[i];
+      frel1[i] = rel[i];
+    }
+    if (i < nmemo) memo[i] = 0;
+  }
+}
+
 constexpr int kFuseCap = 384;  // rectangles of one try staged in shared memory
 
 __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T) {
@@ -2127,23 +2154,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
                  ar.take<int32_t>(N + 1), ar.take<int64_t>(N + 1), ar.take<uint8_t>(N + 1), memo, d_moff, att, acc,
                  acc_tmp, acc_avg};
     if (!ctx.ok()) return ctx.rc;
-#define CPY(dst, src, cnt) STW_CUDA(ctx, cudaMemcpyAsync(dst, src, (cnt) * sizeof(*(src)), cudaMemcpyDeviceToDevice, ctx.stream))
-    CPY(p1.grp, p0.grp, P + 1);
-    CPY(p1.tr, p0.tr, P + 1);
-    CPY(p1.h, p0.h, P + 1);
-    CPY(p1.ts, p0.ts, P + 1);
-    CPY(p1.te, p0.te, P + 1);
-    CPY(p1.k0, p0.k0, P + 1);
-    CPY(p1.k1, p0.k1, P + 1);
-    CPY(p1.minq, p0.minq, P + 1);
-    CPY(p1.used, p0.used, 2 * P + 2);
-    CPY(p1.tmp, p0.tmp, P + 1);
-    CPY(p1.alive, p0.alive, P + 1);
-    CPY(pid1, pid0, N + 1);
-    CPY(frel1, rel, N + 1);
-#undef CPY
-    STW_CUDA(ctx, cudaMemsetAsync(memo, 0, (moff[T] / 32 + 1) * sizeof(uint32_t), ctx.stream));
-    STW_KL(k_iota, grid_for(P + 1, 256), 256, ctx.stream, (uint32_t *)lst, P + 1);
+    // variant-1 state starts as a copy of variant 0; the plan list is the identity;
+    // the rejection memo is clear -- one pass
+    const int64_t nmemo = moff[T] / 32 + 1, nprep = std::max<int64_t>(std::max<int64_t>(P + 1, N + 1), nmemo);
+    STW_KL(k_fusion_prep, grid_for(nprep, 256), 256, ctx.stream, p0, p1, P + 1, pid0, pid1, rel, frel1, N + 1, lst,
+           memo, nmemo);
     STW_LAUNCHED(ctx);
     if (ctx.ok()) {
       STW_KL(k_fusion, T, kPlanThreads, ctx.stream, F, T);
