@@ -1066,35 +1066,28 @@ __global__ void k_widen_u8(const uint8_t *__restrict__ a, uint32_t *__restrict__
 }
 
 // class end (exclusive) for every item: classes are runs of equal size inside a (variant, trace) segment
-__global__ void k_class_heads(Items it, const int64_t *__restrict__ io, int VT, int64_t n, uint32_t *__restrict__ head) {
-  GRID_STRIDE(j, n) {
-    uint32_t h = 1;
-    if (j > 0 && it.size[j] == it.size[j - 1]) {
-      int a = 0, b = VT;  // same segment?
-      while (b - a > 1) {
-        int m = (a + b) >> 1;
-        if (io[m] <= j)
-          a = m;
-        else
-          b = m;
+// cend[j] = end of item j's size class inside its (variant, trace) segment; one
+// warp per segment walks it from the back (suffix minimum of class boundaries)
+__global__ void k_class_ends(Items it, const int64_t *__restrict__ io, int VT, int64_t *__restrict__ cend) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  for (int sgi = w; sgi < VT; sgi += nw) {
+    const int64_t a = io[sgi], b = io[sgi + 1];
+    int64_t carry = b;  // first boundary at or after the chunk's end
+    for (int64_t c = b - 32; c > a - 32; c -= 32) {
+      const int64_t j = c + lane;
+      const bool in = j >= a && j < b;
+      // a class ends after j when j is the segment's last item or the next size differs
+      const bool edge = in && (j + 1 == b || it.size[j + 1] != it.size[j]);
+      int64_t v = edge ? j + 1 : LLONG_MAX;
+      for (int o = 1; o < 32; o <<= 1) {  // suffix minimum over lanes
+        const int64_t u = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = min(v, u);
       }
-      h = io[a] == j;
+      v = min(v, carry);
+      if (in) cend[j] = v;
+      carry = __shfl_sync(0xffffffffu, v, 0);
     }
-    head[j] = h;
-  }
-}
-
-__global__ void k_class_start(const uint32_t *__restrict__ head, const uint32_t *__restrict__ cid_incl, int64_t n,
-                              int64_t *__restrict__ cstart) {
-  GRID_STRIDE(j, n) if (head[j]) cstart[cid_incl[j] - 1] = j;
-}
-
-__global__ void k_class_end(const uint32_t *__restrict__ cid_incl, const int64_t *__restrict__ cstart, int64_t n,
-                            int64_t *__restrict__ cend) {
-  const int64_t nc = cid_incl[n - 1];  // number of classes
-  GRID_STRIDE(j, n) {
-    int64_t c = cid_incl[j];  // id + 1
-    cend[j] = c < nc ? cstart[c] : n;
   }
 }
 
@@ -2089,14 +2082,16 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   LAUNCH(k_group_table, N, e, gperm, head, gid, N, g);
   LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, N, rel, gof);
-  TraceCounts tc{ar.take<int>(T), ar.take<int>(T), ar.take<int>(T), ar.take<int>(T), ar.take<int>(T),
-                 ar.take<int64_t>(T)};
-  uint32_t *is_plan = ar.take<uint32_t>(G + 1), *pidx = ar.take<uint32_t>(G + 1);
+  // per-trace counters and the plan flags in one zeroed block
+  const size_t tc_bytes = (size_t)T * (5 * sizeof(int) + sizeof(int64_t)) + (size_t)(G + 1) * sizeof(uint32_t);
+  char *tcb = ar.take<char>(tc_bytes + 64);
+  uint32_t *pidx = ar.take<uint32_t>(G + 1);
   if (!ctx.ok()) return ctx.rc;
-  for (int *pcnt : {tc.n_static, tc.n_pers, tc.n_groups, tc.n_plans, tc.n_res})
-    STW_CUDA(ctx, cudaMemsetAsync(pcnt, 0, T * sizeof(int), ctx.stream));
-  STW_CUDA(ctx, cudaMemsetAsync(tc.pers_size, 0, T * sizeof(int64_t), ctx.stream));
-  STW_CUDA(ctx, cudaMemsetAsync(is_plan, 0, (G + 1) * sizeof(uint32_t), ctx.stream));
+  int64_t *tc_pers = (int64_t *)tcb;  // 8-byte aligned first
+  int *tc_ints = (int *)(tc_pers + T);
+  TraceCounts tc{tc_ints, tc_ints + T, tc_ints + 2 * T, tc_ints + 3 * T, tc_ints + 4 * T, tc_pers};
+  uint32_t *is_plan = (uint32_t *)(tc_ints + 5 * T);
+  STW_CUDA(ctx, cudaMemsetAsync(tcb, 0, tc_bytes, ctx.stream));
   LAUNCH(k_trace_counts, G, g, d_G, N, tc, is_plan);
   device_scan<uint32_t>(ctx, ar, is_plan, pidx, G, false);
   std::vector<int> h_nplans, h_nstatic, h_nres;
@@ -2297,13 +2292,12 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
   pt.mark("D sort");
   // classes
-  uint32_t *chead = ar.take<uint32_t>(NI + 1), *cid = ar.take<uint32_t>(NI + 1);
-  int64_t *cstart = ar.take<int64_t>(NI + 1), *cend = ar.take<int64_t>(NI + 1);
+  int64_t *cend = ar.take<int64_t>(NI + 1);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_class_heads, NI, it, d_io, V * T, NI, chead);
-  device_scan<uint32_t>(ctx, ar, chead, cid, NI, true);
-  LAUNCH(k_class_start, NI, chead, cid, NI, cstart);
-  LAUNCH(k_class_end, NI, cid, cstart, NI, cend);
+  if (V * T > 0) {
+    STW_KL(k_class_ends, grid_for((int64_t)V * T * 32, 256), 256, ctx.stream, it, d_io, V * T, cend);
+    STW_LAUNCHED(ctx);
+  }
 
   pt.mark("D classes");
   // ---- E: layers per unit (host-side unit layout and CTA packing were prepared during D)
