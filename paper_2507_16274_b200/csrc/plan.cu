@@ -978,44 +978,49 @@ struct Items {
   int32_t *ts, *te, *tie, *ref;  // ref >= 0 plan id, < 0 ~event
 };
 
-__global__ void k_items_plans(Plans p, int64_t P, const uint32_t *__restrict__ alive_excl,
-                              const int64_t *__restrict__ pl_off, const int64_t *__restrict__ io_vt, Items it) {
-  GRID_STRIDE(k, P) {
-    if (!p.alive[k]) continue;
-    int t = p.tr[k];
-    int64_t pos = io_vt[t] + (alive_excl[k] - alive_excl[pl_off[t]]);
-    it.size[pos] = p.h[k];
-    it.ts[pos] = p.ts[k];
-    it.te[pos] = p.te[k];
-    it.tie[pos] = p.minq[k];
-    it.ref[pos] = (int32_t)k;
-  }
-}
-
-__global__ void k_res_flags(Ev e, const int32_t *__restrict__ gof, Groups g, const int32_t *__restrict__ pid0,
-                            int64_t n, uint32_t *__restrict__ flag) {
-  GRID_STRIDE(i, n) {
-    uint32_t f = 0;
-    if (!e.dyn[i] && pid0[i] < 0) {
-      int c = g.cls[gof[i]];
-      f = c == 1;
+// Items of every (variant, trace) segment, one warp per segment: the
+// variant's surviving plans in plan order (planner.py:408-411), then the
+// trace's residual events -- scoped statics of single-phase groups -- in event
+// order (planner.py:397-401, 412-417); compaction by ballots.
+__global__ void k_items(Plans p0, Plans p1, int want0, int want1, const int64_t *__restrict__ pl_off, Ev e,
+                        const int64_t *__restrict__ ev_off, const int32_t *__restrict__ gof, Groups g,
+                        const int32_t *__restrict__ pid0, const int64_t *__restrict__ io, int T, Items it) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const unsigned lt = lanemask_lt();
+  for (int sgi = w; sgi < 2 * T; sgi += nw) {
+    const int v = sgi >= T, t = sgi - v * T;
+    if (!(v ? want1 : want0)) continue;
+    const Plans &pv = v ? p1 : p0;
+    int64_t pos = io[sgi];
+    for (int64_t k0 = pl_off[t]; k0 < pl_off[t + 1]; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const bool alive = k < pl_off[t + 1] && pv.alive[k];
+      const unsigned m = __ballot_sync(0xffffffffu, alive);
+      if (alive) {
+        const int64_t o = pos + __popc(m & lt);
+        it.size[o] = pv.h[k];
+        it.ts[o] = pv.ts[k];
+        it.te[o] = pv.te[k];
+        it.tie[o] = pv.minq[k];
+        it.ref[o] = (int32_t)k;
+      }
+      pos += __popc(m);
     }
-    flag[i] = f;
-  }
-}
-
-__global__ void k_items_res(Ev e, const uint32_t *__restrict__ flag, const uint32_t *__restrict__ res_excl,
-                            const int64_t *__restrict__ ev_off, const int *__restrict__ n_alive,
-                            const int64_t *__restrict__ io_vt, int64_t n, Items it) {
-  GRID_STRIDE(i, n) {
-    if (!flag[i]) continue;
-    int t = e.tr[i];
-    int64_t pos = io_vt[t] + n_alive[t] + (res_excl[i] - res_excl[ev_off[t]]);
-    it.size[pos] = e.size[i];
-    it.ts[pos] = e.ts[i];
-    it.te[pos] = e.te[i];
-    it.tie[pos] = e.q[i];
-    it.ref[pos] = ~(int32_t)i;
+    for (int64_t i0 = ev_off[t]; i0 < ev_off[t + 1]; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool res = i < ev_off[t + 1] && !e.dyn[i] && pid0[i] < 0 && g.cls[gof[i]] == 1;
+      const unsigned m = __ballot_sync(0xffffffffu, res);
+      if (res) {
+        const int64_t o = pos + __popc(m & lt);
+        it.size[o] = e.size[i];
+        it.ts[o] = e.ts[i];
+        it.te[o] = e.te[i];
+        it.tie[o] = e.q[i];
+        it.ref[o] = ~(int32_t)i;
+      }
+      pos += __popc(m);
+    }
   }
 }
 
@@ -1059,10 +1064,6 @@ __global__ void k_item_permute(Items src, Items dst, const uint32_t *__restrict_
     else
       item_of_res[(int64_t)v * N + ~r] = (int32_t)j;
   }
-}
-
-__global__ void k_widen_u8(const uint8_t *__restrict__ a, uint32_t *__restrict__ o, int64_t n) {
-  GRID_STRIDE(x, n) o[x] = a[x];
 }
 
 // class end (exclusive) for every item: classes are runs of equal size inside a (variant, trace) segment
@@ -2177,36 +2178,26 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   pt.mark("C fusion");
   // ---- D: items per (variant, trace)
   std::vector<int64_t> io(V * T + 1, 0);
-  std::vector<int> n_alive(V * T, 0);
   sync(ctx);
   if (!ctx.ok()) return ctx.rc;
   for (int v = 0; v < V; v++)
     for (int t = 0; t < T; t++) {
       int64_t na = want[v] ? (v ? h_nplans[t] - h_acc[t] : h_nplans[t]) : 0;
       int64_t cnt = want[v] ? na + h_nres[t] : 0;
-      n_alive[v * T + t] = (int)na;
       io[v * T + t + 1] = io[v * T + t] + cnt;
     }
   const int64_t NI = io[V * T];
   int64_t *d_io = h2d(ctx, ar, io);
-  int *d_nalive = h2d(ctx, ar, n_alive);
-  uint32_t *rflag = ar.take<uint32_t>(N + 1), *rexcl = ar.take<uint32_t>(N + 1);
-  uint32_t *aexcl = ar.take<uint32_t>(P + 1), *aflag = ar.take<uint32_t>(P + 1);
   Items it0{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
             ar.take<int32_t>(NI + 1)};
   Items it{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
            ar.take<int32_t>(NI + 1)};
   int32_t *item_of_plan = ar.take<int32_t>(V * (P + 1)), *item_of_res = ar.take<int32_t>(V * (N + 1));
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_res_flags, N, e, gof, g, pid0, N, rflag);
-  device_scan<uint32_t>(ctx, ar, rflag, rexcl, N, false);
-  for (int v = 0; v < V; v++) {
-    if (!want[v]) continue;
-    Plans &pv = v ? p1 : p0;
-    LAUNCH(k_widen_u8, P, pv.alive, aflag, P);
-    device_scan<uint32_t>(ctx, ar, aflag, aexcl, P, false);
-    LAUNCH(k_items_plans, P, pv, P, aexcl, d_pl_off, d_io + (int64_t)v * T, it0);
-    LAUNCH(k_items_res, N, e, rflag, rexcl, b.ev_off, d_nalive + (int64_t)v * T, d_io + (int64_t)v * T, N, it0);
+  if (T > 0) {
+    STW_KL(k_items, grid_for((int64_t)V * T * 32, 256), 256, ctx.stream, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0,
+           d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, it0);
+    STW_LAUNCHED(ctx);
   }
   pt.mark("D items");
   // sort items by (variant-trace, size desc, t_s, tie)
