@@ -80,7 +80,7 @@ __device__ T block_reduce_max(T v, T *sh) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // trace index of every event: one warp per trace writes its run (coalesced)
-// Phase A in one pass, one warp per trace: the trace index of every event
+// Phase A in one pass, one CTA per trace: the trace index of every event
 // (coalesced runs); flags[0] = 1 unless every trace's ids increase strictly
 // and its t_s never decrease (then its id order and its (t_s, id) order are
 // both the listing order); id range (mm[0], mm[1]) and max t_s (flags[1]) for
@@ -89,59 +89,42 @@ __device__ T block_reduce_max(T v, T *sh) {
 // (planner.py:371-373) / whose scoped phases are missing from the schedule
 // (model.py:201-205), INT_MAX if none -- and flags[2] = the largest phase
 // index of a scoped static event.
-__global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id,
-                             const int32_t *__restrict__ ts, const int32_t *__restrict__ te,
-                             const int64_t *__restrict__ size, const int32_t *__restrict__ ps,
-                             const int32_t *__restrict__ pe, const uint8_t *__restrict__ dyn,
-                             const int32_t *__restrict__ horizon, const int32_t *__restrict__ n_sched,
-                             long long align, int32_t *__restrict__ tr, int *__restrict__ bad_align,
-                             int *__restrict__ bad_phase, int *__restrict__ flags, long long *__restrict__ mm) {
+__global__ void __launch_bounds__(128) k_trace_scan(
+    const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id, const int32_t *__restrict__ ts,
+    const int32_t *__restrict__ te, const int64_t *__restrict__ size, const int32_t *__restrict__ ps,
+    const int32_t *__restrict__ pe, const uint8_t *__restrict__ dyn, const int32_t *__restrict__ horizon,
+    const int32_t *__restrict__ n_sched, long long align, int32_t *__restrict__ tr, int *__restrict__ bad_align,
+    int *__restrict__ bad_phase, int *__restrict__ flags, long long *__restrict__ mm) {
   constexpr unsigned FULL = 0xffffffffu;
-  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  __shared__ int s_ba, s_bp;
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_ba = s_bp = INT_MAX;
+  __syncthreads();
+  const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
+  const int hz = horizon[t], ns = n_sched[t];
   bool bad = false;
   long long idmin = LLONG_MAX, idmax = LLONG_MIN;
-  int tsmax = 0, pmax = 0;
-  for (int t = w; t < T; t += nw) {
-    const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
-    const int hz = horizon[t], ns = n_sched[t];
-    int ba = INT_MAX, bp = INT_MAX;
-    int64_t pid = 0;  // last id / t_s of the previous chunk
-    int pts = 0;
-    for (int64_t c = e0; c < e1; c += 32) {
-      const int64_t i = c + lane;
-      const bool in = i < e1;
-      const int64_t my_id = in ? id[i] : 0;
-      const int my_ts = in ? ts[i] : 0;
-      if (in) {
-        tr[i] = t;
-        idmin = min(idmin, (long long)my_id);
-        idmax = max(idmax, (long long)my_id);
-        tsmax = max(tsmax, my_ts);
-        if (!dyn[i]) {
-          const int loc = (int)(i - e0);
-          if (size[i] % align) ba = min(ba, loc);
-          if (te[i] < hz) {
-            const int a = ps[i], z = pe[i];
-            if (a >= ns || z >= ns) bp = min(bp, loc);
-            pmax = max(pmax, max(a, z));
-          }
-        }
+  int tsmax = 0, pmax = 0, ba = INT_MAX, bp = INT_MAX;
+  for (int64_t i = e0 + tid; i < e1; i += blockDim.x) {
+    const int64_t my_id = id[i];
+    const int my_ts = ts[i];
+    tr[i] = t;
+    idmin = min(idmin, (long long)my_id);
+    idmax = max(idmax, (long long)my_id);
+    tsmax = max(tsmax, my_ts);
+    if (i > e0) bad |= !(id[i - 1] < my_id && ts[i - 1] <= my_ts);
+    if (!dyn[i]) {
+      const int loc = (int)(i - e0);
+      if (size[i] % align) ba = min(ba, loc);
+      if (te[i] < hz) {
+        const int a = ps[i], z = pe[i];
+        if (a >= ns || z >= ns) bp = min(bp, loc);
+        pmax = max(pmax, max(a, z));
       }
-      int64_t prev_id = __shfl_up_sync(FULL, my_id, 1);
-      int prev_ts = __shfl_up_sync(FULL, my_ts, 1);
-      if (lane == 0) prev_id = pid, prev_ts = pts;
-      if (in && i > e0) bad |= !(prev_id < my_id && prev_ts <= my_ts);
-      pid = __shfl_sync(FULL, my_id, 31);
-      pts = __shfl_sync(FULL, my_ts, 31);
-    }
-    ba = __reduce_min_sync(FULL, ba);
-    bp = __reduce_min_sync(FULL, bp);
-    if (lane == 0) {
-      bad_align[t] = ba;
-      bad_phase[t] = bp;
     }
   }
+  ba = __reduce_min_sync(FULL, ba);
+  bp = __reduce_min_sync(FULL, bp);
   for (int o = 16; o; o >>= 1) {
     idmin = min(idmin, __shfl_xor_sync(FULL, idmin, o));
     idmax = max(idmax, __shfl_xor_sync(FULL, idmax, o));
@@ -150,6 +133,8 @@ __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const in
   pmax = __reduce_max_sync(FULL, pmax);
   const bool anybad = __any_sync(FULL, bad);
   if (lane == 0) {
+    if (ba != INT_MAX) atomicMin(&s_ba, ba);
+    if (bp != INT_MAX) atomicMin(&s_bp, bp);
     if (anybad) atomicOr(flags, 1);
     if (tsmax > 0) atomicMax(flags + 1, tsmax);
     if (pmax > 0) atomicMax(flags + 2, pmax);
@@ -157,6 +142,11 @@ __global__ void k_trace_scan(const int64_t *__restrict__ ev_off, int T, const in
       atomicMin(mm, idmin);
       atomicMax(mm + 1, idmax);
     }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    bad_align[t] = s_ba;
+    bad_phase[t] = s_bp;
   }
 }
 
@@ -978,49 +968,50 @@ struct Items {
   int32_t *ts, *te, *tie, *ref;  // ref >= 0 plan id, < 0 ~event
 };
 
-// Items of every (variant, trace) segment, one warp per segment: the
+// Items of every (variant, trace) segment, one CTA per segment: the
 // variant's surviving plans in plan order (planner.py:408-411), then the
 // trace's residual events -- scoped statics of single-phase groups -- in event
-// order (planner.py:397-401, 412-417); compaction by ballots.
-__global__ void k_items(Plans p0, Plans p1, int want0, int want1, const int64_t *__restrict__ pl_off, Ev e,
-                        const int64_t *__restrict__ ev_off, const int32_t *__restrict__ gof, Groups g,
-                        const int32_t *__restrict__ pid0, const int64_t *__restrict__ io, int T, Items it) {
-  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const unsigned lt = lanemask_lt();
-  for (int sgi = w; sgi < 2 * T; sgi += nw) {
-    const int v = sgi >= T, t = sgi - v * T;
-    if (!(v ? want1 : want0)) continue;
-    const Plans &pv = v ? p1 : p0;
-    int64_t pos = io[sgi];
-    for (int64_t k0 = pl_off[t]; k0 < pl_off[t + 1]; k0 += 32) {
-      const int64_t k = k0 + lane;
-      const bool alive = k < pl_off[t + 1] && pv.alive[k];
-      const unsigned m = __ballot_sync(0xffffffffu, alive);
-      if (alive) {
-        const int64_t o = pos + __popc(m & lt);
-        it.size[o] = pv.h[k];
-        it.ts[o] = pv.ts[k];
-        it.te[o] = pv.te[k];
-        it.tie[o] = pv.minq[k];
-        it.ref[o] = (int32_t)k;
-      }
-      pos += __popc(m);
+// order (planner.py:397-401, 412-417); compaction by block scans.
+__global__ void __launch_bounds__(128) k_items(Plans p0, Plans p1, int want0, int want1,
+                                               const int64_t *__restrict__ pl_off, Ev e,
+                                               const int64_t *__restrict__ ev_off, const int32_t *__restrict__ gof,
+                                               Groups g, const int32_t *__restrict__ pid0,
+                                               const int64_t *__restrict__ io, int T, Items it) {
+  __shared__ uint32_t sh[33];
+  const int sgi = blockIdx.x, tid = threadIdx.x;
+  const int v = sgi >= T, t = sgi - v * T;
+  if (!(v ? want1 : want0)) return;
+  const Plans &pv = v ? p1 : p0;
+  int64_t pos = io[sgi];
+  for (int64_t k0 = pl_off[t]; k0 < pl_off[t + 1]; k0 += blockDim.x) {
+    const int64_t k = k0 + tid;
+    const bool alive = k < pl_off[t + 1] && pv.alive[k];
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<uint32_t>(alive ? 1u : 0u, sh, &tot);
+    if (alive) {
+      const int64_t o = pos + ex;
+      it.size[o] = pv.h[k];
+      it.ts[o] = pv.ts[k];
+      it.te[o] = pv.te[k];
+      it.tie[o] = pv.minq[k];
+      it.ref[o] = (int32_t)k;
     }
-    for (int64_t i0 = ev_off[t]; i0 < ev_off[t + 1]; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const bool res = i < ev_off[t + 1] && !e.dyn[i] && pid0[i] < 0 && g.cls[gof[i]] == 1;
-      const unsigned m = __ballot_sync(0xffffffffu, res);
-      if (res) {
-        const int64_t o = pos + __popc(m & lt);
-        it.size[o] = e.size[i];
-        it.ts[o] = e.ts[i];
-        it.te[o] = e.te[i];
-        it.tie[o] = e.q[i];
-        it.ref[o] = ~(int32_t)i;
-      }
-      pos += __popc(m);
+    pos += tot;
+  }
+  for (int64_t i0 = ev_off[t]; i0 < ev_off[t + 1]; i0 += blockDim.x) {
+    const int64_t i = i0 + tid;
+    const bool res = i < ev_off[t + 1] && !e.dyn[i] && pid0[i] < 0 && g.cls[gof[i]] == 1;
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<uint32_t>(res ? 1u : 0u, sh, &tot);
+    if (res) {
+      const int64_t o = pos + ex;
+      it.size[o] = e.size[i];
+      it.ts[o] = e.ts[i];
+      it.te[o] = e.te[i];
+      it.tie[o] = e.q[i];
+      it.ref[o] = ~(int32_t)i;
     }
+    pos += tot;
   }
 }
 
@@ -2030,7 +2021,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
   if (!ctx.ok()) return ctx.rc;
   if (T > 0) {
-    STW_KL(k_trace_scan, grid_for((int64_t)T * 32, 256), 256, ctx.stream, b.ev_off, T, b.id, b.t_s, b.t_e, b.size,
+    STW_KL(k_trace_scan, (unsigned)T, 128, ctx.stream, b.ev_off, T, b.id, b.t_s, b.t_e, b.size,
            b.ps, b.pe, b.dyn, b.horizon, b.n_sched, (long long)o->alignment, tr, bad_align, bad_phase, im, mm);
     STW_LAUNCHED(ctx);
   }
@@ -2195,7 +2186,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   int32_t *item_of_plan = ar.take<int32_t>(V * (P + 1)), *item_of_res = ar.take<int32_t>(V * (N + 1));
   if (!ctx.ok()) return ctx.rc;
   if (T > 0) {
-    STW_KL(k_items, grid_for((int64_t)V * T * 32, 256), 256, ctx.stream, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0,
+    STW_KL(k_items, (unsigned)(V * T), 128, ctx.stream, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0,
            d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, it0);
     STW_LAUNCHED(ctx);
   }
