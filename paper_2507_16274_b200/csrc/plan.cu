@@ -1095,6 +1095,7 @@ struct LayerArgs {
   Items it;
   const int64_t *cend;
   const int64_t *pers_size;
+  const int32_t *horizon;                  // [T]
   int32_t *sA_ts, *sA_te, *sB_ts, *sB_te;  // [total]
   int32_t *loffA, *loffB;                  // [total + U]
   int32_t *prioA, *prioB, *lastEnd, *nend, *newcnt, *runoff, *run_ts, *run_te;
@@ -1473,13 +1474,23 @@ constexpr int kWN = 32;
 constexpr int kWarpsPerCta = 8;
 constexpr int kLayerSmemInts = 14336;  // 56 KB per CTA: four CTAs per SM
 
-__host__ __device__ constexpr int warpn_smem_ints(int n) { return 4 * n + 4 * (kWN + 1) + kWN; }
+// gap units: per layer an occupancy bitmap over the trace's timeline and its
+// per-word prefix popcounts (see below), kWN layers, plus the priority list
+__host__ __device__ constexpr int gap_words(int horizon) { return (horizon >> 5) + 2; }
+__host__ __device__ constexpr int warpn_smem_ints(int horizon) { return 2 * kWN * gap_words(horizon) + kWN + 1; }
 
 // GAP = the unit's candidate inserts into gaps of earlier classes' layers.
 // Without gap insertion a class only ever fills its own new layers (Alg. 1),
 // so the slot CSR, the fit masks, the insertion ranks and the per-class merge
 // are not needed at all: such a unit uses no shared memory and its per-item
 // step is the Alg. 1 max-reduce + ballot alone.
+// Gap units keep, per layer, a bitmap of the timestamps its slots occupy
+// (closed slot intervals, pairwise disjoint) and the prefix popcount of every
+// bitmap word. fits_gap of [t_s, t_e] against the slots of earlier classes
+// (planner.py:196-205) is then "no set bit in [t_s, t_e]": two rank lookups.
+// A class's slots are added after the class (its own items only meet each
+// other through the `last < t_s` rule), then the touched layers' prefix
+// counts are rebuilt.
 template <bool GAP>
 __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__restrict__ smem, const int2 slot,
                                                 int32_t *__restrict__ over, int *__restrict__ nover) {
@@ -1491,25 +1502,28 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
   const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
   const int n = (int)(a1 - a0);
   const int64_t off = A.uo[u];
-  int32_t *sm = smem;
-  int32_t *sts = sm, *ste = sm + n, *run_ts = sm + 2 * n, *run_te = sm + 3 * n;  // slots + class runs
-  int32_t *tts = A.sB_ts + off, *tte = A.sB_te + off;                              // merge output (global)
-  int32_t *loffA = sm + 4 * n, *loffB = loffA + (kWN + 1), *prio = loffB + (kWN + 1), *runoff = prio + (kWN + 1);
-  int32_t *newcnt = runoff + (kWN + 1);
+  const int Wn = GAP ? gap_words(A.horizon[t]) : 0;
+  uint32_t *bits = (uint32_t *)smem, *pfx = bits + kWN * Wn;  // [kWN][Wn] each
+  int32_t *prio = (int32_t *)(pfx + kWN * Wn);
   const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
   const int64_t *gcend = A.cend + a0;
-  int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
+  int32_t *ilayer = A.ilayer + off;
   int64_t *lsize = A.lsize + off;
-  if (GAP && lane == 0) loffA[0] = 0;
+  if (GAP) {
+    for (int x = lane; x < 2 * kWN * Wn; x += 32) bits[x] = 0;
+  }
   int nl = 0, gapc = 0;
   __syncwarp();
+  // set bits below x in layer l
+  auto rank = [&](int l, int x) -> int {
+    const int w = x >> 5;
+    return (int)pfx[l * Wn + w] + __popc(bits[l * Wn + w] & ((1u << (x & 31)) - 1u));
+  };
   for (int j0 = 0; j0 < n;) {
     const int j1 = (int)(gcend[j0] - a0);
     const int m = j1 - j0;
     const int64_t S = A.it.size[a0 + j0];
     int last = INT_MIN, ne = INT_MIN, nnew = 0;
-    if (GAP) newcnt[lane] = 0;
-    __syncwarp();
     for (int cb = j0; cb < j1; cb += 32) {
       const int mine = cb + lane;
       const int cnt = min(32, j1 - cb);
@@ -1521,7 +1535,7 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
         if (GAP)
           for (int p = 0; p < nl; p++) {
             const int l = prio[p];
-            if (slot_fit(sts, ste, loffA[l], loffA[l + 1], my_ts, my_te)) fm |= 1u << p;
+            if (rank(l, my_te + 1) == rank(l, my_ts)) fm |= 1u << p;
           }
       }
       int my_code = 0;
@@ -1560,7 +1574,7 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
           if (lane == k) my_code = m1 ? host : kWN + best;
         }
       }
-      // lane-parallel: layer ids, gap count, insertion ranks
+      // lane-parallel: layer ids and the gap count
       const bool act = lane < cnt;
       if (!GAP) {  // no shared memory here: every code is a new layer of the class
         if (act) ilayer[mine] = nl + (my_code - kWN);
@@ -1568,85 +1582,47 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
       }
       const int layer = my_code < kWN ? prio[my_code] : nl + (my_code - kWN);
       gapc += __popc(__ballot_sync(FULL, act && my_code < kWN));
-      if (j1 >= n) {  // last class: no merge follows, so no insertion ranks
-        if (act) ilayer[mine] = layer;
-        continue;
-      }
-      const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
-      const int r = __popc(peers & lanemask_lt());
-      const int base = act ? newcnt[layer] : 0;
-      __syncwarp();
-      if (act) {
-        ilayer[mine] = layer;
-        irank[mine] = base + r;
-        if (r == __popc(peers) - 1) newcnt[layer] = base + __popc(peers);
-      }
-      __syncwarp();
+      if (act) ilayer[mine] = layer;
     }
-    // ---- merge the class into the layer-major slot CSR (not after the last class:
-    // nothing reads the CSR any more)
     const int nl2 = nl + nnew;
     if (lane < nnew) lsize[nl + lane] = S;
-    if (!GAP || j1 >= n) {
+    if (!GAP || j1 >= n) {  // nothing reads the bitmaps after the last class
       nl = nl2;
       j0 = j1;
       continue;
     }
-    const int myc = newcnt[lane];
-    const unsigned tm = __ballot_sync(FULL, lane < nl && myc > 0);
-    const int first = tm ? __ffs(tm) - 1 : nl;  // first old layer that received gap insertions
-    {
-      const int cnt_all = lane < nl2 ? (lane < nl ? loffA[lane + 1] - loffA[lane] : 0) + myc : 0;
-      int tot, tot2;
-      const int ex = warp_excl_scan(cnt_all, &tot), ex2 = warp_excl_scan(lane < nl2 ? myc : 0, &tot2);
-      if (lane < nl2) {
-        loffB[lane] = ex;
-        runoff[lane] = ex2;
-      }
-      if (lane == 0) loffB[nl2] = tot;
-    }
     __syncwarp();
-    const int s0 = loffA[first];
-    const int nold = loffA[nl];
-    if (first < nl) {
-      for (int x = lane; x < m; x += 32) {
-        const int l = ilayer[j0 + x];
-        const int pos = runoff[l] + irank[j0 + x];
-        run_ts[pos] = gts[j0 + x];
-        run_te[pos] = gte[j0 + x];
-      }
-      __syncwarp();
-      for (int sidx = s0 + lane; sidx < nold; sidx += 32) {
-        int lo = first, hi = nl;  // layer of slot sidx
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (loffA[mid] <= sidx)
-            lo = mid;
-          else
-            hi = mid;
-        }
-        int l = lo;
-        while (loffA[l + 1] <= sidx) l++;
-        const int ts = sts[sidx];
-        const int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
-        const int dst = loffB[l] + (sidx - loffA[l]) + k - s0;
-        tts[dst] = ts;
-        tte[dst] = ste[sidx];
-      }
-    }
+    // ---- add the class's slots to its layers' bitmaps, then rebuild the touched
+    // layers' prefix counts
+    unsigned touched = 0;
     for (int x = lane; x < m; x += 32) {
       const int l = ilayer[j0 + x];
-      const int ts = gts[j0 + x];
-      const int k = l < nl ? lower_bound_i32(sts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
-      const int dst = loffB[l] + irank[j0 + x] + k - s0;
-      tts[dst] = ts;
-      tte[dst] = gte[j0 + x];
+      const int ts = gts[j0 + x], te = gte[j0 + x];
+      touched |= 1u << l;
+      uint32_t *row = bits + l * Wn;
+      for (int w = ts >> 5; w <= (te >> 5); w++) {
+        const int lo = max(ts, w << 5) & 31, hi = min(te, (w << 5) + 31) & 31;
+        const uint32_t msk = (hi == 31 ? 0xffffffffu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u);
+        atomicOr(row + w, msk);
+      }
     }
+    for (int o = 16; o; o >>= 1) touched |= __shfl_xor_sync(FULL, touched, o);
     __syncwarp();
-    const int ntail = loffB[nl2] - s0;
-    for (int x = lane; x < ntail; x += 32) {
-      sts[s0 + x] = tts[x];
-      ste[s0 + x] = tte[x];
+    while (touched) {
+      const int l = __ffs(touched) - 1;
+      touched &= touched - 1;
+      uint32_t carry = 0;
+      for (int w0 = 0; w0 < Wn; w0 += 32) {
+        const int w = w0 + lane;
+        const uint32_t c1 = w < Wn ? (uint32_t)__popc(bits[l * Wn + w]) : 0u;
+        uint32_t inc = c1;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (w < Wn) pfx[l * Wn + w] = carry + inc - c1;
+        carry += __shfl_sync(FULL, inc, 31);
+      }
     }
     // priority order for later classes: the class's new layers (creation order), then the old list
     {
@@ -1655,7 +1631,6 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
       __syncwarp();
       if (lane < nl2) prio[lane] = lane < nnew ? nl + lane : sv;
     }
-    for (int x = lane; x <= nl2; x += 32) loffA[x] = loffB[x];
     __syncwarp();
     nl = nl2;
     j0 = j1;
@@ -2224,8 +2199,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   order.reserve(U);
   // shared-memory need per unit: units without gap insertion use none
   auto need = [&](int32_t u) {
-    return (hcand[u % C] & STW_CAND_GAP) ? warpn_smem_ints((int)std::min<int64_t>(uo[u + 1] - uo[u], INT_MAX / 8))
-                                         : 0;
+    return (hcand[u % C] & STW_CAND_GAP) ? warpn_smem_ints(std::max(0, b.h_horizon[u / C])) : 0;
   };
   for (int64_t u = 0; u < U; u++) {
     if (need((int32_t)u) <= kLayerSmemInts && uo[u + 1] - uo[u] < INT_MAX / 8)
@@ -2287,7 +2261,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   int64_t *d_uo = h2d(ctx, ar, uo);
   uint8_t *d_cand = h2d(ctx, ar, hcand);
   int32_t *d_var = h2d(ctx, ar, var_of);
-  LayerArgs LA{C, T, d_cand, d_var, d_io, d_uo, it, cend, tc.pers_size,
+  LayerArgs LA{C, T, d_cand, d_var, d_io, d_uo, it, cend, tc.pers_size, b.horizon,
                ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1),
                ar.take<int32_t>(TU + U + 1), ar.take<int32_t>(TU + U + 1),
                ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1), ar.take<int32_t>(TU + 1),
