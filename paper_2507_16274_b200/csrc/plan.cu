@@ -691,39 +691,96 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T)
   }
   __syncthreads();
 
-  bool changed = true;
-  while (changed) {
-    changed = false;
-    for (int i = 0; i < P - 1 && !changed; i++) {
-      const int a = lst[i];
-      int j = i + 1;
-      while (j < P) {
-        // next adjacent (and not memo-rejected) partner in list order
-        int jj = j + tid;
-        bool adj = false, fresh = false;
-        if (jj < P) {
-          int b = lst[jj];
-          adj = A.p.k1[a] == A.p.k0[b] || A.p.k1[b] == A.p.k0[a];
-          if (adj) {
-            fresh = true;
-            if (use_memo) {
-              int x = min(a, b) - (int)p0, y = max(a, b) - (int)p0;
-              int64_t bit = A.memo_off[t] + (int64_t)x * P0 + y;
-              fresh = !((A.memo[bit >> 5] >> (bit & 31)) & 1u);
+  // Scan order of the reference's `for i: for j>i:` restart loop
+  // (planner.py fusion): (ci, cj) is where the scan resumes -- after a
+  // rejected try at (i, j+1), after an accepted one at (0, 1).
+  __shared__ int sh_si, sh_sj;
+  int ci = 0, cj = 1;
+  while (true) {
+    int i, jstar;
+    if (P <= 32) {
+      // one warp finds the next adjacent, not memo-rejected pair with ballots:
+      // one barrier per try instead of two block reductions per row
+      if (warp == 0) {
+        int fi = -1, fj = -1;
+        uint32_t natt = 0;
+        for (int r = ci; r < P - 1; r++) {
+          const int a = lst[r];
+          const int j0 = r == ci ? cj : r + 1;
+          const int jj = j0 + lane;
+          bool adj = false, fresh = false;
+          if (jj < P) {
+            const int b = lst[jj];
+            adj = A.p.k1[a] == A.p.k0[b] || A.p.k1[b] == A.p.k0[a];
+            if (adj) {
+              fresh = true;
+              if (use_memo) {
+                int x = min(a, b) - (int)p0, y = max(a, b) - (int)p0;
+                int64_t bit = A.memo_off[t] + (int64_t)x * P0 + y;
+                fresh = !((A.memo[bit >> 5] >> (bit & 31)) & 1u);
+              }
             }
           }
+          const uint32_t ma = __ballot_sync(0xffffffffu, adj);
+          const uint32_t mf = __ballot_sync(0xffffffffu, adj && fresh);
+          if (mf) {
+            const int k = __ffs(mf) - 1;
+            natt += __popc(ma & (0xffffffffu >> (31 - k)));  // attempts up to and incl. the pick
+            fi = r;
+            fj = j0 + k;
+            break;
+          }
+          natt += __popc(ma);
         }
-        int cand = (adj && fresh) ? jj : INT_MAX;
-        int jstar = block_reduce_min(cand, (int *)shu);
-        // attempts counted for every adjacent pair up to and including jstar
-        uint32_t cnt_adj = (adj && jj <= jstar) ? 1u : 0u;
-        uint32_t tot;
-        block_excl_sum<uint32_t>(cnt_adj, shu, &tot);
-        if (tid == 0) sh_att += tot;
-        if (jstar == INT_MAX) {
-          j += blockDim.x;
-          continue;
+        if (lane == 0) {
+          sh_si = fi;
+          sh_sj = fj;
+          sh_att += natt;
         }
+      }
+      __syncthreads();
+      i = sh_si;
+      jstar = sh_sj;
+    } else {
+      i = -1;
+      jstar = -1;
+      for (int r = ci; r < P - 1 && i < 0; r++) {
+        const int a = lst[r];
+        for (int j = r == ci ? cj : r + 1; j < P; j += blockDim.x) {
+          // next adjacent (and not memo-rejected) partner in list order
+          int jj = j + tid;
+          bool adj = false, fresh = false;
+          if (jj < P) {
+            int b = lst[jj];
+            adj = A.p.k1[a] == A.p.k0[b] || A.p.k1[b] == A.p.k0[a];
+            if (adj) {
+              fresh = true;
+              if (use_memo) {
+                int x = min(a, b) - (int)p0, y = max(a, b) - (int)p0;
+                int64_t bit = A.memo_off[t] + (int64_t)x * P0 + y;
+                fresh = !((A.memo[bit >> 5] >> (bit & 31)) & 1u);
+              }
+            }
+          }
+          int cand = (adj && fresh) ? jj : INT_MAX;
+          int js = block_reduce_min(cand, (int *)shu);
+          // attempts counted for every adjacent pair up to and including js
+          uint32_t cnt_adj = (adj && jj <= js) ? 1u : 0u;
+          uint32_t tot;
+          block_excl_sum<uint32_t>(cnt_adj, shu, &tot);
+          if (tid == 0) sh_att += tot;
+          if (js != INT_MAX) {
+            i = r;
+            jstar = js;
+            break;
+          }
+        }
+      }
+    }
+    if (i < 0) break;
+    {
+      {
+        const int a = lst[i];
         // ---- try_fuse(larger, smaller) --------------------------------------
         const int b = lst[jstar];
         const int L = A.p.h[a] >= A.p.h[b] ? a : b;
@@ -897,7 +954,8 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T)
             A.memo[bit >> 5] |= 1u << (bit & 31);
           }
           __syncthreads();
-          j = jstar + 1;
+          ci = i;
+          cj = jstar + 1;
           continue;
         }
         // commit: plans[i] = fused; del plans[j]
@@ -949,8 +1007,8 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_fusion(FusionArgs A, int T)
           __syncthreads();
         }
         P -= 1;
-        changed = true;
-        break;
+        ci = 0;
+        cj = 1;
       }
     }
   }
