@@ -171,7 +171,12 @@ def plan_batches(batches, cands=((True, True),), alignment: int = DEFAULT_ALIGNM
 
 
 def _unknown_phase_message(ta) -> str:
-    """The phase named by the reference's TraceError (planner.py:390-392 sort order)."""
+    """The reference's TraceError text: an event outside [0, horizon]
+    (model.py:240-241; checked up front so no kernel indexes past its trace's
+    timeline) or the unknown phase (planner.py:390-392 sort order)."""
+    out = np.nonzero((ta.t_s < 0) | (ta.t_s >= ta.horizon) | (ta.t_e > ta.horizon))[0]
+    if out.size:
+        return f"event {int(ta.id[out[0]])}: timestamps outside [0, horizon]"
     n = ta.n_sched
     scoped = np.nonzero((ta.dyn == 0) & (ta.t_e < ta.horizon))[0]
     keys = sorted({(ta.phases[ta.ps[i]], ta.phases[ta.pe[i]]) for i in scoped.tolist()})

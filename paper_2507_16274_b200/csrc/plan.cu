@@ -86,8 +86,9 @@ __device__ T block_reduce_max(T v, T *sh) {
 // both the listing order); id range (mm[0], mm[1]) and max t_s (flags[1]) for
 // the sort key widths; the input checks -- bad_align[t] / bad_phase[t] = the
 // first static event (trace-local index) whose size is not aligned
-// (planner.py:371-373) / whose scoped phases are missing from the schedule
-// (model.py:201-205), INT_MAX if none -- and flags[2] = the largest phase
+// (planner.py:371-373) / whose timestamps leave [0, horizon] (model.py:240-241)
+// or whose scoped phases are missing from the schedule (model.py:201-205),
+// INT_MAX if none -- and flags[2] = the largest phase
 // index of a scoped static event.
 __global__ void __launch_bounds__(128) k_trace_scan(
     const int64_t *__restrict__ ev_off, int T, const int64_t *__restrict__ id, const int32_t *__restrict__ ts,
@@ -113,8 +114,9 @@ __global__ void __launch_bounds__(128) k_trace_scan(
     idmax = max(idmax, (long long)my_id);
     tsmax = max(tsmax, my_ts);
     if (i > e0) bad |= !(id[i - 1] < my_id && ts[i - 1] <= my_ts);
+    const int loc = (int)(i - e0);
+    if (my_ts < 0 || my_ts >= hz || te[i] > hz) bp = min(bp, loc);  // model.py:240-241
     if (!dyn[i]) {
-      const int loc = (int)(i - e0);
       if (size[i] % align) ba = min(ba, loc);
       if (te[i] < hz) {
         const int a = ps[i], z = pe[i];
@@ -1560,7 +1562,8 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
   const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
   const int n = (int)(a1 - a0);
   const int64_t off = A.uo[u];
-  const int Wn = GAP ? gap_words(A.horizon[t]) : 0;
+  const int hz = A.horizon[t];
+  const int Wn = GAP ? gap_words(hz) : 0;
   uint32_t *bits = (uint32_t *)smem, *pfx = bits + kWN * Wn;  // [kWN][Wn] each
   int32_t *prio = (int32_t *)(pfx + kWN * Wn);
   const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
@@ -1581,7 +1584,8 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
     const int j1 = (int)(gcend[j0] - a0);
     const int m = j1 - j0;
     const int64_t S = A.it.size[a0 + j0];
-    int last = INT_MIN, ne = INT_MIN, nnew = 0;
+    // lane q: end of the class's new layer q (INT_MAX while unopened)
+    int last = INT_MIN, ne = INT_MAX, nnew = 0;
     for (int cb = j0; cb < j1; cb += 32) {
       const int mine = cb + lane;
       const int cnt = min(32, j1 - cb);
@@ -1590,11 +1594,16 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
       if (mine < j1) {
         my_ts = gts[mine];
         my_te = gte[mine];
-        if (GAP)
+        if (GAP) {
+          // only a trace the input check rejects has times outside [0, horizon];
+          // clamp so its bitmap lookups stay in bounds
+          my_ts = min(max(my_ts, 0), hz);
+          my_te = min(max(my_te, 0), hz);
           for (int p = 0; p < nl; p++) {
             const int l = prio[p];
             if (rank(l, my_te + 1) == rank(l, my_ts)) fm |= 1u << p;
           }
+        }
       }
       int my_code = 0;
       for (int kg = 0; kg < cnt; kg += 8) {
@@ -1610,27 +1619,26 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
             const unsigned f = __shfl_sync(FULL, fm, k & 31);
             m1 = __ballot_sync(FULL, ((f >> lane) & 1u) && last < ts);
           }
-          // Alg. 1 (planner.py:244-252): new layer with the largest end < ts, ties to the oldest
-          const bool ca = lane < nnew && ne < ts;
-          const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
-          const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
+          // Alg. 1 (planner.py:244-252): the new layer with the largest end < ts,
+          // ties to the oldest -- one max-reduction over (end, 31 - lane) keys
+          // (ends < 2^26: the host routes longer timelines to the CTA kernel)
+          const int key = __reduce_max_sync(FULL, ne < ts ? (int)(((unsigned)ne << 5) | (unsigned)(31 - lane)) : -1);
+          const int tgt = key >= 0 ? 31 - (key & 31) : nnew;  // nnew: open a layer
           const int host = __ffs(m1) - 1;
-          const int best = cma ? __ffs(cma) - 1 : nnew;
-          const bool newl = valid && !m1 && !cma;
-          if (newl && nl + nnew == kWN) {  // a 33rd layer: the CTA kernel redoes the unit
-            if (lane == 0) over[atomicAdd(nover, 1)] = u;
-            return;
-          }
           if (valid) {
             if (m1) {
               if (lane == host) last = te;
-            } else if (lane == best) {
+            } else if (lane == tgt) {
               ne = te;
             }
           }
-          nnew += newl ? 1 : 0;
-          if (lane == k) my_code = m1 ? host : kWN + best;
+          nnew += (valid && !m1 && key < 0) ? 1 : 0;
+          if (lane == k) my_code = m1 ? host : kWN + tgt;
         }
+      }
+      if (nl + nnew > kWN) {  // a 33rd layer: the CTA kernel redoes the unit
+        if (lane == 0) over[atomicAdd(nover, 1)] = u;
+        return;
       }
       // lane-parallel: layer ids and the gap count
       const bool act = lane < cnt;
@@ -1655,7 +1663,7 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
     unsigned touched = 0;
     for (int x = lane; x < m; x += 32) {
       const int l = ilayer[j0 + x];
-      const int ts = gts[j0 + x], te = gte[j0 + x];
+      const int ts = min(max(gts[j0 + x], 0), hz), te = min(max(gte[j0 + x], 0), hz);
       touched |= 1u << l;
       uint32_t *row = bits + l * Wn;
       for (int w = ts >> 5; w <= (te >> 5); w++) {
@@ -2260,7 +2268,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     return (hcand[u % C] & STW_CAND_GAP) ? warpn_smem_ints(std::max(0, b.h_horizon[u / C])) : 0;
   };
   for (int64_t u = 0; u < U; u++) {
-    if (need((int32_t)u) <= kLayerSmemInts && uo[u + 1] - uo[u] < INT_MAX / 8)
+    if (need((int32_t)u) <= kLayerSmemInts && uo[u + 1] - uo[u] < INT_MAX / 8 && b.h_horizon[u / C] < (1 << 26))
       order.push_back((int32_t)u);
     else
       bigs.push_back((int32_t)u);

@@ -115,6 +115,12 @@ def test_plan_errors():
     unk = Trace((MemoryRequestEvent(1, 512, 0, 2, PhaseId.parse("F:0"), PhaseId.parse("B:9")),), tr.phase_schedule)
     with pytest.raises(M.TraceError, match="phase B:9 not in schedule"):
         M.synthesize_static_plan(unk)
+    # times past the horizon (model.py:240-241) are rejected up front, and the
+    # gap-insertion layer path must not index past the trace's timeline
+    late = Trace((MemoryRequestEvent(1, 512, 0, 2, PhaseId.parse("F:0"), PhaseId.parse("F:0")),
+                  MemoryRequestEvent(2, 512, 1, 9000, PhaseId.parse("F:0"), PhaseId.parse("F:0"))), tr.phase_schedule)
+    with pytest.raises(M.TraceError, match="event 2: timestamps outside"):
+        M.synthesize_static_plan(late)
 
 
 # ---------------------------------------------------------------- reuse
