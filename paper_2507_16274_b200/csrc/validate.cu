@@ -244,14 +244,18 @@ static void build_tiles(Ctx &ctx, Arena &ar, const RectSets &rs, Tiles *tl) {
 // sweep order (the first such decision reports its predecessor or a forward
 // neighbour: any other active rectangle it could hit would itself have been a
 // conflict earlier), so a valid plan needs only the overlap test. The warp
-// sweeps 32 decisions at a time: each lane tests its decision against the
-// active list (decisions still live at the tile start) and the tile's earlier
-// decisions, both broadcast from shared memory as int4 (address and end
-// scaled by 2^shift to 32 bits, t_s, t_e); then entries that end before the
-// next tile starts are compacted away. The rectangles stream through once
-// (24 B each, next tile prefetched). A unit that conflicts, does not scale
-// to 32 bits, overflows the active list, or is too long for a serial sweep is
-// flagged and the exact tiled reporter above runs instead.
+// sweeps 32 decisions at a time, scaled to int4 (address and end in units of
+// 2^shift, t_s, t_e). The active list -- decisions still live at the tile
+// start -- is kept sorted by address; while no conflict has been seen its
+// entries are pairwise disjoint, so each lane finds the entries meeting its
+// address range by binary search (O(log active) instead of a scan of the
+// list). The tile's earlier decisions are tested pairwise from shared memory.
+// Between tiles the entries that end before the next tile starts are
+// compacted away and the tile's surviving decisions merged in. The rectangles
+// stream through once (24 B each, next tile prefetched). A unit that
+// conflicts, does not scale to 32 bits, overflows the active list, or is too
+// long for a serial sweep is flagged and the exact tiled reporter above runs
+// instead.
 constexpr int kOvWarps = 8;
 constexpr int kOvCap = 320;
 constexpr int64_t kOvMaxSerial = 1 << 16;
@@ -273,6 +277,7 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
   const int32_t *ts = rs.ts + s0, *te = rs.te + s0;
   int4 *A = act[w], *Tt = tile[w];
   const long long low = (1ll << shift) - 1;
+  const unsigned lt = lanemask_lt();
   int na = 0;
   long long pa = 0, psz = 0;
   int pts = 0, pte = 0;
@@ -287,6 +292,8 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
     const long long a = pa, sz = psz;
     const int dts = pts, dte = pte;
     const int64_t kn = k0 + 32 + lane;
+    pa = psz = 0;  // past the end: an empty rectangle
+    pts = pte = 0;
     if (kn < n) {
       pa = addr[kn];
       psz = size[kn];
@@ -300,27 +307,51 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
       return;
     }
     const int da = (int)(a >> shift), de = (int)(end >> shift);
-    if (valid) Tt[lane] = make_int4(da, de, dts, dte);
+    const int4 mine = make_int4(da, de, dts, dte);  // all zero past the end: meets nothing
+    Tt[lane] = mine;
     __syncwarp();
-    // overlap <=> (c.addr - d.end) < 0, (d.addr - c.end) < 0 and (d.ts - c.te) < 0: the
-    // sign bit of the AND of the three differences (all operands are in [0, 2^31))
-    int acc = 0;
+    bool hit = false;
     if (valid) {
-#pragma unroll 4
-      for (int j = 0; j < na; j++) {
-        const int4 q = A[j];
-        acc |= (q.x - de) & (da - q.y) & (dts - q.w);
+      // The active list is address-sorted and pairwise disjoint (its entries are all
+      // live at the tile start and were checked against each other), so the entries
+      // meeting [da, de) are a contiguous run from the first one ending above da;
+      // any of them still live at dts is a conflict.
+      int lo = 0, hi = na;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A[mid].y > da)
+          hi = mid;
+        else
+          lo = mid + 1;
       }
-      for (int j = 0; j < lane; j++) {
-        const int4 q = Tt[j];
-        acc |= (q.x - de) & (da - q.y) & (dts - q.w);
+      for (int q = lo; q < na; q++) {
+        const int4 e = A[q];
+        if (e.x >= de) break;
+        if (e.w > dts) {
+          hit = true;
+          break;
+        }
       }
     }
-    if (__any_sync(FULL, acc < 0)) {
+    // the tile's decisions among themselves, each unordered pair once: lane i meets
+    // lane i - o (mod 32), o = 1..16. Overlap <=> (c.addr - d.end), (d.addr - c.end),
+    // (d.ts - c.te) and (c.ts - d.te) all negative: the sign bit of their AND
+    // (operands in [0, 2^31)); for a pair in sweep order the last one always is.
+    int acc = 0;
+#pragma unroll
+    for (int o = 1; o <= 16; o++) {
+      const int4 q = Tt[(lane - o) & 31];
+      acc |= (q.x - de) & (da - q.y) & (dts - q.w) & (q.z - dte);
+    }
+    hit |= acc < 0;
+    if (__any_sync(FULL, hit)) {
       if (lane == 0) atomicAdd(nflag, 1);
       return;
     }
-    const int t0n = k0 + 32 < n ? __shfl_sync(FULL, pts, 0) : INT_MAX;  // start of the next tile
+    if (k0 + 32 >= n) break;  // nothing reads the list after the last tile
+    // 1. drop the entries that end by the tile's last start (order kept). What
+    // stays is live at that instant, hence pairwise checked and disjoint.
+    const int t0n = __shfl_sync(FULL, dts, 31);
     int nn = 0;
     for (int cb = 0; cb < na; cb += 32) {
       const int j = cb + lane;
@@ -328,18 +359,61 @@ __global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, in
       const bool keep = j < na && q.w > t0n;
       const unsigned m = __ballot_sync(FULL, keep);
       __syncwarp();
-      if (keep) A[nn + __popc(m & lanemask_lt())] = q;
+      if (keep) A[nn + __popc(m & lt)] = q;
       nn += __popc(m);
       __syncwarp();
     }
+    // 2. the tile's decisions still live then, merged in address order
     const bool keep = valid && dte > t0n;
     const unsigned m = __ballot_sync(FULL, keep);
-    if (nn + __popc(m) > kOvCap) {
+    const int ns = __popc(m);
+    if (nn + ns > kOvCap) {
       if (lane == 0) atomicAdd(nflag, 1);
       return;
     }
-    if (keep) A[nn + __popc(m & lanemask_lt())] = make_int4(da, de, dts, dte);
-    na = nn + __popc(m);
+    if (ns) {
+      int rk = 0;  // rank among the survivors (addresses distinct: pairwise disjoint)
+      for (unsigned mm = m; mm; mm &= mm - 1) rk += __shfl_sync(FULL, da, __ffs(mm) - 1) < da ? 1 : 0;
+      int pos = 0;  // survivors' slot: old entries below it + survivors below it
+      if (keep) {
+        int lo = 0, hi = nn;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (A[mid].x < da)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        pos = lo + rk;
+      }
+      __syncwarp();
+      if (keep) Tt[rk] = mine;  // survivors sorted by address
+      __syncwarp();
+      // old entry i moves up by the survivors below it; back to front, a chunk is
+      // read before the next one down overwrites it, and destinations increase
+      for (int cb = (nn - 1) & ~31; cb >= 0; cb -= 32) {
+        const int j = cb + lane;
+        int4 q = make_int4(0, 0, 0, 0);
+        int dst = j;
+        if (j < nn) {
+          q = A[j];
+          int lo = 0, hi = ns;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (Tt[mid].x < q.x)
+              lo = mid + 1;
+            else
+              hi = mid;
+          }
+          dst = j + lo;
+        }
+        __syncwarp();
+        if (j < nn && dst != j) A[dst] = q;
+        __syncwarp();
+      }
+      if (keep) A[pos] = mine;
+    }
+    na = nn + ns;
     __syncwarp();
   }
 }
