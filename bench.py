@@ -190,7 +190,7 @@ def algo_bytes(kernel: str, w: dict, launches_per_step: float) -> float:
         # K1: 17 B/event (t_s, t_e, size, dyn)
         "k_peak_warp": 17.0 * w["events"],
         # segmented sorts: 12 B/record read + written per sort
-        "k_seg_bitonic": 24.0 * w["events"],
+        "k_seg_radix<8>": 24.0 * w["events"],
         "k_emit": 40.0 * w["unit_events"],
     }.get(kernel)
     if per_step is None:

@@ -16,7 +16,7 @@ P = os.path.join(ROOT, "profiles")
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
-CAPS = [("k_layers_w32", "k_layers_w32"), ("k_fusion", "k_fusion"), ("k_seg_bitonic", "k_seg_bitonic"),
+CAPS = [("k_layers_w32", "k_layers_w32"), ("k_fusion", "k_fusion"), ("k_seg_radix", "k_seg_radix"),
         ("k_overlap_sweep@c4", "k_overlap_sweep_c4"), ("k_overlap_sweep@sweep", "k_overlap_sweep_big"),
         ("k_peak_warp@sweep", "k_peak_warp_big"), ("k_os_pass@sweep", "k_os_pass_big")]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "ms": 1e3}

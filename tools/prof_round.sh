@@ -16,7 +16,7 @@ full() {  # name regex skip cmd...
 }
 NCU_COUNT=2 full k_layers_w32 k_layers_w32 2 python tools/one_plan.py
 full k_fusion k_fusion 1 python tools/one_plan.py
-NCU_COUNT=2 full k_seg_bitonic k_seg_bitonic 2 python tools/one_plan.py
+NCU_COUNT=2 full k_seg_radix k_seg_radix 2 python tools/one_plan.py
 full k_overlap_sweep_c4 k_overlap_sweep 1 python tools/one_plan.py
 full k_overlap_sweep_big k_overlap_sweep 7 $B
 full k_peak_warp_big k_peak_warp 7 $B
