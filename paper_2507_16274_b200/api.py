@@ -259,6 +259,31 @@ def synthesize_static_plan(trace, *, fusion: bool = True, gap_insert: bool = Tru
     return plan
 
 
+def validate_columns(id, addr, size, t_s, t_e) -> np.ndarray:
+    """K7 on one plan given as columns (any order): the reference sweep's report
+    (planner.py:476-505) as an int array [k, 2] of row indices, in its order."""
+    n = int(np.shape(id)[0])
+    if n == 0:
+        return np.zeros((0, 2), np.int64)
+    id = np.ascontiguousarray(id, np.int64)
+    addr = np.ascontiguousarray(addr, np.int64)
+    size = np.ascontiguousarray(size, np.int64)
+    t_s = np.ascontiguousarray(t_s, np.int32)
+    t_e = np.ascontiguousarray(t_e, np.int32)
+    npairs = C.c_int64(0)
+    cap = max(16, 4 * n)
+    err = _lib.errbuf()
+    L = _lib.load()
+    while True:
+        pairs = np.empty(2 * cap, np.int32)
+        _lib.check(L.stw_validate(C.c_int64(n), _lib.ptr(id), _lib.ptr(addr), _lib.ptr(size), _lib.ptr(t_s),
+                                  _lib.ptr(t_e), C.byref(npairs), _lib.ptr(pairs), C.c_int64(cap), None, err,
+                                  C.sizeof(err)), err)
+        if npairs.value <= cap:
+            return pairs[: 2 * npairs.value].reshape(-1, 2).astype(np.int64)
+        cap = npairs.value
+
+
 def validate_plan(plan) -> list:
     """Decision pairs the reference sweep reports as conflicting (planner.py:476-505)."""
     if isinstance(plan, StaticPlan):
@@ -267,26 +292,24 @@ def validate_plan(plan) -> list:
     else:
         decs = tuple(plan.decisions)
         cols = DecisionColumns.from_decisions(decs)
-    n = len(cols)
-    if n == 0:
-        return []
-    npairs = C.c_int64(0)
-    cap = max(16, 4 * n)
-    pairs = np.empty(2 * cap, np.int32)
-    err = _lib.errbuf()
-    L = _lib.load()
-    rc = L.stw_validate(C.c_int64(n), _lib.ptr(cols.id), _lib.ptr(cols.addr), _lib.ptr(cols.size),
-                        _lib.ptr(cols.t_s), _lib.ptr(cols.t_e), C.byref(npairs), _lib.ptr(pairs), C.c_int64(cap),
-                        None, err, C.sizeof(err))
-    _lib.check(rc, err)
-    if npairs.value > cap:
-        cap = npairs.value
-        pairs = np.empty(2 * cap, np.int32)
-        _lib.check(L.stw_validate(C.c_int64(n), _lib.ptr(cols.id), _lib.ptr(cols.addr), _lib.ptr(cols.size),
-                                  _lib.ptr(cols.t_s), _lib.ptr(cols.t_e), C.byref(npairs), _lib.ptr(pairs),
-                                  C.c_int64(cap), None, err, C.sizeof(err)), err)
-    p = pairs[: 2 * npairs.value].reshape(-1, 2).tolist()
+    p = validate_columns(cols.id, cols.addr, cols.size, cols.t_s, cols.t_e).tolist()
     return [(decs[a], decs[b]) for a, b in p]
+
+
+def peak_live_columns(size, t_s, t_e) -> int:
+    """K1 over bare (size, t_s, t_e) columns: max over time of the live bytes
+    (model.py:261-276)."""
+    n = int(np.shape(size)[0])
+    if n == 0:
+        return 0
+    t_s = np.asarray(t_s, np.int32)
+    t_e = np.asarray(t_e, np.int32)
+    hz = int(max(int(t_e.max()), int(t_s.max()) + 1, 1))
+    z = np.zeros(n, np.int32)
+    ta = TraceArrays(np.arange(n, dtype=np.int64), np.asarray(size, np.int64), t_s, t_e, z, z, np.zeros(n, np.uint8),
+                     z, z, [None], np.zeros(1, np.int64), np.asarray([hz], np.int64), [], np.zeros(0, np.int64),
+                     np.zeros(0, np.int64))
+    return peak_live_bytes(ta)
 
 
 # ---------------------------------------------------------------------------
