@@ -36,14 +36,16 @@ static void fetch_small(Ctx &ctx, std::vector<T> &dst, const T *src, int64_t n, 
   dst.resize(n);
   if (n == 0 || !ctx.ok()) return;
   if (on_device) {
-    STW_CUDA(ctx, cudaMemcpyAsync(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
-    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    d2h_async(ctx, dst.data(), src, n * sizeof(T));  // filled by stage_batch's host_sync
   } else {
     memcpy(dst.data(), src, n * sizeof(T));
   }
 }
 
-inline bool stage_batch(Ctx &ctx, Arena &ar, const stw_batch *b, DevBatch *d) {
+// `mirror` (optional): the same batch in host memory, read for the small
+// per-trace arrays instead of a device round trip (stw_plan_batches stages its
+// batches itself and keeps the host originals).
+inline bool stage_batch(Ctx &ctx, Arena &ar, const stw_batch *b, DevBatch *d, const stw_batch *mirror = nullptr) {
   if (!b || b->n_traces < 0 || b->n_events < 0) {
     ctx.fail(STW_EARG, "bad batch descriptor");
     return false;
@@ -55,9 +57,12 @@ inline bool stage_batch(Ctx &ctx, Arena &ar, const stw_batch *b, DevBatch *d) {
   bool dev = b->on_device != 0;
   d->T = b->n_traces;
   d->N = b->n_events;
-  fetch_small(ctx, d->h_ev_off, b->ev_off, (int64_t)b->n_traces + 1, dev);
-  fetch_small(ctx, d->h_horizon, b->horizon, b->n_traces, dev);
-  fetch_small(ctx, d->h_n_sched, b->n_sched, b->n_traces, dev);
+  const stw_batch *hs = mirror ? mirror : b;
+  const bool fetch_dev = mirror ? false : dev;
+  fetch_small(ctx, d->h_ev_off, hs->ev_off, (int64_t)b->n_traces + 1, fetch_dev);
+  fetch_small(ctx, d->h_horizon, hs->horizon, b->n_traces, fetch_dev);
+  fetch_small(ctx, d->h_n_sched, hs->n_sched, b->n_traces, fetch_dev);
+  if (fetch_dev) host_sync(ctx);  // one round trip for the three
   if (!ctx.ok()) return false;
   if (d->h_ev_off[0] != 0 || d->h_ev_off[d->T] != d->N) {
     ctx.fail(STW_EARG, "ev_off must span [0, n_events]");

@@ -80,6 +80,17 @@ struct Arena {
   ~Arena() { release(); }
 };
 
+// Small host<->device transfers of the planner's round trips, kept off the
+// copy engines: a copy engine works through its queue in order, so a few-byte
+// pageable copy issued while stw_plan_batches streams the next batch in (or
+// the previous results out) would wait behind megabytes. These go through a
+// mapped page-locked scratch instead and are moved by a copy kernel on the
+// caller's stream; d2h_async results land in `dst` at the next host_sync.
+// The scratch is reused after each host_sync (every kernel that read it ran).
+void h2d_async(Ctx &ctx, void *ddst, const void *hsrc, size_t bytes);
+void d2h_async(Ctx &ctx, void *dst, const void *dsrc, size_t bytes);
+void host_sync(Ctx &ctx);
+
 // host-side size helpers
 
 inline int bitlen_u64(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }

@@ -11,7 +11,7 @@
 
 namespace stw {
 
-int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
+int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror);
 
 namespace {
 
@@ -133,7 +133,7 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
       db.dyn = s.dyn;
       db.horizon = s.horizon;
       db.n_sched = s.n_sched;
-      plan_batch(ctx, &db, o, &s.dout);
+      plan_batch(ctx, &db, o, &s.dout, &in[k]);
       if (!ctx.ok()) break;
       STW_CUDA(ctx, cudaEventRecord(s.planned, ctx.stream));
       STW_CUDA(cctx, cudaStreamWaitEvent(cs, s.planned, 0));

@@ -1939,16 +1939,15 @@ static cudaEvent_t side_event(int i) {
 template <class T>
 static void d2h(Ctx &ctx, std::vector<T> &h, const T *d, int64_t n) {
   h.resize(n);
-  if (n > 0) STW_CUDA(ctx, cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
+  if (n > 0) d2h_async(ctx, h.data(), d, n * sizeof(T));  // filled at the next sync
 }
 template <class T>
 static T *h2d(Ctx &ctx, Arena &ar, const std::vector<T> &h) {
   T *d = ar.take<T>(h.size() ? h.size() : 1);
-  if (d && h.size())
-    STW_CUDA(ctx, cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx.stream));
+  if (d && h.size()) h2d_async(ctx, d, h.data(), h.size() * sizeof(T));
   return d;
 }
-static void sync(Ctx &ctx) { STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream)); }
+static void sync(Ctx &ctx) { host_sync(ctx); }
 
 template <class T>
 static void out_copy(Ctx &ctx, T *dst, const T *src, int64_t n, bool dst_dev) {
@@ -2024,7 +2023,7 @@ struct PhaseTimer {
   }
 };
 
-int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out) {
+int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror) {
   PhaseTimer pt(ctx);
   Arena ar(&ctx);
   DevBatch b;
@@ -2032,7 +2031,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     ctx.fail(STW_EARG, "bad plan options");
     return ctx.rc;
   }
-  if (!stage_batch(ctx, ar, in, &b)) return ctx.rc;
+  if (!stage_batch(ctx, ar, in, &b, mirror)) return ctx.rc;
   const int T = b.T, C = o->n_cand;
   const int64_t N = b.N, U = (int64_t)T * C;
   std::vector<uint8_t> hcand(o->cand, o->cand + C);
@@ -2056,7 +2055,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   int *im = ar.take<int>(4);
   if (!ctx.ok()) return ctx.rc;
   long long mm_init[2] = {LLONG_MAX, LLONG_MIN};
-  STW_CUDA(ctx, cudaMemcpyAsync(mm, mm_init, sizeof(mm_init), cudaMemcpyHostToDevice, ctx.stream));
+  h2d_async(ctx, mm, mm_init, sizeof(mm_init));
   STW_CUDA(ctx, cudaMemsetAsync(im, 0, 4 * sizeof(int), ctx.stream));
   // one warp-per-trace pass: tr, presortedness, key widths and the input checks
   int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
@@ -2068,8 +2067,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
   long long hmm[2] = {0, 0};
   int him[4] = {0, 0, 0, 0};
-  STW_CUDA(ctx, cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx.stream));
-  STW_CUDA(ctx, cudaMemcpyAsync(him, im, sizeof(him), cudaMemcpyDeviceToHost, ctx.stream));
+  d2h_async(ctx, hmm, mm, sizeof(hmm));
+  d2h_async(ctx, him, im, sizeof(him));
   sync(ctx);
   if (!ctx.ok()) return ctx.rc;
   const int tb = bitlen_u64((uint64_t)(T - 1));
@@ -2201,11 +2200,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   long long *d_imax = ar.take<long long>(2);
   long long h_imax[2] = {LLONG_MAX, 0};
   if (!ctx.ok()) return ctx.rc;
-  STW_CUDA(ctx, cudaMemcpyAsync(d_imax, h_imax, sizeof(h_imax), cudaMemcpyHostToDevice, ctx.stream));
+  h2d_async(ctx, d_imax, h_imax, sizeof(h_imax));
   LAUNCH_RED(k_minmax_i64, P, p0.h, P, d_imax, d_imax + 1);
   if (want[1]) LAUNCH_RED(k_minmax_i64, P, p1.h, P, d_imax, d_imax + 1);
   LAUNCH_RED(k_minmax_i64, N, b.size, N, d_imax, d_imax + 1);
-  STW_CUDA(ctx, cudaMemcpyAsync(h_imax, d_imax, sizeof(h_imax), cudaMemcpyDeviceToHost, ctx.stream));
+  d2h_async(ctx, h_imax, d_imax, sizeof(h_imax));
 
   pt.mark("C fusion");
   // ---- D: items per (variant, trace)
@@ -2383,10 +2382,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     d2h(ctx, htie, it.tie + j0, n0);
     d2h(ctx, href, it.ref + j0, n0);
     d2h(ctx, hce, cend + j0, n0);
-    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
     d2h(ctx, hil, LA.ilayer, n0);
     d2h(ctx, hir, LA.irank, n0);
-    STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+    sync(ctx);
     fprintf(stderr, "unit0: v=%d items=%lld (j0=%lld)\n", v0, (long long)n0, (long long)j0);
     for (int64_t k = 0; k < n0; k++)
       fprintf(stderr, "  it %lld size=%lld ts=%d te=%d tie=%d ref=%d cend=%lld -> layer %d rank %d\n", (long long)k,
@@ -2449,16 +2447,16 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // one host round trip for the deferred checks: conflicts, units the fast
   // validity test could not decide, traces whose peak needs the global timeline
   int hq[3] = {0, 0, 0};
-  STW_CUDA(ctx, cudaMemcpyAsync(hq, d_nconf, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  if (d_nflag) STW_CUDA(ctx, cudaMemcpyAsync(hq + 1, d_nflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  if (ppk.nbig) STW_CUDA(ctx, cudaMemcpyAsync(hq + 2, ppk.nbig, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  d2h_async(ctx, hq, d_nconf, sizeof(int));
+  if (d_nflag) d2h_async(ctx, hq + 1, d_nflag, sizeof(int));
+  if (ppk.nbig) d2h_async(ctx, hq + 2, ppk.nbig, sizeof(int));
   sync(ctx);
   if (!ctx.ok()) return ctx.rc;
   if (hq[1] > 0 || hq[2] > 0) {  // rare: redo the verdicts with the exact validator / global peaks
     if (hq[2] > 0) peak_live_finish(ctx, ar, b, true, peak, ppk);
     if (hq[1] > 0) validate_exact(ctx, ar, rs, vcount, vfirst);
     finalize();
-    STW_CUDA(ctx, cudaMemcpyAsync(hq, d_nconf, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    d2h_async(ctx, hq, d_nconf, sizeof(int));
     sync(ctx);
     if (!ctx.ok()) return ctx.rc;
   }
@@ -2486,7 +2484,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
         h_err2[2 * u + 1] = ev2[1];
       }
     }
-    STW_CUDA(ctx, cudaMemcpyAsync(d_err, h_err2.data(), 2 * U * sizeof(int64_t), cudaMemcpyHostToDevice, ctx.stream));
+    h2d_async(ctx, d_err, h_err2.data(), 2 * U * sizeof(int64_t));
     sync(ctx);
   }
   pt.mark("finalize");

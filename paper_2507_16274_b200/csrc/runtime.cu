@@ -486,6 +486,79 @@ void sort_perm(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *perm, int64_t n, i
   radix_sort_pairs(ctx, ar, keys, perm, n, 0, bits);
 }
 
+
+// ---------------------------------------------------------------------------
+// mapped page-locked scratch for small transfers (see common.cuh)
+
+namespace {
+struct PinnedScratch {
+  std::vector<std::pair<char *, size_t>> blocks;
+  size_t blk = 0, off = 0;
+  struct Pending {
+    void *dst;
+    const void *src;
+    size_t bytes;
+  };
+  std::vector<Pending> pend;
+  char *take(Ctx &ctx, size_t bytes) {
+    bytes = (bytes + 15) & ~(size_t)15;
+    while (blk < blocks.size() && off + bytes > blocks[blk].second) blk++, off = 0;
+    if (blk == blocks.size()) {
+      const size_t cap = std::max<size_t>(bytes, 1 << 20);
+      void *p = nullptr;
+      STW_CUDA(ctx, cudaHostAlloc(&p, cap, cudaHostAllocMapped | cudaHostAllocPortable));
+      if (!p) return nullptr;
+      blocks.push_back({(char *)p, cap});
+      off = 0;
+    }
+    char *p = blocks[blk].first + off;
+    off += bytes;
+    return p;
+  }
+};
+thread_local PinnedScratch g_pin;
+
+__global__ void k_copy_bytes(const unsigned char *__restrict__ src, unsigned char *__restrict__ dst, int64_t n) {
+  const int64_t n16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) ? 0 : n >> 4;
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride) d4[i] = s4[i];
+  for (int64_t i = (n16 << 4) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+
+void copy_launch(Ctx &ctx, void *dst, const void *src, size_t bytes) {
+  STW_KL(k_copy_bytes, grid_for((int64_t)(bytes + 15) / 16, 256, 148 * 4), 256, ctx.stream,
+         (const unsigned char *)src, (unsigned char *)dst, (int64_t)bytes);
+  STW_LAUNCHED(ctx);
+}
+}  // namespace
+
+void h2d_async(Ctx &ctx, void *ddst, const void *hsrc, size_t bytes) {
+  if (!bytes || !ctx.ok()) return;
+  char *p = g_pin.take(ctx, bytes);
+  if (!p) return;
+  memcpy(p, hsrc, bytes);
+  copy_launch(ctx, ddst, p, bytes);
+}
+
+void d2h_async(Ctx &ctx, void *dst, const void *dsrc, size_t bytes) {
+  if (!bytes || !ctx.ok()) return;
+  char *p = g_pin.take(ctx, bytes);
+  if (!p) return;
+  copy_launch(ctx, p, dsrc, bytes);
+  g_pin.pend.push_back({dst, p, bytes});
+}
+
+void host_sync(Ctx &ctx) {
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (ctx.ok())
+    for (auto &q : g_pin.pend) memcpy(q.dst, q.src, q.bytes);
+  g_pin.pend.clear();
+  g_pin.blk = 0;
+  g_pin.off = 0;
+}
+
 }  // namespace stw
 
 extern "C" {
