@@ -84,10 +84,12 @@ struct Arena {
 // copy engines: a copy engine works through its queue in order, so a few-byte
 // pageable copy issued while stw_plan_batches streams the next batch in (or
 // the previous results out) would wait behind megabytes. These go through a
-// mapped page-locked scratch instead and are moved by a copy kernel on the
-// caller's stream; d2h_async results land in `dst` at the next host_sync.
+// mapped page-locked scratch instead and are moved by copy kernels on the
+// caller's stream (pending uploads: one launch right before the stream's next
+// kernel; downloads: one launch at host_sync, where they land in `dst`).
 // The scratch is reused after each host_sync (every kernel that read it ran).
 void h2d_async(Ctx &ctx, void *ddst, const void *hsrc, size_t bytes);
+void h2d_flush(Ctx &ctx);  // before another stream (or an event) must see the uploads
 void d2h_async(Ctx &ctx, void *dst, const void *dsrc, size_t bytes);
 void host_sync(Ctx &ctx);
 

@@ -251,8 +251,10 @@ __global__ void __launch_bounds__(256) k_seg_radix(uint64_t *__restrict__ keys, 
   const unsigned lt = lanemask_lt();
   const int R = (n + 255) >> 8;  // rows of 32 per warp actually used (<= IPT)
   const int run = 32 * R;        // each warp owns a contiguous block of the segment
-  for (int b = bit0; b < bits; b += 8) {
-    const int width = min(8, bits - b);
+  for (int b = bit0, width; b < bits; b += width) {
+    // the fewest 8-bit-or-narrower passes, widths balanced (fewer ballots per pass)
+    const int left = bits - b;
+    width = (left + (left + 7) / 8 - 1) / ((left + 7) / 8);
     const uint32_t mask = (1u << width) - 1;
     for (int x = tid; x < 8 * 256; x += 256) wh[x] = 0;
     __syncthreads();
@@ -1075,8 +1077,14 @@ __global__ void __launch_bounds__(128) k_items(Plans p0, Plans p1, int want0, in
   }
 }
 
+// in_order: every trace is listed in recorded order, so q (the id rank) is the
+// position and t_s never decreases along it. An item's (t_s, tie) is then the
+// (t_s, q) of one event -- its own, or a plan's earliest member (whose t_s is
+// the plan's min t_s and whose q is its min q, fused plans included) -- and
+// (t_s, tie) order is tie order: the low key is tie alone.
 __global__ void k_item_keys(Items it, int64_t n, const int64_t *__restrict__ io, int VT, int qb, long long align,
-                            long long maxsu, int sb, uint64_t *__restrict__ hi, uint64_t *__restrict__ lo) {
+                            long long maxsu, int sb, int in_order, uint64_t *__restrict__ hi,
+                            uint64_t *__restrict__ lo) {
   GRID_STRIDE(j, n) {
     int vt = 0;
     {  // segment of j in io[0..VT]
@@ -1092,7 +1100,7 @@ __global__ void k_item_keys(Items it, int64_t n, const int64_t *__restrict__ io,
     }
     long long su = it.size[j] / align;
     hi[j] = ((uint64_t)vt << sb) | (uint64_t)(maxsu - su);
-    lo[j] = ((uint64_t)(uint32_t)it.ts[j] << qb) | (uint32_t)it.tie[j];
+    lo[j] = in_order ? (uint64_t)(uint32_t)it.tie[j] : ((uint64_t)(uint32_t)it.ts[j] << qb) | (uint32_t)it.tie[j];
   }
 }
 
@@ -2241,11 +2249,12 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     ctx.fail(STW_EARG, "item sort key exceeds 64 bits");
     return ctx.rc;
   }
-  LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, (long long)o->alignment, maxsu, sb, ihi, ilo);
+  const bool in_order = him[0] == 0;
+  LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, (long long)o->alignment, maxsu, sb, in_order ? 1 : 0, ihi, ilo);
   {
     int64_t max_items = 0;
     for (int64_t x = 0; x < V * T; x++) max_items = std::max(max_items, io[x + 1] - io[x]);
-    seg_sort(ctx, ar, ihi, vtb + sb, vtb, ilo, tsb + qb, iperm, NI, d_io, (int64_t)V * T, max_items);
+    seg_sort(ctx, ar, ihi, vtb + sb, vtb, ilo, in_order ? qb : tsb + qb, iperm, NI, d_io, (int64_t)V * T, max_items);
   }
   LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
   // host-side preparation of phase E, overlapped with the D kernels: unit
@@ -2347,6 +2356,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     cudaStream_t side = nullptr;
     if (nctas_ng) {  // fork: non-gap units on the side stream
       side = side_stream();
+      h2d_flush(ctx);  // the side stream reads the unit tables uploaded above
       STW_CUDA(ctx, cudaEventRecord(side_event(0), ctx.stream));
       STW_CUDA(ctx, cudaStreamWaitEvent(side, side_event(0), 0));
       STW_KLS(k_layers_w32, (unsigned)nctas_ng, kWarpsPerCta * 32, 0, side, LA, d_wslot_ng, d_over, d_nover);

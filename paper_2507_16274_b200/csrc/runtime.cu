@@ -44,7 +44,10 @@ static cudaEvent_t get_event() {
   return e;
 }
 
+void h2d_flush_stream(cudaStream_t s);
+
 int prof_pre(cudaStream_t s) {
+  h2d_flush_stream(s);  // uploads queued by h2d_async land before the kernel
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_prof_on.load(std::memory_order_relaxed)) return -1;
   std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -488,23 +491,49 @@ void sort_perm(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *perm, int64_t n, i
 
 
 // ---------------------------------------------------------------------------
-// mapped page-locked scratch for small transfers (see common.cuh)
+// mapped page-locked scratch for small transfers (see common.cuh). Pending
+// uploads are moved by ONE multi-copy kernel launched just before the next
+// kernel on their stream (prof_pre) or at an explicit h2d_flush; pending
+// downloads by one launch at host_sync.
 
 namespace {
+struct CopyDesc {
+  const unsigned char *src;
+  unsigned char *dst;
+  int64_t bytes;
+};
+constexpr int kMaxCopies = 48;
+struct CopyBatch {
+  CopyDesc d[kMaxCopies];
+};
+
+__global__ void k_copy_multi(CopyBatch cb) {
+  const CopyDesc c = cb.d[blockIdx.y];
+  const bool vec = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst)) & 15) == 0;
+  const int64_t n16 = vec ? c.bytes >> 4 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = t; i < n16; i += stride)
+    reinterpret_cast<uint4 *>(c.dst)[i] = reinterpret_cast<const uint4 *>(c.src)[i];
+  for (int64_t i = (n16 << 4) + t; i < c.bytes; i += stride) c.dst[i] = c.src[i];
+}
+
 struct PinnedScratch {
   std::vector<std::pair<char *, size_t>> blocks;
   size_t blk = 0, off = 0;
-  struct Pending {
+  std::vector<CopyDesc> up, down;  // pending uploads / downloads
+  cudaStream_t up_stream = nullptr;
+  struct HostCopy {
     void *dst;
     const void *src;
     size_t bytes;
   };
-  std::vector<Pending> pend;
+  std::vector<HostCopy> out;  // pinned -> caller memory at host_sync
   char *take(Ctx &ctx, size_t bytes) {
     bytes = (bytes + 15) & ~(size_t)15;
     while (blk < blocks.size() && off + bytes > blocks[blk].second) blk++, off = 0;
     if (blk == blocks.size()) {
-      const size_t cap = std::max<size_t>(bytes, 1 << 20);
+      const size_t cap = std::max<size_t>(bytes, 4 << 20);
       void *p = nullptr;
       STW_CUDA(ctx, cudaHostAlloc(&p, cap, cudaHostAllocMapped | cudaHostAllocPortable));
       if (!p) return nullptr;
@@ -518,43 +547,59 @@ struct PinnedScratch {
 };
 thread_local PinnedScratch g_pin;
 
-__global__ void k_copy_bytes(const unsigned char *__restrict__ src, unsigned char *__restrict__ dst, int64_t n) {
-  const int64_t n16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) ? 0 : n >> 4;
-  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride) d4[i] = s4[i];
-  for (int64_t i = (n16 << 4) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
-}
-
-void copy_launch(Ctx &ctx, void *dst, const void *src, size_t bytes) {
-  STW_KL(k_copy_bytes, grid_for((int64_t)(bytes + 15) / 16, 256, 148 * 4), 256, ctx.stream,
-         (const unsigned char *)src, (unsigned char *)dst, (int64_t)bytes);
-  STW_LAUNCHED(ctx);
+void launch_copies(std::vector<CopyDesc> &v, cudaStream_t s) {
+  for (size_t i = 0; i < v.size(); i += kMaxCopies) {
+    CopyBatch cb;
+    const int n = (int)std::min<size_t>(kMaxCopies, v.size() - i);
+    int64_t mx = 0;
+    for (int k = 0; k < n; k++) cb.d[k] = v[i + k], mx = std::max(mx, v[i + k].bytes);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_copy_multi<<<dim3(grid_for((mx + 15) / 16, 256, 64), n), 256, 0, s>>>(cb);
+  }
+  v.clear();
 }
 }  // namespace
 
+void h2d_flush_stream(cudaStream_t s) {
+  if (!g_pin.up.empty() && s == g_pin.up_stream) launch_copies(g_pin.up, s);
+}
+
+void h2d_flush(Ctx &ctx) {
+  if (g_pin.up.empty()) return;
+  launch_copies(g_pin.up, g_pin.up_stream);
+  STW_LAUNCHED(ctx);
+}
+
 void h2d_async(Ctx &ctx, void *ddst, const void *hsrc, size_t bytes) {
   if (!bytes || !ctx.ok()) return;
+  if (!g_pin.up.empty() && g_pin.up_stream != ctx.stream) h2d_flush(ctx);
   char *p = g_pin.take(ctx, bytes);
   if (!p) return;
   memcpy(p, hsrc, bytes);
-  copy_launch(ctx, ddst, p, bytes);
+  g_pin.up.push_back({(const unsigned char *)p, (unsigned char *)ddst, (int64_t)bytes});
+  g_pin.up_stream = ctx.stream;
 }
 
 void d2h_async(Ctx &ctx, void *dst, const void *dsrc, size_t bytes) {
   if (!bytes || !ctx.ok()) return;
   char *p = g_pin.take(ctx, bytes);
   if (!p) return;
-  copy_launch(ctx, p, dsrc, bytes);
-  g_pin.pend.push_back({dst, p, bytes});
+  g_pin.down.push_back({(const unsigned char *)dsrc, (unsigned char *)p, (int64_t)bytes});
+  g_pin.out.push_back({dst, p, bytes});
 }
 
 void host_sync(Ctx &ctx) {
+  h2d_flush(ctx);
+  if (!g_pin.down.empty()) {
+    launch_copies(g_pin.down, ctx.stream);
+    STW_LAUNCHED(ctx);
+  }
   STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
   if (ctx.ok())
-    for (auto &q : g_pin.pend) memcpy(q.dst, q.src, q.bytes);
-  g_pin.pend.clear();
+    for (auto &q : g_pin.out) memcpy(q.dst, q.src, q.bytes);
+  g_pin.out.clear();
+  g_pin.up.clear();
+  g_pin.down.clear();
   g_pin.blk = 0;
   g_pin.off = 0;
 }
