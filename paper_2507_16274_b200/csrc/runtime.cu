@@ -164,7 +164,10 @@ void Arena::release() {
 // order by an atomic counter; each tile publishes its aggregate, then a warp
 // looks back over up to 32 predecessors at a time (flag + value arrays, the
 // value written before its flag behind a fence) for the nearest inclusive
-// prefix; one launch and one read + one write of the data.
+// prefix; one launch and one read + one write of the data. The first
+// kScanDirect tiles instead sum all their predecessors' aggregates at once.
+constexpr int64_t kScanDirect = 1024;
+
 template <class T>
 __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ in, T *__restrict__ out, int64_t n,
                                                           int inclusive, uint32_t *__restrict__ flag,
@@ -189,17 +192,31 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
   const T ex = block_excl_sum<T>(acc, sh, &total);
   volatile uint32_t *vf = flag;
   if (tid == 0) {
-    if (tile == 0) {
-      pre[0] = total;
-      __threadfence();
-      atomicExch(flag, 2u);
-    } else {
-      agg[tile] = total;
-      __threadfence();
-      atomicExch(flag + tile, 1u);
-    }
+    agg[tile] = total;
+    if (tile == 0) pre[0] = total;
+    __threadfence();
+    atomicExch(flag + tile, tile == 0 ? 2u : 1u);
   }
-  if (tid < 32) {
+  if (tile > 0 && tile <= kScanDirect) {
+    // few tiles: sum every predecessor's aggregate directly -- they are all
+    // published at about the same time, so there is no prefix chain to wait on
+    T part = 0;
+    for (int64_t t = tid; t < (int64_t)tile; t += kScanThreads) {
+      while (vf[t] == 0) {
+      }
+      __threadfence();
+      part += *(volatile T *)(agg + t);
+    }
+    __syncthreads();  // `sh` is reused
+    T excl;
+    block_excl_sum<T>(part, sh, &excl);
+    if (tid == 0) {
+      pre[tile] = excl + total;  // an inclusive prefix for the look-back of later tiles
+      __threadfence();
+      atomicExch(flag + tile, 2u);
+      s_excl = excl;
+    }
+  } else if (tid < 32) {
     T excl = 0;
     if (tile > 0) {
       for (int64_t t0 = (int64_t)tile - 1;; t0 -= 32) {
