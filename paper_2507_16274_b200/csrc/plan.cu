@@ -106,23 +106,27 @@ __global__ void __launch_bounds__(128) k_trace_scan(
   bool bad = false;
   long long idmin = LLONG_MAX, idmax = LLONG_MIN;
   int tsmax = 0, pmax = 0, ba = INT_MAX, bp = INT_MAX;
+  const bool pow2 = (align & (align - 1)) == 0;
+  // every column loaded up front and branch-free (more loads in flight per warp)
+#pragma unroll 2
   for (int64_t i = e0 + tid; i < e1; i += blockDim.x) {
-    const int64_t my_id = id[i];
-    const int my_ts = ts[i];
+    const int64_t my_id = id[i], sz = size[i];
+    const int my_ts = ts[i], my_te = te[i], a = ps[i], z = pe[i];
+    const bool dy = dyn[i] != 0;
+    const int64_t prev_id = i > e0 ? id[i - 1] : LLONG_MIN;
+    const int prev_ts = i > e0 ? ts[i - 1] : INT_MIN;
     tr[i] = t;
     idmin = min(idmin, (long long)my_id);
     idmax = max(idmax, (long long)my_id);
     tsmax = max(tsmax, my_ts);
-    if (i > e0) bad |= !(id[i - 1] < my_id && ts[i - 1] <= my_ts);
+    bad |= !(prev_id < my_id && prev_ts <= my_ts);
     const int loc = (int)(i - e0);
-    if (my_ts < 0 || my_ts >= hz || te[i] > hz) bp = min(bp, loc);  // model.py:240-241
-    if (!dyn[i]) {
-      if (size[i] % align) ba = min(ba, loc);
-      if (te[i] < hz) {
-        const int a = ps[i], z = pe[i];
-        if (a >= ns || z >= ns) bp = min(bp, loc);
-        pmax = max(pmax, max(a, z));
-      }
+    if (my_ts < 0 || my_ts >= hz || my_te > hz) bp = min(bp, loc);  // model.py:240-241
+    const bool misal = pow2 ? (sz & (align - 1)) != 0 : (sz % align) != 0;
+    if (!dy && misal) ba = min(ba, loc);
+    if (!dy && my_te < hz) {
+      if (a >= ns || z >= ns) bp = min(bp, loc);
+      pmax = max(pmax, max(a, z));
     }
   }
   ba = __reduce_min_sync(FULL, ba);
@@ -134,21 +138,37 @@ __global__ void __launch_bounds__(128) k_trace_scan(
   tsmax = __reduce_max_sync(FULL, tsmax);
   pmax = __reduce_max_sync(FULL, pmax);
   const bool anybad = __any_sync(FULL, bad);
+  __shared__ int s_bad, s_ts, s_pm;
+  __shared__ long long s_lo, s_hi;
+  if (tid == 0) {
+    s_bad = 0, s_ts = 0, s_pm = 0;
+    s_lo = LLONG_MAX, s_hi = LLONG_MIN;
+  }
+  __syncthreads();
   if (lane == 0) {
     if (ba != INT_MAX) atomicMin(&s_ba, ba);
     if (bp != INT_MAX) atomicMin(&s_bp, bp);
-    if (anybad) atomicOr(flags, 1);
-    if (tsmax > 0) atomicMax(flags + 1, tsmax);
-    if (pmax > 0) atomicMax(flags + 2, pmax);
-    if (idmin != LLONG_MAX) {
-      atomicMin(mm, idmin);
-      atomicMax(mm + 1, idmax);
-    }
+    if (anybad) s_bad = 1;
+    atomicMax(&s_ts, tsmax);
+    atomicMax(&s_pm, pmax);
+    atomicMin(&s_lo, idmin);
+    atomicMax(&s_hi, idmax);
   }
   __syncthreads();
   if (tid == 0) {
     bad_align[t] = s_ba;
     bad_phase[t] = s_bp;
+    // batch-wide values: one CTA-level update each, and only when it changes the
+    // current value (thousands of CTAs would otherwise serialise on five words)
+    volatile int *vf = flags;
+    volatile long long *vm = mm;
+    if (s_bad) atomicOr(flags, 1);
+    if (s_ts > vf[1]) atomicMax(flags + 1, s_ts);
+    if (s_pm > vf[2]) atomicMax(flags + 2, s_pm);
+    if (s_lo != LLONG_MAX) {
+      if (s_lo < vm[0]) atomicMin(mm, s_lo);
+      if (s_hi > vm[1]) atomicMax(mm + 1, s_hi);
+    }
   }
 }
 
