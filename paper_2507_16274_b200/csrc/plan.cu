@@ -242,32 +242,12 @@ __global__ void k_local_key(uint64_t *__restrict__ hi, const uint64_t *__restric
 // offsets and the elements are scattered to the other shared buffer. Stable;
 // ~40 instructions per element per pass instead of the bitonic network's
 // ~log2(P)^2/2 compare-exchanges.
+// The passes of the CTA-local sort: (key, value) pairs kA/vA[0, n) in shared
+// memory, stable by key bits [bit0, bits); wh = 8 x 256 counters; sh = 33.
 template <int IPT>
-__global__ void __launch_bounds__(256) k_seg_radix(uint64_t *__restrict__ keys, uint32_t *__restrict__ perm,
-                                                   const int64_t *__restrict__ seg_off, int bit0, int bits) {
-  constexpr int P = 256 * IPT;
-  extern __shared__ __align__(16) unsigned char srx[];
-  uint64_t *kA = (uint64_t *)srx;  // one buffer: a pass holds its elements in registers
-  uint32_t *vA = (uint32_t *)(kA + P);
-  uint32_t *wh = vA + P;  // [8 warps][256 digits]
-  __shared__ uint32_t sh[33];
-  const int64_t s0 = seg_off[blockIdx.x];
-  const int n = (int)(seg_off[blockIdx.x + 1] - s0);
+__device__ __forceinline__ void cta_radix(uint64_t *kA, uint32_t *vA, uint32_t *wh, uint32_t *sh, int n, int bit0,
+                                          int bits) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  {
-    bool all = true;  // no bits to sort, or already in order: the stable result is the identity
-    if (bit0 < bits)
-      for (int i = tid; i + 1 < n; i += 256) all &= keys[s0 + i] <= keys[s0 + i + 1];
-    if (__syncthreads_and(all)) {
-      for (int i = tid; i < n; i += 256) perm[s0 + i] = (uint32_t)(s0 + i);
-      return;
-    }
-  }
-  for (int i = tid; i < n; i += 256) {
-    kA[i] = keys[s0 + i];
-    vA[i] = (uint32_t)(s0 + i);
-  }
-  __syncthreads();
   const unsigned lt = lanemask_lt();
   const int R = (n + 255) >> 8;  // rows of 32 per warp actually used (<= IPT)
   const int run = 32 * R;        // each warp owns a contiguous block of the segment
@@ -329,6 +309,35 @@ __global__ void __launch_bounds__(256) k_seg_radix(uint64_t *__restrict__ keys, 
     }
     __syncthreads();
   }
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(256) k_seg_radix(uint64_t *__restrict__ keys, uint32_t *__restrict__ perm,
+                                                   const int64_t *__restrict__ seg_off, int bit0, int bits) {
+  constexpr int P = 256 * IPT;
+  extern __shared__ __align__(16) unsigned char srx[];
+  uint64_t *kA = (uint64_t *)srx;  // one buffer: a pass holds its elements in registers
+  uint32_t *vA = (uint32_t *)(kA + P);
+  uint32_t *wh = vA + P;  // [8 warps][256 digits]
+  __shared__ uint32_t sh[33];
+  const int64_t s0 = seg_off[blockIdx.x];
+  const int n = (int)(seg_off[blockIdx.x + 1] - s0);
+  const int tid = threadIdx.x;
+  {
+    bool all = true;  // no bits to sort, or already in order: the stable result is the identity
+    if (bit0 < bits)
+      for (int i = tid; i + 1 < n; i += 256) all &= keys[s0 + i] <= keys[s0 + i + 1];
+    if (__syncthreads_and(all)) {
+      for (int i = tid; i < n; i += 256) perm[s0 + i] = (uint32_t)(s0 + i);
+      return;
+    }
+  }
+  for (int i = tid; i < n; i += 256) {
+    kA[i] = keys[s0 + i];
+    vA[i] = (uint32_t)(s0 + i);
+  }
+  __syncthreads();
+  cta_radix<IPT>(kA, vA, wh, sh, n, bit0, bits);
   for (int i = tid; i < n; i += 256) {
     keys[s0 + i] = kA[i];
     perm[s0 + i] = vA[i];
@@ -1094,6 +1103,86 @@ __global__ void __launch_bounds__(128) k_items(Plans p0, Plans p1, int want0, in
       it.ref[o] = ~(int32_t)i;
     }
     pos += tot;
+  }
+}
+
+// Phase D fused (segments of <= 4096 items, keys of <= 64 bits): one CTA per
+// (variant, trace) gathers the segment's items (alive plans in plan order,
+// then residual events in event order -- the order k_items lists them), sorts
+// (size desc, t_s, tie) keys with their source refs in shared memory
+// (cta_radix, stable) and writes the items in sorted order together with the
+// plan/event -> item maps: k_items + k_item_keys + the segmented sort +
+// k_item_permute in one pass over the data.
+template <int IPT>
+__global__ void __launch_bounds__(256) k_items_sorted(Plans p0, Plans p1, int want0, int want1,
+                                                      const int64_t *__restrict__ pl_off, Ev e,
+                                                      const int64_t *__restrict__ ev_off,
+                                                      const int32_t *__restrict__ gof, Groups g,
+                                                      const int32_t *__restrict__ pid0, const int64_t *__restrict__ io,
+                                                      int T, int64_t P, int64_t N, Items it,
+                                                      int32_t *__restrict__ item_of_plan,
+                                                      int32_t *__restrict__ item_of_res, long long maxsu, int ashift,
+                                                      long long align, int qb, int lobits, int in_order) {
+  constexpr int CAP = 256 * IPT;
+  extern __shared__ __align__(16) unsigned char sis[];
+  uint64_t *kA = (uint64_t *)sis;
+  uint32_t *vA = (uint32_t *)(kA + CAP);
+  uint32_t *wh = vA + CAP;
+  __shared__ uint32_t sh[33];
+  const int sgi = blockIdx.x, tid = threadIdx.x;
+  const int v = sgi >= T, t = sgi - v * T;
+  if (!(v ? want1 : want0)) return;
+  const Plans &pv = v ? p1 : p0;
+  auto key = [&](int64_t size, int ts, int tie) -> uint64_t {
+    const long long su = ashift >= 0 ? (size >> ashift) : size / align;
+    const uint64_t lo = in_order ? (uint64_t)(uint32_t)tie : ((uint64_t)(uint32_t)ts << qb) | (uint32_t)tie;
+    return ((uint64_t)(maxsu - su) << lobits) | lo;
+  };
+  int pos = 0;
+  for (int64_t k0 = pl_off[t]; k0 < pl_off[t + 1]; k0 += blockDim.x) {
+    const int64_t k = k0 + tid;
+    const bool alive = k < pl_off[t + 1] && pv.alive[k];
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<uint32_t>(alive ? 1u : 0u, sh, &tot);
+    if (alive) {
+      kA[pos + ex] = key(pv.h[k], pv.ts[k], pv.minq[k]);
+      vA[pos + ex] = (uint32_t)k;
+    }
+    pos += tot;
+  }
+  for (int64_t i0 = ev_off[t]; i0 < ev_off[t + 1]; i0 += blockDim.x) {
+    const int64_t i = i0 + tid;
+    const bool res = i < ev_off[t + 1] && !e.dyn[i] && pid0[i] < 0 && g.cls[gof[i]] == 1;
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<uint32_t>(res ? 1u : 0u, sh, &tot);
+    if (res) {
+      kA[pos + ex] = key(e.size[i], e.ts[i], e.q[i]);
+      vA[pos + ex] = (uint32_t)~(int32_t)i;
+    }
+    pos += tot;
+  }
+  __syncthreads();
+  const int n = pos;
+  cta_radix<IPT>(kA, vA, wh, sh, n, 0, lobits + bitlen_dev((u128)maxsu));
+  const int64_t o0 = io[sgi];
+  for (int j = tid; j < n; j += blockDim.x) {
+    const int32_t r = (int32_t)vA[j];
+    const int64_t o = o0 + j;
+    if (r >= 0) {
+      it.size[o] = pv.h[r];
+      it.ts[o] = pv.ts[r];
+      it.te[o] = pv.te[r];
+      it.tie[o] = pv.minq[r];
+      item_of_plan[(int64_t)v * P + r] = (int32_t)o;
+    } else {
+      const int64_t i = ~r;
+      it.size[o] = e.size[i];
+      it.ts[o] = e.ts[i];
+      it.te[o] = e.te[i];
+      it.tie[o] = e.q[i];
+      item_of_res[(int64_t)v * N + i] = (int32_t)o;
+    }
+    it.ref[o] = r;
   }
 }
 
@@ -2247,36 +2336,55 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     }
   const int64_t NI = io[V * T];
   int64_t *d_io = h2d(ctx, ar, io);
-  Items it0{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
-            ar.take<int32_t>(NI + 1)};
   Items it{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
            ar.take<int32_t>(NI + 1)};
   int32_t *item_of_plan = ar.take<int32_t>(V * (P + 1)), *item_of_res = ar.take<int32_t>(V * (N + 1));
   if (!ctx.ok()) return ctx.rc;
-  if (T > 0) {
-    STW_KL(k_items, (unsigned)(V * T), 128, ctx.stream, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0,
-           d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, it0);
-    STW_LAUNCHED(ctx);
-  }
-  pt.mark("D items");
   // sort items by (variant-trace, size desc, t_s, tie)
   const long long maxsu = NI ? std::max(0ll, h_imax[1]) / o->alignment : 0;
-  uint64_t *ihi = ar.take<uint64_t>(NI + 1), *ilo = ar.take<uint64_t>(NI + 1);
-  uint32_t *iperm = ar.take<uint32_t>(NI + 1);
-  if (!ctx.ok()) return ctx.rc;
   const int vtb = bitlen_u64((uint64_t)(V * T - 1)), sb = bitlen_u64((uint64_t)maxsu);
   if (vtb + sb > 64) {
     ctx.fail(STW_EARG, "item sort key exceeds 64 bits");
     return ctx.rc;
   }
   const bool in_order = him[0] == 0;
-  LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, (long long)o->alignment, maxsu, sb, in_order ? 1 : 0, ihi, ilo);
-  {
-    int64_t max_items = 0;
-    for (int64_t x = 0; x < V * T; x++) max_items = std::max(max_items, io[x + 1] - io[x]);
-    seg_sort(ctx, ar, ihi, vtb + sb, vtb, ilo, in_order ? qb : tsb + qb, iperm, NI, d_io, (int64_t)V * T, max_items);
+  const int ilobits = in_order ? qb : tsb + qb;
+  int64_t max_items = 0;
+  for (int64_t x = 0; x < V * T; x++) max_items = std::max(max_items, io[x + 1] - io[x]);
+  const long long al = o->alignment;
+  const int ashift = (al & (al - 1)) == 0 ? __builtin_ctzll((unsigned long long)al) : -1;
+  if (T > 0 && max_items <= kSegSortMax && sb + ilobits <= 64) {
+    // fused gather + sort + write (every c4 segment)
+    if (max_items <= 2048) {
+      constexpr int smem = 2048 * 12 + 8 * 256 * 4;
+      STW_KLS(k_items_sorted<8>, (unsigned)(V * T), 256, smem, ctx.stream, p0, p1, want[0] ? 1 : 0,
+              want[1] ? 1 : 0, d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, P, N, it, item_of_plan, item_of_res,
+              maxsu, ashift, al, qb, ilobits, in_order ? 1 : 0);
+    } else {
+      constexpr int smem = 4096 * 12 + 8 * 256 * 4;
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_items_sorted<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      STW_KLS(k_items_sorted<16>, (unsigned)(V * T), 256, smem, ctx.stream, p0, p1, want[0] ? 1 : 0,
+              want[1] ? 1 : 0, d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, P, N, it, item_of_plan, item_of_res,
+              maxsu, ashift, al, qb, ilobits, in_order ? 1 : 0);
+    }
+    STW_LAUNCHED(ctx);
+    pt.mark("D items");
+  } else {
+    Items it0{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
+              ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1)};
+    uint64_t *ihi = ar.take<uint64_t>(NI + 1), *ilo = ar.take<uint64_t>(NI + 1);
+    uint32_t *iperm = ar.take<uint32_t>(NI + 1);
+    if (!ctx.ok()) return ctx.rc;
+    if (T > 0) {
+      STW_KL(k_items, (unsigned)(V * T), 128, ctx.stream, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0,
+             d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, it0);
+      STW_LAUNCHED(ctx);
+    }
+    pt.mark("D items");
+    LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, al, maxsu, sb, in_order ? 1 : 0, ihi, ilo);
+    seg_sort(ctx, ar, ihi, vtb + sb, vtb, ilo, ilobits, iperm, NI, d_io, (int64_t)V * T, max_items);
+    LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
   }
-  LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
   // host-side preparation of phase E, overlapped with the D kernels: unit
   // scratch offsets and the warp-per-unit CTA packing
   std::vector<int64_t> uo(U + 1, 0);
