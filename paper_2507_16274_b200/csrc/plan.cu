@@ -1122,7 +1122,8 @@ __global__ void __launch_bounds__(256) k_items_sorted(Plans p0, Plans p1, int wa
                                                       int T, int64_t P, int64_t N, Items it,
                                                       int32_t *__restrict__ item_of_plan,
                                                       int32_t *__restrict__ item_of_res, long long maxsu, int ashift,
-                                                      long long align, int qb, int lobits, int in_order) {
+                                                      long long align, int qb, int lobits, int in_order,
+                                                      int64_t *__restrict__ cend) {
   constexpr int CAP = 256 * IPT;
   extern __shared__ __align__(16) unsigned char sis[];
   uint64_t *kA = (uint64_t *)sis;
@@ -1183,6 +1184,33 @@ __global__ void __launch_bounds__(256) k_items_sorted(Plans p0, Plans p1, int wa
       item_of_res[(int64_t)v * N + i] = (int32_t)o;
     }
     it.ref[o] = r;
+  }
+  // class ends (k_class_ends): cend[j] = the first class edge after j, an edge
+  // being the segment's last item or a change of the key's size bits. Edges go
+  // to vA (read above), then a suffix minimum: per-thread chunks + warp shuffles.
+  __syncthreads();
+  for (int j = tid; j < n; j += blockDim.x)
+    vA[j] = (j + 1 == n || lobits >= 64 || (kA[j + 1] >> lobits) != (kA[j] >> lobits)) ? (uint32_t)(j + 1)
+                                                                                       : 0xffffffffu;
+  __syncthreads();
+  const int per = (n + 255) >> 8, c0 = min(n, tid * per), c1 = min(n, c0 + per);
+  uint32_t agg = 0xffffffffu;
+  for (int j = c0; j < c1; j++) agg = min(agg, vA[j]);
+  const int w = tid >> 5, lane = tid & 31;
+  uint32_t x = agg;  // inclusive suffix minimum over the warp's lanes
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, x, d);
+    if (lane + d < 32) x = min(x, y);
+  }
+  uint32_t later = __shfl_down_sync(0xffffffffu, x, 1);
+  if (lane == 31) later = 0xffffffffu;
+  __shared__ uint32_t wmin[8];
+  if (lane == 0) wmin[w] = x;
+  __syncthreads();
+  for (int w2 = w + 1; w2 < 8; w2++) later = min(later, wmin[w2]);
+  for (int j = c1 - 1; j >= c0; j--) {
+    later = min(later, vA[j]);
+    cend[o0 + j] = o0 + later;
   }
 }
 
@@ -1860,34 +1888,39 @@ struct EmitArgs {
   int32_t *layer;   // [C * N]
 };
 
+// thread per event, every candidate in turn: the event's columns are read once
+// and the candidates' dependent lookups (item -> layer -> base) overlap
 __global__ void k_emit(EmitArgs A) {
-  GRID_STRIDE(x, (int64_t)A.C * A.N) {
-    int c = (int)(x / A.N);
-    int64_t i = x - (int64_t)c * A.N;
-    int t = A.e.tr[i];
-    int64_t u = (int64_t)t * A.C + c;
-    int v = A.var_of[c];
-    int cl = ev_class(A.e.dyn[i], A.e.te[i], A.e.horizon[t]);
-    long long ad = -1;
-    int ly = -1;
-    if (cl == 0) {
-      ad = A.rel[i];
-    } else if (cl == 1) {
-      int p = v ? A.pid1[i] : A.pid0[i];
-      int64_t j;
-      long long fr = 0;
-      if (p >= 0) {
-        j = A.item_of_plan[(int64_t)v * A.P + p];
-        fr = v ? A.frel1[i] : A.rel[i];
-      } else {
-        j = A.item_of_res[(int64_t)v * A.N + i];
+  GRID_STRIDE(i, A.N) {
+    const int t = A.e.tr[i];
+    const int cl = ev_class(A.e.dyn[i], A.e.te[i], A.e.horizon[t]);
+    const int64_t rel = cl == 2 ? 0 : A.rel[i];
+    const int p0 = cl == 1 ? A.pid0[i] : -1;
+    const int p1 = cl == 1 && A.pid1 ? A.pid1[i] : -1;
+    for (int c = 0; c < A.C; c++) {
+      const int64_t u = (int64_t)t * A.C + c;
+      const int v = A.var_of[c];
+      long long ad = -1;
+      int ly = -1;
+      if (cl == 0) {
+        ad = rel;
+      } else if (cl == 1) {
+        const int p = v ? p1 : p0;
+        int64_t j;
+        long long fr = 0;
+        if (p >= 0) {
+          j = A.item_of_plan[(int64_t)v * A.P + p];
+          fr = v ? A.frel1[i] : rel;
+        } else {
+          j = A.item_of_res[(int64_t)v * A.N + i];
+        }
+        const int64_t local = j - A.io[(int64_t)v * A.T + t];
+        ly = A.ilayer[A.uo[u] + local];
+        ad = A.lbase[A.uo[u] + ly] + fr;
       }
-      int64_t local = j - A.io[(int64_t)v * A.T + t];
-      ly = A.ilayer[A.uo[u] + local];
-      ad = A.lbase[A.uo[u] + ly] + fr;
+      A.addr[(int64_t)c * A.N + i] = ad;
+      A.layer[(int64_t)c * A.N + i] = ly;
     }
-    A.addr[x] = ad;
-    A.layer[x] = ly;
   }
 }
 
@@ -2353,19 +2386,22 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   for (int64_t x = 0; x < V * T; x++) max_items = std::max(max_items, io[x + 1] - io[x]);
   const long long al = o->alignment;
   const int ashift = (al & (al - 1)) == 0 ? __builtin_ctzll((unsigned long long)al) : -1;
-  if (T > 0 && max_items <= kSegSortMax && sb + ilobits <= 64) {
+  int64_t *cend = ar.take<int64_t>(NI + 1);
+  if (!ctx.ok()) return ctx.rc;
+  const bool fused_items = T > 0 && max_items <= kSegSortMax && sb + ilobits <= 64;
+  if (fused_items) {
     // fused gather + sort + write (every c4 segment)
     if (max_items <= 2048) {
       constexpr int smem = 2048 * 12 + 8 * 256 * 4;
       STW_KLS(k_items_sorted<8>, (unsigned)(V * T), 256, smem, ctx.stream, p0, p1, want[0] ? 1 : 0,
               want[1] ? 1 : 0, d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, P, N, it, item_of_plan, item_of_res,
-              maxsu, ashift, al, qb, ilobits, in_order ? 1 : 0);
+              maxsu, ashift, al, qb, ilobits, in_order ? 1 : 0, cend);
     } else {
       constexpr int smem = 4096 * 12 + 8 * 256 * 4;
       STW_CUDA(ctx, cudaFuncSetAttribute(k_items_sorted<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       STW_KLS(k_items_sorted<16>, (unsigned)(V * T), 256, smem, ctx.stream, p0, p1, want[0] ? 1 : 0,
               want[1] ? 1 : 0, d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, P, N, it, item_of_plan, item_of_res,
-              maxsu, ashift, al, qb, ilobits, in_order ? 1 : 0);
+              maxsu, ashift, al, qb, ilobits, in_order ? 1 : 0, cend);
     }
     STW_LAUNCHED(ctx);
     pt.mark("D items");
@@ -2449,10 +2485,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     }
   }
   pt.mark("D sort");
-  // classes
-  int64_t *cend = ar.take<int64_t>(NI + 1);
-  if (!ctx.ok()) return ctx.rc;
-  if (V * T > 0) {
+  // classes (written by k_items_sorted on the fused path)
+  if (V * T > 0 && !fused_items) {
     STW_KL(k_class_ends, grid_for((int64_t)V * T * 32, 256), 256, ctx.stream, it, d_io, V * T, cend);
     STW_LAUNCHED(ctx);
   }
@@ -2536,7 +2570,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   EmitArgs EA{C, T, N, P, d_var, e, rel, frel1, pid0, pid1, item_of_plan, item_of_res, d_io, d_uo,
               LA.ilayer, LA.lbase, addr, layer};
-  LAUNCH(k_emit, (int64_t)C * N, EA);
+  LAUNCH(k_emit, N, EA);
 
   pt.mark("F emit");
   // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
