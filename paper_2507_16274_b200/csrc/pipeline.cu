@@ -11,7 +11,8 @@
 
 namespace stw {
 
-int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror);
+int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror,
+               void (*after_uploads)(void *), void *hook_arg);
 
 namespace {
 
@@ -103,7 +104,6 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
       Slot &s = sl[k & 1];
       const stw_batch &b = in[k];
       const int64_t N = b.n_events, T = b.n_traces;
-      if (k >= 2) STW_CUDA(cctx, cudaStreamWaitEvent(cs, s.d2h, 0));  // slot's previous results are out
       h2d(cctx, s.ev_off, b.ev_off, T + 1, cs);
       h2d(cctx, s.id, b.id, N, cs);
       h2d(cctx, s.size, b.size, N, cs);
@@ -116,26 +116,8 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
       h2d(cctx, s.n_sched, b.n_sched, T, cs);
       STW_CUDA(cctx, cudaEventRecord(s.h2d, cs));
     };
-    stage(0);
-    for (int k = 0; k < n && ctx.ok() && cctx.ok(); k++) {
+    auto download = [&](int k) {  // batch k's results, once it is planned
       Slot &s = sl[k & 1];
-      if (k + 1 < n) stage(k + 1);  // overlaps this batch's planning
-      STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, s.h2d, 0));
-      stw_batch db = in[k];
-      db.on_device = 1;
-      db.ev_off = s.ev_off;
-      db.id = s.id;
-      db.size = s.size;
-      db.t_s = s.t_s;
-      db.t_e = s.t_e;
-      db.ps = s.ps;
-      db.pe = s.pe;
-      db.dyn = s.dyn;
-      db.horizon = s.horizon;
-      db.n_sched = s.n_sched;
-      plan_batch(ctx, &db, o, &s.dout, &in[k]);
-      if (!ctx.ok()) break;
-      STW_CUDA(ctx, cudaEventRecord(s.planned, ctx.stream));
       STW_CUDA(cctx, cudaStreamWaitEvent(cs, s.planned, 0));
       const int64_t N = in[k].n_events, T = in[k].n_traces, U = T * C;
       const stw_plan_out &h = out[k];
@@ -153,7 +135,50 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
       d2h(cctx, h.addr_best, s.dout.addr_best, N, cs);
       d2h(cctx, h.best_pool, s.dout.best_pool, T, cs);
       STW_CUDA(cctx, cudaEventRecord(s.d2h, cs));
+    };
+    // Batch k+1's upload and batch k-1's download are issued from inside batch
+    // k's planning, once its last host->device transfer is done (after phase E):
+    // the planner's own small round trips then never queue behind them, and
+    // both overlap the rest of batch k.
+    struct Hook {
+      int k, n;
+      decltype(stage) *st;
+      decltype(download) *dl;
+      bool ran;
+      static void run(void *p) {
+        Hook *h = (Hook *)p;
+        h->ran = true;
+        if (h->k + 1 < h->n) (*h->st)(h->k + 1);
+        if (h->k >= 1) (*h->dl)(h->k - 1);
+      }
+    };
+    stage(0);
+    int done = 0;  // batches whose download was issued
+    for (int k = 0; k < n && ctx.ok() && cctx.ok(); k++) {
+      Slot &s = sl[k & 1];
+      STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, s.h2d, 0));
+      if (k >= 2) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, s.d2h, 0));  // the slot's results are out
+      stw_batch db = in[k];
+      db.on_device = 1;
+      db.ev_off = s.ev_off;
+      db.id = s.id;
+      db.size = s.size;
+      db.t_s = s.t_s;
+      db.t_e = s.t_e;
+      db.ps = s.ps;
+      db.pe = s.pe;
+      db.dyn = s.dyn;
+      db.horizon = s.horizon;
+      db.n_sched = s.n_sched;
+      Hook hk{k, n, &stage, &download, false};
+      plan_batch(ctx, &db, o, &s.dout, &in[k], &Hook::run, &hk);
+      if (!ctx.ok()) break;
+      if (!hk.ran) Hook::run(&hk);  // a batch that returned before phase E (no traces)
+      STW_CUDA(ctx, cudaEventRecord(s.planned, ctx.stream));
+      done = k;  // downloads of batches < k were issued by the hook
     }
+    if (ctx.ok() && cctx.ok())
+      for (int k = done; k < n; k++) download(k);
     STW_CUDA(cctx, cudaStreamSynchronize(cs));
     // the arena frees on the compute stream: order it after the copy stream's last use
     STW_CUDA(ctx, cudaEventRecord(ready, cs));

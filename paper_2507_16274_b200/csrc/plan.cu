@@ -172,6 +172,21 @@ __global__ void __launch_bounds__(128) k_trace_scan(
   }
 }
 
+// off[0..n] = exclusive prefix sums of cnt[0..n) (int64), one CTA
+__global__ void __launch_bounds__(1024) k_offsets_i32(const int *__restrict__ cnt, int n, int64_t *__restrict__ off) {
+  __shared__ long long sh[33];
+  long long carry = 0;
+  for (int b = 0; b < n; b += blockDim.x) {
+    const int i = b + threadIdx.x;
+    const long long v = i < n ? cnt[i] : 0;
+    long long tot;
+    const long long ex = block_excl_sum<long long>(v, sh, &tot);
+    if (i < n) off[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[n] = carry;
+}
+
 __global__ void k_minmax_i64(const int64_t *__restrict__ v, int64_t n, long long *mn, long long *mx) {
   __shared__ long long sh[33];
   long long lo = LLONG_MAX, hi = LLONG_MIN;
@@ -2173,7 +2188,8 @@ struct PhaseTimer {
   }
 };
 
-int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror) {
+int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror,
+               void (*after_uploads)(void *), void *hook_arg) {
   PhaseTimer pt(ctx);
   Arena ar(&ctx);
   DevBatch b;
@@ -2564,6 +2580,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
 
   pt.mark("E layers");
+  // the call's last host->device transfer is behind us: a pipelining caller
+  // starts streaming its next batch in now, so it does not contend with them
+  if (after_uploads) after_uploads(hook_arg);
   // ---- F: emission
   int64_t *addr = ar.take<int64_t>((int64_t)C * N + 1);
   int32_t *layer = ar.take<int32_t>((int64_t)C * N + 1);
@@ -2584,7 +2603,10 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   std::vector<int64_t> so(T + 1, 0);
   for (int t = 0; t < T; t++) so[t + 1] = so[t] + h_nstatic[t];
   const int64_t NS = so[T];
-  int64_t *d_so = h2d(ctx, ar, so);
+  int64_t *d_so = ar.take<int64_t>(T + 1);  // the same offsets, made on the device (no upload)
+  if (!ctx.ok()) return ctx.rc;
+  STW_KL(k_offsets_i32, 1, 1024, ctx.stream, tc.n_static, T, d_so);
+  STW_LAUNCHED(ctx);
   int32_t *rs_ev = ar.take<int32_t>(NS + 1), *rts = ar.take<int32_t>(NS + 1), *rte = ar.take<int32_t>(NS + 1);
   int64_t *rsz = ar.take<int64_t>(NS + 1), *raddr = ar.take<int64_t>((int64_t)C * NS + 1);
   long long *vcount = ar.take<long long>(U);
