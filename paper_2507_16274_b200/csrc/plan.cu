@@ -172,6 +172,22 @@ __global__ void __launch_bounds__(128) k_trace_scan(
   }
 }
 
+// off[0..n] = exclusive prefix sums of cnt[0..n) (uint32), one CTA
+__global__ void __launch_bounds__(1024) k_offsets_u32(const uint32_t *__restrict__ cnt, int n,
+                                                      uint32_t *__restrict__ off) {
+  __shared__ uint32_t sh[33];
+  uint32_t carry = 0;
+  for (int b = 0; b < n; b += blockDim.x) {
+    const int i = b + threadIdx.x;
+    const uint32_t v = i < n ? cnt[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<uint32_t>(v, sh, &tot);
+    if (i < n) off[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[n] = carry;
+}
+
 // off[0..n] = exclusive prefix sums of cnt[0..n) (int64), one CTA
 __global__ void __launch_bounds__(1024) k_offsets_i32(const int *__restrict__ cnt, int n, int64_t *__restrict__ off) {
   __shared__ long long sh[33];
@@ -487,11 +503,78 @@ struct Groups {
   int64_t *height;
 };
 
+// Phase B fused (traces of <= 4096 events): one CTA per trace sorts the
+// trace's events by (class, p_s, p_e, r) in shared memory (k_key_group + the
+// segmented sort), then marks group heads and makes the trace-local group ids
+// (inclusive count of heads) and size prefix sums S (exclusive; only
+// differences inside a group are used) by chunked block scans -- k_group_heads
+// and the two global scans. Group ids become global in k_group_table (+ the
+// trace's offset from the group counts written here).
+template <int IPT>
+__global__ void __launch_bounds__(256) k_groups_fused(Ev e, const int64_t *__restrict__ ev_off,
+                                                      const int32_t *__restrict__ r, int pb, int qb, int bit0,
+                                                      uint32_t *__restrict__ gperm, uint32_t *__restrict__ head,
+                                                      uint32_t *__restrict__ lgid, int64_t *__restrict__ szs,
+                                                      int64_t *__restrict__ S, uint32_t *__restrict__ ngroups) {
+  constexpr int CAP = 256 * IPT;
+  extern __shared__ __align__(16) unsigned char sgs[];
+  uint64_t *kA = (uint64_t *)sgs;
+  uint32_t *vA = (uint32_t *)(kA + CAP);
+  uint32_t *wh = vA + CAP;
+  __shared__ uint32_t sh[33];
+  __shared__ long long shl[33];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int64_t g0 = ev_off[t];
+  const int n = (int)(ev_off[t + 1] - g0);
+  const int hz = e.horizon[t];
+  for (int j = tid; j < n; j += blockDim.x) {
+    const int64_t i = g0 + j;
+    const int c = ev_class(e.dyn[i], e.te[i], hz);
+    const uint64_t a = c == 1 ? (uint32_t)e.ps[i] : 0, b = c == 1 ? (uint32_t)e.pe[i] : 0;
+    kA[j] = ((((uint64_t)c << (2 * pb)) | (a << pb) | b) << qb) | (uint32_t)r[i];
+    vA[j] = (uint32_t)j;
+  }
+  __syncthreads();
+  cta_radix<IPT>(kA, vA, wh, sh, n, bit0, qb + 2 + 2 * pb);
+  // chunked scans: thread tid owns sorted positions [c0, c1)
+  const int per = (n + 255) >> 8, c0 = min(n, tid * per), c1 = min(n, c0 + per);
+  uint32_t hm = 0, nh = 0;  // head bits of the chunk (per <= 16)
+  long long ssum = 0;
+  for (int k = c0; k < c1; k++) {
+    const bool h = k == 0 || (kA[k] >> qb) != (kA[k - 1] >> qb);
+    hm |= (h ? 1u : 0u) << (k - c0);
+    nh += h;
+    const int64_t i = g0 + vA[k];
+    const long long sz = e.size[i];
+    szs[g0 + k] = sz;
+    gperm[g0 + k] = (uint32_t)i;
+    ssum += sz;
+  }
+  uint32_t htot;
+  const uint32_t hex = block_excl_sum<uint32_t>(nh, sh, &htot);
+  const long long sex = block_excl_sum<long long>(ssum, shl, nullptr);
+  uint32_t gcount = hex;
+  long long run = sex;
+  for (int k = c0; k < c1; k++) {
+    const bool h = (hm >> (k - c0)) & 1u;
+    gcount += h;
+    head[g0 + k] = h;
+    lgid[g0 + k] = gcount;
+    S[g0 + k] = run;
+    run += szs[g0 + k];
+  }
+  if (tid == 0) ngroups[t] = htot;
+}
+
+// goff (optional): per-trace group offsets when gid holds trace-local ids
+// (k_groups_fused); gid is rewritten to the global inclusive id
 __global__ void k_group_table(Ev e, const uint32_t *__restrict__ gperm, const uint32_t *__restrict__ head,
-                              const uint32_t *__restrict__ gid_incl, int64_t n, Groups g) {
+                              uint32_t *__restrict__ gid_incl, const uint32_t *__restrict__ goff, int64_t n,
+                              Groups g) {
   GRID_STRIDE(k, n) {
-    if (!head[k]) continue;
     uint32_t i = gperm[k];
+    if (goff) gid_incl[k] += goff[e.tr[i]];
+    if (!head[k]) continue;
     int gi = (int)gid_incl[k] - 1;
     int c, a, b;
     group_key(e, i, &c, &a, &b);
@@ -505,8 +588,9 @@ __global__ void k_group_table(Ev e, const uint32_t *__restrict__ gperm, const ui
 
 __global__ void k_group_rel(const uint32_t *__restrict__ gperm, const uint32_t *__restrict__ gid_incl,
                             const int64_t *__restrict__ S, const int64_t *__restrict__ szs, Groups g,
-                            int64_t n, int64_t *__restrict__ rel, int32_t *__restrict__ gof) {
-  const int G = (int)gid_incl[n - 1];  // number of groups
+                            int64_t n, const uint32_t *__restrict__ Gp, int64_t *__restrict__ rel,
+                            int32_t *__restrict__ gof) {
+  const int G = (int)*Gp;  // number of groups
   GRID_STRIDE(k, n) {
     int gi = (int)gid_incl[k] - 1;
     uint32_t i = gperm[k];
@@ -2260,26 +2344,47 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   pt.mark("A checks");
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
-  LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
-  seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events,
-           /*lo_in_order=*/him[0] == 0);
   uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
   int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
   int64_t *rel = ar.take<int64_t>(N + 1);
   int32_t *gof = ar.take<int32_t>(N + 1);
+  uint32_t *ngroups = ar.take<uint32_t>(T + 1), *goff = ar.take<uint32_t>(T + 1);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_group_heads, N, e, gperm, b.ev_off, N, head, szs);
-  device_scan<uint32_t>(ctx, ar, head, gid, N, true);
-  device_scan<int64_t>(ctx, ar, szs, S, N, false);
   // the group count stays on the device (G <= N): tables are sized by N and
-  // the group kernels read G = gid[N-1] themselves
+  // the group kernels read G themselves
+  const uint32_t *d_G = nullptr;
+  const bool fused_groups = T > 0 && b.max_trace_events <= kSegSortMax && qb + 2 + 2 * pb <= 64;
+  if (fused_groups) {
+    const int gbit0 = him[0] == 0 ? qb : 0;  // recorded order: r is the position, already in order
+    if (b.max_trace_events <= 2048) {
+      constexpr int smem = 2048 * 12 + 8 * 256 * 4;
+      STW_KLS(k_groups_fused<8>, (unsigned)T, 256, smem, ctx.stream, e, b.ev_off, r, pb, qb, gbit0, gperm, head,
+              gid, szs, S, ngroups);
+    } else {
+      constexpr int smem = 4096 * 12 + 8 * 256 * 4;
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_groups_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      STW_KLS(k_groups_fused<16>, (unsigned)T, 256, smem, ctx.stream, e, b.ev_off, r, pb, qb, gbit0, gperm, head,
+              gid, szs, S, ngroups);
+    }
+    STW_LAUNCHED(ctx);
+    STW_KL(k_offsets_u32, 1, 1024, ctx.stream, ngroups, T, goff);
+    STW_LAUNCHED(ctx);
+    d_G = goff + T;
+  } else {
+    LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
+    seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events,
+             /*lo_in_order=*/him[0] == 0);
+    LAUNCH(k_group_heads, N, e, gperm, b.ev_off, N, head, szs);
+    device_scan<uint32_t>(ctx, ar, head, gid, N, true);
+    device_scan<int64_t>(ctx, ar, szs, S, N, false);
+    d_G = gid + (N > 0 ? N - 1 : 0);
+  }
   const int G = (int)N;  // capacity
-  const uint32_t *d_G = gid + (N > 0 ? N - 1 : 0);
   Groups g{ar.take<int64_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1),
            ar.take<int32_t>(G + 1), ar.take<int64_t>(G + 1)};
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_group_table, N, e, gperm, head, gid, N, g);
-  LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, N, rel, gof);
+  LAUNCH(k_group_table, N, e, gperm, head, gid, fused_groups ? goff : nullptr, N, g);
+  LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, N, d_G, rel, gof);
   // per-trace counters and the plan flags in one zeroed block
   const size_t tc_bytes = (size_t)T * (5 * sizeof(int) + sizeof(int64_t)) + (size_t)(G + 1) * sizeof(uint32_t);
   char *tcb = ar.take<char>(tc_bytes + 64);
