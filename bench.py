@@ -132,10 +132,14 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # the sampler is live before the timed region starts
+            while not self.lines and time.time() - t0 < 5 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.first = len(self.lines)  # samples from here on fall inside the region
         except OSError:
             self.proc = None
         return self
@@ -146,13 +150,17 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc:
+            t0 = time.time()  # one sample at (or just after) the end of the region
+            n = len(self.lines)
+            while len(self.lines) == n and time.time() - t0 < 1 and self.proc.poll() is None:
+                time.sleep(0.002)
             self.proc.terminate()
             self.proc.wait()
 
     def summary(self):
         sm, mx, reasons = [], 0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "first", 0):]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -488,13 +496,13 @@ def main():
             prof = _lib.profile_collect(reset=True)
         return total / 1e3, launches, prof
 
-    with ClockSampler(local) as clk:
-        t_dev, launches, prof = timed(step_device, args.steps, True)
-    t_plain, _, _ = timed(step_device, args.steps, False)  # unprofiled timing is the headline
     step_e2e()  # warm-up of the host-buffer path (its input staging grows the memory pool once)
-    t_e2e_serial, _, _ = timed(step_e2e, args.steps, False)
     e2e_pipelined(2)  # warm-up of the pipelined path
-    t_e2e = e2e_pipelined(args.steps)
+    with ClockSampler(local) as clk:  # clocks sampled (every 20 ms) across all the timed regions
+        t_dev, launches, prof = timed(step_device, args.steps, True)
+        t_plain, _, _ = timed(step_device, args.steps, False)  # unprofiled timing is the headline
+        t_e2e_serial, _, _ = timed(step_e2e, args.steps, False)
+        t_e2e = e2e_pipelined(args.steps)
 
     def max_all(x):
         if world == 1:
