@@ -260,7 +260,7 @@ constexpr int kOvWarps = 8;
 constexpr int kOvCap = 320;
 constexpr int64_t kOvMaxSerial = 1 << 16;
 
-__global__ void __launch_bounds__(kOvWarps * 32) k_overlap_sweep(RectSets rs, int shift, int *__restrict__ nflag) {
+__global__ void __launch_bounds__(kOvWarps * 32, 5) k_overlap_sweep(RectSets rs, int shift, int *__restrict__ nflag) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ int4 act[kOvWarps][kOvCap];
   __shared__ int4 tile[kOvWarps][32];
