@@ -2543,39 +2543,53 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     LAUNCH(k_item_permute, NI, it0, it, iperm, NI, d_io, T, P, N, item_of_plan, item_of_res);
   }
   // host-side preparation of phase E, overlapped with the D kernels: unit
-  // scratch offsets and the warp-per-unit CTA packing
+  // scratch offsets and the warp-per-unit CTA packing (flat per-unit arrays:
+  // this runs while the GPU sorts the items and must finish before it does)
   std::vector<int64_t> uo(U + 1, 0);
-  for (int t = 0; t < T; t++)
-    for (int c = 0; c < C; c++) {
-      int v = var_of[c];
-      int64_t u = (int64_t)t * C + c;
-      uo[u + 1] = uo[u] + (io[(int64_t)v * T + t + 1] - io[(int64_t)v * T + t]);
+  std::vector<int32_t> ucnt(U), uneed(U);
+  {
+    std::vector<uint8_t> gapc(C);
+    for (int c = 0; c < C; c++) gapc[c] = (hcand[c] & STW_CAND_GAP) ? 1 : 0;
+    int64_t acc = 0;
+    for (int t = 0, u = 0; t < T; t++) {
+      const int wn = warpn_smem_ints(std::max(0, b.h_horizon[t]));
+      for (int c = 0; c < C; c++, u++) {
+        const int v = var_of[c];
+        const int64_t n_u = io[(int64_t)v * T + t + 1] - io[(int64_t)v * T + t];
+        ucnt[u] = (int32_t)std::min<int64_t>(n_u, INT_MAX);
+        uneed[u] = gapc[c] ? wn : 0;
+        acc += n_u;
+        uo[u + 1] = acc;
+      }
     }
+  }
+  pt.mark("D host uo");
   // narrow units: one warp each, packed into fixed-budget CTAs (largest unit
   // first, then the smallest ones that still fit); units too large for a
   // CTA's budget, and any unit that needs > 32 layers, go to the CTA kernel
   std::vector<int32_t> order, bigs;
   order.reserve(U);
-  // shared-memory need per unit: units without gap insertion use none
-  auto need = [&](int32_t u) {
-    return (hcand[u % C] & STW_CAND_GAP) ? warpn_smem_ints(std::max(0, b.h_horizon[u / C])) : 0;
-  };
-  for (int64_t u = 0; u < U; u++) {
-    if (need((int32_t)u) <= kLayerSmemInts && uo[u + 1] - uo[u] < INT_MAX / 8 && b.h_horizon[u / C] < (1 << 26))
-      order.push_back((int32_t)u);
-    else
-      bigs.push_back((int32_t)u);
+  for (int t = 0, u = 0; t < T; t++) {
+    const bool longh = b.h_horizon[t] >= (1 << 26);
+    for (int c = 0; c < C; c++, u++) {
+      if (uneed[u] <= kLayerSmemInts && ucnt[u] < INT_MAX / 8 && !longh)
+        order.push_back(u);
+      else
+        bigs.push_back(u);
+    }
   }
+  pt.mark("D host order");
   {  // stable counting sort by item count, descending
-    int64_t mx = 0;
-    for (int32_t u : order) mx = std::max(mx, uo[u + 1] - uo[u]);
-    std::vector<int64_t> pos(mx + 2, 0);
-    for (int32_t u : order) pos[mx - (uo[u + 1] - uo[u]) + 1]++;
-    for (int64_t k = 0; k <= mx; k++) pos[k + 1] += pos[k];
+    int32_t mx = 0;
+    for (int32_t u : order) mx = std::max(mx, ucnt[u]);
+    std::vector<int32_t> pos(mx + 2, 0);
+    for (int32_t u : order) pos[mx - ucnt[u] + 1]++;
+    for (int32_t k = 0; k <= mx; k++) pos[k + 1] += pos[k];
     std::vector<int32_t> sorted(order.size());
-    for (int32_t u : order) sorted[pos[mx - (uo[u + 1] - uo[u])]++] = u;
+    for (int32_t u : order) sorted[pos[mx - ucnt[u]]++] = u;
     order.swap(sorted);
   }
+  pt.mark("D host csort");
   // gap units: CTAs packed to the shared-memory budget; non-gap units need no
   // shared memory and go eight to a CTA in a second launch (dynamic smem 0),
   // which runs concurrently on a side stream
@@ -2583,27 +2597,30 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   {
     std::vector<int32_t> og;
     og.reserve(order.size());
+    wslot_ng.reserve(order.size() + kWarpsPerCta);
     for (int32_t u : order) {
-      if (need(u) > 0)
+      if (uneed[u] > 0)
         og.push_back(u);
       else
         wslot_ng.push_back(make_int2(u, 0));
     }
     while (wslot_ng.size() % kWarpsPerCta) wslot_ng.push_back(make_int2(-1, 0));
-    wslot.reserve(og.size() + kWarpsPerCta);
+    wslot.resize(og.size() * kWarpsPerCta + kWarpsPerCta);  // upper bound: one unit per CTA
+    size_t ws = 0;
     for (size_t i = 0, j = og.size(); i < j;) {
-      const size_t base = wslot.size();
+      const size_t base = ws;
       int used = 0, k = 0;
       auto put = [&](int32_t u) {
-        wslot.push_back(make_int2(u, used));
-        used += need(u);
+        wslot[ws++] = make_int2(u, used);
+        used += uneed[u];
         k++;
       };
       put(og[i++]);
-      while (k < kWarpsPerCta && i < j && used + need(og[i]) <= kLayerSmemInts) put(og[i++]);
-      while (k < kWarpsPerCta && i < j && used + need(og[j - 1]) <= kLayerSmemInts) put(og[--j]);
-      while (wslot.size() < base + kWarpsPerCta) wslot.push_back(make_int2(-1, 0));
+      while (k < kWarpsPerCta && i < j && used + uneed[og[i]] <= kLayerSmemInts) put(og[i++]);
+      while (k < kWarpsPerCta && i < j && used + uneed[og[j - 1]] <= kLayerSmemInts) put(og[--j]);
+      while (ws < base + kWarpsPerCta) wslot[ws++] = make_int2(-1, 0);
     }
+    wslot.resize(ws);
   }
   pt.mark("D sort");
   // classes (written by k_items_sorted on the fused path)
@@ -2657,7 +2674,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       STW_KL(k_layers, (unsigned)bigs.size(), kPlanThreads, ctx.stream, LA, d_bigs, (const int *)nullptr);
       STW_LAUNCHED(ctx);
     }
-    if (nctas) {  // units that overflowed 32 layers (the kernel reads the count on the device)
+    if (nctas || nctas_ng) {  // units of either launch that overflowed 32 layers (count read on the device)
       STW_KL(k_layers, 296, kPlanThreads, ctx.stream, LA, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }

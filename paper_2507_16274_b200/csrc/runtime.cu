@@ -128,8 +128,10 @@ static void raise_pool_threshold() {
 }
 
 // Scratch is bump-allocated (256 B aligned) from stream-ordered chunks of at
-// least 32 MiB, so a planner call costs a handful of cudaMallocAsync calls
+// least 256 MiB, so a planner call costs a handful of cudaMallocAsync calls
 // instead of one per buffer.
+constexpr size_t kArenaChunk = (size_t)256 << 20;
+
 void *Arena::raw(size_t bytes) {
   if (!ctx->ok()) return nullptr;
   const size_t need = ((bytes ? bytes : 16) + 255) & ~(size_t)255;
@@ -139,7 +141,9 @@ void *Arena::raw(size_t bytes) {
       return nullptr;
     }
     raise_pool_threshold();
-    const size_t chunk = need > (32u << 20) ? need : (32u << 20);
+    // large chunks: one planner call takes a few (each cudaMallocAsync is host
+    // time the GPU may wait on); the pool keeps them cached between calls
+    const size_t chunk = need > kArenaChunk ? need : kArenaChunk;
     void *p = nullptr;
     STW_CUDA(*ctx, cudaMallocAsync(&p, chunk, ctx->stream));
     if (!ctx->ok()) return nullptr;

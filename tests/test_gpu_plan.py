@@ -107,6 +107,10 @@ def test_plan_many_layers_overflow_paths():
     tas.append(_manual_trace(specs, [("F:0", 0, 3000)]))
     check_batch(tas)
     check_batch(tas[2:])
+    # without gap insertion every narrow unit runs in the zero-smem launch: its
+    # > 32-layer units must still reach the CTA kernel
+    check_batch(tas, ((True, False), (False, False)))
+    check_batch(tas[:1], ((False, False),))
 
 
 def test_plan_batches_pipeline_matches_single_calls():
