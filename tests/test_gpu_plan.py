@@ -148,3 +148,34 @@ def test_plan_invariant_to_event_listing_order():
             ma = dict(zip(ta.id.tolist(), a.addr[c, sa:sa + n].tolist()))
             mb = dict(zip(tb.id.tolist(), b.addr[c, sb:sb + n].tolist()))
             assert ma == mb, (t, c)
+
+
+@pytest.mark.parametrize("cands", [((True, True),), ((False, True),), ((True, False),), ((False, False),),
+                                   ((False, True), (True, False)), CANDS])
+def test_plan_edge_traces_and_candidate_subsets(cands):
+    """Empty, single-event, persistent-only and cross-phase-only traces mixed into
+    one batch with regular ones, under every candidate subset (each subset takes
+    different launch paths: fusion on/off, gap/zero-smem layer launches)."""
+    tas = [_manual_trace([], [("F:0", 0, 10)]),
+           _manual_trace([(5, 1024, 2, 3, "F:0", "F:0")], [("F:0", 0, 10)]),
+           _manual_trace([(i, 512 * (1 + i % 3), i, 40, "F:0", "B:0") for i in range(20)],
+                         [("F:0", 0, 20), ("B:0", 20, 40)]),
+           _manual_trace([(i, 512 * (1 + i % 2), i, 25 + i, "F:0", "B:0") for i in range(12)],
+                         [("F:0", 0, 20), ("B:0", 20, 40)])]
+    tas += [tracegen.synth_arrays(fuzz_cfg(s)) for s in (3, 11)]
+    tas.insert(3, _manual_trace([], [("F:0", 0, 4)]))
+    check_batch(tas, cands)
+
+
+def test_plan_batches_with_empty_and_tiny_batches():
+    """The pipelined call over batches of all-empty traces, one event, and a
+    regular batch gives each batch's single-call result."""
+    groups = [[_manual_trace([], [("F:0", 0, 10)]), _manual_trace([], [("F:0", 0, 3)])],
+              [_manual_trace([(5, 1024, 2, 3, "F:0", "F:0")], [("F:0", 0, 10)])],
+              [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(3)],
+              [_manual_trace([], [("F:0", 0, 10)])]]
+    many = api.plan_batches(groups, CANDS, select_best=True)
+    for g, got in zip(groups, many):
+        want = api.plan_batch(g, CANDS, select_best=True)
+        for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
+            assert np.array_equal(getattr(got, f), getattr(want, f)), f
