@@ -112,7 +112,10 @@ struct PeakPending {
 };
 // shift: timeline entries count bytes in units of 2^shift (traces whose sizes
 // are not multiples fall back to the global-timeline path)
-PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak, int shift);
+// pinned: upload the CTA packing through the pinned scratch (h2d_async; the
+// caller ends with host_sync) instead of a copy-engine transfer
+PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak, int shift,
+                             bool pinned = false);
 void peak_live_finish(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
                       const PeakPending &pp);
 

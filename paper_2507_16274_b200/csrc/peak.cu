@@ -183,7 +183,7 @@ void peak_live_finish(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, 
 }
 
 PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static_only, int64_t *d_peak,
-                             int shift) {
+                             int shift, bool pinned) {
   PeakPending pp{};
   if (!ctx.ok() || b.T == 0) return pp;
   const int T = b.T;
@@ -231,14 +231,22 @@ PeakPending peak_live_launch(Ctx &ctx, Arena &ar, const DevBatch &b, bool static
   int2 *d_wslot = nctas ? ar.take<int2>(wslot.size()) : nullptr;
   if (!ctx.ok()) return pp;
   if (!longh.empty()) {  // long horizons go straight to the global path
-    STW_CUDA(ctx, cudaMemcpyAsync(big, longh.data(), longh.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
-                                  ctx.stream));
     const int nl = (int)longh.size();
-    STW_CUDA(ctx, cudaMemcpyAsync(nbig, &nl, sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
+    if (pinned) {
+      h2d_async(ctx, big, longh.data(), longh.size() * sizeof(int32_t));
+      h2d_async(ctx, nbig, &nl, sizeof(int));
+    } else {
+      STW_CUDA(ctx, cudaMemcpyAsync(big, longh.data(), longh.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                    ctx.stream));
+      STW_CUDA(ctx, cudaMemcpyAsync(nbig, &nl, sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
+    }
   }
   if (nctas) {
-    STW_CUDA(ctx, cudaMemcpyAsync(d_wslot, wslot.data(), wslot.size() * sizeof(int2), cudaMemcpyHostToDevice,
-                                  ctx.stream));
+    if (pinned)
+      h2d_async(ctx, d_wslot, wslot.data(), wslot.size() * sizeof(int2));
+    else
+      STW_CUDA(ctx, cudaMemcpyAsync(d_wslot, wslot.data(), wslot.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                    ctx.stream));
     STW_CUDA(ctx, cudaFuncSetAttribute(k_peak_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kPeakSmem));
     STW_KLS(k_peak_warp, (unsigned)nctas, kPeakWarps * 32, kPeakSmem, ctx.stream, b.ev_off, b.size, b.t_s, b.t_e,
             b.dyn, b.horizon, static_only ? 1 : 0, shift, d_wslot, (long long *)d_peak, nbig, big);

@@ -2717,7 +2717,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
   int64_t *peak = ar.take<int64_t>(T);
   if (!ctx.ok()) return ctx.rc;
-  const PeakPending ppk = peak_live_launch(ctx, ar, b, true, peak, __builtin_ctzll((unsigned long long)o->alignment));  // finished at the finalize round trip
+  // finished at the finalize round trip
+  const PeakPending ppk =
+      peak_live_launch(ctx, ar, b, true, peak, __builtin_ctzll((unsigned long long)o->alignment), /*pinned=*/true);
   uint32_t *sflag = ar.take<uint32_t>(N + 1), *spos = ar.take<uint32_t>(N + 1);
   if (!ctx.ok()) return ctx.rc;
   LAUNCH(k_static_flag, N, rperm, b.dyn, N, sflag);
