@@ -1781,7 +1781,12 @@ constexpr int kLayerSmemInts = 14336;  // 56 KB per CTA: four CTAs per SM
 // gap units: per layer an occupancy bitmap over the trace's timeline and its
 // per-word prefix popcounts (see below), kWN layers, plus the priority list
 __host__ __device__ constexpr int gap_words(int horizon) { return (horizon >> 5) + 2; }
-__host__ __device__ constexpr int warpn_smem_ints(int horizon) { return 2 * kWN * gap_words(horizon) + kWN + 1; }
+// bitmap words (32 bits) + their prefix counts (16 bits: at most 32 * Wn < 2^16
+// set bits before a word, as a CTA's budget caps Wn) + the priority list
+__host__ __device__ constexpr int gap_pfx_ints(int horizon) { return (kWN * gap_words(horizon) + 1) / 2; }
+__host__ __device__ constexpr int warpn_smem_ints(int horizon) {
+  return kWN * gap_words(horizon) + gap_pfx_ints(horizon) + kWN + 1;
+}
 
 // GAP = the unit's candidate inserts into gaps of earlier classes' layers.
 // Without gap insertion a class only ever fills its own new layers (Alg. 1),
@@ -1808,14 +1813,15 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
   const int64_t off = A.uo[u];
   const int hz = A.horizon[t];
   const int Wn = GAP ? gap_words(hz) : 0;
-  uint32_t *bits = (uint32_t *)smem, *pfx = bits + kWN * Wn;  // [kWN][Wn] each
-  int32_t *prio = (int32_t *)(pfx + kWN * Wn);
+  uint32_t *bits = (uint32_t *)smem;                  // [kWN][Wn]
+  uint16_t *pfx = (uint16_t *)(bits + kWN * Wn);       // [kWN][Wn]
+  int32_t *prio = (int32_t *)(bits + kWN * Wn) + (GAP ? gap_pfx_ints(hz) : 0);
   const int32_t *gts = A.it.ts + a0, *gte = A.it.te + a0;
   const int64_t *gcend = A.cend + a0;
   int32_t *ilayer = A.ilayer + off;
   int64_t *lsize = A.lsize + off;
   if (GAP) {
-    for (int x = lane; x < 2 * kWN * Wn; x += 32) bits[x] = 0;
+    for (int x = lane; x < kWN * Wn + gap_pfx_ints(hz); x += 32) bits[x] = 0;
   }
   int nl = 0, gapc = 0;
   __syncwarp();
@@ -1930,7 +1936,7 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
           const uint32_t y = __shfl_up_sync(FULL, inc, o);
           if (lane >= o) inc += y;
         }
-        if (w < Wn) pfx[l * Wn + w] = carry + inc - c1;
+        if (w < Wn) pfx[l * Wn + w] = (uint16_t)(carry + inc - c1);
         carry += __shfl_sync(FULL, inc, 31);
       }
     }
@@ -1957,7 +1963,7 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
   }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_layers_w32(LayerArgs A, const int2 *__restrict__ wslot,
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 5) k_layers_w32(LayerArgs A, const int2 *__restrict__ wslot,
                                                                   int32_t *__restrict__ over, int *__restrict__ nover) {
   extern __shared__ int32_t smem[];
   const int2 slot = wslot[blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5)];
@@ -2594,6 +2600,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // shared memory and go eight to a CTA in a second launch (dynamic smem 0),
   // which runs concurrently on a side stream
   std::vector<int2> wslot, wslot_ng;
+  int cta_smem_ints = 0;  // the largest packed CTA's footprint: the launch asks for no more
   {
     std::vector<int32_t> og;
     og.reserve(order.size());
@@ -2607,6 +2614,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     while (wslot_ng.size() % kWarpsPerCta) wslot_ng.push_back(make_int2(-1, 0));
     wslot.resize(og.size() * kWarpsPerCta + kWarpsPerCta);  // upper bound: one unit per CTA
     size_t ws = 0;
+    cta_smem_ints = 0;
     for (size_t i = 0, j = og.size(); i < j;) {
       const size_t base = ws;
       int used = 0, k = 0;
@@ -2619,6 +2627,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       while (k < kWarpsPerCta && i < j && used + uneed[og[i]] <= kLayerSmemInts) put(og[i++]);
       while (k < kWarpsPerCta && i < j && used + uneed[og[j - 1]] <= kLayerSmemInts) put(og[--j]);
       while (ws < base + kWarpsPerCta) wslot[ws++] = make_int2(-1, 0);
+      cta_smem_ints = std::max(cta_smem_ints, used);
     }
     wslot.resize(ws);
   }
@@ -2664,8 +2673,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       STW_CUDA(ctx, cudaEventRecord(side_event(1), side));
     }
     if (nctas) {
-      const int smem = kLayerSmemInts * (int)sizeof(int32_t);
-      STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_w32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      const int smem = cta_smem_ints * (int)sizeof(int32_t);
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_layers_w32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kLayerSmemInts * (int)sizeof(int32_t)));
       STW_KLS(k_layers_w32, (unsigned)nctas, kWarpsPerCta * 32, smem, ctx.stream, LA, d_wslot, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }
