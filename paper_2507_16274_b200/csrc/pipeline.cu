@@ -137,9 +137,9 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
       STW_CUDA(cctx, cudaEventRecord(s.d2h, cs));
     };
     // Batch k+1's upload and batch k-1's download are issued from inside batch
-    // k's planning, once its last host->device transfer is done (after phase E):
-    // the planner's own small round trips then never queue behind them, and
-    // both overlap the rest of batch k.
+    // k's planning once its host round trips are done (at the phase D launch):
+    // the planner's round trips then never wait behind them, and both overlap
+    // the rest of batch k.
     struct Hook {
       int k, n;
       decltype(stage) *st;

@@ -2532,6 +2532,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     }
     STW_LAUNCHED(ctx);
     pt.mark("D items");
+    // a pipelining caller starts streaming its next batch in (and the previous
+    // results out) here: the round trips are behind us, and the remaining small
+    // uploads of phase E go through the pinned scratch (kernel copies), so the
+    // transfer overlaps phases D-G (measured best among the hook points)
+    if (after_uploads) after_uploads(hook_arg), after_uploads = nullptr;
   } else {
     Items it0{ar.take<int64_t>(NI + 1), ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1),
               ar.take<int32_t>(NI + 1), ar.take<int32_t>(NI + 1)};
@@ -2712,9 +2717,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
 
   pt.mark("E layers");
-  // the call's last host->device transfer is behind us: a pipelining caller
-  // starts streaming its next batch in now, so it does not contend with them
-  if (after_uploads) after_uploads(hook_arg);
+  if (after_uploads) after_uploads(hook_arg);  // the unfused path: after phase E
   // ---- F: emission
   int64_t *addr = ar.take<int64_t>((int64_t)C * N + 1);
   int32_t *layer = ar.take<int32_t>((int64_t)C * N + 1);
