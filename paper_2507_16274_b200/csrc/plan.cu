@@ -1158,59 +1158,114 @@ struct Items {
   int32_t *ts, *te, *tie, *ref;  // ref >= 0 plan id, < 0 ~event
 };
 
-// Items of every (variant, trace) segment, one CTA per segment: the
-// variant's surviving plans in plan order (planner.py:408-411), then the
-// trace's residual events -- scoped statics of single-phase groups -- in event
-// order (planner.py:397-401, 412-417); compaction by block scans.
-__global__ void __launch_bounds__(128) k_items(Plans p0, Plans p1, int want0, int want1,
-                                               const int64_t *__restrict__ pl_off, Ev e,
-                                               const int64_t *__restrict__ ev_off, const int32_t *__restrict__ gof,
-                                               Groups g, const int32_t *__restrict__ pid0,
-                                               const int64_t *__restrict__ io, int T, Items it) {
-  __shared__ uint32_t sh[33];
-  const int sgi = blockIdx.x, tid = threadIdx.x;
-  const int v = sgi >= T, t = sgi - v * T;
-  if (!(v ? want1 : want0)) return;
-  const Plans &pv = v ? p1 : p0;
-  int64_t pos = io[sgi];
-  for (int64_t k0 = pl_off[t]; k0 < pl_off[t + 1]; k0 += blockDim.x) {
-    const int64_t k = k0 + tid;
-    const bool alive = k < pl_off[t + 1] && pv.alive[k];
-    uint32_t tot;
-    const uint32_t ex = block_excl_sum<uint32_t>(alive ? 1u : 0u, sh, &tot);
-    if (alive) {
-      const int64_t o = pos + ex;
-      it.size[o] = pv.h[k];
-      it.ts[o] = pv.ts[k];
-      it.te[o] = pv.te[k];
-      it.tie[o] = pv.minq[k];
-      it.ref[o] = (int32_t)k;
-    }
-    pos += tot;
+
+// Phase D for segments too large for one CTA (e.g. a single 10^6-event trace).
+// A segment's items are the variant's surviving plans in plan order
+// (planner.py:408-411), then the trace's residual events -- scoped statics of
+// single-phase groups -- in event order (planner.py:397-401, 412-417). All
+// segments form one virtual sequence -- per variant v, per trace t: its plans,
+// then its events -- whose selected entries are compacted by one global scan;
+// the scan value at an entry is its item index (segments are in item order).
+__device__ __forceinline__ bool item_virtual(int64_t x, int T, int64_t P, int64_t N, const int64_t *pl_off,
+                                             const int64_t *ev_off, int *v, int *t, int64_t *src, bool *is_plan) {
+  *v = (int)(x / (P + N));
+  const int64_t y = x - (int64_t)*v * (P + N);  // position inside the variant: pl_off[t] + ev_off[t] + ...
+  int lo = 0, hi = T;  // last t with pl_off[t] + ev_off[t] <= y
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pl_off[mid] + ev_off[mid] <= y)
+      lo = mid;
+    else
+      hi = mid;
   }
-  for (int64_t i0 = ev_off[t]; i0 < ev_off[t + 1]; i0 += blockDim.x) {
-    const int64_t i = i0 + tid;
-    const bool res = i < ev_off[t + 1] && !e.dyn[i] && pid0[i] < 0 && g.cls[gof[i]] == 1;
-    uint32_t tot;
-    const uint32_t ex = block_excl_sum<uint32_t>(res ? 1u : 0u, sh, &tot);
-    if (res) {
-      const int64_t o = pos + ex;
-      it.size[o] = e.size[i];
-      it.ts[o] = e.ts[i];
-      it.te[o] = e.te[i];
-      it.tie[o] = e.q[i];
-      it.ref[o] = ~(int32_t)i;
+  *t = lo;
+  const int64_t r = y - pl_off[lo] - ev_off[lo], np = pl_off[lo + 1] - pl_off[lo];
+  *is_plan = r < np;
+  *src = *is_plan ? pl_off[lo] + r : ev_off[lo] + (r - np);
+  return true;
+}
+
+__global__ void k_item_flags(Plans p0, Plans p1, int want0, int want1, const int64_t *__restrict__ pl_off, Ev e,
+                             const int64_t *__restrict__ ev_off, const int32_t *__restrict__ gof, Groups g,
+                             const int32_t *__restrict__ pid0, int T, int64_t P, int64_t N, uint32_t *__restrict__ f) {
+  GRID_STRIDE(x, 2 * (P + N)) {
+    int v, t;
+    int64_t src;
+    bool pl;
+    item_virtual(x, T, P, N, pl_off, ev_off, &v, &t, &src, &pl);
+    bool sel = false;
+    if (v ? want1 : want0) {
+      if (pl)
+        sel = (v ? p1 : p0).alive[src];
+      else
+        sel = !e.dyn[src] && pid0[src] < 0 && g.cls[gof[src]] == 1;
     }
-    pos += tot;
+    f[x] = sel ? 1u : 0u;
+  }
+}
+
+__global__ void k_item_scatter(Plans p0, Plans p1, const int64_t *__restrict__ pl_off, Ev e,
+                               const int64_t *__restrict__ ev_off, int T, int64_t P, int64_t N,
+                               const uint32_t *__restrict__ f, const uint32_t *__restrict__ pos, Items it) {
+  GRID_STRIDE(x, 2 * (P + N)) {
+    if (!f[x]) continue;
+    int v, t;
+    int64_t src;
+    bool pl;
+    item_virtual(x, T, P, N, pl_off, ev_off, &v, &t, &src, &pl);
+    const int64_t o = pos[x];
+    if (pl) {
+      const Plans &pv = v ? p1 : p0;
+      it.size[o] = pv.h[src];
+      it.ts[o] = pv.ts[src];
+      it.te[o] = pv.te[src];
+      it.tie[o] = pv.minq[src];
+      it.ref[o] = (int32_t)src;
+    } else {
+      it.size[o] = e.size[src];
+      it.ts[o] = e.ts[src];
+      it.te[o] = e.te[src];
+      it.tie[o] = e.q[src];
+      it.ref[o] = ~(int32_t)src;
+    }
+  }
+}
+
+// class ends for large segments: items are sorted by size descending inside
+// their segment, so j's class ends at the first later item of smaller size
+// (binary search; the segment from io by binary search)
+__global__ void k_class_ends_bs(Items it, const int64_t *__restrict__ io, int VT, int64_t n,
+                                int64_t *__restrict__ cend) {
+  GRID_STRIDE(j, n) {
+    int lo = 0, hi = VT;  // segment: last s with io[s] <= j
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (io[mid] <= j)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    while (io[lo + 1] <= j) lo++;  // skip empty segments
+    const int64_t b = io[lo + 1];
+    const int64_t sz = it.size[j];
+    int64_t a = j + 1, z = b;  // first k in [j+1, b) with size < sz
+    while (a < z) {
+      const int64_t m = (a + z) >> 1;
+      if (it.size[m] < sz)
+        z = m;
+      else
+        a = m + 1;
+    }
+    cend[j] = a;
   }
 }
 
 // Phase D fused (segments of <= 4096 items, keys of <= 64 bits): one CTA per
 // (variant, trace) gathers the segment's items (alive plans in plan order,
-// then residual events in event order -- the order k_items lists them), sorts
+// then residual events in event order), sorts
 // (size desc, t_s, tie) keys with their source refs in shared memory
 // (cta_radix, stable) and writes the items in sorted order together with the
-// plan/event -> item maps: k_items + k_item_keys + the segmented sort +
+// plan/event -> item maps: the gather + k_item_keys + the segmented sort +
 // k_item_permute in one pass over the data.
 template <int IPT>
 __global__ void __launch_bounds__(256) k_items_sorted(Plans p0, Plans p1, int want0, int want1,
@@ -1284,7 +1339,7 @@ __global__ void __launch_bounds__(256) k_items_sorted(Plans p0, Plans p1, int wa
     }
     it.ref[o] = r;
   }
-  // class ends (k_class_ends): cend[j] = the first class edge after j, an edge
+  // class ends: cend[j] = the first class edge after j, an edge
   // being the segment's last item or a change of the key's size bits. Edges go
   // to vA (read above), then a suffix minimum: per-thread chunks + warp shuffles.
   __syncthreads();
@@ -1361,31 +1416,6 @@ __global__ void k_item_permute(Items src, Items dst, const uint32_t *__restrict_
   }
 }
 
-// class end (exclusive) for every item: classes are runs of equal size inside a (variant, trace) segment
-// cend[j] = end of item j's size class inside its (variant, trace) segment; one
-// warp per segment walks it from the back (suffix minimum of class boundaries)
-__global__ void k_class_ends(Items it, const int64_t *__restrict__ io, int VT, int64_t *__restrict__ cend) {
-  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  for (int sgi = w; sgi < VT; sgi += nw) {
-    const int64_t a = io[sgi], b = io[sgi + 1];
-    int64_t carry = b;  // first boundary at or after the chunk's end
-    for (int64_t c = b - 32; c > a - 32; c -= 32) {
-      const int64_t j = c + lane;
-      const bool in = j >= a && j < b;
-      // a class ends after j when j is the segment's last item or the next size differs
-      const bool edge = in && (j + 1 == b || it.size[j + 1] != it.size[j]);
-      int64_t v = edge ? j + 1 : LLONG_MAX;
-      for (int o = 1; o < 32; o <<= 1) {  // suffix minimum over lanes
-        const int64_t u = __shfl_down_sync(0xffffffffu, v, o);
-        if (lane + o < 32) v = min(v, u);
-      }
-      v = min(v, carry);
-      if (in) cend[j] = v;
-      carry = __shfl_sync(0xffffffffu, v, 0);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // E: HomoSize layers, one CTA per unit (planner.py:189-254, 414-439)
@@ -2543,10 +2573,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     uint64_t *ihi = ar.take<uint64_t>(NI + 1), *ilo = ar.take<uint64_t>(NI + 1);
     uint32_t *iperm = ar.take<uint32_t>(NI + 1);
     if (!ctx.ok()) return ctx.rc;
-    if (T > 0) {
-      STW_KL(k_items, (unsigned)(V * T), 128, ctx.stream, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0,
-             d_pl_off, e, b.ev_off, gof, g, pid0, d_io, T, it0);
-      STW_LAUNCHED(ctx);
+    if (T > 0) {  // one global compaction (segments this large would serialise a CTA each)
+      const int64_t NV = 2 * (P + N);
+      uint32_t *iflag = ar.take<uint32_t>(NV + 1), *ipos = ar.take<uint32_t>(NV + 1);
+      if (!ctx.ok()) return ctx.rc;
+      LAUNCH(k_item_flags, NV, p0, p1, want[0] ? 1 : 0, want[1] ? 1 : 0, d_pl_off, e, b.ev_off, gof, g, pid0, T,
+             P, N, iflag);
+      device_scan<uint32_t>(ctx, ar, iflag, ipos, NV, false);
+      LAUNCH(k_item_scatter, NV, p0, p1, d_pl_off, e, b.ev_off, T, P, N, iflag, ipos, it0);
     }
     pt.mark("D items");
     LAUNCH(k_item_keys, NI, it0, NI, d_io, V * T, qb, al, maxsu, sb, in_order ? 1 : 0, ihi, ilo);
@@ -2590,7 +2624,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     }
   }
   pt.mark("D host order");
-  {  // stable counting sort by item count, descending
+  if (order.size() < 1024) {  // few units (one huge trace): a comparison sort
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return ucnt[x] > ucnt[y]; });
+  } else {  // stable counting sort by item count, descending
     int32_t mx = 0;
     for (int32_t u : order) mx = std::max(mx, ucnt[u]);
     std::vector<int32_t> pos(mx + 2, 0);
@@ -2638,10 +2674,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   }
   pt.mark("D sort");
   // classes (written by k_items_sorted on the fused path)
-  if (V * T > 0 && !fused_items) {
-    STW_KL(k_class_ends, grid_for((int64_t)V * T * 32, 256), 256, ctx.stream, it, d_io, V * T, cend);
-    STW_LAUNCHED(ctx);
-  }
+  if (V * T > 0 && !fused_items) LAUNCH(k_class_ends_bs, NI, it, d_io, V * T, NI, cend);
 
   pt.mark("D classes");
   // ---- E: layers per unit (host-side unit layout and CTA packing were prepared during D)
