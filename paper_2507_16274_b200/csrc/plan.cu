@@ -2693,20 +2693,24 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   {
     const int nctas = (int)(wslot.size() / kWarpsPerCta), nctas_ng = (int)(wslot_ng.size() / kWarpsPerCta);
-    int32_t *d_over = ar.take<int32_t>(U + 1);
-    int *d_nover = ar.take<int>(1);
+    // overflow lists (units that need > 32 layers), one per launch: each launch's
+    // overflow units are redone by the CTA kernel on that launch's stream
+    int32_t *d_over = ar.take<int32_t>(U + 1), *d_over_ng = ar.take<int32_t>(U + 1);
+    int *d_nover = ar.take<int>(2), *d_nover_ng = d_nover + 1;
     int2 *d_wslot = nctas ? h2d(ctx, ar, wslot) : nullptr;
     int2 *d_wslot_ng = nctas_ng ? h2d(ctx, ar, wslot_ng) : nullptr;
     int32_t *d_bigs = bigs.empty() ? nullptr : h2d(ctx, ar, bigs);
     if (!ctx.ok()) return ctx.rc;
-    STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, sizeof(int), ctx.stream));
+    STW_CUDA(ctx, cudaMemsetAsync(d_nover, 0, 2 * sizeof(int), ctx.stream));
     cudaStream_t side = nullptr;
-    if (nctas_ng) {  // fork: non-gap units on the side stream
+    if (nctas_ng) {  // fork: non-gap units (and their overflow) on the side stream
       side = side_stream();
       h2d_flush(ctx);  // the side stream reads the unit tables uploaded above
       STW_CUDA(ctx, cudaEventRecord(side_event(0), ctx.stream));
       STW_CUDA(ctx, cudaStreamWaitEvent(side, side_event(0), 0));
-      STW_KLS(k_layers_w32, (unsigned)nctas_ng, kWarpsPerCta * 32, 0, side, LA, d_wslot_ng, d_over, d_nover);
+      STW_KLS(k_layers_w32, (unsigned)nctas_ng, kWarpsPerCta * 32, 0, side, LA, d_wslot_ng, d_over_ng, d_nover_ng);
+      STW_LAUNCHED(ctx);
+      STW_KL(k_layers, 296, kPlanThreads, side, LA, d_over_ng, d_nover_ng);
       STW_LAUNCHED(ctx);
       STW_CUDA(ctx, cudaEventRecord(side_event(1), side));
     }
@@ -2717,15 +2721,15 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       STW_KLS(k_layers_w32, (unsigned)nctas, kWarpsPerCta * 32, smem, ctx.stream, LA, d_wslot, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }
-    if (side) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, side_event(1), 0));  // join
-    if (!bigs.empty()) {
+    if (!bigs.empty()) {  // units too large for a warp's shared memory (runs beside the side stream)
       STW_KL(k_layers, (unsigned)bigs.size(), kPlanThreads, ctx.stream, LA, d_bigs, (const int *)nullptr);
       STW_LAUNCHED(ctx);
     }
-    if (nctas || nctas_ng) {  // units of either launch that overflowed 32 layers (count read on the device)
+    if (nctas) {  // gap units that overflowed 32 layers (count read on the device)
       STW_KL(k_layers, 296, kPlanThreads, ctx.stream, LA, d_over, d_nover);
       STW_LAUNCHED(ctx);
     }
+    if (side) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, side_event(1), 0));  // join
   }
 
   if (getenv("STW_DEBUG_DUMP")) {  // developer aid: dump unit 0's sorted items and layer choices
