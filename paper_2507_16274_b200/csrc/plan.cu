@@ -2210,15 +2210,25 @@ __global__ void k_scatter_fusions(const int32_t *__restrict__ ptr, const int64_t
 // call (created once per host thread, reused; the call stays synchronous).
 // per-thread side stream and fork/join events (a call's work is joined back
 // into its own stream before the call returns)
+// per thread and per device (streams and events belong to the device that was
+// current when they were created)
+constexpr int kMaxDevices = 64;
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < kMaxDevices ? d : 0;
+}
 static cudaStream_t side_stream() {
-  thread_local cudaStream_t s = nullptr;
-  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-  return s;
+  thread_local cudaStream_t s[kMaxDevices] = {};
+  cudaStream_t &x = s[cur_device()];
+  if (!x) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  return x;
 }
 static cudaEvent_t side_event(int i) {
-  thread_local cudaEvent_t e[2] = {};
-  if (!e[i]) cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming);
-  return e[i];
+  thread_local cudaEvent_t e[kMaxDevices][2] = {};
+  cudaEvent_t &x = e[cur_device()][i];
+  if (!x) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  return x;
 }
 
 template <class T>
