@@ -28,6 +28,26 @@ def test_radix_sort_stable_matches_numpy(cuda, n, bits):
     assert np.array_equal(k.cpu().numpy(), keys[order])
 
 
+def test_radix_sort_full_bench_size_properties(cuda):
+    """The bench's K2 size (2^27 pairs, 42 key bits, >> L2), checked on the
+    device by size-independent properties: keys nondecreasing, values a
+    permutation, and values increasing inside runs of equal keys (stable)."""
+    import torch
+
+    n, bits = 1 << 27, 42
+    g = torch.Generator(device=cuda).manual_seed(3)
+    k = torch.randint(0, 1 << bits, (n,), generator=g, device=cuda, dtype=torch.int64)
+    k[::5] = k[1]  # long runs of one key
+    v = torch.arange(n, dtype=torch.int32, device=cuda)
+    api.radix_sort_pairs(k, v, 0, bits)
+    assert bool((k[1:] >= k[:-1]).all())
+    same = k[1:] == k[:-1]
+    assert bool((v[1:][same] > v[:-1][same]).all())
+    seen = torch.zeros(n, dtype=torch.bool, device=cuda)
+    seen[v.long()] = True
+    assert bool(seen.all())
+
+
 def test_radix_sort_partial_bits(cuda):
     import torch
 
