@@ -281,8 +281,9 @@ template void device_scan<int32_t>(Ctx &, Arena &, const int32_t *, int32_t *, i
 //  k_os_hist  one read of the keys -> the digit histograms of every pass
 //  k_os_bins  exclusive scan of each pass's 256 bins
 //  k_os_pass  per 3840-key tile (tile ids handed out in launch order by an
-//             atomic counter): warp-level stable ranking with match_any into
-//             per-warp digit counters, publish the tile's digit counts, look
+//             atomic counter): warp-level stable ranking (8 ballots) into
+//             per-warp digit counters, publish the tile's digit counts (the
+//             sum of the warps' counters), look
 //             back over earlier tiles' published counts/prefixes (one thread
 //             per digit), stage the tile in shared memory in digit order and
 //             write it out in digit runs (coalesced).
@@ -349,12 +350,10 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
   uint32_t *wh = sv + kOsTile;             // [warp][digit] counts, then warp offsets
   uint32_t *texcl = wh + kOsWarps * 256;   // tile-local exclusive offsets per digit
   int64_t *gbase = (int64_t *)(texcl + 256);  // global base per digit (minus texcl)
-  uint32_t *th = (uint32_t *)(gbase + 256);  // tile histogram
-  uint32_t *stile = th + 256;
+  uint32_t *stile = (uint32_t *)(gbase + 256) + 256;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   if (tid == 0) *stile = atomicAdd(ctr, 1u);
   for (int x = tid; x < kOsWarps * 256; x += kOsThreads) wh[x] = 0;
-  th[tid] = 0;
   __syncthreads();
   const uint32_t tile = *stile;
   const int64_t base = (int64_t)tile * kOsTile + (int64_t)w * (kOsItems * 32);
@@ -363,17 +362,6 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
   for (int j = 0; j < kOsItems; j++) {
     const int64_t i = base + j * 32 + lane;
     k[j] = i < n ? kin[i] : 0;
-  }
-  // tile histogram first, so the tile's aggregate is published as early as possible
-#pragma unroll
-  for (int j = 0; j < kOsItems; j++)
-    if (base + j * 32 + lane < n) atomicAdd(th + ((uint32_t)(k[j] >> shift) & mask), 1u);
-  __syncthreads();
-  const uint32_t cnt = th[tid];
-  if (tile == 0) {
-    atomicExch(status + tid, kOsPrefix | cnt);
-  } else {
-    atomicExch(status + (int64_t)tile * 256 + tid, kOsAgg | cnt);
   }
   // stable rank inside the warp: peers with the same digit from 8 ballots (one
   // per digit bit, independent, so they pipeline); the highest peer bumps the
@@ -400,7 +388,9 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
     rk[j] = (uint16_t)(old + __popc(peers & lt));
   }
   __syncthreads();
-  // digit tid: offsets of each warp inside the tile's run of that digit
+  // digit tid: offsets of each warp inside the tile's run of that digit; the
+  // warps' counts sum to the tile's count, published at once
+  uint32_t cnt;
   {
     uint32_t run = 0;
 #pragma unroll
@@ -409,6 +399,12 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
       wh[x * 256 + tid] = run;
       run += c;
     }
+    cnt = run;
+  }
+  if (tile == 0) {
+    atomicExch(status + tid, kOsPrefix | cnt);
+  } else {
+    atomicExch(status + (int64_t)tile * 256 + tid, kOsAgg | cnt);
   }
   // look back over the earlier tiles for this digit
   volatile uint32_t *st = status;
