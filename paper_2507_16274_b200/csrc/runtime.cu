@@ -406,6 +406,25 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
   } else {
     atomicExch(status + (int64_t)tile * 256 + tid, kOsAgg | cnt);
   }
+  // the tile's digit runs (block scan) and each (warp, digit) block's start:
+  // the staging needs nothing from earlier tiles, so it runs before the
+  // look-back (which then finds more predecessors published)
+  __shared__ uint32_t shs[33];
+  const uint32_t tx = block_excl_sum<uint32_t>(cnt, shs, nullptr);
+#pragma unroll
+  for (int x = 0; x < kOsWarps; x++) wh[x * 256 + tid] += tx;
+  __syncthreads();
+  // stage the tile in digit order
+#pragma unroll
+  for (int j = 0; j < kOsItems; j++) {
+    const int64_t i = base + j * 32 + lane;
+    if (i < n) {
+      const uint32_t d = (uint32_t)(k[j] >> shift) & mask;
+      const uint32_t pos = wh[w * 256 + d] + rk[j];
+      sk[pos] = k[j];
+      sv[pos] = vin[i];
+    }
+  }
   // look back over the earlier tiles for this digit
   volatile uint32_t *st = status;
   uint32_t excl = 0;
@@ -432,22 +451,7 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
     }
     atomicExch(status + (int64_t)tile * 256 + tid, kOsPrefix | (excl + cnt));
   }
-  __shared__ uint32_t shs[33];
-  const uint32_t tx = block_excl_sum<uint32_t>(cnt, shs, nullptr);
-  texcl[tid] = tx;
   gbase[tid] = (int64_t)bins[tid] + excl - tx;
-  __syncthreads();
-  // stage the tile in digit order (values are read only now: fewer live registers)
-#pragma unroll
-  for (int j = 0; j < kOsItems; j++) {
-    const int64_t i = base + j * 32 + lane;
-    if (i < n) {
-      const uint32_t d = (uint32_t)(k[j] >> shift) & mask;
-      const uint32_t pos = texcl[d] + wh[w * 256 + d] + rk[j];
-      sk[pos] = k[j];
-      sv[pos] = vin[i];
-    }
-  }
   __syncthreads();
   const int64_t t0 = (int64_t)tile * kOsTile;
   const int cnt_tile = (int)(n - t0 < kOsTile ? n - t0 : kOsTile);
