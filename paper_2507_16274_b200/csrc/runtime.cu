@@ -293,6 +293,7 @@ constexpr int kOsThreads = 256;  // one thread per digit in the look-back
 constexpr int kOsItems = 15;
 constexpr int kOsTile = kOsThreads * kOsItems;
 constexpr int kOsWarps = kOsThreads / 32;
+constexpr int kOsAhead = 148 * 3;  // tiles: one wave of resident CTAs (3 per SM)
 constexpr uint32_t kOsAgg = 1u << 30, kOsPrefix = 2u << 30, kOsVal = kOsAgg - 1;
 constexpr size_t kOsSmem = (size_t)kOsTile * 12 + (size_t)kOsWarps * 256 * 4 + 256 * 4 + 256 * 8 + 256 * 4 + 16;
 
@@ -362,6 +363,16 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
   for (int j = 0; j < kOsItems; j++) {
     const int64_t i = base + j * 32 + lane;
     k[j] = i < n ? kin[i] : 0;
+  }
+  {  // warm L2 for the tile a CTA will claim about one residency wave from now
+    const int64_t ahead = (int64_t)kOsAhead * kOsTile;
+#pragma unroll
+    for (int j = 0; j < kOsItems; j += 2) {  // one 128-byte line per 16 lanes and key row pair
+      const int64_t i = base + ahead + j * 32 + lane * 2;
+      if (i < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(kin + i));
+    }
+    const int64_t iv = base + ahead + lane * 32;  // 32 values = one line
+    if (lane < 15 && iv < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(vin + iv));
   }
   // stable rank inside the warp: peers with the same digit from 8 ballots (one
   // per digit bit, independent, so they pipeline); the highest peer bumps the
