@@ -293,7 +293,7 @@ constexpr int kOsThreads = 256;  // one thread per digit in the look-back
 constexpr int kOsItems = 15;
 constexpr int kOsTile = kOsThreads * kOsItems;
 constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsAhead = 148 * 3;  // tiles: one wave of resident CTAs (3 per SM)
+constexpr int kOsAhead = 148 * 2;  // tiles ahead (measured: 2 per SM beats 3 and 6)
 constexpr uint32_t kOsAgg = 1u << 30, kOsPrefix = 2u << 30, kOsVal = kOsAgg - 1;
 constexpr size_t kOsSmem = (size_t)kOsTile * 12 + (size_t)kOsWarps * 256 * 4 + 256 * 4 + 256 * 8 + 256 * 4 + 16;
 
