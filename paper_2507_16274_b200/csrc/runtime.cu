@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
                                                         const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
                                                         uint32_t *__restrict__ vout, int64_t n, int shift,
                                                         uint32_t mask, const uint32_t *__restrict__ bins,
-                                                        uint32_t *__restrict__ status, uint32_t *__restrict__ ctr) {
+                                                        uint32_t *__restrict__ status, uint32_t *__restrict__ ctr,
+                                                        uint32_t *__restrict__ status_next) {
   extern __shared__ __align__(16) unsigned char os_smem[];
   uint64_t *sk = (uint64_t *)os_smem;
   uint32_t *sv = (uint32_t *)(sk + kOsTile);
@@ -357,6 +358,9 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
   for (int x = tid; x < kOsWarps * 256; x += kOsThreads) wh[x] = 0;
   __syncthreads();
   const uint32_t tile = *stile;
+  // the next pass's look-back flags start cleared: each tile clears its own
+  // (this pass's predecessor left them set; the next pass starts after this one)
+  if (status_next) status_next[(int64_t)tile * 256 + tid] = 0;
   const int64_t base = (int64_t)tile * kOsTile + (int64_t)w * (kOsItems * 32);
   uint64_t k[kOsItems];
 #pragma unroll
@@ -483,7 +487,7 @@ void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64
   uint64_t *k2 = ar.take<uint64_t>(n);
   uint32_t *v2 = ar.take<uint32_t>(n);
   uint32_t *hist = ar.take<uint32_t>((size_t)passes * 256);
-  uint32_t *status = ar.take<uint32_t>((size_t)ntiles * 256);
+  uint32_t *status = ar.take<uint32_t>((size_t)ntiles * 256 * 2);  // two buffers, alternating by pass
   uint32_t *ctr = ar.take<uint32_t>(passes);
   if (!ctx.ok()) return;
   STW_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)passes * 256 * sizeof(uint32_t), ctx.stream));
@@ -496,9 +500,10 @@ void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64
   uint32_t *va = vals, *vb = v2;
   for (int p = 0; p < passes && ctx.ok(); p++) {
     const int b = begin_bit + 8 * p, w = end_bit - b < 8 ? end_bit - b : 8;
-    STW_CUDA(ctx, cudaMemsetAsync(status, 0, (size_t)ntiles * 256 * sizeof(uint32_t), ctx.stream));
+    uint32_t *cur = status + (size_t)(p & 1) * ntiles * 256, *nxt = status + (size_t)((p + 1) & 1) * ntiles * 256;
+    if (p == 0) STW_CUDA(ctx, cudaMemsetAsync(cur, 0, (size_t)ntiles * 256 * sizeof(uint32_t), ctx.stream));
     STW_KLS(k_os_pass, (unsigned)ntiles, kOsThreads, kOsSmem, ctx.stream, ka, va, kb, vb, n, b, (1u << w) - 1,
-            hist + p * 256, status, ctr + p);
+            hist + p * 256, cur, ctr + p, p + 1 < passes ? nxt : (uint32_t *)nullptr);
     STW_LAUNCHED(ctx);
     std::swap(ka, kb);
     std::swap(va, vb);
