@@ -92,6 +92,8 @@ void h2d_async(Ctx &ctx, void *ddst, const void *hsrc, size_t bytes);
 void h2d_flush(Ctx &ctx);  // before another stream (or an event) must see the uploads
 void d2h_async(Ctx &ctx, void *dst, const void *dsrc, size_t bytes);
 void host_sync(Ctx &ctx);
+// drop anything a failed earlier call left pending (start of a planner call)
+void pinned_reset();
 
 // host-side size helpers
 

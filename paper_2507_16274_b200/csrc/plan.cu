@@ -2320,6 +2320,7 @@ struct PhaseTimer {
 
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror,
                void (*after_uploads)(void *), void *hook_arg) {
+  pinned_reset();  // a call that failed midway may have left transfers pending
   PhaseTimer pt(ctx);
   Arena ar(&ctx);
   DevBatch b;

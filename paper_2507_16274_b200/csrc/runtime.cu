@@ -597,6 +597,14 @@ void launch_copies(std::vector<CopyDesc> &v, cudaStream_t s) {
 }
 }  // namespace
 
+void pinned_reset() {
+  g_pin.up.clear();
+  g_pin.down.clear();
+  g_pin.out.clear();
+  g_pin.blk = 0;
+  g_pin.off = 0;
+}
+
 void h2d_flush_stream(cudaStream_t s) {
   if (!g_pin.up.empty() && s == g_pin.up_stream) launch_copies(g_pin.up, s);
 }
