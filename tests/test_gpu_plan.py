@@ -179,3 +179,13 @@ def test_plan_batches_with_empty_and_tiny_batches():
         want = api.plan_batch(g, CANDS, select_best=True)
         for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
             assert np.array_equal(getattr(got, f), getattr(want, f)), f
+
+
+def test_failed_call_leaves_no_state_behind():
+    """A call that fails midway (item sort key wider than 64 bits: one 2^61-byte
+    event in a 4096-trace batch) raises, and the next call is still exact."""
+    tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(4095)]
+    tas.append(_manual_trace([(1, 1 << 61, 0, 2, "F:0", "F:0")], [("F:0", 0, 4)]))
+    with pytest.raises(Exception, match="64 bits"):
+        api.plan_batch(tas, CANDS)
+    check_batch(tas[:8])
