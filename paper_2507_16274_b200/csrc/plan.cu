@@ -511,7 +511,7 @@ struct Groups {
 // and the two global scans. Group ids become global in k_group_table (+ the
 // trace's offset from the group counts written here).
 template <int IPT>
-__global__ void __launch_bounds__(256, 4) k_groups_fused(Ev e, const int64_t *__restrict__ ev_off,
+__global__ void __launch_bounds__(256, IPT == 8 ? 4 : 1) k_groups_fused(Ev e, const int64_t *__restrict__ ev_off,
                                                       const int32_t *__restrict__ r, int pb, int qb, int bit0,
                                                       uint32_t *__restrict__ gperm, uint32_t *__restrict__ head,
                                                       uint32_t *__restrict__ lgid, int64_t *__restrict__ szs,
@@ -1268,7 +1268,7 @@ __global__ void k_class_ends_bs(Items it, const int64_t *__restrict__ io, int VT
 // plan/event -> item maps: the gather + k_item_keys + the segmented sort +
 // k_item_permute in one pass over the data.
 template <int IPT>
-__global__ void __launch_bounds__(256, 5) k_items_sorted(Plans p0, Plans p1, int want0, int want1,
+__global__ void __launch_bounds__(256, IPT == 8 ? 5 : 1) k_items_sorted(Plans p0, Plans p1, int want0, int want1,
                                                       const int64_t *__restrict__ pl_off, Ev e,
                                                       const int64_t *__restrict__ ev_off,
                                                       const int32_t *__restrict__ gof, Groups g,
