@@ -1,9 +1,13 @@
 /*
  * libstw -- B200-native (sm_100a) spatio-temporal memory planner and trace
  * replay scorer. Plain C ABI: pointers, sizes and a cudaStream_t passed as
- * void*; no framework types. Every call is synchronous on return and has no
- * global state (reentrant per stream). There is no CPU fallback: without a
- * usable CUDA device every call returns STW_ECUDA.
+ * void*; no framework types. Every call is synchronous on return and keeps no
+ * state between calls that changes its results; calls from different threads
+ * may run concurrently. Kept across calls for speed (never for results): a
+ * private device memory pool per device for scratch (its memory stays mapped
+ * until stw_release_scratch), and per calling thread a mapped page-locked
+ * staging buffer plus two side streams and events per device. There is no CPU
+ * fallback: without a usable CUDA device every call returns STW_ECUDA.
  *
  * Each entry point replaces a function of the reference Python package
  * (/root/reference/pkg/src/memplan); the citation is next to it. The Python
@@ -192,6 +196,77 @@ int stw_simulate(const stw_batch *trace, const stw_bundle *plan, stw_report *rep
                  int64_t *err_id, void *stream, char *err, size_t errlen);
 int stw_baseline(const stw_batch *trace, stw_report *rep, stw_log *log, int64_t *err_id,
                  void *stream, char *err, size_t errlen);
+
+/* ---- sub-operations (the reference's public helpers, one call each) -----
+ * Host pointers in and out; the library stages them to HBM. */
+
+/* group_by_phase (planner.py:74-85): rows sorted by (ps, pe, t_s, id) -- ps/pe
+ * are order-preserving phase codes (PhaseId order: kind, microbatch, chunk) --
+ * into perm[n]; group g = perm[grp_off[g] .. grp_off[g+1]), g < *n_groups
+ * (grp_off needs n+1 entries). */
+int stw_group_events(int64_t n, const int64_t *ps, const int64_t *pe, const int64_t *t_s, const int64_t *id,
+                     int32_t *perm, int64_t *grp_off, int64_t *n_groups, void *stream, char *err, size_t errlen);
+
+/* pack_group / _plan_from_decisions / compute_tmp (planner.py:88-115) over
+ * n_plans plans, plan p = members [off[p], off[p+1]) in member order.
+ * addr == NULL packs the members contiguously (prefix sums of sizes, written
+ * to addr_out if non-NULL); otherwise the given addresses are used. height /
+ * t_lo / t_hi = max end address, min t_s, max t_e unless the *_in overrides
+ * are given (compute_tmp of an existing LocalPlan). tmp = sum(size * (t_e -
+ * t_s)) / (height * (t_hi - t_lo)), correctly rounded (Python int / int);
+ * rc[p] = STW_EPLAN for a degenerate lifespan (t_hi <= t_lo). */
+typedef struct {
+  int64_t n_plans, n;
+  const int64_t *off, *size, *t_s, *t_e;
+  const int64_t *addr;
+  const int64_t *height_in, *t_lo_in, *t_hi_in;
+  int64_t *addr_out, *height, *t_lo, *t_hi;
+  double *tmp;
+  int32_t *rc;
+} stw_lplans;
+int stw_local_plans(const stw_lplans *p, void *stream, char *err, size_t errlen);
+
+/* weighted_tmp_average (planner.py:118-121): sum(tmp_i * height_i * dur_i) /
+ * sum(height_i * dur_i) with CPython float semantics (float(int) round-half-
+ * even, the builtin sum's compensated accumulation). */
+int stw_weighted_tmp(int64_t n, const double *tmp, const int64_t *height, const int64_t *dur, double *out,
+                     void *stream, char *err, size_t errlen);
+
+/* fuse_plans / try_fuse (planner.py:124-182): places the smaller plan's
+ * decisions (s_*) into the larger plan's (l_*) by the cursor walk. Outputs:
+ * out_addr[i] = address of smaller decision i, out_order = smaller decision
+ * indices in placement order; result_i = {fused height, t_s, t_e, rc};
+ * result_d = {fused tmp, weighted_tmp_average([larger, smaller])} (given
+ * each plan's tmp, height and duration). try_fuse accepts iff
+ * result_d[0] > result_d[1]. */
+typedef struct {
+  int64_t n_large, n_small;
+  const int64_t *l_addr, *l_size, *l_ts, *l_te;
+  const int64_t *s_id, *s_size, *s_ts, *s_te;
+  double l_tmp, s_tmp;
+  int64_t l_height, l_dur, s_height, s_dur;
+  int64_t *out_addr;
+  int32_t *out_order;
+  int64_t *result_i;
+  double *result_d;
+} stw_fusion;
+int stw_fuse_plans(const stw_fusion *f, void *stream, char *err, size_t errlen);
+
+/* build_layers_for_size, Alg. 1 (planner.py:236-254): items sorted by
+ * (t_s, tie) (order[k] = item index), each joins the layer with the largest
+ * end strictly below its start (ties: oldest), else opens a new one.
+ * Timestamps are doubles (exact for integers < 2^53). */
+int stw_build_layers(int64_t n, const double *t_s, const double *t_e, const int64_t *tie, int32_t *layer_of,
+                     int32_t *order, int64_t *n_layers, void *stream, char *err, size_t errlen);
+
+/* compute_metrics (sim.py:67-117) over a columnar log (stw_log encoding;
+ * size = pool_size for init records, bytes for reserve records). */
+int stw_metrics(int64_t n, const int8_t *kind, const int64_t *size, const int8_t *space, const int8_t *route,
+                stw_report *rep, void *stream, char *err, size_t errlen);
+
+/* Return the scratch pool's cached device memory to the driver (synchronizes
+ * the device first). */
+int stw_release_scratch(void);
 
 /* library identification: returns "stw <version> sm_100a" */
 const char *stw_version(void);

@@ -27,12 +27,19 @@
 extern "C" {
 #endif
 
-/* Reserve the pool on `device` (cudaMalloc of pool_size bytes). */
+/* Reserve ONE virtual range on `device`: the pool [0, pool_size) backed at
+ * once, then fallback_va bytes (0 = 256 GiB) where the fallback segments are
+ * mapped on first use. Device pointer = range base + the replay's address
+ * (pool offset, or cache address >= pool_size). STW_EARG if already
+ * initialised. */
 int stw_alloc_init(int device, int64_t pool_size, int64_t alignment);
+int stw_alloc_init_ex(int device, int64_t pool_size, int64_t alignment, int64_t fallback_va);
 
-/* Load the plan: decisions (any order) with the phase index of their event,
- * size, planned offset, t_s and id (queue order = (t_s, id), sim.py:156-162),
- * and the reuse spaces per dynamic key (key k: sp_lo/sp_hi[sp_off[k]..sp_off[k+1])). */
+/* Load (or reload) the plan: decisions (any order) with the phase index of
+ * their event, size, planned offset, t_s and id (queue order = (t_s, id),
+ * sim.py:156-162), and the reuse spaces per dynamic key (key k:
+ * sp_lo/sp_hi[sp_off[k]..sp_off[k+1])). Live allocations are kept; STW_EPLAN
+ * if a decision or space leaves the reserved pool. */
 int stw_alloc_load_plan(int64_t n_dec, const int32_t *phase, const int64_t *size, const int64_t *addr,
                         const int32_t *t_s, const int64_t *id, int64_t n_keys, const int64_t *sp_off,
                         const int64_t *sp_lo, const int64_t *sp_hi);
@@ -42,20 +49,50 @@ int stw_alloc_load_plan(int64_t n_dec, const int32_t *phase, const int64_t *size
 void stw_set_phase(int32_t phase);
 void stw_set_layer(int32_t key, int32_t dynamic);
 
-/* CUDAPluggableAllocator entry points */
+/* CUDAPluggableAllocator entry points. stw_malloc commits nothing (queue
+ * position, counters) unless the memory is there: on failure it returns NULL
+ * with the state unchanged. Unknown or double frees are counted (the replay
+ * raises SimulationError for them, sim.py:231-232) and make stw_alloc_report
+ * return STW_ESIM. */
 void *stw_malloc(size_t size, int device, void *stream);
 void stw_free(void *ptr, size_t size, int device, void *stream);
 
-/* Virtual address of a live block (pool offset, or cache virtual address >=
+/* Replay address of a live block (pool offset, or cache address >=
  * pool_size), -1 if unknown; route of its allocation (0 planned, 1 reuse,
  * 2 fallback, 3 mismatch). */
 int64_t stw_alloc_vaddr(const void *ptr, int32_t *route);
 
-/* Replay metrics of everything served so far (sim.py:67-117). */
+/* Replay metrics of everything served so far (sim.py:67-117); STW_ESIM if a
+ * planned address was found occupied or an unknown pointer was freed. */
 int stw_alloc_report(stw_report *rep);
 
-/* Release every device allocation and forget the plan. */
-void stw_alloc_shutdown(void);
+/* out[7] = {initialised, pool_size, live blocks, occupied-planned count,
+ * bad frees, mapped bytes of the range, range base}. */
+int stw_alloc_status(int64_t *out);
+
+/* Unmap and release the range and forget the plan; STW_EARG (nothing done)
+ * while any block is live. */
+int stw_alloc_shutdown(void);
+
+/* ---- the same policies as standalone host objects ----------------------
+ * CachingAllocator (baseline.py:35-95) over virtual addresses starting at
+ * `base`: malloc returns STW_ESIM if rid is live, free STW_ESIM if unknown. */
+void *stw_cache_new(int64_t base, int64_t min_segment);
+void stw_cache_delete(void *cache);
+int stw_cache_malloc(void *cache, int64_t rid, int64_t size, int64_t *addr, int64_t *grown);
+int stw_cache_free(void *cache, int64_t rid, int64_t *addr, int64_t *size);
+int stw_cache_owns(void *cache, int64_t rid);
+/* out[5] = {reserved, live_bytes, segments, free blocks, next base} */
+void stw_cache_stats(void *cache, int64_t *out);
+/* segment g: base/size, free blocks blk_lo/blk_hi[blk_off[g] .. blk_off[g+1]) */
+void stw_cache_segments(void *cache, int64_t *seg_base, int64_t *seg_size, int64_t *blk_off, int64_t *blk_lo,
+                        int64_t *blk_hi);
+
+/* dynamic_allocate's placement (sim.py:120-140): best fit of `size` in
+ * free ∩ space (both sorted, coalesced); lowest address of the chosen piece,
+ * -1 when nothing fits. */
+int64_t stw_reuse_best_fit(int64_t n_free, const int64_t *free_lo, const int64_t *free_hi, int64_t n_space,
+                           const int64_t *sp_lo, const int64_t *sp_hi, int64_t size);
 
 #ifdef __cplusplus
 }

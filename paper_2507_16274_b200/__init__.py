@@ -5,6 +5,11 @@
     plan, rmap = memplan.plan_trace(trace)
     report, log = memplan.simulate(trace, plan.to_bundle(rmap))
 
+The reference's module paths work too (`paper_2507_16274_b200.planner`,
+`.sim`, `.reuse`, `.baseline`, `.model`, `.intervals`, `.traceio`, `.synth`),
+sub-operations included (`pack_group`, `try_fuse`, `build_layers_for_size`,
+`CachingAllocator`, `dynamic_allocate`, `compute_metrics`, ...).
+
 Every planning / validation / reuse / replay call runs hand-written sm_100a
 CUDA through libstw.so (include/stw.h); there is no CPU fallback.
 """
@@ -49,7 +54,20 @@ from .api import (
     synthesize_static_plan,
     validate_plan,
 )
-from .planio import read_plan, write_plan
+from .planner import (
+    HomoPhaseGroup,
+    LocalPlan,
+    build_layers_for_size,
+    compute_tmp,
+    fuse_plans,
+    group_by_phase,
+    pack_group,
+    try_fuse,
+    weighted_tmp_average,
+)
+from .baseline import CachingAllocator
+from .sim import PoolState, compute_metrics, dynamic_allocate
+from .traceio import parse_trace, read_plan, write_plan, write_trace
 from .tracegen import PRESETS, SynthConfig, SynthConfigError, synth_trace
 
 __version__ = "0.1.0"

@@ -69,9 +69,24 @@ class RectSets(C.Structure):
         (n, C.c_void_p) for n in ("set_off", "t_s", "t_e", "size", "addr")]
 
 
+class LPlans(C.Structure):
+    _fields_ = [("n_plans", C.c_int64), ("n", C.c_int64)] + [(n, C.c_void_p) for n in (
+        "off", "size", "t_s", "t_e", "addr", "height_in", "t_lo_in", "t_hi_in", "addr_out", "height", "t_lo",
+        "t_hi", "tmp", "rc")]
+
+
+class Fusion(C.Structure):
+    _fields_ = [("n_large", C.c_int64), ("n_small", C.c_int64)] + [(n, C.c_void_p) for n in (
+        "l_addr", "l_size", "l_ts", "l_te", "s_id", "s_size", "s_ts", "s_te")] + [
+        ("l_tmp", C.c_double), ("s_tmp", C.c_double)] + [(n, C.c_int64) for n in (
+            "l_height", "l_dur", "s_height", "s_dur")] + [(n, C.c_void_p) for n in (
+                "out_addr", "out_order", "result_i", "result_d")]
+
+
 EXPORTS = (
     "stw_version", "stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_plan_batches", "stw_validate",
-    "stw_validate_sets", "stw_reuse_map", "stw_simulate", "stw_baseline",
+    "stw_validate_sets", "stw_reuse_map", "stw_simulate", "stw_baseline", "stw_group_events", "stw_local_plans",
+    "stw_weighted_tmp", "stw_fuse_plans", "stw_build_layers", "stw_metrics", "stw_release_scratch",
 )
 
 _lib = None

@@ -78,7 +78,7 @@ import time as _time
 from dataclasses import dataclass as _dataclass
 
 from .domain import DEFAULT_ALIGNMENT, PlanError, TraceError
-from .plan_types import DecisionColumns, MemoryLayer, PlanStats, StaticPlan
+from .plan_types import DecisionColumns, MemoryLayer, PlanStats, StaticPlan, _Keyed
 
 
 @_dataclass
@@ -237,10 +237,11 @@ def _unit_plan(bp: BatchPlan, t: int, c: int, trace, alignment: int, stats) -> S
 
             def slots(members=members):
                 ev = events_fn()
-                return sorted((int(ta.t_s[i]), int(ta.t_e[i]), ev[i]) for i in members.tolist())
+                rows = sorted((int(ta.t_s[i]), int(ta.t_e[i]), i) for i in members.tolist())
+                return [(a, b, _Keyed(ev[i])) for a, b, i in rows]
 
             end = int(ta.t_e[members].max()) if members.size else -1
-            out.append((int(lb[l]), MemoryLayer(int(lsz[l]), int(lb[l]), end, slots_fn=slots)))
+            out.append((int(lb[l]), MemoryLayer(int(lsz[l]), end=end, base=int(lb[l]), slots_fn=slots)))
         return tuple(out)
 
     return StaticPlan.from_columns(int(st[9]), alignment, cols, events_fn, int(st[11]), layers)

@@ -13,6 +13,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libstw.so")
 ALLOC_LIB = os.path.join(PKG, "libstw_alloc.so")
 ALLOC_SRC = os.path.join(PKG, "csrc_alloc", "stw_alloc.cpp")
+IO_LIB = os.path.join(PKG, "libstw_io.so")
+IO_SRC = os.path.join(PKG, "csrc_io", "stw_io.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
@@ -54,8 +56,18 @@ def build_alloc(force: bool = False, verbose: bool = False) -> str:
     return ALLOC_LIB
 
 
+def build_io(force: bool = False, verbose: bool = False) -> str:
+    """libstw_io.so: trace / plan files (host C++ only)."""
+    deps = [IO_SRC, os.path.join(ROOT, "include", "stw_io.h"), os.path.join(ROOT, "include", "stw.h")]
+    if force or not os.path.exists(IO_LIB) or any(os.path.getmtime(p) > os.path.getmtime(IO_LIB) for p in deps):
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-I" + os.path.join(ROOT, "include"), "-o",
+              IO_LIB, IO_SRC], verbose)
+    return IO_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     build_alloc(force, verbose)
+    build_io(force, verbose)
     if force or stale():
         cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *sources()]
         if verbose:

@@ -52,7 +52,7 @@ int stw_peak_live(const stw_batch *b, int32_t static_only, int64_t *peak, void *
 int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begin_bit, int32_t end_bit,
                          void *stream, char *err, size_t errlen) {
   STW_ENTRY(stream, err, errlen);
-  if (begin_bit < 0 || end_bit > 64 || n < 0 || n >= (int64_t)1 << 30) {
+  if (begin_bit < 0 || end_bit > 64 || n < 0 || n > kSortMax) {
     ctx.fail(STW_EARG, "bad sort arguments");
     return ctx.rc;
   }
@@ -88,7 +88,7 @@ int stw_validate(int64_t n, const int64_t *id, const int64_t *addr, const int64_
                  const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap, void *stream, char *err,
                  size_t errlen) {
   STW_ENTRY(stream, err, errlen);
-  if (n < 0 || n >= (int64_t)INT32_MAX || !n_pairs) {
+  if (n < 0 || n > kSortMax || !n_pairs) {  // sorts n decisions (K2 limit)
     ctx.fail(STW_EARG, "bad validate arguments");
     return ctx.rc;
   }
@@ -116,7 +116,7 @@ int stw_reuse_map(int64_t n, const int64_t *addr, const int64_t *size, const int
                   int64_t K, const int64_t *t_lo, const int64_t *t_hi, int64_t *out_off, int64_t *out_lo,
                   int64_t *out_hi, int64_t cap, int64_t *total, void *stream, char *err, size_t errlen) {
   STW_ENTRY(stream, err, errlen);
-  if (n < 0 || n >= (int64_t)INT32_MAX || K < 0 || !total) {
+  if (n < 0 || n > kSortMax || K < 0 || !total) {  // sorts n decisions (K2 limit)
     ctx.fail(STW_EARG, "bad reuse_map arguments");
     return ctx.rc;
   }
@@ -131,6 +131,10 @@ int stw_simulate(const stw_batch *trace, const stw_bundle *plan, stw_report *rep
     ctx.fail(STW_EARG, "null argument");
     return ctx.rc;
   }
+  if (2 * trace->n_events > kSortMax) {  // the op order sorts 2n records
+    ctx.fail(STW_EARG, "trace too large for replay: %lld events (limit 2^29-1)", (long long)trace->n_events);
+    return ctx.rc;
+  }
   replay(ctx, trace, plan, rep, log, err_id);
   return finish(ctx);
 }
@@ -140,6 +144,10 @@ int stw_baseline(const stw_batch *trace, stw_report *rep, stw_log *log, int64_t 
   STW_ENTRY(stream, err, errlen);
   if (!trace || !rep || !err_id) {
     ctx.fail(STW_EARG, "null argument");
+    return ctx.rc;
+  }
+  if (2 * trace->n_events > kSortMax) {  // the op order sorts 2n records
+    ctx.fail(STW_EARG, "trace too large for replay: %lld events (limit 2^29-1)", (long long)trace->n_events);
     return ctx.rc;
   }
   replay(ctx, trace, nullptr, rep, log, err_id);

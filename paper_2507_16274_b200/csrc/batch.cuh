@@ -50,8 +50,8 @@ inline bool stage_batch(Ctx &ctx, Arena &ar, const stw_batch *b, DevBatch *d, co
     ctx.fail(STW_EARG, "bad batch descriptor");
     return false;
   }
-  if (b->n_events >= (int64_t)INT32_MAX) {
-    ctx.fail(STW_EARG, "batch too large: %lld events (limit 2^31-1)", (long long)b->n_events);
+  if (b->n_events > kSortMax) {  // every event-shaped sort goes through K2
+    ctx.fail(STW_EARG, "batch too large: %lld events (limit 2^30-1)", (long long)b->n_events);
     return false;
   }
   bool dev = b->on_device != 0;

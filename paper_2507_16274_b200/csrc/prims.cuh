@@ -18,6 +18,10 @@ void device_scan(Ctx &ctx, Arena &ar, const T *in, T *out, int64_t n, bool inclu
 // ---------------------------------------------------------------------------
 // radix sort
 
+// K2's records per sort: the decoupled look-back packs each digit's running
+// count into 30 bits (flag bits above), so every sort checks n <= kSortMax.
+constexpr int64_t kSortMax = ((int64_t)1 << 30) - 1;
+
 
 void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64_t n, int begin_bit,
                       int end_bit);

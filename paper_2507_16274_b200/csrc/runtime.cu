@@ -114,17 +114,31 @@ void Ctx::fail(int code, const char *fmt, ...) {
   }
 }
 
-static void raise_pool_threshold() {
-  static std::once_flag once;
-  bool first = false;
-  std::call_once(once, [&] { first = true; });
-  if (!first) return;
+// The arena draws from a private memory pool per device (not the device's
+// default pool, which torch's cudaMallocAsync backend shares): its release
+// threshold is raised so chunks stay mapped between calls, and
+// stw_release_scratch() trims it back to the driver.
+static std::mutex g_pool_mu;
+static std::map<int, cudaMemPool_t> g_pools;
+
+static cudaMemPool_t scratch_pool(Ctx &ctx) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  STW_CUDA(ctx, cudaGetDevice(&dev));
+  if (!ctx.ok()) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_pools.find(dev);
+  if (it != g_pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  STW_CUDA(ctx, cudaMemPoolCreate(&pool, &props));
+  if (!ctx.ok()) return nullptr;
   uint64_t thr = UINT64_MAX;
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  g_pools[dev] = pool;
+  return pool;
 }
 
 // Scratch is bump-allocated (256 B aligned) from stream-ordered chunks of at
@@ -140,12 +154,13 @@ void *Arena::raw(size_t bytes) {
       ctx->fail(STW_ECUDA, "scratch arena: too many chunks");
       return nullptr;
     }
-    raise_pool_threshold();
+    cudaMemPool_t pool = scratch_pool(*ctx);
+    if (!pool) return nullptr;
     // large chunks: one planner call takes a few (each cudaMallocAsync is host
     // time the GPU may wait on); the pool keeps them cached between calls
     const size_t chunk = need > kArenaChunk ? need : kArenaChunk;
     void *p = nullptr;
-    STW_CUDA(*ctx, cudaMallocAsync(&p, chunk, ctx->stream));
+    STW_CUDA(*ctx, cudaMallocFromPoolAsync(&p, chunk, pool, ctx->stream));
     if (!ctx->ok()) return nullptr;
     ptrs[n++] = p;
     cur = (char *)p;
@@ -482,6 +497,10 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
 void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64_t n, int begin_bit,
                       int end_bit) {
   if (n <= 1 || end_bit <= begin_bit || !ctx.ok()) return;
+  if (n > kSortMax) {  // the look-back status words hold 30-bit counts
+    ctx.fail(STW_EARG, "radix sort of %lld records exceeds the limit of 2^30-1", (long long)n);
+    return;
+  }
   const int passes = (end_bit - begin_bit + 7) / 8;
   const int64_t ntiles = (n + kOsTile - 1) / kOsTile;
   uint64_t *k2 = ar.take<uint64_t>(n);
@@ -654,6 +673,15 @@ void host_sync(Ctx &ctx) {
 extern "C" {
 
 long long stw_launch_count(void) { return stw::g_launches.load(); }
+
+int stw_release_scratch(void) {
+  using namespace stw;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (cudaDeviceSynchronize() != cudaSuccess) return STW_ECUDA;
+  for (auto &kv : g_pools)
+    if (cudaMemPoolTrimTo(kv.second, 0) != cudaSuccess) return STW_ECUDA;
+  return STW_OK;
+}
 
 void stw_prof_enable(int on) { stw::g_prof_on.store(on != 0); }
 

@@ -1,13 +1,26 @@
-// libstw_alloc -- CUDAPluggableAllocator serving a plan at runtime (include/stw_alloc.h).
+// libstw_alloc -- the runtime side of a plan (include/stw_alloc.h).
 //
-// Host-side state machine with the reference replay's routing (sim.py:143-232,
-// baseline.py:35-95); the memory itself is one cudaMalloc'd pool plus
-// power-of-two fallback segments in HBM.
+// 1. A CUDAPluggableAllocator serving a plan with the reference replay's
+//    routing (sim.py:143-232): planned offsets for static requests, best fit
+//    inside the reuse space for dynamic ones, the CachingAllocator policy
+//    (baseline.py:35-95) for everything else. All of it lives in ONE reserved
+//    virtual range: [base, base + pool_size) is the pool, the fallback
+//    segments follow at base + pool_size + ... exactly where the replay puts
+//    them (sim.py:154), each backed by physical memory mapped on first use
+//    (cuMemCreate / cuMemMap; segments are never returned, like the
+//    reference's). So device pointer = base + replay address for every route.
+// 2. The same CachingAllocator and reuse best fit as standalone host objects
+//    (stw_cache_*, stw_reuse_best_fit) -- what the Python mirror's
+//    CachingAllocator / dynamic_allocate call.
+//
+// Driver entry points come through cudaGetDriverEntryPoint, so the library
+// loads (and the standalone allocator objects work) without a GPU.
 #include "../../include/stw_alloc.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
-
 #include <math.h>
+#include <string.h>
 
 #include <algorithm>
 #include <deque>
@@ -18,13 +31,132 @@
 
 namespace {
 
-constexpr int64_t kMinSegment = 2ll * 1024 * 1024;
+constexpr int64_t kMinSegment = 2ll * 1024 * 1024;  // baseline.py:17
+constexpr int64_t kDefaultFallbackVa = 256ll << 30;
 
-struct Segment {
-  int64_t vbase, size;
-  char *dev;
-  std::vector<std::pair<int64_t, int64_t>> free;  // sorted (lo, hi) virtual
+typedef std::pair<int64_t, int64_t> Iv;  // [lo, hi)
+
+int64_t next_pow2(int64_t n) {  // baseline.py:20-21
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// CachingAllocator policy over virtual addresses (baseline.py:35-95)
+
+struct Seg {
+  int64_t base, size;
+  std::vector<Iv> free;  // sorted, disjoint
 };
+
+struct CacheCore {
+  int64_t next_base = 0, min_segment = kMinSegment, reserved = 0, live_bytes = 0;
+  std::vector<Seg> segs;
+
+  // best fit over every free block in (segment, address) order; the first
+  // minimal block wins (baseline.py:54-59)
+  bool find(int64_t size, int *g, int *i) const {
+    int bg = -1, bi = -1;
+    int64_t blen = 0;
+    for (int s = 0; s < (int)segs.size(); s++)
+      for (int k = 0; k < (int)segs[s].free.size(); k++) {
+        const int64_t len = segs[s].free[k].second - segs[s].free[k].first;
+        if (len >= size && (bg < 0 || len < blen)) bg = s, bi = k, blen = len;
+      }
+    *g = bg;
+    *i = bi;
+    return bg >= 0;
+  }
+  int64_t segment_size(int64_t size) const { return std::max(min_segment, next_pow2(size)); }
+  int add_segment(int64_t ss) {  // a miss: a fresh segment at the next base (baseline.py:61-69)
+    segs.push_back(Seg{next_base, ss, {Iv(next_base, next_base + ss)}});
+    next_base += ss;
+    reserved += ss;
+    return (int)segs.size() - 1;
+  }
+  int64_t carve(int g, int i, int64_t size) {  // split the block (baseline.py:71-76)
+    auto &fr = segs[g].free;
+    const Iv b = fr[i];
+    fr.erase(fr.begin() + i);
+    if (b.first + size < b.second) fr.insert(fr.begin() + i, Iv(b.first + size, b.second));
+    live_bytes += size;
+    return b.first;
+  }
+  void give_back(int g, int64_t lo, int64_t size) {  // insort + merge (baseline.py:79-95)
+    auto &fr = segs[g].free;
+    const int64_t hi = lo + size;
+    auto pos = std::lower_bound(fr.begin(), fr.end(), Iv(lo, hi));
+    size_t i = pos - fr.begin();
+    fr.insert(pos, Iv(lo, hi));
+    if (i + 1 < fr.size() && fr[i + 1].first == hi) {
+      fr[i].second = fr[i + 1].second;
+      fr.erase(fr.begin() + i + 1);
+    }
+    if (i > 0 && fr[i - 1].second == lo) {
+      fr[i - 1].second = fr[i].second;
+      fr.erase(fr.begin() + i);
+    }
+    live_bytes -= size;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// best fit inside free ∩ space (sim.py:120-140 over intervals.py:138-176): the
+// smallest intersection piece holding `size`, ties to the lowest address.
+// Free and space are coalesced, so the pieces come out disjoint and ascending.
+
+template <class It>
+int64_t best_fit_pieces(It f, It fend, const Iv *sp, int64_t nsp, int64_t size) {
+  int64_t best_len = INT64_MAX, best_lo = -1;
+  for (int64_t s = 0; s < nsp; s++) {
+    while (f != fend && f->second <= sp[s].first) ++f;
+    for (It g = f; g != fend && g->first < sp[s].second; ++g) {
+      const int64_t lo = std::max(g->first, sp[s].first), hi = std::min(g->second, sp[s].second);
+      if (hi - lo >= size && hi - lo < best_len) best_len = hi - lo, best_lo = lo;
+    }
+  }
+  return best_lo;
+}
+
+// ---------------------------------------------------------------------------
+// driver entry points (virtual memory management)
+
+struct Drv {
+  bool ok = false;
+  decltype(&cuMemAddressReserve) addressReserve;
+  decltype(&cuMemAddressFree) addressFree;
+  decltype(&cuMemCreate) create;
+  decltype(&cuMemRelease) release;
+  decltype(&cuMemMap) map;
+  decltype(&cuMemUnmap) unmap;
+  decltype(&cuMemSetAccess) setAccess;
+  decltype(&cuMemGetAllocationGranularity) granularity;
+};
+
+template <class F>
+bool entry(const char *name, F *f) {
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
+  *f = reinterpret_cast<F>(p);
+  return true;
+}
+
+Drv &drv() {
+  static Drv d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    d.ok = entry("cuMemAddressReserve", &d.addressReserve) && entry("cuMemAddressFree", &d.addressFree) &&
+           entry("cuMemCreate", &d.create) && entry("cuMemRelease", &d.release) && entry("cuMemMap", &d.map) &&
+           entry("cuMemUnmap", &d.unmap) && entry("cuMemSetAccess", &d.setAccess) &&
+           entry("cuMemGetAllocationGranularity", &d.granularity);
+  });
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// the pluggable allocator's state
 
 struct Live {
   int space;  // 0 pool, 1 cache
@@ -33,21 +165,28 @@ struct Live {
   int seg;
 };
 
+struct Mapping {
+  int64_t off, size;
+  CUmemGenericAllocationHandle h;
+};
+
 struct State {
   std::mutex mu;
+  bool inited = false;
   int device = 0;
   int64_t pool_size = 0, alignment = 512;
-  char *pool = nullptr;
+  CUdeviceptr base = 0;
+  int64_t va_size = 0, gran = 0, mapped_hi = 0;  // [0, mapped_hi) of the range is backed
+  std::vector<Mapping> maps;
   std::map<int64_t, int64_t> free;  // coalesced free intervals of the pool (lo -> hi)
   std::map<std::pair<int32_t, int64_t>, std::deque<int64_t>> queues;
-  std::vector<std::vector<std::pair<int64_t, int64_t>>> spaces;
-  std::vector<Segment> segs;
-  int64_t next_vbase = 0;
+  std::vector<std::vector<Iv>> spaces;
+  CacheCore cache;
   std::unordered_map<const void *, Live> live;
   int32_t phase = 0, key = -1, dynamic = 0;
   // metrics (sim.py:67-117)
-  int64_t cur = 0, peak = 0, cache_cur = 0, cache_peak = 0, reserved = 0;
-  int64_t fallback = 0, reuse = 0, mismatch = 0, occupied = 0;
+  int64_t cur = 0, peak = 0, cache_cur = 0, cache_peak = 0;
+  int64_t fallback = 0, reuse = 0, mismatch = 0, occupied = 0, bad_frees = 0;
 };
 
 State &S() {
@@ -55,7 +194,63 @@ State &S() {
   return s;
 }
 
-bool pool_contains(State &s, int64_t lo, int64_t hi) {
+// back [mapped_hi, roundup(end)) of the reserved range with fresh physical memory
+bool map_upto(State &s, int64_t end) {
+  if (end <= s.mapped_hi) return true;
+  if (end > s.va_size) return false;
+  Drv &d = drv();
+  const int64_t hi = (end + s.gran - 1) / s.gran * s.gran, sz = hi - s.mapped_hi;
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = s.device;
+  CUmemGenericAllocationHandle h;
+  if (d.create(&h, (size_t)sz, &prop, 0) != CUDA_SUCCESS) return false;
+  if (d.map(s.base + s.mapped_hi, (size_t)sz, 0, h, 0) != CUDA_SUCCESS) {
+    d.release(h);
+    return false;
+  }
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = s.device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.setAccess(s.base + s.mapped_hi, (size_t)sz, &acc, 1) != CUDA_SUCCESS) {
+    d.unmap(s.base + s.mapped_hi, (size_t)sz);
+    d.release(h);
+    return false;
+  }
+  s.maps.push_back(Mapping{s.mapped_hi, sz, h});
+  s.mapped_hi = hi;
+  return true;
+}
+
+void unmap_all(State &s) {
+  Drv &d = drv();
+  for (auto &m : s.maps) {
+    d.unmap(s.base + m.off, (size_t)m.size);
+    d.release(m.h);
+  }
+  s.maps.clear();
+  if (s.base) d.addressFree(s.base, (size_t)s.va_size);
+  s.base = 0;
+  s.va_size = s.mapped_hi = 0;
+}
+
+void reset(State &s) {
+  s.inited = false;
+  s.free.clear();
+  s.queues.clear();
+  s.spaces.clear();
+  s.cache = CacheCore();
+  s.live.clear();
+  s.cur = s.peak = s.cache_cur = s.cache_peak = 0;
+  s.fallback = s.reuse = s.mismatch = s.occupied = s.bad_frees = 0;
+  s.phase = 0;
+  s.key = -1;
+  s.dynamic = 0;
+}
+
+bool pool_contains(State &s, int64_t lo, int64_t hi) {  // IntervalSet.contains_interval (intervals.py:95-98)
   auto it = s.free.upper_bound(lo);
   if (it == s.free.begin()) return false;
   --it;
@@ -65,7 +260,7 @@ bool pool_contains(State &s, int64_t lo, int64_t hi) {
 void pool_remove(State &s, int64_t lo, int64_t hi) {  // [lo, hi) lies inside one free interval
   auto it = s.free.upper_bound(lo);
   --it;
-  int64_t a = it->first, b = it->second;
+  const int64_t a = it->first, b = it->second;
   s.free.erase(it);
   if (a < lo) s.free[a] = lo;
   if (hi < b) s.free[hi] = b;
@@ -85,69 +280,12 @@ void pool_add(State &s, int64_t lo, int64_t hi) {  // IntervalSet.add (intervals
   s.free[lo] = hi;
 }
 
-// best fit inside free ∩ space (sim.py:120-140, intervals.py:138-176)
 int64_t reuse_fit(State &s, int key, int64_t size) {
   if (key < 0 || key >= (int)s.spaces.size() || s.spaces[key].empty()) return -1;
-  int64_t best_len = INT64_MAX, best_lo = -1;
-  for (auto &sp : s.spaces[key]) {
-    auto it = s.free.upper_bound(sp.first);
-    if (it != s.free.begin()) --it;
-    for (; it != s.free.end() && it->first < sp.second; ++it) {
-      int64_t lo = std::max(it->first, sp.first), hi = std::min(it->second, sp.second);
-      if (hi - lo >= size && hi - lo < best_len) best_len = hi - lo, best_lo = lo;
-    }
-  }
-  return best_lo;
-}
-
-int64_t next_pow2(int64_t n) {
-  int64_t p = 1;
-  while (p < n) p <<= 1;
-  return p;
-}
-
-// CachingAllocator.malloc (baseline.py:49-77); returns virtual address or -1
-int64_t cache_malloc(State &s, int64_t size, int *seg_out) {
-  int bs = -1, bi = -1;
-  int64_t blen = 0;
-  for (int g = 0; g < (int)s.segs.size(); g++)
-    for (int i = 0; i < (int)s.segs[g].free.size(); i++) {
-      int64_t len = s.segs[g].free[i].second - s.segs[g].free[i].first;
-      if (len >= size && (bs < 0 || len < blen)) bs = g, bi = i, blen = len;
-    }
-  if (bs < 0) {
-    int64_t ss = std::max(kMinSegment, next_pow2(size));
-    Segment seg{s.next_vbase, ss, nullptr, {}};
-    if (cudaMalloc(&seg.dev, (size_t)ss) != cudaSuccess) return -1;
-    seg.free.push_back({seg.vbase, seg.vbase + ss});
-    s.next_vbase += ss;
-    s.reserved += ss;
-    s.segs.push_back(std::move(seg));
-    bs = (int)s.segs.size() - 1;
-    bi = 0;
-  }
-  Segment &seg = s.segs[bs];
-  auto blk = seg.free[bi];
-  seg.free.erase(seg.free.begin() + bi);
-  if (blk.first + size < blk.second) seg.free.insert(seg.free.begin() + bi, {blk.first + size, blk.second});
-  *seg_out = bs;
-  return blk.first;
-}
-
-void cache_free(State &s, int g, int64_t lo, int64_t size) {  // CachingAllocator.free (baseline.py:79-95)
-  auto &fr = s.segs[g].free;
-  int64_t hi = lo + size;
-  auto pos = std::lower_bound(fr.begin(), fr.end(), std::make_pair(lo, hi));
-  size_t i = pos - fr.begin();
-  fr.insert(pos, {lo, hi});
-  if (i + 1 < fr.size() && fr[i + 1].first == hi) {
-    fr[i].second = fr[i + 1].second;
-    fr.erase(fr.begin() + i + 1);
-  }
-  if (i > 0 && fr[i - 1].second == lo) {
-    fr[i - 1].second = fr[i].second;
-    fr.erase(fr.begin() + i);
-  }
+  const auto &sp = s.spaces[key];
+  auto f = s.free.upper_bound(sp[0].first);
+  if (f != s.free.begin()) --f;
+  return best_fit_pieces(f, s.free.end(), sp.data(), (int64_t)sp.size(), size);
 }
 
 // correctly rounded a / b, like Python's int true division (sim.py:103-106)
@@ -196,26 +334,56 @@ void account_alloc(State &s, int64_t size, bool cache, int route) {
   if (route == 1) s.reuse++;
 }
 
+// standalone CachingAllocator object of the handle API
+struct CacheObj {
+  CacheCore core;
+  struct Blk {
+    int seg;
+    int64_t lo, size;
+  };
+  std::unordered_map<int64_t, Blk> live;
+};
+
 }  // namespace
 
 extern "C" {
 
-int stw_alloc_init(int device, int64_t pool_size, int64_t alignment) {
+int stw_alloc_init_ex(int device, int64_t pool_size, int64_t alignment, int64_t fallback_va) {
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
-  if (s.pool) return STW_EARG;
-  if (cudaSetDevice(device) != cudaSuccess) return STW_ECUDA;
+  if (s.inited || pool_size < 0) return STW_EARG;
+  Drv &d = drv();
+  if (!d.ok || cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) return STW_ECUDA;
+  reset(s);
   s.device = device;
   s.pool_size = pool_size;
   s.alignment = alignment > 0 ? alignment : 512;
-  if (pool_size > 0 && cudaMalloc(&s.pool, (size_t)pool_size) != cudaSuccess) {
-    s.pool = nullptr;
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  size_t g = 0;
+  if (d.granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || g == 0) return STW_ECUDA;
+  s.gran = (int64_t)g;
+  const int64_t fb = fallback_va > 0 ? fallback_va : kDefaultFallbackVa;
+  s.va_size = ((pool_size + fb) + s.gran - 1) / s.gran * s.gran;
+  if (d.addressReserve(&s.base, (size_t)s.va_size, 0, 0, 0) != CUDA_SUCCESS) {
+    s.base = 0;
     return STW_ECUDA;
   }
-  s.free.clear();
+  s.mapped_hi = 0;
+  if (pool_size > 0 && !map_upto(s, pool_size)) {  // the pool is backed up front
+    unmap_all(s);
+    return STW_ECUDA;
+  }
   if (pool_size > 0) s.free[0] = pool_size;
-  s.next_vbase = pool_size;
+  s.cache.next_base = pool_size;  // the replay's cache starts at pool_size (sim.py:154)
+  s.inited = true;
   return STW_OK;
+}
+
+int stw_alloc_init(int device, int64_t pool_size, int64_t alignment) {
+  return stw_alloc_init_ex(device, pool_size, alignment, 0);
 }
 
 int stw_alloc_load_plan(int64_t n_dec, const int32_t *phase, const int64_t *size, const int64_t *addr,
@@ -223,19 +391,23 @@ int stw_alloc_load_plan(int64_t n_dec, const int32_t *phase, const int64_t *size
                         const int64_t *sp_lo, const int64_t *sp_hi) {
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
+  if (!s.inited) return STW_EARG;
   std::vector<int64_t> order(n_dec);
-  for (int64_t k = 0; k < n_dec; k++) order[k] = k;
+  for (int64_t k = 0; k < n_dec; k++) {
+    order[k] = k;
+    if (addr[k] < 0 || addr[k] + size[k] > s.pool_size) return STW_EPLAN;
+  }
+  for (int64_t k = 0; k < n_keys; k++)
+    for (int64_t j = sp_off[k]; j < sp_off[k + 1]; j++)
+      if (sp_lo[j] < 0 || sp_hi[j] > s.pool_size) return STW_EPLAN;
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
     return t_s[a] != t_s[b] ? t_s[a] < t_s[b] : id[a] < id[b];
   });
   s.queues.clear();
-  for (int64_t k : order) {
-    if (addr[k] < 0 || addr[k] + size[k] > s.pool_size) return STW_EPLAN;
-    s.queues[{phase[k], size[k]}].push_back(addr[k]);
-  }
+  for (int64_t k : order) s.queues[{phase[k], size[k]}].push_back(addr[k]);
   s.spaces.assign(n_keys, {});
   for (int64_t k = 0; k < n_keys; k++)
-    for (int64_t j = sp_off[k]; j < sp_off[k + 1]; j++) s.spaces[k].push_back({sp_lo[j], sp_hi[j]});
+    for (int64_t j = sp_off[k]; j < sp_off[k + 1]; j++) s.spaces[k].push_back(Iv(sp_lo[j], sp_hi[j]));
   return STW_OK;
 }
 
@@ -257,47 +429,46 @@ void *stw_malloc(size_t nbytes, int device, void *stream) {
   (void)stream;
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
+  if (!s.inited) return nullptr;
   if (nbytes == 0) nbytes = 1;
-  int64_t size = (int64_t)((nbytes + s.alignment - 1) / s.alignment * s.alignment);
+  const int64_t size = (int64_t)((nbytes + s.alignment - 1) / s.alignment * s.alignment);
+  // decide the route first; nothing is committed until the memory is there
   int route;
   int64_t vaddr = -1;
+  std::deque<int64_t> *q = nullptr;
   if (s.dynamic) {
     vaddr = reuse_fit(s, s.key, size);
-    if (vaddr >= 0) {
-      pool_remove(s, vaddr, vaddr + size);
-      route = 1;
-    } else {
-      route = 2;
-    }
+    route = vaddr >= 0 ? 1 : 2;
   } else {
     route = 3;
-    auto q = s.queues.find({s.phase, size});
-    if (q != s.queues.end() && !q->second.empty()) {
-      int64_t a = q->second.front();
-      q->second.pop_front();
-      if (pool_contains(s, a, a + size)) {
-        pool_remove(s, a, a + size);
-        vaddr = a;
+    auto it = s.queues.find({s.phase, size});
+    if (it != s.queues.end() && !it->second.empty()) {
+      q = &it->second;
+      if (pool_contains(s, q->front(), q->front() + size)) {
+        vaddr = q->front();
         route = 0;
-      } else {
-        s.occupied++;  // the replay would raise SimulationError; a live run falls back instead
       }
     }
   }
   Live lv{0, route, vaddr, size, -1};
-  char *ptr;
-  if (route == 0 || route == 1) {
-    ptr = s.pool + vaddr;
-  } else {
-    int g;
-    int64_t before = s.reserved;
-    vaddr = cache_malloc(s, size, &g);
-    if (vaddr < 0) return nullptr;
-    (void)before;
-    ptr = s.segs[g].dev + (vaddr - s.segs[g].vbase);
-    lv = Live{1, route, vaddr, size, g};
+  if (route == 2 || route == 3) {
+    int g, i;
+    if (!s.cache.find(size, &g, &i)) {
+      const int64_t ss = s.cache.segment_size(size);
+      if (!map_upto(s, s.cache.next_base + ss)) return nullptr;  // out of memory: state untouched
+      g = s.cache.add_segment(ss);
+      i = 0;
+    }
+    lv = Live{1, route, s.cache.carve(g, i, size), size, g};
+    // the replay raises SimulationError on an occupied planned address; a live
+    // run serves the request from the cache and reports it (stw_alloc_report)
+    if (q && route == 3) s.occupied++;
+  } else if (route == 0 || route == 1) {
+    pool_remove(s, vaddr, vaddr + size);
   }
+  if (q) q->pop_front();
   account_alloc(s, size, lv.space == 1, route);
+  void *ptr = reinterpret_cast<void *>(s.base + lv.vaddr);
   s.live[ptr] = lv;
   return ptr;
 }
@@ -309,15 +480,18 @@ void stw_free(void *ptr, size_t nbytes, int device, void *stream) {
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
   auto it = s.live.find(ptr);
-  if (it == s.live.end()) return;
-  Live lv = it->second;
+  if (it == s.live.end()) {  // unknown or double free (sim.py:231-232): counted, reported by stw_alloc_report
+    s.bad_frees++;
+    return;
+  }
+  const Live lv = it->second;
   s.live.erase(it);
   s.cur -= lv.size;
   if (lv.space == 0) {
     pool_add(s, lv.vaddr, lv.vaddr + lv.size);
   } else {
     s.cache_cur -= lv.size;
-    cache_free(s, lv.seg, lv.vaddr, lv.size);
+    s.cache.give_back(lv.seg, lv.vaddr, lv.size);
   }
 }
 
@@ -334,7 +508,7 @@ int stw_alloc_report(stw_report *rep) {
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
   rep->allocated_peak = s.peak;
-  rep->reserved_peak = s.pool_size + s.reserved;
+  rep->reserved_peak = s.pool_size + s.cache.reserved;
   rep->pool_size = s.pool_size;
   rep->fallback_count = s.fallback;
   rep->fallback_bytes_peak = s.cache_peak;
@@ -342,25 +516,106 @@ int stw_alloc_report(stw_report *rep) {
   rep->mismatch_count = s.mismatch;
   rep->efficiency = rep->reserved_peak ? exact_div((uint64_t)rep->allocated_peak, (uint64_t)rep->reserved_peak) : 1.0;
   rep->fragmentation = 1.0 - rep->efficiency;
-  return s.occupied ? STW_ESIM : STW_OK;
+  return s.occupied || s.bad_frees ? STW_ESIM : STW_OK;
 }
 
-void stw_alloc_shutdown(void) {
+int stw_alloc_status(int64_t *out) {
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
-  if (s.pool) cudaFree(s.pool);
-  for (auto &g : s.segs) cudaFree(g.dev);
-  s.pool = nullptr;
-  s.segs.clear();
-  s.free.clear();
-  s.queues.clear();
-  s.spaces.clear();
-  s.live.clear();
-  s.cur = s.peak = s.cache_cur = s.cache_peak = s.reserved = 0;
-  s.fallback = s.reuse = s.mismatch = s.occupied = 0;
-  s.phase = 0;
-  s.key = -1;
-  s.dynamic = 0;
+  out[0] = s.inited;
+  out[1] = s.pool_size;
+  out[2] = (int64_t)s.live.size();
+  out[3] = s.occupied;
+  out[4] = s.bad_frees;
+  out[5] = s.mapped_hi;
+  out[6] = (int64_t)s.base;
+  return STW_OK;
+}
+
+int stw_alloc_shutdown(void) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  if (!s.live.empty()) return STW_EARG;  // live tensors still point into the range
+  if (s.inited) unmap_all(s);
+  reset(s);
+  return STW_OK;
+}
+
+// ---- standalone allocator objects ---------------------------------------
+
+void *stw_cache_new(int64_t base, int64_t min_segment) {
+  CacheObj *c = new CacheObj();
+  c->core.next_base = base;
+  c->core.min_segment = min_segment;
+  return c;
+}
+
+void stw_cache_delete(void *h) { delete static_cast<CacheObj *>(h); }
+
+int stw_cache_malloc(void *h, int64_t rid, int64_t size, int64_t *addr, int64_t *grown) {
+  CacheObj *c = static_cast<CacheObj *>(h);
+  if (c->live.count(rid)) return STW_ESIM;  // "request {rid} already live in cache"
+  int g, i;
+  *grown = 0;
+  if (!c->core.find(size, &g, &i)) {
+    const int64_t ss = c->core.segment_size(size);
+    g = c->core.add_segment(ss);
+    i = 0;
+    *grown = ss;
+  }
+  *addr = c->core.carve(g, i, size);
+  c->live[rid] = CacheObj::Blk{g, *addr, size};
+  return STW_OK;
+}
+
+int stw_cache_free(void *h, int64_t rid, int64_t *addr, int64_t *size) {
+  CacheObj *c = static_cast<CacheObj *>(h);
+  auto it = c->live.find(rid);
+  if (it == c->live.end()) return STW_ESIM;  // "free of unknown id {rid} in cache"
+  const CacheObj::Blk b = it->second;
+  c->live.erase(it);
+  c->core.give_back(b.seg, b.lo, b.size);
+  *addr = b.lo;
+  *size = b.size;
+  return STW_OK;
+}
+
+int stw_cache_owns(void *h, int64_t rid) { return static_cast<CacheObj *>(h)->live.count(rid) ? 1 : 0; }
+
+void stw_cache_stats(void *h, int64_t *out) {
+  CacheObj *c = static_cast<CacheObj *>(h);
+  int64_t blocks = 0;
+  for (auto &g : c->core.segs) blocks += (int64_t)g.free.size();
+  out[0] = c->core.reserved;
+  out[1] = c->core.live_bytes;
+  out[2] = (int64_t)c->core.segs.size();
+  out[3] = blocks;
+  out[4] = c->core.next_base;
+}
+
+void stw_cache_segments(void *h, int64_t *seg_base, int64_t *seg_size, int64_t *blk_off, int64_t *blk_lo,
+                        int64_t *blk_hi) {
+  CacheObj *c = static_cast<CacheObj *>(h);
+  int64_t k = 0;
+  for (size_t g = 0; g < c->core.segs.size(); g++) {
+    const Seg &s = c->core.segs[g];
+    seg_base[g] = s.base;
+    seg_size[g] = s.size;
+    blk_off[g] = k;
+    for (auto &b : s.free) blk_lo[k] = b.first, blk_hi[k] = b.second, k++;
+  }
+  blk_off[c->core.segs.size()] = k;
+}
+
+int64_t stw_reuse_best_fit(int64_t n_free, const int64_t *free_lo, const int64_t *free_hi, int64_t n_space,
+                           const int64_t *sp_lo, const int64_t *sp_hi, int64_t size) {
+  std::vector<Iv> fr(n_free), sp(n_space);
+  for (int64_t k = 0; k < n_free; k++) fr[k] = Iv(free_lo[k], free_hi[k]);
+  for (int64_t k = 0; k < n_space; k++) sp[k] = Iv(sp_lo[k], sp_hi[k]);
+  if (sp.empty()) return -1;
+  auto f = std::upper_bound(fr.begin(), fr.end(), Iv(sp[0].first, INT64_MAX));
+  if (f != fr.begin()) --f;
+  return best_fit_pieces(f, fr.end(), sp.data(), n_space, size);
 }
 
 }  // extern "C"

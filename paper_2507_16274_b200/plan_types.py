@@ -8,6 +8,7 @@ array consumers (the replay scorer, the batched sweep) never pay for objects.
 
 from __future__ import annotations
 
+from bisect import bisect_left
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -52,27 +53,73 @@ class PlanStats:
         }
 
 
+class _Keyed:
+    """Opaque slot payload holder (planner.py:215-222): slots compare by their
+    lifespans only, the payload rides along as `.value`."""
+
+    __slots__ = ("value",)
+
+    def __init__(self, value):
+        self.value = value
+
+    def __repr__(self) -> str:
+        return f"_Keyed({self.value!r})"
+
+
 class MemoryLayer:
-    """A size-S address band of the final plan (planner.py:189-212), as emitted by
-    the device: its occupants' lifespans, sorted by start."""
+    """A size-S address band time-shared by lifespan-disjoint occupants
+    (planner.py:189-212). `slots` holds (t_s, t_e, _Keyed(payload)) sorted by
+    start; `end` is the largest t_e inserted. Layers of a device plan fill
+    their slots lazily from the plan's columns, one slot per member event."""
 
-    __slots__ = ("size", "base", "end", "_slots_fn", "_slots")
+    __slots__ = ("size", "base", "end", "_slots", "_starts", "_slots_fn")
 
-    def __init__(self, size: int, base: Optional[int] = None, end: int = -1, slots=None, slots_fn=None):
+    def __init__(self, size: int, slots=None, end: int = -1, base: Optional[int] = None, *, slots_fn=None):
         self.size = size
         self.base = base
         self.end = end
-        self._slots = slots
+        self._slots = list(slots) if slots is not None else (None if slots_fn else [])
+        self._starts = None
         self._slots_fn = slots_fn
 
     @property
     def slots(self) -> list:
         if self._slots is None:
-            self._slots = self._slots_fn() if self._slots_fn else []
+            self._slots = self._slots_fn()
         return self._slots
 
+    def _starts_list(self) -> list:
+        if self._starts is None or len(self._starts) != len(self.slots):
+            self._starts = [s[0] for s in self.slots]
+        return self._starts
+
+    def fits_gap(self, t_s, t_e) -> bool:
+        """True iff [t_s, t_e] (closed) touches no slot (planner.py:199-205)."""
+        starts = self._starts_list()
+        i = bisect_left(starts, t_s)
+        if i and self.slots[i - 1][1] >= t_s:
+            return False
+        return not (i < len(starts) and starts[i] <= t_e)
+
+    def insert(self, t_s, t_e, payload) -> None:
+        """Add an occupant, keeping slots sorted by start (planner.py:207-212)."""
+        starts = self._starts_list()
+        i = bisect_left(starts, t_s)
+        starts.insert(i, t_s)
+        self.slots.insert(i, (t_s, t_e, _Keyed(payload)))
+        if t_e > self.end:
+            self.end = t_e
+
+    def __eq__(self, other):
+        if not isinstance(other, MemoryLayer):
+            return NotImplemented
+        return (self.size, self.end, self.base, [s[:2] for s in self.slots]) == (
+            other.size, other.end, other.base, [s[:2] for s in other.slots])
+
+    __hash__ = None
+
     def __repr__(self) -> str:
-        return f"MemoryLayer(size={self.size}, base={self.base})"
+        return f"MemoryLayer(size={self.size}, base={self.base}, end={self.end})"
 
 
 @dataclass(frozen=True)

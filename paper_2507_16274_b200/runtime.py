@@ -46,7 +46,21 @@ def load() -> C.CDLL:
         L.stw_alloc_vaddr.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.stw_set_phase.restype = None
         L.stw_set_layer.restype = None
-        L.stw_alloc_shutdown.restype = None
+        L.stw_alloc_shutdown.restype = C.c_int
+        L.stw_cache_new.restype = C.c_void_p
+        L.stw_cache_new.argtypes = [C.c_int64, C.c_int64]
+        L.stw_cache_delete.restype = None
+        L.stw_cache_delete.argtypes = [C.c_void_p]
+        L.stw_cache_malloc.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        L.stw_cache_free.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.stw_cache_owns.argtypes = [C.c_void_p, C.c_int64]
+        L.stw_cache_stats.restype = None
+        L.stw_cache_stats.argtypes = [C.c_void_p, C.c_void_p]
+        L.stw_cache_segments.restype = None
+        L.stw_cache_segments.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        L.stw_reuse_best_fit.restype = C.c_int64
+        L.stw_reuse_best_fit.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_int64]
         _alib = L
     return _alib
 
@@ -58,10 +72,18 @@ class PlanAllocator:
         self.ta = from_trace(trace)
         self.bundle = bundle
         L = load()
-        L.stw_alloc_shutdown()
-        rc = L.stw_alloc_init(C.c_int(device), C.c_int64(int(bundle.pool_size)), C.c_int64(int(bundle.alignment)))
-        if rc != 0:
-            raise DeviceError(f"stw_alloc_init failed ({rc})")
+        st = self.status()
+        if st["initialised"] and st["live"] == 0:
+            L.stw_alloc_shutdown()  # nothing points into the old range
+            st["initialised"] = 0
+        if not st["initialised"]:
+            rc = L.stw_alloc_init(C.c_int(device), C.c_int64(int(bundle.pool_size)),
+                                  C.c_int64(int(bundle.alignment)))
+            if rc != 0:
+                raise DeviceError(f"stw_alloc_init failed ({rc})")
+        elif st["pool_size"] < int(bundle.pool_size):
+            raise DeviceError(f"allocator installed with a {st['pool_size']}-byte pool and {st['live']} live blocks; "
+                              f"cannot serve a {int(bundle.pool_size)}-byte plan without freeing them")
         cols = getattr(bundle, "_cols", None) or DecisionColumns.from_decisions(tuple(bundle.decisions))
         # decision -> phase of its event (events_by_id, last one wins: sim.py:156-161); unknown/dynamic ids skipped
         idx = {int(i): k for k, i in enumerate(self.ta.id.tolist())}
@@ -135,6 +157,9 @@ class PlanAllocator:
         out = SimReport(rep.allocated_peak, rep.reserved_peak, rep.efficiency, rep.fragmentation, rep.pool_size,
                         rep.fallback_count, rep.fallback_bytes_peak, rep.reuse_hits, rep.mismatch_count)
         if rc == _lib.STW_ESIM:
+            st = PlanAllocator.status()
+            if st["bad_frees"]:
+                raise SimulationError(f"{st['bad_frees']} free(s) of unknown or already freed blocks")
             raise SimulationError("a planned address was occupied at runtime")
         return out
 
@@ -173,5 +198,14 @@ class PlanAllocator:
         return out
 
     @staticmethod
+    def status() -> dict:
+        out = np.zeros(7, np.int64)
+        load().stw_alloc_status(_lib.ptr(out))
+        keys = ("initialised", "pool_size", "live", "occupied", "bad_frees", "mapped_bytes", "base")
+        return {k: int(v) for k, v in zip(keys, out)}
+
+    @staticmethod
     def shutdown() -> None:
-        load().stw_alloc_shutdown()
+        """Release the reserved range; refused while blocks are live."""
+        if load().stw_alloc_shutdown() != 0:
+            raise DeviceError("stw_alloc_shutdown refused: blocks are still live")

@@ -37,6 +37,37 @@ def test_library_exports_every_declared_symbol():
     assert set(declared_functions()) <= exported
 
 
+def _declared(header):
+    text = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", header)).read(), flags=re.S)
+    return sorted(set(re.findall(r"\b(stw_\w+)\s*\(", text)))
+
+
+@pytest.mark.parametrize("header,lib", [("stw_alloc.h", "libstw_alloc.so"), ("stw_io.h", "libstw_io.so")])
+def test_host_libraries_export_their_headers(header, lib):
+    """libstw_alloc.so (runtime allocator + CachingAllocator core) and
+    libstw_io.so (trace/plan files) export every function their header
+    declares and load without a GPU."""
+    from paper_2507_16274_b200 import build, runtime, traceio
+
+    build.build_alloc()
+    build.build_io()
+    path = os.path.join(ROOT, "paper_2507_16274_b200", lib)
+    L = runtime.load() if lib == "libstw_alloc.so" else traceio.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (stw_\w+)", out))
+    names = set(_declared(header)) - set(declared_functions())
+    assert names and names <= exported, names - exported
+    for n in names:
+        assert hasattr(L, n)
+
+
+def test_sub_operations_declared():
+    names = declared_functions()
+    for must in ("stw_group_events", "stw_local_plans", "stw_weighted_tmp", "stw_fuse_plans", "stw_build_layers",
+                 "stw_metrics", "stw_release_scratch"):
+        assert must in names
+
+
 def test_library_is_sm100a_only():
     from paper_2507_16274_b200 import _lib
 

@@ -47,3 +47,36 @@ def test_allocator_as_torch_pluggable_allocator():
                          text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "torch pluggable allocator ok" in res.stdout
+
+
+def test_one_reserved_range_and_misuse_reporting():
+    """Every block (pool or fallback) sits at range base + its replay address;
+    unknown / double frees are reported; no teardown under live blocks; a plan
+    reload keeps live blocks."""
+    import ctypes as C
+
+    from paper_2507_16274_b200 import runtime as R
+
+    ta = tracegen.synth_arrays(tracegen.SynthConfig.for_preset("moe", seed=2, num_layers=4, num_microbatches=2))
+    tr = M.Trace.from_arrays(ta)
+    plan, rmap = M.plan_trace(tr)
+    bundle = plan.to_bundle(rmap)
+    rt = PlanAllocator(bundle, tr)
+    L = R.load()
+    base = rt.status()["base"]
+    try:
+        L.stw_set_layer(C.c_int32(-1), C.c_int32(1))  # dynamic with no reuse entry -> fallback segment
+        p = L.stw_malloc(C.c_size_t(3 << 20), 0, None)
+        v, route = PlanAllocator.vaddr(p)
+        assert route == "fallback" and v >= bundle.pool_size and p == base + v
+        with pytest.raises(M.DeviceError):
+            PlanAllocator.shutdown()  # a block is live
+        PlanAllocator(bundle, tr)  # reload keeps the live block
+        assert PlanAllocator.vaddr(p)[0] == v
+        L.stw_free(C.c_void_p(p), C.c_size_t(0), 0, None)
+        L.stw_free(C.c_void_p(p), C.c_size_t(0), 0, None)  # double free
+        with pytest.raises(M.SimulationError, match="unknown or already freed"):
+            PlanAllocator.report()
+    finally:
+        L.stw_set_layer(C.c_int32(-1), C.c_int32(0))
+        PlanAllocator.shutdown()
