@@ -3,11 +3,19 @@
 
 One step = plan 4096 reference-exact synthetic dense-model traces under the 4
 (fusion, gap_insert) candidates, self-check every plan (static peak + the
-rectangle sweep), and pick the best candidate per trace -- i.e. 16,384 calls of
-the reference's synthesize_static_plan. Weak scaling: rank r plans its own 4096
-traces (seeds r*4096 .. r*4096+4095; rank 0's batch is exactly c4).
+rectangle sweep), pick the best candidate per trace -- i.e. 16,384 calls of
+the reference's synthesize_static_plan -- and exchange the per-trace best
+plans across the ranks (NCCL allreduce MIN over int64[4096] packed
+(pool << 2 | cand), SUM of failing units).
+
+Scaling (BASELINE config 4, "sharded across 8 B200"): strong by default -- the
+4096 traces are split into contiguous blocks over the N ranks; `--scaling
+weak` gives every rank its own 4096 (rank r: seeds r*4096..).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl stw|reference]
+
+`--gpus N` outside torchrun re-launches itself under torch.distributed.run
+with N ranks (one process per GPU).
 
 `--impl reference` times the CPU parity oracle (a C port of the reference
 planner, oracle/) on the same workload with every host thread; it is the
@@ -42,7 +50,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="stw", choices=["stw", "reference"])
-    ap.add_argument("--traces", type=int, default=4096, help="traces per rank (c4: 4096)")
+    ap.add_argument("--traces", type=int, default=4096,
+                    help="traces in the sweep (strong: split over the ranks; weak: per rank); c4 = 4096")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default, BASELINE config 4): c4's 4096 traces sharded over the N GPUs; "
+                         "weak: every rank plans its own 4096 (rank r: seeds r*4096..)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend (gloo + --share-gpu: several ranks on one GPU, for tests)")
+    ap.add_argument("--share-gpu", action="store_true", help="every rank uses cuda:0 (tests on a 1-GPU box)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-sweep", action="store_true", help="skip the K1/K7/K2 >>L2 roofline sweep")
     ap.add_argument("--sweep-reps", type=int, default=64, help="c4 copies in the K1/K7 sweep")
@@ -55,60 +70,128 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def make_traces(rank: int, n: int):
+def seeds_of(rank: int, world: int, n: int, scaling: str) -> range:
+    """The c4 seeds a rank plans: strong = a contiguous block of the n-trace
+    sweep; weak = its own n traces."""
+    if scaling == "weak":
+        return range(rank * n, (rank + 1) * n)
+    return range(rank * n // world, (rank + 1) * n // world)
+
+
+def make_traces(seeds):
     from paper_2507_16274_b200 import tracegen
 
-    return [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(rank * n, (rank + 1) * n)]
+    return [tracegen.synth_arrays(tracegen.c4_config(s)) for s in seeds]
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run under torch.distributed.run
+    with N ranks (one process per GPU); rank 0 prints the line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 # ---------------------------------------------------------------------------
 # CPU side (oracle port of the reference planner)
 
-def cpu_sweep(traces, threads: int):
-    """Plan every trace x candidate with the C oracle on `threads` host threads.
-    Returns (seconds, planned allocations)."""
-    from concurrent.futures import ThreadPoolExecutor
+_POOL_TRACES = {}  # seed -> TraceArrays, filled before the pool forks (workers inherit it)
 
+
+def _pool_plan(seeds):
+    """One pool task: plan the seeds' traces under the 4 candidates with the C oracle."""
     from oracle import oracle as O
 
-    O.lib()
-
-    def work(ta):
-        n = 0
+    n = 0
+    for s in seeds:
+        ta = _POOL_TRACES[s]
         for f, g in CANDS:
             r = O.plan(ta, f, g)
             assert r.rc == 0, r.err
             n += r.stats["num_events"]
-        return n
+    return n
 
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        total = sum(ex.map(work, traces))
-    return time.perf_counter() - t0, total
+
+class CpuSweep:
+    """The reference planner's CPU cost on this host: the C port of the
+    reference (oracle/) over c4 traces x 4 candidates, one process per host
+    core (multiprocessing.Pool); the traces are generated
+    before the pool forks, so no timed call pays for them."""
+
+    def __init__(self, seeds, procs=None, traces=None):
+        import multiprocessing as mp
+
+        from oracle import oracle as O
+
+        self.procs = procs or os.cpu_count() or 1
+        seeds = list(seeds)
+        for s, ta in zip(seeds, traces if traces is not None else make_traces(seeds)):
+            _POOL_TRACES[s] = ta
+        O.lib()  # loaded once, inherited by the workers
+        k = self.procs * 4  # tasks: contiguous chunks, four per worker
+        self.chunks = [seeds[i * len(seeds) // k:(i + 1) * len(seeds) // k] for i in range(k)]
+        self.pool = mp.get_context("fork").Pool(self.procs)
+        self.pool.map(_pool_plan, [c[:1] for c in self.chunks if c])  # every worker started and warm
+
+    def run(self):
+        """(seconds, planned allocations) of one full pass."""
+        t0 = time.perf_counter()
+        total = sum(self.pool.map(_pool_plan, self.chunks))
+        return time.perf_counter() - t0, total
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+
+def host_info() -> dict:
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    import platform
+
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "python": platform.python_version()}
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the C port of the reference planner (oracle/) on every
+    host core, on this run's config (the c4 sweep). Under torchrun only rank 0
+    works; the others exit."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    traces = make_traces(0, args.traces)
-    for _ in range(args.warmup):
-        cpu_sweep(traces[: max(1, len(traces) // 16)], threads)
-    times, total = [], 0
-    for _ in range(args.steps):
-        dt, total = cpu_sweep(traces, threads)
-        times.append(dt)
+    cpu = CpuSweep(range(args.traces))
+    try:
+        for _ in range(max(args.warmup - 1, 0)):
+            cpu.run()
+        times, total = [], 0
+        for _ in range(args.steps):
+            dt, total = cpu.run()
+            times.append(dt)
+    finally:
+        cpu.close()
     t = sum(times)
     value = total * args.steps / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
         "data": "synthetic: reference-exact c4 traces (seeds 0..4095) regenerated from seeds",
-        "config": {"workload": "c4_batched_sweep", "traces": len(traces), "candidates": 4,
+        "config": {"workload": "c4_batched_sweep", "traces": args.traces, "candidates": 4,
                    "planned_allocs_per_step": total},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full c4 sweep ({len(traces)} traces x 4 candidates) per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu.procs, "kind": "port",
+                         "sample": f"full c4 sweep ({args.traces} traces x 4 candidates) per step, "
+                                   f"multiprocessing.Pool({cpu.procs})", **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -324,39 +407,69 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
 # single-trace configs: plan / replay / baseline on the device,
 # replay ops/s and the bit-exact fragmentation ratios
 
-def config_sweep(names, reps: int = 3):
-    """Per config: Python Trace in -> StaticPlan out (synthesize_static_plan +
-    derive_reuse_map), simulate (replay scorer) and run_baseline, each timed
-    end to end through the package API (host arrays in, host objects out),
-    best of `reps`; plus the fragmentation ratios they return."""
+STAGES = ("plan", "reuse", "validate", "simulate", "baseline", "peak")
+
+
+def config_sweep(names, reps: int = 3, cpu: bool = True):
+    """Per config, per stage (synthesize_static_plan,
+    derive_reuse_map, validate_plan, simulate, run_baseline, peak_live_bytes):
+    the device path through the package API (host arrays in, host objects /
+    columns out), best of `reps`, beside the C port of the reference (oracle/,
+    one host thread) on the same inputs in the same run -- plus the
+    bit-exact fragmentation ratios."""
     import paper_2507_16274_b200 as M
-    from paper_2507_16274_b200 import tracegen
+    from paper_2507_16274_b200 import api, tracegen
+
+    if cpu:
+        from oracle import oracle as O
+
+    def best(fn, k=reps):
+        t, r = float("inf"), None
+        for _ in range(k):
+            t0 = time.perf_counter()
+            r = fn()
+            t = min(t, time.perf_counter() - t0)
+        return t, r
 
     out = {}
     for name in names:
         ta = tracegen.synth_arrays(tracegen.config(name))
         tr = M.Trace.from_arrays(ta)
-
-        def best(fn):
-            t, r = float("inf"), None
-            for _ in range(reps):
-                t0 = time.perf_counter()
-                r = fn()
-                t = min(t, time.perf_counter() - t0)
-            return t, r
-
-        t_plan, (plan, rmap) = best(lambda: M.plan_trace(tr))
+        g = {}
+        g["plan"], plan = best(lambda: M.synthesize_static_plan(tr))
+        g["reuse"], rmap = best(lambda: M.derive_reuse_map(plan, tr))
+        c = plan.columns()
+        g["validate"], _pairs = best(lambda: api.validate_columns(c.id, c.addr, c.size, c.t_s, c.t_e))
         bundle = plan.to_bundle(rmap)
-        t_sim, (rep, _log) = best(lambda: M.simulate(tr, bundle))
-        t_base, base = best(lambda: M.run_baseline(tr))
+        g["simulate"], (rep, _log) = best(lambda: M.simulate(tr, bundle))
+        g["baseline"], base = best(lambda: M.run_baseline(tr))
+        g["peak"], peak = best(lambda: M.peak_live_bytes(ta))
         n = len(ta)
-        out[name] = {"events": n, "pool_size": int(plan.pool_size),
-                     "plan_ms": 1e3 * t_plan, "planned_allocs_per_s": int((ta.dyn == 0).sum()) / t_plan,
-                     "replay_ms": 1e3 * t_sim, "replay_ops_per_s": 2 * n / t_sim,
-                     "baseline_ms": 1e3 * t_base,
-                     "fragmentation": rep.fragmentation, "efficiency": rep.efficiency,
-                     "baseline_fragmentation": base.fragmentation,
-                     "fallbacks": int(rep.fallback_count), "reuse_hits": int(rep.reuse_hits)}
+        row = {"events": n, "pool_size": int(plan.pool_size),
+               "planned_allocs_per_s": int((ta.dyn == 0).sum()) / g["plan"],
+               "replay_ops_per_s": 2 * n / g["simulate"],
+               "fragmentation": rep.fragmentation, "efficiency": rep.efficiency,
+               "baseline_fragmentation": base.fragmentation,
+               "fallbacks": int(rep.fallback_count), "reuse_hits": int(rep.reuse_hits),
+               "gpu_ms": {k: 1e3 * v for k, v in g.items()}}
+        if cpu:
+            keys, kidx = ta.dynamic_keys()
+            t_lo = np.asarray([rmap.entries[k].t_lo for k in keys], np.int64)
+            t_hi = np.asarray([rmap.entries[k].t_hi for k in keys], np.int64)
+            h = {}
+            h["plan"], op = best(lambda: O.plan(ta), 1)
+            h["reuse"], (off, lo, hi) = best(lambda: O.reuse(c.addr, c.size, c.t_s, c.t_e, t_lo, t_hi), 1)
+            h["validate"], _ = best(lambda: O.validate(c.id, c.addr, c.size, c.t_s, c.t_e), 1)
+            key = np.where(kidx >= 0, kidx, -1).astype(np.int32)
+            h["simulate"], orep = best(lambda: O.simulate(ta, key, plan.pool_size, 512, c.id, c.addr, c.size, c.t_s,
+                                                          c.t_e, off, lo, hi, True), 1)
+            h["baseline"], obase = best(lambda: O.baseline(ta), 1)
+            h["peak"], opeak = best(lambda: O.peak_live(ta.size, ta.t_s, ta.t_e), 1)
+            assert op.stats["pool_size"] == plan.pool_size and opeak == peak
+            assert orep.report == rep.to_dict() and obase.report == base.to_dict(), name
+            row["cpu_ms"] = {k: 1e3 * v for k, v in h.items()}
+            row["cpu_over_gpu"] = {k: h[k] / g[k] for k in STAGES}
+        out[name] = row
     return out
 
 
@@ -373,14 +486,11 @@ def ncu_traffic(key):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
     rank, world, local = dist_env()
     if args.impl == "reference":
-        if world > 1:
-            import torch.distributed as dist
-
-            # no collective is needed: rank 0 alone runs the CPU reference
-            pass
-        run_reference(args, rank, world)
+        run_reference(args, rank, world)  # rank 0 alone runs the CPU reference; no collective
         return
 
     import torch
@@ -388,17 +498,24 @@ def main():
     from paper_2507_16274_b200 import _lib, api
     from paper_2507_16274_b200.batching import HostBatch
 
+    if args.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     L = _lib.load()
 
     t_gen = time.perf_counter()
-    traces = make_traces(rank, args.traces)
+    seeds = seeds_of(rank, world, args.traces, args.scaling)
+    traces = make_traces(seeds)
     t_gen = time.perf_counter() - t_gen
+    n_sweep = args.traces if args.scaling == "strong" else args.traces * world  # traces of the whole job
     hb = HostBatch(traces, pinned=True)
     db = hb.to_device(dev)
     T, N = hb.T, hb.N
@@ -421,8 +538,37 @@ def main():
     dstruct = db.struct()
     err = _lib.errbuf()
 
+    # the sweep's one exchange: the best plan of every trace of the
+    # job as packed (pool << 2 | cand), INT64_MAX outside this rank's block,
+    # allreduce MIN over int64[n_sweep] (ties -> lowest candidate, the
+    # reference's order); the failing units' count, allreduce SUM
+    g_keys = torch.empty(n_sweep, dtype=torch.int64, device=dev)
+    g_bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    off0 = seeds.start
+    i64max = torch.iinfo(torch.int64).max
+
+    def allreduce(t, op):
+        if world == 1:
+            return
+        if args.backend == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op)
+
+    def combine(bpool, best, rc):
+        g_keys.fill_(i64max)
+        g_keys[off0:off0 + T].copy_((bpool.to(dev, non_blocking=True) << 2) | best.to(dev, torch.int64,
+                                                                                    non_blocking=True))
+        g_bad.copy_((rc.to(dev, non_blocking=True) != 0).sum().view(1))
+        if world > 1:
+            allreduce(g_keys, dist.ReduceOp.MIN)
+            allreduce(g_bad, dist.ReduceOp.SUM)
+
     def step_device():
         _lib.check(L.stw_plan_batch(C.byref(dstruct), C.byref(opts), C.byref(dev_out), err, 1024), err)
+        combine(o_bpool, o_best, o_rc)
 
     # host-side buffers for the end-to-end path (pinned in, pinned out)
     h_rc = torch.empty(T * Cn, dtype=torch.int32).pin_memory()
@@ -437,6 +583,7 @@ def main():
 
     def step_e2e():
         _lib.check(L.stw_plan_batch(C.byref(hstruct), C.byref(opts), C.byref(host_out), err, 1024), err)
+        combine(h_bpool, h_best, h_rc)
 
     def e2e_pipelined(k):
         """K steps through stw_plan_batches: every step copies its batch from pinned
@@ -452,6 +599,8 @@ def main():
             dist.barrier()
         ev0.record(stream)
         _lib.check(L.stw_plan_batches(k, bs, C.byref(opts), os_, err, 1024), err)
+        for _ in range(k):  # every step's results go through the exchange
+            combine(h_bpool, h_best, h_rc)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         return ev0.elapsed_time(ev1) / 1e3
@@ -504,26 +653,34 @@ def main():
         t_e2e_serial, _, _ = timed(step_e2e, args.steps, False)
         t_e2e = e2e_pipelined(args.steps)
 
-    def max_all(x):
+    def reduce_scalar(x, op):
         if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(t, op)
         return float(t.item())
 
-    def sum_all(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
-    t_plain_max = max_all(t_plain)
-    t_e2e_max = max_all(t_e2e)
-    t_e2e_serial_max = max_all(t_e2e_serial)
-    total_planned = sum_all(planned) * args.steps
+    t_plain_max = reduce_scalar(t_plain, dist.ReduceOp.MAX if world > 1 else None)
+    t_e2e_max = reduce_scalar(t_e2e, dist.ReduceOp.MAX if world > 1 else None)
+    t_e2e_serial_max = reduce_scalar(t_e2e_serial, dist.ReduceOp.MAX if world > 1 else None)
+    total_planned = reduce_scalar(planned, dist.ReduceOp.SUM if world > 1 else None) * args.steps
     value = total_planned / t_plain_max
     e2e_value = total_planned / t_e2e_max
+
+    # the exchange's result, checked against the reference's c4 anchor (sum of
+    # the best pools over seeds 0..4095, tests/golden/anchors.json)
+    step_device()
+    torch.cuda.synchronize(dev)
+    keys = g_keys.cpu().numpy()
+    verified = None
+    if n_sweep >= 4096:
+        with open(os.path.join(ROOT, "tests", "golden", "anchors.json")) as fh:
+            want = json.load(fh)["c4"]["sum_best_pool"]
+        got = int((keys[:4096] >> 2).sum())
+        verified = {"c4_sum_best_pool": got, "matches_reference": got == want,
+                    "failing_units": int(g_bad.item())}
+        if got != want or int(g_bad.item()):
+            raise SystemExit(f"sweep result differs from the reference anchor: {verified}")
 
     # roofline of the dominant kernel (profiled run, same stream)
     peaks = measured_peaks()
@@ -547,30 +704,37 @@ def main():
             print(f"{k:28s} launches {c:6d}  total {ms:9.3f} ms  avg {ms / c:8.4f} ms", file=sys.stderr)
 
     sweep = None
-    if not args.no_kernel_sweep:
+    if not args.no_kernel_sweep and world == 1:
         sweep = kernel_sweep(dev, db, hb, o_addr, args.sweep_reps, hbm)
     configs = None
-    if rank == 0 and not args.no_configs:
+    if rank == 0 and world == 1 and not args.no_configs:
         configs = config_sweep(["c1_llama2_7b_1f1b", "c2_llama2_7b_vpp_rcp", "c3_mixtral_moe", "c3b_mixtral_moe_rcp",
-                                "c5_llama3_70b"])
+                                "c5_llama3_70b"], cpu=not args.no_cpu_baseline)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        sample = traces[:1024]
-        dt, n_cpu = cpu_sweep(sample, threads)
-        cpu = {"value": n_cpu / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"oracle C port of the reference planner, first {len(sample)} c4 traces x 4 candidates"}
+        k = min(1024, len(traces))
+        sweep_cpu = CpuSweep(seeds[:k], traces=traces[:k])
+        try:
+            dt, n_cpu = sweep_cpu.run()
+        finally:
+            sweep_cpu.close()
+        cpu = {"value": n_cpu / dt, "unit": UNIT, "cores": sweep_cpu.procs, "kind": "port",
+               "sample": f"oracle C port of the reference planner, c4 seeds 0..{k - 1} x 4 candidates, "
+                         f"multiprocessing.Pool({sweep_cpu.procs})", **host_info()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_plain_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic: reference-exact c4 traces regenerated from seeds (rank r: seeds r*4096..)",
-            "config": {"workload": "c4_batched_sweep", "traces_per_rank": T, "candidates": Cn,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic: reference-exact c4 traces regenerated from their seeds",
+            "config": {"workload": "c4_batched_sweep", "traces": n_sweep, "traces_per_rank": T, "candidates": Cn,
                        "events_per_rank": N, "planned_allocs_per_step_per_rank": planned,
-                       "parallelism": f"dp{world} (independent traces per rank)",
+                       "parallelism": f"dp{world}: " + ("the sweep's traces in contiguous blocks per rank"
+                                                         if args.scaling == "strong" else "own traces per rank")
+                       + "; allreduce MIN over int64[traces] of (pool << 2 | cand) + SUM of failing units per step",
+                       "backend": args.backend if world > 1 else None,
                        "l2": "256 MiB buffer written between timed steps (flush)", "trace_gen_s": round(t_gen, 2)},
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": hb.nbytes,
@@ -580,6 +744,7 @@ def main():
                     "serial_value": total_planned / t_e2e_serial_max,
                     "serial_how": "one synchronous stw_plan_batch call per step with host buffers"},
             "gpu_launches": int(launches),
+            "verified": verified,
             "roofline": roofline,
             "kernel_roofline": sweep,
             "configs": configs,
