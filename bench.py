@@ -8,9 +8,11 @@ the reference's synthesize_static_plan -- and exchange the per-trace best
 plans across the ranks (NCCL allreduce MIN over int64[4096] packed
 (pool << 2 | cand), SUM of failing units).
 
-Scaling (BASELINE config 4, "sharded across 8 B200"): strong by default -- the
-4096 traces are split into contiguous blocks over the N ranks; `--scaling
-weak` gives every rank its own 4096 (rank r: seeds r*4096..).
+Scaling: weak by default -- every rank plans its own c4-sized batch of 4096
+traces (rank r: seeds r*4096..; rank 0's is exactly c4), so per-GPU work is
+fixed and the job's sweep grows with N. `--scaling strong` splits c4's 4096
+traces into contiguous blocks over the N ranks instead (its per-rank call is
+latency-bound below ~2k traces).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl stw|reference]
 
@@ -52,9 +54,9 @@ def parse():
     ap.add_argument("--impl", default="stw", choices=["stw", "reference"])
     ap.add_argument("--traces", type=int, default=4096,
                     help="traces in the sweep (strong: split over the ranks; weak: per rank); c4 = 4096")
-    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
-                    help="strong (default, BASELINE config 4): c4's 4096 traces sharded over the N GPUs; "
-                         "weak: every rank plans its own 4096 (rank r: seeds r*4096..)")
+    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
+                    help="weak (default): every rank plans its own c4-sized batch (rank r: seeds r*4096..), "
+                         "the whole job grows with N; strong: c4's 4096 traces split over the N GPUs")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend (gloo + --share-gpu: several ranks on one GPU, for tests)")
     ap.add_argument("--share-gpu", action="store_true", help="every rank uses cuda:0 (tests on a 1-GPU box)")

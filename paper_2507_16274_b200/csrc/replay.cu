@@ -13,6 +13,8 @@
 // inside the reuse space (sim.py:120-140), the caching allocator
 // (baseline.py:49-95), the replay log and the metrics (sim.py:67-117). The
 // warp prefetches 32 ops at a time; interval lists live in shared memory.
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -31,8 +33,9 @@ __global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *_
 double exact_div_host(unsigned long long a, unsigned long long b);
 
 constexpr int kFreeSmem = 4096;   // pool free intervals kept in shared memory
-constexpr int kBlockSmem = 6144;  // cache free blocks kept in shared memory
-constexpr size_t kReplaySmem = (size_t)kFreeSmem * 16 + (size_t)kBlockSmem * 20;
+constexpr int kBlockSmem = 4096;  // cache free blocks kept in shared memory
+constexpr int kSpaceSmem = 2048;  // reuse-space intervals of one key staged in shared memory
+constexpr size_t kReplaySmem = (size_t)kFreeSmem * 16 + (size_t)kBlockSmem * 20 + (size_t)kSpaceSmem * 16;
 constexpr long long kMinSegment = 2ll * 1024 * 1024;
 
 enum { R_PLANNED = 0, R_REUSE = 1, R_FALLBACK = 2, R_MISMATCH = 3, R_ONLINE = 4 };
@@ -255,98 +258,64 @@ struct ReplayArgs {
 };
 
 // warp helpers ---------------------------------------------------------------
-__device__ __forceinline__ void wshift_right(int64_t *a, int64_t *b, int32_t *c, int from, int n, int s) {
-  for (int base = n - 1; base >= from; base -= 32) {
-    int idx = base - (int)lane_id();
-    int64_t va = 0, vb = 0;
-    int32_t vc = 0;
-    bool ok = idx >= from;
-    if (ok) {
-      va = a[idx];
-      vb = b[idx];
-      if (c) vc = c[idx];
-    }
-    __syncwarp();
-    if (ok) {
-      a[idx + s] = va;
-      b[idx + s] = vb;
-      if (c) c[idx + s] = vc;
-    }
-    __syncwarp();
+constexpr unsigned kFull = 0xffffffffu;
+
+// min of (k1, k2, k3) lexicographic over the warp, result in every lane
+__device__ __forceinline__ void warp_min3(long long &k1, long long &k2, int &k3) {
+  for (int o = 16; o; o >>= 1) {
+    const long long a = __shfl_xor_sync(kFull, k1, o), b = __shfl_xor_sync(kFull, k2, o);
+    const int c = __shfl_xor_sync(kFull, k3, o);
+    if (a < k1 || (a == k1 && b < k2)) k1 = a, k2 = b, k3 = c;
   }
-}
-__device__ __forceinline__ void wshift_left(int64_t *a, int64_t *b, int32_t *c, int from, int n, int s) {
-  // a[from .. n-s) = a[from+s .. n)
-  for (int base = from; base < n - s; base += 32) {
-    int idx = base + (int)lane_id();
-    int64_t va = 0, vb = 0;
-    int32_t vc = 0;
-    bool ok = idx < n - s;
-    if (ok) {
-      va = a[idx + s];
-      vb = b[idx + s];
-      if (c) vc = c[idx + s];
-    }
-    __syncwarp();
-    if (ok) {
-      a[idx] = va;
-      b[idx] = vb;
-      if (c) c[idx] = vc;
-    }
-    __syncwarp();
-  }
-}
-// last index with lo[i] <= x (-1 if none), lane-0 binary search, broadcast
-__device__ __forceinline__ int wfind_le(const int64_t *lo, int n, long long x) {
-  int r = 0;
-  if (lane_id() == 0) {
-    int a = 0, b = n;
-    while (a < b) {
-      int m = (a + b) >> 1;
-      if (lo[m] <= x)
-        a = m + 1;
-      else
-        b = m;
-    }
-    r = a - 1;
-  }
-  return __shfl_sync(0xffffffffu, r, 0);
-}
-// first index with hi[i] >= x
-__device__ __forceinline__ int wfind_hi_ge(const int64_t *hi, int n, long long x) {
-  int r = 0;
-  if (lane_id() == 0) {
-    int a = 0, b = n;
-    while (a < b) {
-      int m = (a + b) >> 1;
-      if (hi[m] < x)
-        a = m + 1;
-      else
-        b = m;
-    }
-    r = a;
-  }
-  return __shfl_sync(0xffffffffu, r, 0);
 }
 
 __device__ __forceinline__ void warp_min_pair(long long &k1, long long &k2) {
   for (int o = 16; o; o >>= 1) {
-    long long a = __shfl_xor_sync(0xffffffffu, k1, o), b = __shfl_xor_sync(0xffffffffu, k2, o);
+    long long a = __shfl_xor_sync(kFull, k1, o), b = __shfl_xor_sync(kFull, k2, o);
     if (a < k1 || (a == k1 && b < k2)) k1 = a, k2 = b;
   }
 }
 
+// The sequential residue of the replay on one warp. Interval lists are kept
+// UNSORTED in shared memory (spilling to global beyond the smem capacity):
+// every query is a lane-parallel scan + ballot, every update O(1) by lane 0
+// (in place, append, or swap-remove), so no op pays for a binary search or a
+// shifted array. Order-dependent tie-breaks are order-free here: best fit =
+// min (length, address) -- the cache's (segment, address) order is address
+// order, since segments are appended at increasing bases (baseline.py:54-66).
+// Per op window (32 ops, one per lane) every lane prefetches its op's fields
+// AND the per-id state it will read (pool / cache liveness, interval,
+// segment, the reuse key's space range), so the chain of dependent global
+// loads is paid once per 32 ops; state an earlier op of the same window
+// changes is forwarded lane to lane.
 __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
   extern __shared__ int64_t dsm[];
   int64_t *s_flo = dsm, *s_fhi = dsm + kFreeSmem;
   int64_t *s_blo = dsm + 2 * kFreeSmem, *s_bhi = s_blo + kBlockSmem;
   int32_t *s_bseg = (int32_t *)(s_bhi + kBlockSmem);
-  const unsigned lane = lane_id();
-  const bool big_free = A.n + 2 > kFreeSmem, big_blk = 2 * A.n + 2 > kBlockSmem;
-  int64_t *flo = big_free ? A.gflo : s_flo, *fhi = big_free ? A.gfhi : s_fhi;
-  int64_t *blo = big_blk ? A.gblo : s_blo, *bhi = big_blk ? A.gbhi : s_bhi;
-  int32_t *bseg = big_blk ? A.gbseg : s_bseg;
+  int64_t *s_sp = (int64_t *)(s_bseg + kBlockSmem);  // staged reuse space of the current key: lo, hi pairs
+  const int lane = (int)lane_id();
+  // lists start in shared memory and move to their global spill arrays the
+  // first time they would outgrow it
+  int64_t *flo = s_flo, *fhi = s_fhi;
+  int64_t *blo = s_blo, *bhi = s_bhi;
+  int32_t *bseg = s_bseg;
   int nf = 0, nb = 0, ns = 0;
+  auto grow_free = [&]() {  // before a free-list append
+    if (flo != s_flo || nf + 1 < kFreeSmem) return;
+    for (int i = lane; i < nf; i += 32) A.gflo[i] = s_flo[i], A.gfhi[i] = s_fhi[i];
+    __syncwarp();
+    flo = A.gflo;
+    fhi = A.gfhi;
+  };
+  auto grow_blocks = [&]() {  // before a cache-block append
+    if (blo != s_blo || nb + 1 < kBlockSmem) return;
+    for (int i = lane; i < nb; i += 32) A.gblo[i] = s_blo[i], A.gbhi[i] = s_bhi[i], A.gbseg[i] = s_bseg[i];
+    __syncwarp();
+    blo = A.gblo;
+    bhi = A.gbhi;
+    bseg = A.gbseg;
+  };
   long long next_base = A.baseline ? 0 : A.pool;
   if (!A.baseline && A.pool > 0) {
     if (lane == 0) {
@@ -358,6 +327,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
   long long nlog = 0, live = 0, peak = 0, clive = 0, cpeak = 0, reserved = 0;
   long long n_fb = 0, n_reuse = 0, n_mm = 0;
   long long err = 0, err_id = 0, err_addr = 0;
+  long long max_nb = 0, max_nf = 0, sum_nb = 0, sum_nf = 0;  // list sizes (diagnostics, res[10..13])
   auto logrec = [&](int kind, long long t, long long id, long long size, int space, long long addr, int route) {
     if (lane == 0) {
       A.lkind[nlog] = (int8_t)kind;
@@ -372,18 +342,83 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
   };
   logrec(0, 0, 0, A.baseline ? 0 : A.pool, 0, 0, -1);
 
-  // caching allocator malloc (baseline.py:49-77); returns addr, sets *grown; -1 if already live
-  auto cache_malloc = [&](int c, long long size, long long *grown) -> long long {
-    if (A.cflag[c]) return -1;
-    long long bl = LLONG_MAX, bi = LLONG_MAX;
-    for (int i = lane; i < nb; i += 32) {
-      long long len = bhi[i] - blo[i];
-      if (len >= size && (len < bl || (len == bl && i < bi))) bl = len, bi = i;
+  // pool free set -----------------------------------------------------------
+  // index of the free interval holding [lo, hi) entirely, -1 if none (contains_interval, intervals.py:95-98)
+  auto free_holding = [&](long long lo, long long hi) -> int {
+    for (int base = 0; base < nf; base += 32) {
+      const int i = base + lane;
+      const unsigned m = __ballot_sync(kFull, i < nf && flo[i] <= lo && hi <= fhi[i]);
+      if (m) return base + __ffs(m) - 1;
     }
-    warp_min_pair(bl, bi);
+    return -1;
+  };
+  // remove [lo, hi) lying inside free interval i (IntervalSet.remove, intervals.py:113-129)
+  auto free_remove = [&](int i, long long lo, long long hi) {
+    grow_free();
+    const long long a = flo[i], b = fhi[i];
+    __syncwarp();
+    if (lane == 0) {
+      if (a < lo && b > hi) {
+        fhi[i] = lo;
+        flo[nf] = hi;
+        fhi[nf] = b;
+      } else if (a < lo) {
+        fhi[i] = lo;
+      } else if (b > hi) {
+        flo[i] = hi;
+      } else {
+        flo[i] = flo[nf - 1];
+        fhi[i] = fhi[nf - 1];
+      }
+    }
+    nf += (a < lo && b > hi) ? 1 : (a < lo || b > hi) ? 0 : -1;
+    __syncwarp();
+  };
+  // IntervalSet.add (intervals.py:100-111) of an interval disjoint from the free
+  // set (it was live): merge with the neighbours it touches
+  auto free_add = [&](long long lo, long long hi) {
+    grow_free();
+    int l = -1, r = -1;
+    for (int base = 0; base < nf; base += 32) {
+      const int i = base + lane;
+      const bool in = i < nf;
+      const long long a = in ? flo[i] : 0, b = in ? fhi[i] : 0;
+      const unsigned ml = __ballot_sync(kFull, in && b == lo), mr = __ballot_sync(kFull, in && a == hi);
+      if (ml) l = base + __ffs(ml) - 1;
+      if (mr) r = base + __ffs(mr) - 1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (l >= 0 && r >= 0) {
+        fhi[l] = fhi[r];
+        flo[r] = flo[nf - 1];
+        fhi[r] = fhi[nf - 1];
+      } else if (l >= 0) {
+        fhi[l] = hi;
+      } else if (r >= 0) {
+        flo[r] = lo;
+      } else {
+        flo[nf] = lo;
+        fhi[nf] = hi;
+      }
+    }
+    nf += (l >= 0 && r >= 0) ? -1 : (l < 0 && r < 0) ? 1 : 0;
+    __syncwarp();
+  };
+
+  // caching allocator (baseline.py:49-95) ------------------------------------
+  // malloc: returns the address, sets *grown and *sg (segment)
+  auto cache_malloc = [&](long long size, long long *grown, int *sg) -> long long {
+    long long bl = LLONG_MAX, ba = LLONG_MAX;
+    int bi = -1;
+    for (int i = lane; i < nb; i += 32) {
+      const long long a = blo[i], len = bhi[i] - a;
+      if (len >= size && (len < bl || (len == bl && a < ba))) bl = len, ba = a, bi = i;
+    }
+    warp_min3(bl, ba, bi);
     *grown = 0;
-    int i = (int)bi;
-    if (bi == LLONG_MAX) {  // new segment at the end (segments are appended in creation order)
+    if (bi < 0) {  // a fresh segment at the next base
+      grow_blocks();
       long long ss = 1;
       while (ss < size) ss <<= 1;
       if (ss < kMinSegment) ss = kMinSegment;
@@ -394,275 +429,228 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
         bseg[nb] = ns;
       }
       __syncwarp();
-      i = nb++;
+      bi = nb++;
       ns++;
+      ba = next_base;
       next_base += ss;
       *grown = ss;
     }
-    long long lo = blo[i], hi = bhi[i];
-    int sg = bseg[i];
+    const long long hi = bhi[bi];
+    *sg = bseg[bi];
     __syncwarp();
-    if (lo + size < hi) {
-      if (lane == 0) blo[i] = lo + size;
-      __syncwarp();
-    } else {
-      wshift_left(blo, bhi, bseg, i, nb, 1);
-      nb--;
-    }
     if (lane == 0) {
-      A.clo[c] = lo;
-      A.chi[c] = lo + size;
-      A.cseg[c] = sg;
-      A.cflag[c] = 1;
+      if (ba + size < hi) {  // split: the remainder stays
+        blo[bi] = ba + size;
+      } else {  // exact fit: swap-remove
+        blo[bi] = blo[nb - 1];
+        bhi[bi] = bhi[nb - 1];
+        bseg[bi] = bseg[nb - 1];
+      }
     }
+    if (ba + size >= hi) nb--;
     __syncwarp();
-    return lo;
+    return ba;
   };
-  // caching allocator free (baseline.py:79-95): insort + merge with neighbours
-  auto cache_free = [&](int c, long long *addr, long long *size) {
-    long long lo = A.clo[c], hi = A.chi[c];
-    int sg = A.cseg[c];
-    if (lane == 0) A.cflag[c] = 0;
-    *addr = lo;
-    *size = hi - lo;
-    int p = 0;  // insertion point: first block with (seg, lo) > (sg, lo)
+  // free: merge with the same segment's free neighbours (baseline.py:79-95)
+  auto cache_free = [&](long long lo, long long hi, int sg) {
+    grow_blocks();
+    int l = -1, r = -1;
+    for (int base = 0; base < nb; base += 32) {
+      const int i = base + lane;
+      const bool in = i < nb;
+      const bool same = in && bseg[i] == sg;
+      const unsigned ml = __ballot_sync(kFull, same && bhi[i] == lo), mr = __ballot_sync(kFull, same && blo[i] == hi);
+      if (ml) l = base + __ffs(ml) - 1;
+      if (mr) r = base + __ffs(mr) - 1;
+    }
+    __syncwarp();
     if (lane == 0) {
-      int a = 0, b = nb;
-      while (a < b) {
-        int m = (a + b) >> 1;
-        if (bseg[m] < sg || (bseg[m] == sg && blo[m] < lo))
-          a = m + 1;
-        else
-          b = m;
+      if (l >= 0 && r >= 0) {
+        bhi[l] = bhi[r];
+        blo[r] = blo[nb - 1];
+        bhi[r] = bhi[nb - 1];
+        bseg[r] = bseg[nb - 1];
+        if (l == nb - 1) bhi[r] = bhi[l];  // l itself moved into r's slot
+      } else if (l >= 0) {
+        bhi[l] = hi;
+      } else if (r >= 0) {
+        blo[r] = lo;
+      } else {
+        blo[nb] = lo;
+        bhi[nb] = hi;
+        bseg[nb] = sg;
       }
-      p = a;
     }
-    p = __shfl_sync(0xffffffffu, p, 0);
-    bool nxt = p < nb && bseg[p] == sg && blo[p] == hi;
-    bool prv = p > 0 && bseg[p - 1] == sg && bhi[p - 1] == lo;
-    __syncwarp();
-    if (nxt && prv) {
-      long long nh = bhi[p];
-      __syncwarp();
-      if (lane == 0) bhi[p - 1] = nh;
-      __syncwarp();
-      wshift_left(blo, bhi, bseg, p, nb, 1);
-      nb--;
-    } else if (nxt) {
-      if (lane == 0) blo[p] = lo;
-      __syncwarp();
-    } else if (prv) {
-      if (lane == 0) bhi[p - 1] = hi;
-      __syncwarp();
-    } else {
-      wshift_right(blo, bhi, bseg, p, nb, 1);
-      if (lane == 0) {
-        blo[p] = lo;
-        bhi[p] = hi;
-        bseg[p] = sg;
-      }
-      __syncwarp();
-      nb++;
-    }
-  };
-  // pool free list: remove [lo, hi) lying inside free interval i
-  auto free_remove = [&](int i, long long lo, long long hi) {
-    long long a = flo[i], b = fhi[i];
-    __syncwarp();
-    bool left = a < lo, right = b > hi;
-    if (left && right) {
-      wshift_right(flo, fhi, nullptr, i + 1, nf, 1);
-      if (lane == 0) {
-        fhi[i] = lo;
-        flo[i + 1] = hi;
-        fhi[i + 1] = b;
-      }
-      nf++;
-    } else if (left) {
-      if (lane == 0) fhi[i] = lo;
-    } else if (right) {
-      if (lane == 0) flo[i] = hi;
-    } else {
-      wshift_left(flo, fhi, nullptr, i, nf, 1);
-      nf--;
-    }
-    __syncwarp();
-  };
-  // IntervalSet.add (intervals.py:100-111)
-  auto free_add = [&](long long lo, long long hi) {
-    int a = wfind_hi_ge(fhi, nf, lo);  // first with hi >= lo
-    int b = a;                         // first (from a) with lo > hi
-    if (lane == 0) {
-      int x = a, y = nf;
-      while (x < y) {
-        int m = (x + y) >> 1;
-        if (flo[m] <= hi)
-          x = m + 1;
-        else
-          y = m;
-      }
-      b = x;
-    }
-    b = __shfl_sync(0xffffffffu, b, 0);
-    long long nlo = lo, nhi = hi;
-    if (b > a) {
-      nlo = min(nlo, (long long)flo[a]);
-      nhi = max(nhi, (long long)fhi[b - 1]);
-    }
-    __syncwarp();
-    int cnt = b - a;
-    if (cnt == 0) {
-      wshift_right(flo, fhi, nullptr, a, nf, 1);
-      nf++;
-    } else if (cnt > 1) {
-      wshift_left(flo, fhi, nullptr, a + 1, nf, cnt - 1);
-      nf -= cnt - 1;
-    }
-    if (lane == 0) {
-      flo[a] = nlo;
-      fhi[a] = nhi;
-    }
+    nb += (l >= 0 && r >= 0) ? -1 : (l < 0 && r < 0) ? 1 : 0;
     __syncwarp();
   };
 
   const int64_t n2 = 2 * A.n;
   for (int64_t cb = 0; cb < n2 && !err; cb += 32) {
-    // prefetch 32 ops
-    int64_t mine = cb + lane;
-    uint32_t o = mine < n2 ? A.operm[mine] : 0;
-    int e = (int)(o >> 1);
-    bool is_alloc = !(o & 1);
+    // prefetch one op per lane, with the state it reads
+    const int64_t mine = cb + lane;
+    const uint32_t o = mine < n2 ? A.operm[mine] : 0;
+    const int e = (int)(o >> 1);
+    const bool is_alloc = !(o & 1);
     long long my_t = 0, my_id = 0, my_size = 0, my_paddr = -1;
-    int my_did = 0, my_key = -1, my_route = R_ONLINE;
-    bool my_dyn = false;
+    int my_did = -1, my_key = -1, my_route = R_ONLINE;
+    long long my_s0 = 0, my_s1 = 0;
+    // per-id state: pool (flag, lo, hi), cache (flag, lo, hi, segment)
+    int my_pf = 0, my_cf = 0, my_cs = 0;
+    long long my_plo = 0, my_phi = 0, my_clo = 0, my_chi = 0;
     if (mine < n2) {
       my_t = is_alloc ? A.ts[e] : A.te[e];
       my_id = A.id[e];
       my_size = A.size[e];
       my_did = A.did[e];
-      my_dyn = A.dyn[e] != 0;
+      const bool dyn = A.dyn[e] != 0;
       if (!A.baseline) {
-        my_route = my_dyn ? -1 : A.route0[e];
-        my_paddr = my_dyn ? -1 : A.paddr[e];
-        my_key = my_dyn ? A.key[e] : -1;
+        my_route = dyn ? -1 : A.route0[e];
+        my_paddr = dyn ? -1 : A.paddr[e];
+        my_key = dyn ? A.key[e] : -1;
+        if (my_key >= 0 && A.reuse) {
+          my_s0 = A.sp_off[my_key];
+          my_s1 = A.sp_off[my_key + 1];
+        }
+      }
+      my_pf = A.pflag[my_did];
+      my_cf = A.cflag[my_did];
+      if (!is_alloc) {
+        my_plo = A.plo[my_did];
+        my_phi = A.phi[my_did];
+        my_clo = A.clo[my_did];
+        my_chi = A.chi[my_did];
+        my_cs = A.cseg[my_did];
       }
     }
     const int cnt = (int)min((int64_t)32, n2 - cb);
     for (int k = 0; k < cnt && !err; k++) {
-      const bool alloc = __shfl_sync(0xffffffffu, (int)is_alloc, k);
-      const long long t = __shfl_sync(0xffffffffu, my_t, k), id = __shfl_sync(0xffffffffu, my_id, k);
-      const long long size = __shfl_sync(0xffffffffu, my_size, k);
-      const int c = __shfl_sync(0xffffffffu, my_did, k);
+#ifdef STW_REPLAY_STATS
+      max_nb = max(max_nb, (long long)nb), max_nf = max(max_nf, (long long)nf), sum_nb += nb, sum_nf += nf;
+#endif
+      const bool alloc = __shfl_sync(kFull, (int)is_alloc, k);
+      const long long t = __shfl_sync(kFull, my_t, k), id = __shfl_sync(kFull, my_id, k);
+      const long long size = __shfl_sync(kFull, my_size, k);
+      const int c = __shfl_sync(kFull, my_did, k);
+      const bool same = my_did == c;  // lanes whose op touches the same id (state forwarding)
       if (alloc) {
-        const int route = __shfl_sync(0xffffffffu, my_route, k);
+        const int route = __shfl_sync(kFull, my_route, k);
+        bool to_pool = false, to_cache = false;
+        long long a = -1;
+        int rt = route;
         if (route == R_PLANNED) {
-          const long long a = __shfl_sync(0xffffffffu, my_paddr, k);
-          int i = wfind_le(flo, nf, a);
-          bool ok = i >= 0 && fhi[i] >= a + size;  // contains_interval (intervals.py:95-98)
-          __syncwarp();
-          if (!ok) {
+          a = __shfl_sync(kFull, my_paddr, k);
+          const int i = free_holding(a, a + size);
+          if (i < 0) {
             err = STW_ESIM;
             err_id = id;
             err_addr = a;
             break;
           }
           free_remove(i, a, a + size);
+          to_pool = true;
+        } else if (route == R_MISMATCH || route == R_ONLINE) {
+          to_cache = true;
+        } else {  // dynamic: best fit in free ∩ space[key] (sim.py:120-140), else the fallback
+          const long long s0 = __shfl_sync(kFull, my_s0, k), s1 = __shfl_sync(kFull, my_s1, k);
+          const int ns_ = (int)(s1 - s0);
+          rt = R_FALLBACK;
+          if (ns_ > 0) {
+            // the key's space, staged in shared memory when it fits
+            const bool staged = ns_ <= kSpaceSmem;
+            if (staged) {
+              for (int j = lane; j < ns_; j += 32) {
+                s_sp[2 * j] = A.sp_lo[s0 + j];
+                s_sp[2 * j + 1] = A.sp_hi[s0 + j];
+              }
+              __syncwarp();
+            }
+            auto sp_lo = [&](int64_t j) { return staged ? s_sp[2 * j] : (long long)A.sp_lo[s0 + j]; };
+            auto sp_hi = [&](int64_t j) { return staged ? s_sp[2 * j + 1] : (long long)A.sp_hi[s0 + j]; };
+            long long best_len = LLONG_MAX, best_lo = LLONG_MAX;
+            for (int i = lane; i < nf; i += 32) {
+              const long long fa = flo[i], fb = fhi[i];
+              int64_t x = 0, y = ns_;  // first space interval with hi > fa
+              while (x < y) {
+                const int64_t m = (x + y) >> 1;
+                if (sp_hi(m) <= fa)
+                  x = m + 1;
+                else
+                  y = m;
+              }
+              for (int64_t j = x; j < ns_ && sp_lo(j) < fb; j++) {
+                const long long lo = max(fa, sp_lo(j)), hi = min(fb, sp_hi(j));
+                const long long len = hi - lo;
+                if (len >= size && (len < best_len || (len == best_len && lo < best_lo))) best_len = len, best_lo = lo;
+              }
+            }
+            warp_min_pair(best_len, best_lo);
+            __syncwarp();
+            if (best_len != LLONG_MAX) {
+              a = best_lo;
+              free_remove(free_holding(a, a + size), a, a + size);
+              to_pool = true;
+              rt = R_REUSE;
+            }
+          }
+          if (!to_pool) to_cache = true;
+        }
+        if (to_pool) {
           if (lane == 0) {
             A.plo[c] = a;
             A.phi[c] = a + size;
             A.pflag[c] = 1;
           }
-          logrec(2, t, id, size, 0, a, R_PLANNED);
+          if (same) my_pf = 1, my_plo = a, my_phi = a + size;
+          logrec(2, t, id, size, 0, a, rt);
           live += size;
           peak = max(peak, live);
-        } else if (route == R_MISMATCH || route == R_ONLINE) {
-          long long grown;
-          long long a = cache_malloc(c, size, &grown);
-          if (a < 0) {
-            err = STW_ESIM + 100;  // already live in cache
+          if (rt == R_REUSE) n_reuse++;
+        } else if (to_cache) {
+          if (__shfl_sync(kFull, my_cf, k)) {  // request already live in cache
+            err = STW_ESIM + 100;
             err_id = id;
             break;
           }
+          long long grown;
+          int sg;
+          a = cache_malloc(size, &grown, &sg);
+          if (lane == 0) {
+            A.clo[c] = a;
+            A.chi[c] = a + size;
+            A.cseg[c] = sg;
+            A.cflag[c] = 1;
+          }
+          if (same) my_cf = 1, my_clo = a, my_chi = a + size, my_cs = sg;
           if (grown) {
             logrec(1, t, 0, grown, 0, 0, -1);
             reserved += grown;
           }
-          logrec(2, t, id, size, 1, a, route);
+          logrec(2, t, id, size, 1, a, rt);
           live += size;
           peak = max(peak, live);
           clive += size;
           cpeak = max(cpeak, clive);
-          if (route == R_MISMATCH) n_fb++, n_mm++;
-        } else {  // dynamic: best fit in free ∩ space[key], else fallback
-          const int kk = __shfl_sync(0xffffffffu, my_key, k);
-          long long best_len = LLONG_MAX, best_lo = LLONG_MAX;
-          int best_i = -1;
-          if (A.reuse && kk >= 0 && A.sp_off[kk + 1] > A.sp_off[kk]) {
-            const int64_t s0 = A.sp_off[kk], s1 = A.sp_off[kk + 1];
-            for (int i = lane; i < nf; i += 32) {
-              long long a = flo[i], b = fhi[i];
-              int64_t lo_j = s0, hi_j = s1;  // first space interval with hi > a
-              while (lo_j < hi_j) {
-                int64_t m = (lo_j + hi_j) >> 1;
-                if (A.sp_hi[m] <= a)
-                  lo_j = m + 1;
-                else
-                  hi_j = m;
-              }
-              for (int64_t j = lo_j; j < s1 && A.sp_lo[j] < b; j++) {
-                long long lo = max(a, (long long)A.sp_lo[j]), hi = min(b, (long long)A.sp_hi[j]);
-                long long len = hi - lo;
-                if (len >= size && (len < best_len || (len == best_len && lo < best_lo))) best_len = len, best_lo = lo;
-              }
-            }
-            warp_min_pair(best_len, best_lo);
-            if (best_len != LLONG_MAX) best_i = wfind_le(flo, nf, best_lo);
-          }
-          if (best_i >= 0) {
-            free_remove(best_i, best_lo, best_lo + size);
-            if (lane == 0) {
-              A.plo[c] = best_lo;
-              A.phi[c] = best_lo + size;
-              A.pflag[c] = 1;
-            }
-            logrec(2, t, id, size, 0, best_lo, R_REUSE);
-            live += size;
-            peak = max(peak, live);
-            n_reuse++;
-          } else {
-            long long grown;
-            long long a = cache_malloc(c, size, &grown);
-            if (a < 0) {
-              err = STW_ESIM + 100;
-              err_id = id;
-              break;
-            }
-            if (grown) {
-              logrec(1, t, 0, grown, 0, 0, -1);
-              reserved += grown;
-            }
-            logrec(2, t, id, size, 1, a, R_FALLBACK);
-            live += size;
-            peak = max(peak, live);
-            clive += size;
-            cpeak = max(cpeak, clive);
-            n_fb++;
-          }
+          if (rt == R_MISMATCH || rt == R_FALLBACK) n_fb++;
+          if (rt == R_MISMATCH) n_mm++;
         }
       } else {
-        if (A.pflag[c]) {
-          long long lo = A.plo[c], hi = A.phi[c];
+        if (__shfl_sync(kFull, my_pf, k)) {
+          const long long lo = __shfl_sync(kFull, my_plo, k), hi = __shfl_sync(kFull, my_phi, k);
           if (lane == 0) A.pflag[c] = 0;
-          __syncwarp();
+          if (same) my_pf = 0;
           free_add(lo, hi);
           logrec(3, t, id, hi - lo, 0, lo, -1);
           live -= hi - lo;
-        } else if (A.cflag[c]) {
-          long long a, s;
-          cache_free(c, &a, &s);
-          logrec(3, t, id, s, 1, a, -1);
-          live -= s;
-          clive -= s;
+        } else if (__shfl_sync(kFull, my_cf, k)) {
+          const long long lo = __shfl_sync(kFull, my_clo, k), hi = __shfl_sync(kFull, my_chi, k);
+          const int sg = __shfl_sync(kFull, my_cs, k);
+          if (lane == 0) A.cflag[c] = 0;
+          if (same) my_cf = 0;
+          cache_free(lo, hi, sg);
+          logrec(3, t, id, hi - lo, 1, lo, -1);
+          live -= hi - lo;
+          clive -= hi - lo;
         } else {
           err = STW_ESIM + 200;  // double free / unknown id
           err_id = id;
@@ -670,6 +658,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
         }
       }
     }
+    __syncwarp();  // this window's state stores are visible to the next window's prefetch
   }
   if (lane == 0) {
     A.res[0] = nlog;
@@ -682,6 +671,10 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
     A.res[7] = n_fb;
     A.res[8] = n_reuse;
     A.res[9] = n_mm;
+    A.res[10] = max_nb;
+    A.res[11] = max_nf;
+    A.res[12] = sum_nb;
+    A.res[13] = sum_nf;
   }
 }
 
@@ -1033,6 +1026,9 @@ int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep
   STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
   if (!ctx.ok()) return ctx.rc;
   const long long nlog = res[0], err = res[1];
+  if (getenv("STW_REPLAY_STATS"))  // list sizes, when built with -DSTW_REPLAY_STATS
+    fprintf(stderr, "replay: n=%lld max_nb=%lld max_nf=%lld avg_nb=%.1f avg_nf=%.1f\n", (long long)n, res[10], res[11],
+            (double)res[12] / (2.0 * n), (double)res[13] / (2.0 * n));
   if (err) {
     *err_id = res[2];
     if (err == STW_ESIM)
