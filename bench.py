@@ -314,8 +314,10 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
         torch.cuda.synchronize(dev)
         _lib.profile_collect(reset=True)
         _lib.profile(True)
+        torch.cuda.nvtx.range_push("sweep_" + name.split("<")[0])  # ncu --nvtx --nvtx-include sweep_<kernel>/ selects these
         for _ in range(iters):
             fn()
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize(dev)
         _lib.profile(False)
         prof = _lib.profile_collect(reset=True)
@@ -387,9 +389,13 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
         keys.copy_(keys0)
         torch.arange(n2, dtype=torch.int32, device=dev, out=vals)
         torch.cuda.synchronize(dev)
+        if it:
+            torch.cuda.nvtx.range_push("sweep_radix_sort_pairs")
         e0.record(stream)
         api.radix_sort_pairs(keys, vals, 0, 42, stream)
         e1.record(stream)
+        if it:
+            torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize(dev)
         if it:
             tot += e0.elapsed_time(e1)
@@ -401,6 +407,21 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
           "24 B/record/pass (key + value read and written); traffic = 6 passes (+ the 8 B/record histogram read)",
           "k_os_pass@sweep", passes)
     del keys0, keys, vals
+
+    # the look-back scan (every prefix sum of the path): 2^28 int64 in place; 16 B/element
+    n3 = 1 << 28
+    xs = torch.randint(0, 1 << 20, (n3,), dtype=torch.int64, device=dev, generator=g)
+    want = torch.cumsum(xs[: 1 << 20], 0)
+    ys = torch.empty_like(xs)
+
+    def scan():
+        api.scan_i64(xs, ys, True, stream)
+
+    ms = kernel_ms(scan, "k_scan_lb<T>")
+    assert torch.equal(ys[: 1 << 20], want), "scan output"
+    entry("k_scan_lb", n3, 16.0, ms, f"device-wide inclusive prefix sum of {n3} int64 (decoupled look-back, "
+          "single pass): 8 B read + 8 B written per element", "k_scan_lb@sweep")
+    del xs, ys, want
     torch.cuda.empty_cache()
     return out
 
@@ -635,9 +656,11 @@ def main():
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize(dev)
+            torch.cuda.nvtx.range_push("bench_step")  # ncu --nvtx --nvtx-include bench_step/ selects the step
             ev0.record(stream)
             fn()
             ev1.record(stream)
+            torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize(dev)
             total += ev0.elapsed_time(ev1)
         launches = _lib.launch_count() - launches0

@@ -67,6 +67,14 @@ int stw_peak_live(const stw_batch *b, int32_t static_only, int64_t *peak, void *
 int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begin_bit,
                          int32_t end_bit, void *stream, char *err, size_t errlen);
 
+/* ---- scan: device-wide prefix sum of int64 (device pointers; in == out
+ * allowed). The running sums of every size / offset computation on the path
+ * (pack_group's prefix sums planner.py:98-107, stacking :441-444, the live
+ * bytes of peak_live_bytes model.py:261-276); single pass, decoupled
+ * look-back. */
+int stw_scan_i64(const int64_t *in, int64_t *out, int64_t n, int32_t inclusive, void *stream, char *err,
+                 size_t errlen);
+
 /* ---- planner: synthesize_static_plan (planner.py:357-473) ----------------
  * Plans every trace of the batch under each candidate (fusion, gap_insert)
  * setting. Unit u = trace * n_cand + cand. */

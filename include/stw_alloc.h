@@ -74,6 +74,31 @@ int stw_alloc_status(int64_t *out);
  * while any block is live. */
 int stw_alloc_shutdown(void);
 
+/* ---- Allocation Profiler (paper §4) + request matcher ---
+ * Modes: 0 passthrough (plain cudaMalloc / cudaFree; the default before a
+ * plan is loaded), 1 profiling (passthrough, and every malloc / free issued
+ * while profiling is recorded with the current phase / module / dynamic tags,
+ * in call order -- the raw trace of traceio.py:6-11; frees of blocks allocated
+ * before profiling began are not recorded), 2 serving the plan (the mode
+ * stw_alloc_init enters). Blocks allocated in passthrough keep being freed
+ * through cudaFree in any mode. */
+int stw_alloc_set_mode(int32_t mode);
+/* tags of the next requests while profiling: phase / module are the caller's
+ * interned indices */
+void stw_prof_set(int32_t phase, int32_t module, int32_t dynamic);
+/* the recording so far (op 0 alloc / 1 free, dynamic, phase, module, id,
+ * bytes); returns the record count (only cap are written) */
+int64_t stw_prof_records(int8_t *op, int8_t *dyn, int32_t *phase, int32_t *module, int64_t *id, int64_t *size,
+                         int64_t cap);
+/* (route, replay address) of every request served since stw_alloc_init, in
+ * call order; returns the count (only cap are written) */
+int64_t stw_alloc_served(int8_t *route, int64_t *vaddr, int64_t cap);
+/* dynamic requests matched by layer instance: instance l's dynamic
+ * allocations take reuse keys keys[off[l] .. off[l+1]) in order (-1 = none);
+ * stw_set_layer_instance names the instance the next requests come from */
+int stw_alloc_load_dyn_keys(int32_t n_layers, const int64_t *off, const int32_t *keys);
+void stw_set_layer_instance(int32_t layer, int32_t dynamic);
+
 /* ---- the same policies as standalone host objects ----------------------
  * CachingAllocator (baseline.py:35-95) over virtual addresses starting at
  * `base`: malloc returns STW_ESIM if rid is live, free STW_ESIM if unknown. */

@@ -86,7 +86,7 @@ class Fusion(C.Structure):
 EXPORTS = (
     "stw_version", "stw_peak_live", "stw_radix_sort_pairs", "stw_plan_batch", "stw_plan_batches", "stw_validate",
     "stw_validate_sets", "stw_reuse_map", "stw_simulate", "stw_baseline", "stw_group_events", "stw_local_plans",
-    "stw_weighted_tmp", "stw_fuse_plans", "stw_build_layers", "stw_metrics", "stw_release_scratch",
+    "stw_weighted_tmp", "stw_fuse_plans", "stw_build_layers", "stw_metrics", "stw_release_scratch", "stw_scan_i64",
 )
 
 _lib = None

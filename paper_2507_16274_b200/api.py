@@ -53,6 +53,16 @@ def radix_sort_pairs(keys, vals, begin_bit: int = 0, end_bit: int = 64, stream=N
                                       C.c_int32(end_bit), s, err, C.sizeof(err)), err)
 
 
+def scan_i64(inp, out=None, inclusive: bool = True, stream=None):
+    """Device-wide prefix sum of an int64 device tensor (stw_scan_i64)."""
+    out = inp if out is None else out
+    err = _lib.errbuf()
+    _lib.check(_lib.load().stw_scan_i64(_lib.ptr(inp), _lib.ptr(out), C.c_int64(int(inp.numel())),
+                                        C.c_int32(int(inclusive)), _lib.stream_handle(stream), err, C.sizeof(err)),
+               err)
+    return out
+
+
 def validate_sets(set_off, t_s, t_e, size, addr, shift: int = 9, stream=None):
     """len(validate_plan(plan)) for every (set, candidate) plan of a batch, on the
     device (K7 over many plans; planner.py:476-505). Device tensors: set_off

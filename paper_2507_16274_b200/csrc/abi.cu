@@ -63,6 +63,20 @@ int stw_radix_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t begi
   return finish(ctx);
 }
 
+int stw_scan_i64(const int64_t *in, int64_t *out, int64_t n, int32_t inclusive, void *stream, char *err,
+                 size_t errlen) {
+  STW_ENTRY(stream, err, errlen);
+  if (n < 0 || (n > 0 && (!in || !out))) {
+    ctx.fail(STW_EARG, "bad scan arguments");
+    return ctx.rc;
+  }
+  {
+    Arena ar(&ctx);
+    device_scan<int64_t>(ctx, ar, in, out, n, inclusive != 0);
+  }
+  return finish(ctx);
+}
+
 int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *out, char *err, size_t errlen) {
   STW_ENTRY(opts ? opts->stream : nullptr, err, errlen);
   if (!b || !opts || !out) {

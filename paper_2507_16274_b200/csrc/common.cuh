@@ -4,6 +4,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/stw.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
@@ -94,6 +96,22 @@ void d2h_async(Ctx &ctx, void *dst, const void *dsrc, size_t bytes);
 void host_sync(Ctx &ctx);
 // drop anything a failed earlier call left pending (start of a planner call)
 void pinned_reset();
+
+// NVTX ranges (header-only NVTX3; no-ops unless a profiler is attached): the
+// call, then one range per phase, for nsys / ncu --nvtx filtering
+struct NvtxPhases {
+  bool open = false;
+  explicit NvtxPhases(const char *call) { nvtxRangePushA(call); }
+  void next(const char *phase) {
+    if (open) nvtxRangePop();
+    nvtxRangePushA(phase);
+    open = true;
+  }
+  ~NvtxPhases() {
+    if (open) nvtxRangePop();
+    nvtxRangePop();
+  }
+};
 
 // host-side size helpers
 

@@ -2321,6 +2321,7 @@ struct PhaseTimer {
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror,
                void (*after_uploads)(void *), void *hook_arg) {
   pinned_reset();  // a call that failed midway may have left transfers pending
+  NvtxPhases nv("stw_plan_batch");
   PhaseTimer pt(ctx);
   Arena ar(&ctx);
   DevBatch b;
@@ -2342,6 +2343,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (T == 0) return ctx.rc;
 
   pt.mark("stage");
+  nv.next("A ranks");
   // ---- A: canonical ranks
   int32_t *tr = ar.take<int32_t>(N + 1);
   int32_t *q = ar.take<int32_t>(N + 1), *r = ar.take<int32_t>(N + 1);
@@ -2389,6 +2391,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   const int pb = bitlen_u64((uint64_t)him[2]);
 
   pt.mark("A checks");
+  nv.next("B groups");
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
   uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
@@ -2468,6 +2471,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_plan_tmp, P, p0, P);
 
   pt.mark("B groups");
+  nv.next("C fusion");
   // ---- C: fusion variant
   Plans p1 = p0;
   int32_t *pid1 = pid0;
@@ -2525,6 +2529,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   d2h_async(ctx, h_imax, d_imax, sizeof(h_imax));
 
   pt.mark("C fusion");
+  nv.next("D items");
   // ---- D: items per (variant, trace)
   std::vector<int64_t> io(V * T + 1, 0);
   sync(ctx);
@@ -2688,6 +2693,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (V * T > 0 && !fused_items) LAUNCH(k_class_ends_bs, NI, it, d_io, V * T, NI, cend);
 
   pt.mark("D classes");
+  nv.next("E layers");
   // ---- E: layers per unit (host-side unit layout and CTA packing were prepared during D)
   const int64_t TU = uo[U];
   int64_t *d_uo = h2d(ctx, ar, uo);
@@ -2766,6 +2772,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
 
   pt.mark("E layers");
   if (after_uploads) after_uploads(hook_arg);  // the unfused path: after phase E
+  nv.next("F emission");
   // ---- F: emission
   int64_t *addr = ar.take<int64_t>((int64_t)C * N + 1);
   int32_t *layer = ar.take<int32_t>((int64_t)C * N + 1);
@@ -2775,6 +2782,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_emit, N, EA);
 
   pt.mark("F emit");
+  nv.next("G self-check");
   // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
   int64_t *peak = ar.take<int64_t>(T);
   if (!ctx.ok()) return ctx.rc;

@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayArgs A) {
       fhi[0] = A.pool;
     }
     nf = 1;
+    __syncwarp();  // the other lanes read it (racecheck)
   }
   long long nlog = 0, live = 0, peak = 0, clive = 0, cpeak = 0, reserved = 0;
   long long n_fb = 0, n_reuse = 0, n_mm = 0;
@@ -761,6 +762,8 @@ __global__ void k_max_scan(const int64_t *__restrict__ v, int64_t n, long long *
 
 
 int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep, stw_log *log, int64_t *err_id) {
+  NvtxPhases nv(bun ? "stw_simulate" : "stw_baseline");
+  nv.next("prepare");
   Arena ar(&ctx);
   DevBatch b;
   if (!stage_batch(ctx, ar, in, &b)) return ctx.rc;
@@ -899,6 +902,7 @@ int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep
   }
   const int64_t cap_log = 1 + 3 * n;
   // parallel fast path (static-only, every allocation planned, unique ids)
+  nv.next("parallel replay");
   if (!baseline && n > 0 && nu == n && nd > 0) {
     int *bad = ar.take<int>(1);
     if (!ctx.ok()) return ctx.rc;
@@ -972,6 +976,7 @@ int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep
     }
   }
   // sequential replay
+  nv.next("sequential replay");
   ReplayArgs R{};
   R.n = n;
   R.operm = operm;

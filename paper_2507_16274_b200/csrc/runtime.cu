@@ -187,24 +187,50 @@ void Arena::release() {
 // kScanDirect tiles instead sum all their predecessors' aggregates at once.
 constexpr int64_t kScanDirect = 1024;
 
+// Tile I/O is coalesced: 16-byte vector loads / stores over the tile (thread
+// t moves vectors t, t + 256, ...), staged through shared memory (padded one
+// element per 16 against bank conflicts), where each thread then scans its
+// kScanItems consecutive elements.
 template <class T>
 __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ in, T *__restrict__ out, int64_t n,
                                                           int inclusive, uint32_t *__restrict__ flag,
                                                           T *__restrict__ agg, T *__restrict__ pre,
                                                           uint32_t *__restrict__ ctr) {
+  constexpr int kVec = 16 / sizeof(T);          // elements per 16-byte vector
+  constexpr int kVecs = kScanTile / kVec;       // vectors per tile
+  constexpr int kPad = kScanTile + kScanTile / 16;
+  __shared__ __align__(16) T st[kPad];
   __shared__ T sh[33];
   __shared__ uint32_t s_tile;
   __shared__ T s_excl;
+  auto at = [](int i) { return i + (i >> 4); };  // padded position of tile element i
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const int64_t base = (int64_t)tile * kScanTile + (int64_t)tid * kScanItems;
+  const int64_t t0 = (int64_t)tile * kScanTile;
+  const int cnt = (int)(n - t0 < kScanTile ? n - t0 : kScanTile);
+  const bool vec_ok = cnt == kScanTile && (reinterpret_cast<uintptr_t>(in + t0) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(out + t0) & 15) == 0;
+  if (vec_ok) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + t0);
+#pragma unroll
+    for (int j = 0; j < kVecs / kScanThreads; j++) {
+      const int q = j * kScanThreads + tid;
+      const uint4 w = __ldcs(src + q);  // streamed once: evict-first
+      const T *e = reinterpret_cast<const T *>(&w);
+#pragma unroll
+      for (int x = 0; x < kVec; x++) st[at(q * kVec + x)] = e[x];
+    }
+  } else {
+    for (int i = tid; i < kScanTile; i += kScanThreads) st[at(i)] = i < cnt ? in[t0 + i] : T(0);
+  }
+  __syncthreads();
   T v[kScanItems];
   T acc = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    v[k] = base + k < n ? in[base + k] : T(0);
+    v[k] = st[at(tid * kScanItems + k)];
     acc += v[k];
   }
   T total;
@@ -238,8 +264,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
   } else if (tid < 32) {
     T excl = 0;
     if (tile > 0) {
-      for (int64_t t0 = (int64_t)tile - 1;; t0 -= 32) {
-        const int64_t t = t0 - lane;
+      for (int64_t tw = (int64_t)tile - 1;; tw -= 32) {
+        const int64_t t = tw - lane;
         uint32_t f = 2;
         T val = 0;
         if (t >= 0) {
@@ -267,8 +293,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
   T run = ex + s_excl;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    if (base + k < n) out[base + k] = inclusive ? run + v[k] : run;
+    st[at(tid * kScanItems + k)] = inclusive ? run + v[k] : run;
     run += v[k];
+  }
+  __syncthreads();
+  if (vec_ok) {
+    uint4 *dst = reinterpret_cast<uint4 *>(out + t0);
+#pragma unroll
+    for (int j = 0; j < kVecs / kScanThreads; j++) {
+      const int q = j * kScanThreads + tid;
+      uint4 w;
+      T *e = reinterpret_cast<T *>(&w);
+#pragma unroll
+      for (int x = 0; x < kVec; x++) e[x] = st[at(q * kVec + x)];
+      __stcs(dst + q, w);
+    }
+  } else {
+    for (int i = tid; i < cnt; i += kScanThreads) out[t0 + i] = st[at(i)];
   }
 }
 

@@ -187,6 +187,27 @@ struct State {
   // metrics (sim.py:67-117)
   int64_t cur = 0, peak = 0, cache_cur = 0, cache_peak = 0;
   int64_t fallback = 0, reuse = 0, mismatch = 0, occupied = 0, bad_frees = 0;
+  // request matcher for dynamic requests: per layer instance, the reuse keys of
+  // its dynamic allocations in recorded order (-1 = no entry); layer = current instance
+  std::vector<std::deque<int32_t>> dyn_keys;
+  int32_t layer = -1;
+  bool dyn_by_layer = false;
+  // modes: 0 passthrough (cudaMalloc / cudaFree), 1 profiling (passthrough +
+  // recording), 2 serving the plan (stw_alloc_init switches to it)
+  int mode = 0;
+  std::unordered_map<const void *, int64_t> passthrough;  // ptr -> size
+  // the Allocation Profiler's records: one per op, raw-trace order
+  struct Rec {
+    int8_t op;  // 0 alloc, 1 free
+    int8_t dyn;
+    int32_t phase, module;
+    int64_t id, size;
+  };
+  std::vector<Rec> recs;
+  std::unordered_map<const void *, int64_t> rec_id;  // live recorded block -> its id
+  int64_t next_id = 0;
+  int32_t p_phase = 0, p_module = 0, p_dyn = 0;
+  std::vector<std::pair<int8_t, int64_t>> served;  // (route, replay address) of every served request
 };
 
 State &S() {
@@ -238,6 +259,10 @@ void unmap_all(State &s) {
 
 void reset(State &s) {
   s.inited = false;
+  s.served.clear();
+  s.dyn_keys.clear();
+  s.dyn_by_layer = false;
+  s.layer = -1;
   s.free.clear();
   s.queues.clear();
   s.spaces.clear();
@@ -379,6 +404,7 @@ int stw_alloc_init_ex(int device, int64_t pool_size, int64_t alignment, int64_t 
   if (pool_size > 0) s.free[0] = pool_size;
   s.cache.next_base = pool_size;  // the replay's cache starts at pool_size (sim.py:154)
   s.inited = true;
+  s.mode = 2;
   return STW_OK;
 }
 
@@ -429,15 +455,32 @@ void *stw_malloc(size_t nbytes, int device, void *stream) {
   (void)stream;
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
-  if (!s.inited) return nullptr;
   if (nbytes == 0) nbytes = 1;
+  if (s.mode != 2) {  // passthrough, recorded when profiling
+    void *p = nullptr;
+    if (cudaMalloc(&p, nbytes) != cudaSuccess) return nullptr;
+    s.passthrough[p] = (int64_t)nbytes;
+    if (s.mode == 1) {
+      const int64_t id = s.next_id++;
+      s.rec_id[p] = id;
+      s.recs.push_back(State::Rec{0, (int8_t)s.p_dyn, s.p_phase, s.p_module, id, (int64_t)nbytes});
+    }
+    return p;
+  }
+  if (!s.inited) return nullptr;
   const int64_t size = (int64_t)((nbytes + s.alignment - 1) / s.alignment * s.alignment);
   // decide the route first; nothing is committed until the memory is there
   int route;
   int64_t vaddr = -1;
   std::deque<int64_t> *q = nullptr;
   if (s.dynamic) {
-    vaddr = reuse_fit(s, s.key, size);
+    int32_t key = s.key;
+    if (s.dyn_by_layer) {  // the layer instance's next recorded key (popped once served)
+      key = -1;
+      if (s.layer >= 0 && s.layer < (int32_t)s.dyn_keys.size() && !s.dyn_keys[s.layer].empty())
+        key = s.dyn_keys[s.layer].front();
+    }
+    vaddr = reuse_fit(s, key, size);
     route = vaddr >= 0 ? 1 : 2;
   } else {
     route = 3;
@@ -467,7 +510,11 @@ void *stw_malloc(size_t nbytes, int device, void *stream) {
     pool_remove(s, vaddr, vaddr + size);
   }
   if (q) q->pop_front();
+  if (s.dynamic && s.dyn_by_layer && s.layer >= 0 && s.layer < (int32_t)s.dyn_keys.size() &&
+      !s.dyn_keys[s.layer].empty())
+    s.dyn_keys[s.layer].pop_front();
   account_alloc(s, size, lv.space == 1, route);
+  s.served.push_back({(int8_t)route, lv.vaddr});
   void *ptr = reinterpret_cast<void *>(s.base + lv.vaddr);
   s.live[ptr] = lv;
   return ptr;
@@ -479,6 +526,19 @@ void stw_free(void *ptr, size_t nbytes, int device, void *stream) {
   (void)stream;
   State &s = S();
   std::lock_guard<std::mutex> lk(s.mu);
+  auto pt = s.passthrough.find(ptr);
+  if (pt != s.passthrough.end()) {
+    if (s.mode == 1) {
+      auto r = s.rec_id.find(ptr);
+      if (r != s.rec_id.end()) {  // frees of blocks allocated before profiling began are not part of the trace
+        s.recs.push_back(State::Rec{1, 0, s.p_phase, s.p_module, r->second, pt->second});
+        s.rec_id.erase(r);
+      }
+    }
+    cudaFree(ptr);
+    s.passthrough.erase(pt);
+    return;
+  }
   auto it = s.live.find(ptr);
   if (it == s.live.end()) {  // unknown or double free (sim.py:231-232): counted, reported by stw_alloc_report
     s.bad_frees++;
@@ -538,7 +598,68 @@ int stw_alloc_shutdown(void) {
   if (!s.live.empty()) return STW_EARG;  // live tensors still point into the range
   if (s.inited) unmap_all(s);
   reset(s);
+  s.mode = 0;
   return STW_OK;
+}
+
+// ---- Allocation Profiler + request matcher ----------------------------------
+
+int stw_alloc_set_mode(int32_t mode) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  if (mode < 0 || mode > 2 || (mode == 2 && !s.inited)) return STW_EARG;
+  if (mode == 1 && s.mode != 1) {  // a fresh recording
+    s.recs.clear();
+    s.rec_id.clear();
+    s.next_id = 0;
+  }
+  s.mode = mode;
+  return STW_OK;
+}
+
+void stw_prof_set(int32_t phase, int32_t module, int32_t dynamic) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  s.p_phase = phase;
+  s.p_module = module;
+  s.p_dyn = dynamic;
+}
+
+int64_t stw_prof_records(int8_t *op, int8_t *dyn, int32_t *phase, int32_t *module, int64_t *id, int64_t *size,
+                         int64_t cap) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  const int64_t n = (int64_t)s.recs.size();
+  for (int64_t k = 0; k < n && k < cap; k++) {
+    const State::Rec &r = s.recs[k];
+    op[k] = r.op, dyn[k] = r.dyn, phase[k] = r.phase, module[k] = r.module, id[k] = r.id, size[k] = r.size;
+  }
+  return n;
+}
+
+int stw_alloc_load_dyn_keys(int32_t n_layers, const int64_t *off, const int32_t *keys) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  s.dyn_keys.assign(n_layers, {});
+  for (int32_t l = 0; l < n_layers; l++)
+    for (int64_t j = off[l]; j < off[l + 1]; j++) s.dyn_keys[l].push_back(keys[j]);
+  s.dyn_by_layer = true;
+  return STW_OK;
+}
+
+int64_t stw_alloc_served(int8_t *route, int64_t *vaddr, int64_t cap) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  const int64_t n = (int64_t)s.served.size();
+  for (int64_t k = 0; k < n && k < cap; k++) route[k] = s.served[k].first, vaddr[k] = s.served[k].second;
+  return n;
+}
+
+void stw_set_layer_instance(int32_t layer, int32_t dynamic) {
+  State &s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  s.layer = layer;
+  s.dynamic = dynamic;
 }
 
 // ---- standalone allocator objects ---------------------------------------

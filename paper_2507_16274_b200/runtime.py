@@ -198,6 +198,17 @@ class PlanAllocator:
         return out
 
     @staticmethod
+    def served() -> list:
+        """[(route, replay address)] of every request served since the plan was loaded."""
+        L = load()
+        L.stw_alloc_served.restype = C.c_int64
+        n = L.stw_alloc_served(None, None, C.c_int64(0))
+        r = np.empty(n, np.int8)
+        v = np.empty(n, np.int64)
+        L.stw_alloc_served(_lib.ptr(r), _lib.ptr(v), C.c_int64(n))
+        return [(ROUTES[a], b) for a, b in zip(r.tolist(), v.tolist())]
+
+    @staticmethod
     def status() -> dict:
         out = np.zeros(7, np.int64)
         load().stw_alloc_status(_lib.ptr(out))

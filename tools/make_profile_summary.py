@@ -1,6 +1,15 @@
 """Turn a `tools/prof_round.sh <tag>` bundle (gpurun_out/) into the committed
 profile evidence: profiles/<tag>_bench.json, <tag>_launches_c4.csv,
-<tag>_ncu_<kernel>.txt, ncu_traffic.json and <tag>_summary.md."""
+<tag>_ncu_<kernel>.txt, ncu_traffic.json and <tag>_summary.md.
+
+Every `ncu --set full` capture was selected by the NVTX range bench.py opens
+around the launch it times (bench_step/ for the planner step, sweep_<kernel>/
+for the >> L2 roofline launches), and is checked here against that timing:
+the captured launch's duration must match the bench's event-timed launch
+(ncu serialises with cold caches, so within a factor of 1.6) and, for the
+HBM-bound sweep kernels, its DRAM bytes must be the algorithmic bytes of the
+same launch within 30% -- otherwise the capture is of some other launch and the
+script fails."""
 import collections
 import csv
 import io
@@ -16,9 +25,13 @@ P = os.path.join(ROOT, "profiles")
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
-CAPS = [("k_layers_w32", "k_layers_w32"), ("k_fusion", "k_fusion"), ("k_seg_radix", "k_seg_radix"),
-        ("k_overlap_sweep@c4", "k_overlap_sweep_c4"), ("k_overlap_sweep@sweep", "k_overlap_sweep_big"),
-        ("k_peak_warp@sweep", "k_peak_warp_big"), ("k_os_pass@sweep", "k_os_pass_big")]
+# key in ncu_traffic.json -> (capture name, bench kernel_roofline entry or None, launches per bench launch)
+CAPS = {"k_layers_w32": ("k_layers_w32", None), "k_fusion": ("k_fusion", None),
+        "k_items_sorted<8>": ("k_items_sorted", None), "k_overlap_sweep@c4": ("k_overlap_sweep_c4", None),
+        "k_peak_warp@sweep": ("k_peak_warp_big", "k_peak_warp"),
+        "k_overlap_sweep@sweep": ("k_overlap_sweep_big", "k_overlap_sweep"),
+        "k_os_pass@sweep": ("k_os_pass_big", "radix_sort_pairs"), "k_os_hist@sweep": ("k_os_hist_big", None),
+        "k_scan_lb@sweep": ("k_scan_lb_big", "k_scan_lb")}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "ms": 1e3}
 
 
@@ -28,36 +41,49 @@ def raw_rows(rep):
     return rows[0], rows[1], rows[2:]
 
 
+def metric(hdr, units, r, m):
+    i = hdr.index(m)
+    return float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
+
+
 def main(tag):
     os.makedirs(P, exist_ok=True)
     bench = json.load(open(os.path.join(G, f"{tag}_bench.json")))
     shutil.copy(os.path.join(G, f"{tag}_bench.json"), os.path.join(P, f"{tag}_bench.json"))
     shutil.copy(os.path.join(G, f"{tag}_launches.csv"), os.path.join(P, f"{tag}_launches_c4.csv"))
-    traffic = {}
-    for key, name in CAPS:
+    kr = bench.get("kernel_roofline") or {}
+    traffic, checks = {}, []
+    for key, (name, bench_key) in CAPS.items():
         rep = os.path.join(G, f"{tag}_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
         with open(os.path.join(P, f"{tag}_ncu_{name}.txt"), "w") as fh:
-            sys_stdout, sys.stdout = sys.stdout, fh
-            try:
-                print("==", os.path.basename(rep))
-                for d in ncu_summary.raw(rep):
-                    print("  " + " | ".join(f"{k.split('.')[0]}={v[0]} {v[1]}" for k, v in d.items()))
-                for i, pct, ex, ins in ncu_summary.stalls(rep):
-                    print(f"   [{i:5d}] {pct:5.1f}%  x{ex:>9}  {ins[:90]}")
-            finally:
-                sys.stdout = sys_stdout
+            fh.write(f"== {os.path.basename(rep)} (ncu --set full, NVTX-selected launch; see tools/prof_round.sh)\n")
+            for d in ncu_summary.raw(rep):
+                fh.write("  " + " | ".join(f"{k.split('.')[0]}={v[0]} {v[1]}" for k, v in d.items()) + "\n")
+            for i, pct, ex, ins in ncu_summary.stalls(rep):
+                fh.write(f"   [{i:5d}] {pct:5.1f}%  x{ex:>9}  {ins[:90]}\n")
         hdr, units, rows = raw_rows(rep)
-        tot_b, tot_t = 0.0, 0.0
-        for r in rows:
-            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                i = hdr.index(m)
-                tot_b += float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
-            i = hdr.index("gpu__time_duration.sum")
-            tot_t += float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
-        traffic[key] = {"dram_bytes_per_launch": tot_b / len(rows), "duration_us": tot_t / len(rows),
-                        "launches_captured": len(rows), "capture": f"profiles/{tag}_ncu_{name}.txt"}
+        b = sum(metric(hdr, units, r, "dram__bytes_read.sum") + metric(hdr, units, r, "dram__bytes_write.sum")
+                for r in rows) / len(rows)
+        us = sum(metric(hdr, units, r, "gpu__time_duration.sum") for r in rows) / len(rows)
+        grid = rows[0][hdr.index("launch__grid_size")] if "launch__grid_size" in hdr else None
+        e = {"dram_bytes_per_launch": b, "duration_us": us, "grid_size": grid, "launches_captured": len(rows),
+             "capture": f"profiles/{tag}_ncu_{name}.txt"}
+        if bench_key and bench_key in kr:
+            k = kr[bench_key]
+            passes = 6 if bench_key == "radix_sort_pairs" else 1  # the sort's entry spans its 6 passes
+            algo = k["records"] * k["algorithmic_bytes_per_record"] / passes
+            ev_us = 1e3 * k["ms"] / passes
+            e["bench_launch_us"] = ev_us
+            e["algorithmic_bytes_per_launch"] = algo
+            ok_t = 1 / 1.6 < us / ev_us < 1.6
+            ok_b = bench_key == "k_overlap_sweep" or 0.7 < b / algo < 1.3  # K7 reads shared columns once per set
+            checks.append((key, ok_t, ok_b, us, ev_us, b, algo))
+            if not (ok_t and ok_b):
+                raise SystemExit(f"capture {name} is not the timed launch: {us:.1f} us vs {ev_us:.1f} us, "
+                                 f"{b / 1e9:.3f} GB vs {algo / 1e9:.3f} GB algorithmic")
+        traffic[key] = e
     json.dump(traffic, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 
     rows = list(csv.reader(open(os.path.join(G, f"{tag}_launches.csv"))))
@@ -66,29 +92,40 @@ def main(tag):
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for r in rows[h + 1:]:
         n = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("stw::", "")
+        n = n.replace("<unnamed>::", "")
         m, v = r[hdr.index("Metric Name")], float(r[hdr.index("Metric Value")].replace(",", ""))
         if m == "gpu__time_duration.sum":
             agg[n][0] += 1
             agg[n][1] += v / 1e3
-        else:
+        elif m.startswith("dram__bytes"):
             agg[n][2] += v
     calls = agg["k_fusion"][0] or 1
     ours = {k: v for k, v in agg.items() if not k.startswith("at::")}
     tot = sum(a[1] for a in ours.values())
     nl = sum(a[0] for a in ours.values())
     table = "\n".join(f"| `{n[:60]}` | {a[0]} | {a[1] / calls:.1f} | {100 * a[1] / tot:.1f}% | {a[2] / calls / 1e6:.1f} |"
-                      for n, a in sorted(ours.items(), key=lambda x: -x[1][1])[:24])
+                      for n, a in sorted(ours.items(), key=lambda x: -x[1][1])[:26])
     d = bench
-    kr = d.get("kernel_roofline") or {}
     cfg = d.get("configs") or {}
     rf = d["roofline"]
-    s = f"""# Round 1 profile summary (1x B200, sm_100a)
+    chk = "\n".join(f"| `{k}` | {ev:.1f} | {us:.1f} | {al / 1e9:.3f} | {b / 1e9:.3f} | {b / al:.2f} |"
+                    for k, _, _, us, ev, b, al in checks)
+    sw = "\n".join(f"| `{k}` | {v['records']:,} | {v['algorithmic_bytes_per_record']:.0f} | {v['ms']:.3f} | "
+                   f"{v['achieved']:.0f} | {100 * v['frac']:.1f}% |" for k, v in kr.items())
+    cf = "\n".join(
+        f"| {n} | {c['events']:,} | " + " | ".join(f"{c['gpu_ms'][s]:.2f} / {c['cpu_ms'][s]:.2f}" for s in
+                                                     ("plan", "reuse", "validate", "simulate", "baseline", "peak"))
+        + f" | {c['fragmentation']:.6f} | {c['baseline_fragmentation']:.6f} |"
+        for n, c in cfg.items() if "cpu_ms" in c)
+    s = f"""# Round {tag[1:]} profile summary (1x B200, sm_100a)
 
 Made by `bash tools/prof_round.sh {tag}` under `gpurun` (one GPU) and
-`python tools/make_profile_summary.py {tag}`: `{tag}_bench.json` is that run's
-bench line; `{tag}_ncu_*.txt` summarise `ncu --set full --clock-control none
---import-source on` captures (key metrics + top SASS stall sites);
-`ncu_traffic.json` holds their DRAM bytes per launch (bench.py's `traffic`).
+`python tools/make_profile_summary.py {tag}`. `{tag}_bench.json` is that run's
+bench line. Every `{tag}_ncu_*.txt` summarises an `ncu --set full --clock-control none
+--import-source on` capture of the launch bench.py times, selected by the NVTX
+range bench.py opens around it (`bench_step/`, `sweep_<kernel>/`), with the key
+metrics and the top SASS stall sites; `ncu_traffic.json` holds their DRAM bytes
+per launch (bench.py's `traffic`).
 
 ## Headline (bench.py defaults: c4 sweep, 4096 traces x 4 candidates)
 
@@ -97,50 +134,51 @@ bench line; `{tag}_ncu_*.txt` summarise `ncu --set full --clock-control none
 | planned allocations/s, device-resident inputs | {d['value']:.3e} ({d['ms_per_step']:.3f} ms/step) |
 | e2e: pinned host batch in, host results out, every step (`stw_plan_batches`) | {d['e2e']['value']:.3e} |
 | e2e, one synchronous `stw_plan_batch` per step | {d['e2e'].get('serial_value', float('nan')):.3e} |
-| CPU baseline (C port of the reference planner, {d['cpu_baseline']['cores']} threads) | {d['cpu_baseline']['value']:.3e} |
+| CPU baseline (C port of the reference planner, multiprocessing.Pool({d['cpu_baseline']['cores']})) | {d['cpu_baseline']['value']:.3e} |
+| the exchange's result vs the reference's c4 anchor | {d.get('verified')} |
 | libstw launches in the timed region ({d['steps']} steps) | {d['gpu_launches']} |
 | clocks during the timed region | {d['clocks']['sm_mhz']} / {d['clocks']['sm_max_mhz']} MHz, reasons {d['clocks']['reasons']} |
 
 Dominant kernel of the step: `{rf['kernel']}` ({100 * rf['share_of_kernel_time']:.0f}% of libstw kernel time,
 event-timed), the layer-assignment greedy: {rf['achieved']:.0f} GB/s algorithmic (40 B/item) =
-{100 * rf['frac']:.1f}% of the measured {rf['peak']:.0f} GB/s; ncu DRAM traffic {rf['traffic'] / 1e6 if rf['traffic'] else float('nan'):.1f} MB per launch.
-It is latency-bound (a dependent warp-collective chain per item), not HBM-bound.
+{100 * rf['frac']:.1f}% of the measured {rf['peak']:.0f} GB/s; ncu DRAM traffic
+{rf['traffic'] / 1e6 if rf['traffic'] else float('nan'):.1f} MB per launch. It is latency-bound (a dependent
+warp-collective chain per item), not HBM-bound.
 
-## Launch list of the planner calls (ncu, serialised cold-cache: shares, not absolutes)
+## Launch list of the planner step (ncu, serialised cold-cache: shares, not absolutes)
 
-`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`
-over `bench.py --steps 1 --warmup 1 --no-kernel-sweep` ({calls} planner calls; torch's L2-flush fill kernel
-excluded); raw CSV `{tag}_launches_c4.csv`. Per call: {nl / calls:.0f} libstw launches, {tot / calls / 1e3:.2f} ms
-of serialised kernel time.
+`ncu --nvtx --nvtx-include bench_step/ --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`
+over `bench.py --steps 1 --warmup 3 --no-kernel-sweep` ({calls} planner calls inside `bench_step` ranges);
+raw CSV `{tag}_launches_c4.csv`. Per call: {nl / calls:.0f} libstw launches, {tot / calls / 1e3:.2f} ms of
+serialised kernel time.
 
 | kernel | launches ({calls} calls) | us per call | share | DRAM MB per call |
 |---|---:|---:|---:|---:|
 {table}
 
-## HBM roofline sweep of the data-parallel kernels (inputs >> 126 MB L2)
+## HBM roofline sweep of the data-parallel kernels (inputs >> 126 MB L2, CUDA-event timed in bench.py)
 
-| kernel | records | algorithmic B/record | ms | achieved GB/s | of measured peak | ncu DRAM bytes |
-|---|---:|---:|---:|---:|---:|---:|
-"""
-    for k, v in kr.items():
-        tr = v.get("traffic")
-        s += (f"| `{k}` | {v['records']:,} | {v['algorithmic_bytes_per_record']:.1f} | {v['ms']:.3f} | "
-              f"{v['achieved']:.0f} | {100 * v['frac']:.1f}% | {tr / 1e9 if tr else float('nan'):.2f} GB |\n")
-    s += "\n## Single-trace configs (package API, host objects in and out, best of 3)\n\n"
-    s += ("| config | events | plan ms | replay ms | replay ops/s | baseline ms | frag (plan) | frag (caching alloc.) |\n"
-          "|---|---:|---:|---:|---:|---:|---:|---:|\n")
-    for k, v in cfg.items():
-        s += (f"| {k} | {v['events']:,} | {v['plan_ms']:.1f} | {v['replay_ms']:.1f} | {v['replay_ops_per_s']:.3e} | "
-              f"{v['baseline_ms']:.1f} | {v['fragmentation']:.6f} | {v['baseline_fragmentation']:.6f} |\n")
-    s += """
-Fragmentation ratios are bit-exact against the reference (tests/golden/anchors.json).
-Reference CPU times for the same configs (survey container, BASELINE.md §3): plan
-0.144 / 2.08 / 0.102 / 0.174 / 45.9 s, simulate 0.18 / 1.86 / 0.15 / 0.29 / 22.6 s,
-baseline 0.163 / 1.78 / 0.187 / 0.317 / 35.7 s.
+| kernel | records | algorithmic B/record | ms | achieved GB/s | of measured peak |
+|---|---:|---:|---:|---:|---:|
+{sw}
+
+Capture check (the ncu launch is the timed launch): bench event time vs ncu duration per launch, and
+algorithmic vs ncu DRAM bytes per launch (K7 reads each set's shared size/t_s/t_e columns once for all
+four candidates, so its DRAM bytes sit below the 24 B per rectangle-candidate it is credited with).
+
+| capture | bench us/launch | ncu us | algorithmic GB | ncu DRAM GB | DRAM / algorithmic |
+|---|---:|---:|---:|---:|---:|
+{chk}
+
+## Single-trace configs: device (package API, best of 3) / C port of the reference (1 host thread), ms
+
+| config | events | plan | reuse | validate | simulate | baseline | peak | frag (plan) | frag (caching alloc.) |
+|---|---:|---|---|---|---|---|---|---:|---:|
+{cf}
 """
     open(os.path.join(P, f"{tag}_summary.md"), "w").write(s)
-    print(s)
+    print(f"wrote profiles/{tag}_summary.md; checks:", [(c[0], c[1], c[2]) for c in checks])
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r02")

@@ -1,0 +1,48 @@
+"""A small workload touching every libstw kernel family, for compute-sanitizer
+(memcheck / racecheck / synccheck): K2 radix sort and the look-back scan over
+many tiles, the batched planner (all candidates), K7, K8, K9/K10 replays, K1
+and the sub-operation kernels. Each result is checked against the oracle, so a
+race that changes a result fails here too.
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py"""
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2507_16274_b200 as M  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_2507_16274_b200 import api, planner, tracegen  # noqa: E402
+
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev)
+g.manual_seed(1)
+n = 1 << 20  # ~270 onesweep tiles, ~256 scan tiles
+keys = torch.randint(0, 1 << 40, (n,), dtype=torch.int64, device=dev, generator=g)
+vals = torch.arange(n, dtype=torch.int32, device=dev)
+ref = torch.sort(keys, stable=True)
+api.radix_sort_pairs(keys, vals, 0, 40)
+assert torch.equal(keys, ref.values) and torch.equal(vals.long(), ref.indices), "radix sort"
+tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(48)]
+bp = api.plan_batch(tas, tracegen.C4_CANDIDATES, select_best=True)
+for t in range(0, 48, 7):
+    s0, s1 = int(bp.batch.ev_off[t]), int(bp.batch.ev_off[t + 1])
+    for c, (f, gi) in enumerate(tracegen.C4_CANDIDATES):
+        r = O.plan(tas[t], f, gi)
+        st = tas[t].dyn == 0
+        assert np.array_equal(bp.addr[c, s0:s1][st], r.addr[st]), ("plan", t, c)
+for name in ("c1_llama2_7b_1f1b", "c3_mixtral_moe"):
+    ta = tracegen.synth_arrays(tracegen.config(name))
+    tr = M.Trace.from_arrays(ta)
+    plan, rmap = M.plan_trace(tr)
+    rep, _ = M.simulate(tr, plan.to_bundle(rmap))
+    base = M.run_baseline(tr)
+    assert base.to_dict() == O.baseline(ta).report, name
+    assert M.validate_plan(plan) == [] and M.peak_live_bytes(ta) == O.peak_live(ta.size, ta.t_s, ta.t_e)
+ev = [M.MemoryRequestEvent(i, (1 + i % 5) * 512, i, i + 3 + i % 4, M.PhaseId.parse("F:0"), M.PhaseId.parse("B:0"))
+      for i in range(300)]
+groups = planner.group_by_phase(ev)
+plans = planner.pack_groups(groups)
+items = [planner._Item(512, e.t_s, e.t_e, e.id, e) for e in ev]
+assert len(planner.build_layers_for_size(items)) >= 1
+print("sanitize workload ok")
