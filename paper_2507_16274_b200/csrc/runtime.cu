@@ -353,12 +353,13 @@ constexpr int kOsAhead = 148 * 2;  // tiles ahead (measured: 2 per SM beats 3 an
 constexpr uint32_t kOsAgg = 1u << 30, kOsPrefix = 2u << 30, kOsVal = kOsAgg - 1;
 constexpr size_t kOsSmem = (size_t)kOsTile * 12 + (size_t)kOsWarps * 256 * 4 + 256 * 4 + 256 * 8 + 256 * 4 + 16;
 
+// One read of the keys -> the digit histograms of every pass (one shared
+// histogram per CTA; 16-byte loads, four in flight per thread).
 __global__ void __launch_bounds__(256) k_os_hist(const uint64_t *__restrict__ keys, int64_t n, int begin_bit,
                                                  int end_bit, int passes, uint32_t *__restrict__ hist) {
   __shared__ uint32_t h[8][256];
   for (int x = threadIdx.x; x < 8 * 256; x += blockDim.x) (&h[0][0])[x] = 0;
   __syncthreads();
-  // 16-byte loads, four in flight per thread (two keys each)
   const int64_t n2 = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
   const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(keys);
   const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
@@ -396,6 +397,7 @@ __global__ void __launch_bounds__(256) k_os_bins(uint32_t *__restrict__ hist) {
   hp[threadIdx.x] = block_excl_sum<uint32_t>(v, sh, nullptr);
 }
 
+template <int W>  // digit bits of this pass (8, or fewer for a key's last bits)
 __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__restrict__ kin,
                                                         const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
                                                         uint32_t *__restrict__ vout, int64_t n, int shift,
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(kOsThreads, 3) k_os_pass(const uint64_t *__res
     const uint32_t d = (uint32_t)(k[j] >> shift) & mask;
     unsigned peers = __ballot_sync(0xffffffffu, valid);  // (8 ballots beat __match_any_sync here: 6.6 vs 8.7 ms)
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
+    for (int b = 0; b < W; b++) {
       const bool bit = (d >> b) & 1u;
       const unsigned bb = __ballot_sync(0xffffffffu, bit);
       peers &= bit ? bb : ~bb;
@@ -555,15 +557,32 @@ void radix_sort_pairs(Ctx &ctx, Arena &ar, uint64_t *keys, uint32_t *vals, int64
   STW_KL(k_os_hist, grid_for(n, 256, 148 * 8), 256, ctx.stream, keys, n, begin_bit, end_bit, passes, hist);
   STW_KL(k_os_bins, passes, 256, ctx.stream, hist);
   STW_LAUNCHED(ctx);
-  STW_CUDA(ctx, cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOsSmem));
+  auto pass_kernel = [](int w) {
+    switch (w) {
+      case 1: return k_os_pass<1>;
+      case 2: return k_os_pass<2>;
+      case 3: return k_os_pass<3>;
+      case 4: return k_os_pass<4>;
+      case 5: return k_os_pass<5>;
+      case 6: return k_os_pass<6>;
+      case 7: return k_os_pass<7>;
+      default: return k_os_pass<8>;
+    }
+  };
   uint64_t *ka = keys, *kb = k2;
   uint32_t *va = vals, *vb = v2;
   for (int p = 0; p < passes && ctx.ok(); p++) {
     const int b = begin_bit + 8 * p, w = end_bit - b < 8 ? end_bit - b : 8;
     uint32_t *cur = status + (size_t)(p & 1) * ntiles * 256, *nxt = status + (size_t)((p + 1) & 1) * ntiles * 256;
     if (p == 0) STW_CUDA(ctx, cudaMemsetAsync(cur, 0, (size_t)ntiles * 256 * sizeof(uint32_t), ctx.stream));
-    STW_KLS(k_os_pass, (unsigned)ntiles, kOsThreads, kOsSmem, ctx.stream, ka, va, kb, vb, n, b, (1u << w) - 1,
-            hist + p * 256, cur, ctr + p, p + 1 < passes ? nxt : (uint32_t *)nullptr);
+    auto kern = pass_kernel(w);
+    STW_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOsSmem));
+    {
+      const int slot = prof_pre(ctx.stream);
+      kern<<<(unsigned)ntiles, kOsThreads, kOsSmem, ctx.stream>>>(ka, va, kb, vb, n, b, (1u << w) - 1, hist + p * 256,
+                                                                  cur, ctr + p, p + 1 < passes ? nxt : nullptr);
+      prof_post(ctx.stream, "k_os_pass", slot);
+    }
     STW_LAUNCHED(ctx);
     std::swap(ka, kb);
     std::swap(va, vb);
