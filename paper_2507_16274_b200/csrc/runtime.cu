@@ -181,21 +181,45 @@ void Arena::release() {
 
 // Single-pass scan with decoupled look-back: tiles of kScanTile claimed in
 // order by an atomic counter; each tile publishes its aggregate, then a warp
-// looks back over up to 32 predecessors at a time (flag + value arrays, the
-// value written before its flag behind a fence) for the nearest inclusive
+// looks back over up to 128 predecessors at a time for the nearest inclusive
 // prefix; one launch and one read + one write of the data. The first
 // kScanDirect tiles instead sum all their predecessors' aggregates at once.
+//
+// Look-back records are 16 bytes {token, value}, written and read as single
+// 16-byte accesses (naturally aligned vector accesses are single-copy atomic
+// on this hardware), so neither side needs a fence between flag and value.
+// A record is valid iff its token equals the launch's token (unique per
+// launch), so the record arrays need no clearing. Each tile has an aggregate
+// record and an inclusive-prefix record (the direct path needs aggregates).
 constexpr int64_t kScanDirect = 1024;
+constexpr int kScanWin = 4;  // look-back entries per lane (window = 128 tiles)
+
+struct __align__(16) ScanRec {
+  unsigned long long tok, val;
+};
+__device__ __forceinline__ void scan_rec_put(ScanRec *p, unsigned long long tok, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(tok), "l"(v) : "memory");
+}
+__device__ __forceinline__ ScanRec scan_rec_get(const ScanRec *p) {
+  ScanRec r;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.tok), "=l"(r.val) : "l"(p) : "memory");
+  return r;
+}
+template <class T>
+__device__ __forceinline__ unsigned long long scan_bits(T v) {
+  return (unsigned long long)(long long)v;  // 32-bit types widen; only the low bits are read back
+}
 
 // Tile I/O is coalesced: 16-byte vector loads / stores over the tile (thread
 // t moves vectors t, t + 256, ...), staged through shared memory (padded one
 // element per 16 against bank conflicts), where each thread then scans its
-// kScanItems consecutive elements.
+// kScanItems consecutive elements in place (nothing held in registers across
+// the look-back).
 template <class T>
 __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ in, T *__restrict__ out, int64_t n,
-                                                          int inclusive, uint32_t *__restrict__ flag,
-                                                          T *__restrict__ agg, T *__restrict__ pre,
-                                                          uint32_t *__restrict__ ctr) {
+                                                          int inclusive, ScanRec *__restrict__ agg,
+                                                          ScanRec *__restrict__ pre, uint32_t *__restrict__ ctr,
+                                                          unsigned long long tok) {
   constexpr int kVec = 16 / sizeof(T);          // elements per 16-byte vector
   constexpr int kVecs = kScanTile / kVec;       // vectors per tile
   constexpr int kPad = kScanTile + kScanTile / 16;
@@ -214,11 +238,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
                       (reinterpret_cast<uintptr_t>(out + t0) & 15) == 0;
   if (vec_ok) {
     const uint4 *src = reinterpret_cast<const uint4 *>(in + t0);
+    uint4 w[kVecs / kScanThreads];
+#pragma unroll
+    for (int j = 0; j < kVecs / kScanThreads; j++) w[j] = __ldcs(src + j * kScanThreads + tid);  // streamed once
 #pragma unroll
     for (int j = 0; j < kVecs / kScanThreads; j++) {
       const int q = j * kScanThreads + tid;
-      const uint4 w = __ldcs(src + q);  // streamed once: evict-first
-      const T *e = reinterpret_cast<const T *>(&w);
+      const T *e = reinterpret_cast<const T *>(&w[j]);
 #pragma unroll
       for (int x = 0; x < kVec; x++) st[at(q * kVec + x)] = e[x];
     }
@@ -226,66 +252,74 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
     for (int i = tid; i < kScanTile; i += kScanThreads) st[at(i)] = i < cnt ? in[t0 + i] : T(0);
   }
   __syncthreads();
-  T v[kScanItems];
   T acc = 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; k++) {
-    v[k] = st[at(tid * kScanItems + k)];
-    acc += v[k];
-  }
+  for (int k = 0; k < kScanItems; k++) acc += st[at(tid * kScanItems + k)];
   T total;
   const T ex = block_excl_sum<T>(acc, sh, &total);
-  volatile uint32_t *vf = flag;
   if (tid == 0) {
-    agg[tile] = total;
-    if (tile == 0) pre[0] = total;
-    __threadfence();
-    atomicExch(flag + tile, tile == 0 ? 2u : 1u);
+    scan_rec_put(agg + tile, tok, scan_bits(total));
+    if (tile == 0) scan_rec_put(pre, tok, scan_bits(total));
   }
   if (tile > 0 && tile <= kScanDirect) {
     // few tiles: sum every predecessor's aggregate directly -- they are all
     // published at about the same time, so there is no prefix chain to wait on
     T part = 0;
     for (int64_t t = tid; t < (int64_t)tile; t += kScanThreads) {
-      while (vf[t] == 0) {
-      }
-      __threadfence();
-      part += *(volatile T *)(agg + t);
+      ScanRec r;
+      do r = scan_rec_get(agg + t);
+      while (r.tok != tok);
+      part += (T)r.val;
     }
-    __syncthreads();  // `sh` is reused
     T excl;
     block_excl_sum<T>(part, sh, &excl);
     if (tid == 0) {
-      pre[tile] = excl + total;  // an inclusive prefix for the look-back of later tiles
-      __threadfence();
-      atomicExch(flag + tile, 2u);
+      scan_rec_put(pre + tile, tok, scan_bits(excl + total));  // for the look-back of later tiles
       s_excl = excl;
     }
   } else if (tid < 32) {
     T excl = 0;
     if (tile > 0) {
-      for (int64_t tw = (int64_t)tile - 1;; tw -= 32) {
-        const int64_t t = tw - lane;
-        uint32_t f = 2;
-        T val = 0;
-        if (t >= 0) {
-          while ((f = vf[t]) == 0) {
+      // window of 128 predecessors, entry d = j * 32 + lane at tile tw - d:
+      // the nearest published inclusive prefix ends the walk, aggregates
+      // between it and this tile are added; every entry must be published
+      for (int64_t tw = (int64_t)tile - 1;; tw -= 32 * kScanWin) {
+        T val[kScanWin];
+        bool isp[kScanWin];
+#pragma unroll
+        for (int j = 0; j < kScanWin; j++) {
+          const int64_t t = tw - j * 32 - lane;
+          val[j] = 0;
+          isp[j] = t < 0;  // before tile 0: acts as a zero prefix
+          if (t >= 0) {
+            const ScanRec p = scan_rec_get(pre + t);
+            if (p.tok == tok) {
+              isp[j] = true;
+              val[j] = (T)p.val;
+            } else {
+              ScanRec a;
+              do {
+                a = scan_rec_get(agg + t);
+              } while (a.tok != tok);
+              // an inclusive prefix may have landed meanwhile; either is exact
+              val[j] = (T)a.val;
+            }
           }
-          __threadfence();
-          val = f == 2 ? *(volatile T *)(pre + t) : *(volatile T *)(agg + t);
         }
-        const unsigned pm = __ballot_sync(0xffffffffu, f == 2);
-        const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest inclusive prefix in this window
-        T part = lane <= stop ? val : T(0);
+        int stop = 32 * kScanWin;  // first entry (by distance) holding a prefix
+#pragma unroll
+        for (int j = kScanWin - 1; j >= 0; j--) {
+          const unsigned pm = __ballot_sync(0xffffffffu, isp[j]);
+          if (pm) stop = j * 32 + __ffs(pm) - 1;
+        }
+        T part = 0;
+#pragma unroll
+        for (int j = 0; j < kScanWin; j++) part += j * 32 + lane <= stop ? val[j] : T(0);
         for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         excl += part;
-        if (pm) break;
+        if (stop < 32 * kScanWin) break;
       }
-      if (lane == 0) {
-        pre[tile] = excl + total;
-        __threadfence();
-        atomicExch(flag + tile, 2u);
-      }
+      if (lane == 0) scan_rec_put(pre + tile, tok, scan_bits(excl + total));
     }
     if (lane == 0) s_excl = excl;
   }
@@ -293,8 +327,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
   T run = ex + s_excl;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    st[at(tid * kScanItems + k)] = inclusive ? run + v[k] : run;
-    run += v[k];
+    T &x = st[at(tid * kScanItems + k)];
+    const T v = x;
+    x = inclusive ? run + v : run;
+    run += v;
   }
   __syncthreads();
   if (vec_ok) {
@@ -313,16 +349,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const T *__restrict__ 
   }
 }
 
+static std::atomic<unsigned long long> g_scan_tok{0x5ca1ab1e00000000ull};
+
 template <class T>
 void device_scan(Ctx &ctx, Arena &ar, const T *in, T *out, int64_t n, bool inclusive) {
   if (n <= 0 || !ctx.ok()) return;
   const int64_t nb = (n + kScanTile - 1) / kScanTile;
-  uint32_t *flag = ar.take<uint32_t>(nb + 1);
-  T *agg = ar.take<T>(nb), *pre = ar.take<T>(nb);
+  ScanRec *agg = ar.take<ScanRec>(nb), *pre = ar.take<ScanRec>(nb);
+  uint32_t *ctr = ar.take<uint32_t>(1);
   if (!ctx.ok()) return;
-  STW_CUDA(ctx, cudaMemsetAsync(flag, 0, (nb + 1) * sizeof(uint32_t), ctx.stream));
-  STW_KL(k_scan_lb<T>, (unsigned)nb, kScanThreads, ctx.stream, in, out, n, inclusive ? 1 : 0, flag, agg, pre,
-         flag + nb);
+  // a token no earlier launch used: stale records in recycled scratch never match it
+  const unsigned long long tok = g_scan_tok.fetch_add(1, std::memory_order_relaxed) + 1;
+  STW_CUDA(ctx, cudaMemsetAsync(ctr, 0, sizeof(uint32_t), ctx.stream));
+  STW_KL(k_scan_lb<T>, (unsigned)nb, kScanThreads, ctx.stream, in, out, n, inclusive ? 1 : 0, agg, pre, ctr, tok);
   STW_LAUNCHED(ctx);
 }
 template void device_scan<uint32_t>(Ctx &, Arena &, const uint32_t *, uint32_t *, int64_t, bool);
