@@ -69,7 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     build_alloc(force, verbose)
     build_io(force, verbose)
     if force or stale():
-        cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *sources()]
+        extra = os.environ.get("STW_NVCC_EXTRA", "").split()  # e.g. -DSTW_REPLAY_CLOCK (diagnostic builds)
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", LIB, *sources()]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         res = subprocess.run(cmd, capture_output=True, text=True)

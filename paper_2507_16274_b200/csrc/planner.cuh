@@ -44,4 +44,27 @@ void validate_exact(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count,
 // whose first reporting decision is at sweep position `first` (device data).
 void first_pair(Ctx &ctx, const RectSets &rs, int set, int cand, int first, int *pa, int *pb);
 
+// Register-resident sequential replay (replay_reg.cu) of one trace: inputs in
+// op order (operm: op 2e = alloc of event e, 2e+1 = its free; apos[e] = op
+// index of e's alloc), routes / planned addresses from the queue matching.
+// Requires unique ids. Returns 0 done (hout[4..10] = metrics, the log written
+// when asked), 1 outside its preconditions (the caller runs k_replay), 2 a
+// replay error (hout[1] code, hout[2] id, hout[3] address).
+struct RegIn {
+  int64_t n;
+  const uint32_t *operm;
+  const int32_t *apos;
+  const int64_t *id, *size;
+  const int32_t *ts, *te;
+  const uint8_t *dyn;
+  const int8_t *route0;
+  const int64_t *paddr;
+  const int32_t *key;
+  const int64_t *sp_off, *sp_lo, *sp_hi;
+  int64_t nsp;
+  int reuse, baseline;
+  long long pool;
+};
+int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log);
+
 }  // namespace stw

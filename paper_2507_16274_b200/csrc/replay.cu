@@ -975,7 +975,33 @@ int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep
       }
     }
   }
-  // sequential replay
+  // sequential replay: the register-resident warp when ids are unique and the
+  // state fits (replay_reg.cu), else the general warp below
+  if (n > 0 && nu == n && !getenv("STW_REPLAY_GENERAL")) {
+    nv.next("sequential replay (registers)");
+    RegIn ri{n, operm, apos, b.id, b.size, b.t_s, b.t_e, b.dyn, route, paddr, key, sp_off, sp_lo, sp_hi,
+             baseline ? 0 : (K ? bun->sp_off[K] : 0), baseline ? 0 : bun->reuse, baseline ? 1 : 0, pool};
+    long long ho[16] = {0};
+    const int st = replay_reg(ctx, ar, ri, ho, log);
+    if (!ctx.ok()) return ctx.rc;
+    if (st == 2) {
+      *err_id = ho[2];
+      ctx.fail(STW_ESIM, "planned address %lld for event %lld is occupied", ho[3], ho[2]);
+      return ctx.rc;
+    }
+    if (st == 0) {
+      rep->allocated_peak = ho[4];
+      rep->reserved_peak = pool + ho[5];
+      rep->pool_size = pool;
+      rep->fallback_count = ho[7];
+      rep->fallback_bytes_peak = ho[6];
+      rep->reuse_hits = ho[8];
+      rep->mismatch_count = ho[9];
+      rep->efficiency = rep->reserved_peak ? exact_div_host(rep->allocated_peak, rep->reserved_peak) : 1.0;
+      rep->fragmentation = 1.0 - rep->efficiency;
+      return ctx.rc;
+    }
+  }
   nv.next("sequential replay");
   ReplayArgs R{};
   R.n = n;

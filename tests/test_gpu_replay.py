@@ -149,3 +149,29 @@ def test_replay_fast_path_conflicts_fuzz():
             with pytest.raises(SimulationError) as ei:
                 api.simulate(tr, bundle)
             assert str(o.err_id) in str(ei.value), (str(ei.value), o.err)
+
+
+@pytest.mark.parametrize("general", [False, True])
+def test_replay_fuzz_both_warps(general, monkeypatch):
+    """The register-resident warp (replay_reg.cu) and the general warp
+    (k_replay, forced by STW_REPLAY_GENERAL) give the oracle's exact reports and logs."""
+    if general:
+        monkeypatch.setenv("STW_REPLAY_GENERAL", "1")
+    for s in range(48, 72):
+        check_trace(tracegen.synth_arrays(fuzz_cfg(s)))
+
+
+@pytest.mark.parametrize("k", [100, 200, 300, 600])
+def test_replay_register_capacity(k):
+    """k live requests of 3 MiB leave k cache segments with a 1 MiB free tail
+    each: > 128 blocks outgrow 4 rows per lane, > 512 the register warp entirely
+    (the call falls back to k_replay). Every size gives the oracle's report."""
+    from paper_2507_16274_b200.domain import MemoryRequestEvent, PhaseId, PhaseSpan, Trace
+
+    MIB = 1 << 20
+    F, B = PhaseId.parse("F:0"), PhaseId.parse("B:0")
+    sched = (PhaseSpan(F, 0, k), PhaseSpan(B, k, 2 * k + 1))
+    evs = tuple(MemoryRequestEvent(i, 3 * MIB + 512 * (i % 3), i, k + 1 + i, F, B) for i in range(k))
+    tr = Trace(evs, sched)
+    b = api.run_baseline(tr)
+    assert b.to_dict() == O.baseline(api._arrays_of(tr)).report
