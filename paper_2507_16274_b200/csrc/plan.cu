@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "planner.cuh"
 
 namespace stw {
@@ -1482,6 +1484,12 @@ __device__ void block_scan_into(int n, F f, int32_t *out, int *shi) {
 }
 
 __device__ void layers_unit(const LayerArgs &A, const int u);
+#ifdef STW_LAYERS_CLOCK
+__device__ unsigned long long g_layers_clk[8];
+#define LCLK(i) if (threadIdx.x == 0) { long long _n = clock64(); atomicAdd(&g_layers_clk[i], (unsigned long long)(_n - _lc)); _lc = _n; }
+#else
+#define LCLK(i)
+#endif
 
 // ulist[0 .. *ucount) (or [0, gridDim.x) without a count), grid-stride
 __global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A, const int32_t *__restrict__ ulist,
@@ -1491,6 +1499,224 @@ __global__ void __launch_bounds__(kPlanThreads) k_layers(LayerArgs A, const int3
     layers_unit(A, ulist[i]);
     __syncthreads();
   }
+}
+
+// Step 2 of a class (planner.py:414-439): the warp-serial resolve -- gap
+// insertion (the lowest fitting priority whose same-class last end is before
+// t_s), else Alg. 1 among this class's new layers. Run by a whole CTA (warp 0
+// works). Writes ilayer / irank / newcnt, *out_nnew and adds to *out_gap
+// (shared variables of the calling CTA).
+__device__ void resolve_class(const LayerArgs &A, const bool gap, const int nl, const int64_t j0, const int64_t j1,
+                              const int64_t a0, const int64_t off, const uint32_t *__restrict__ fitw,
+                              const int32_t *__restrict__ prioA, const int32_t *__restrict__ sAts,
+                              const int32_t *__restrict__ sAte, const int32_t *__restrict__ loffA, int32_t *last,
+                              int32_t *newcnt, int32_t *ilayer, int32_t *irank, int32_t *sm_nend, int *out_nnew,
+                              long long *out_gap) {
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  // ---- 2. warp-serial resolve: gap insertion, else Alg. 1 among this class's new layers.
+  // Narrow case (<= 32 layers): the register-resident chain of k_layers_w32;
+  // if the class would open a 33rd layer it is redone by the general loop.
+  __shared__ int sh_cnt[32], sh_fast;
+  if (warp == 0) {
+    constexpr unsigned FULL = 0xffffffffu;
+    bool fast = nl <= 32;
+    int nnew = 0, gapc = 0;
+    if (fast) {
+      int lastp = INT_MIN, ne = INT_MIN;
+      sh_cnt[lane] = 0;
+      __syncwarp();
+      const int my_prio = lane < nl ? prioA[lane] : 0;  // lane p: the layer at priority p
+      // each chunk's item fields are loaded one chunk ahead (the chain never waits on global memory)
+      int nx_ts = 0, nx_te = 0;
+      unsigned nx_fm = 0;
+      if (j0 + lane < j1) {
+        nx_ts = A.it.ts[j0 + lane];
+        nx_te = A.it.te[j0 + lane];
+        if (gap && nl > 0) nx_fm = fitw[(j0 + lane - a0) * kFitWords];
+      }
+      for (int64_t cb = j0; cb < j1 && fast; cb += 32) {
+        const int64_t mine = cb + lane;
+        const int cnt = (int)min((int64_t)32, j1 - cb);
+        const int my_ts = nx_ts, my_te = nx_te;
+        const unsigned fm = nx_fm;
+        if (mine + 32 < j1) {
+          nx_ts = A.it.ts[mine + 32];
+          nx_te = A.it.te[mine + 32];
+          if (gap && nl > 0) nx_fm = fitw[(mine + 32 - a0) * kFitWords];
+        }
+        int my_code = 0;
+#ifdef STW_LAYERS_CLOCK
+        long long _c0 = clock64();
+#endif
+        // Hot loop: consecutive gap-hosted items, one vote each (lane p:
+        // priority p). The host lane tests (m1 & lanemask_le) == lanemask_eq;
+        // the raw vote is kept by lane k and decoded (ffs) after the chunk, so
+        // nothing variable-latency sits on the per-item chain. The next item's
+        // fields are broadcast one item ahead. An item no layer hosts leaves
+        // the loop for Alg. 1 (a max-reduction over the class's new layers).
+        const unsigned lm_eq = 1u << lane, lm_le = lm_eq | (lm_eq - 1u);
+        unsigned my_m1 = 0;  // lane k: item k's vote (0: Alg. 1, code in my_code)
+        int k = 0;
+        int ts = __shfl_sync(FULL, my_ts, 0), te = __shfl_sync(FULL, my_te, 0);
+        unsigned f = __shfl_sync(FULL, fm, 0);
+        while (k < cnt) {
+          if (gap) {
+            for (; k < cnt; k++) {
+              const int k1 = (k + 1) & 31;
+              const int nts = __shfl_sync(FULL, my_ts, k1), nte = __shfl_sync(FULL, my_te, k1);
+              const unsigned nf = __shfl_sync(FULL, fm, k1);
+              const unsigned m1 = __ballot_sync(FULL, (f & lm_eq) && lastp < ts);
+              if (!m1) break;
+              lastp = (m1 & lm_le) == lm_eq ? te : lastp;
+              my_m1 = lane == k ? m1 : my_m1;
+              ts = nts, te = nte, f = nf;
+            }
+            if (k >= cnt) break;
+          }
+          // Alg. 1 for item k (planner.py:236-254): the largest end < t_s among
+          // the class's new layers, ties to the oldest; none: a new layer
+          const bool ca = lane < nnew && ne < ts;
+          const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
+          const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
+          const int best = cma ? __ffs(cma) - 1 : nnew;
+          if (!cma && nl + nnew == 32) {
+            fast = false;
+            break;
+          }
+          if (lane == best) ne = te;
+          nnew += cma ? 0 : 1;
+          if (lane == k) my_m1 = 0, my_code = 32 + best;
+          k++;
+          const int kk = k & 31;
+          ts = __shfl_sync(FULL, my_ts, kk), te = __shfl_sync(FULL, my_te, kk);
+          f = __shfl_sync(FULL, fm, kk);
+        }
+        if (my_m1) my_code = __ffs(my_m1) - 1;
+#ifdef STW_LAYERS_CLOCK
+        if (lane == 0) atomicAdd(&g_layers_clk[3], (unsigned long long)(clock64() - _c0)), atomicAdd(&g_layers_clk[5], (unsigned long long)cnt);
+#endif
+        if (!fast) break;
+        const bool act = lane < cnt;
+        const int hp = __shfl_sync(FULL, my_prio, my_code & 31);  // layer of priority my_code (gap host)
+        const int layer = my_code < 32 ? hp : nl + (my_code - 32);
+        gapc += __popc(__ballot_sync(FULL, act && my_code < 32));
+        const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
+        const int r = __popc(peers & lanemask_lt());
+        const int base = act ? sh_cnt[layer] : 0;
+        __syncwarp();
+        if (act) {
+          ilayer[mine - a0] = layer;
+          irank[mine - a0] = base + r;
+          if (r == __popc(peers) - 1) sh_cnt[layer] = base + __popc(peers);
+        }
+        __syncwarp();
+      }
+      if (fast) {
+        for (int l = lane; l < nl + nnew; l += 32) newcnt[l] = sh_cnt[l];
+        if (lane == 0) {
+          *out_nnew = nnew;
+          *out_gap += gapc;
+        }
+      } else {  // restart the class on the general path
+        nnew = 0;
+        for (int p = lane; p < nl; p += 32) last[p] = INT_MIN;
+        for (int l = lane; l < nl; l += 32) newcnt[l] = 0;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) sh_fast = fast;
+  }
+  __syncthreads();
+  if (!sh_fast && warp == 0) {
+    int nnew = 0;
+    long long gapc = 0;
+    int32_t *nend = A.nend + off;  // spill path when a class opens > kSmemLayers layers
+    for (int64_t cb = j0; cb < j1; cb += 32) {
+      int64_t mine = cb + lane;
+      int my_ts = 0, my_te = 0;
+      uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+      if (mine < j1) {
+        my_ts = A.it.ts[mine];
+        my_te = A.it.te[mine];
+        if (gap && nl > 0) {
+          const uint32_t *f = fitw + (mine - a0) * kFitWords;
+          w0 = f[0];
+          w1 = f[1];
+          w2 = f[2];
+          w3 = f[3];
+        }
+      }
+      const int cnt = (int)min((int64_t)32, j1 - cb);
+      for (int k = 0; k < cnt; k++) {
+        const int ts = __shfl_sync(0xffffffffu, my_ts, k), te = __shfl_sync(0xffffffffu, my_te, k);
+        const uint32_t f0 = __shfl_sync(0xffffffffu, w0, k), f1 = __shfl_sync(0xffffffffu, w1, k),
+                       f2 = __shfl_sync(0xffffffffu, w2, k), f3 = __shfl_sync(0xffffffffu, w3, k);
+        const int64_t jj = cb + k;
+        int host_p = -1;
+        if (gap) {
+          for (int pb = 0; pb < nl && host_p < 0; pb += 32) {
+            int p = pb + lane;
+            bool ok = false;
+            if (p < nl) {
+              bool fit;
+              if (p < 32 * kFitWords) {
+                uint32_t w = pb == 0 ? f0 : pb == 32 ? f1 : pb == 64 ? f2 : f3;
+                fit = (w >> lane) & 1u;
+              } else {
+                int l = prioA[p];
+                fit = slot_fit(sAts, sAte, loffA[l], loffA[l + 1], ts, te);
+              }
+              ok = fit && last[p] < ts;
+            }
+            unsigned msk = __ballot_sync(0xffffffffu, ok);
+            if (msk) host_p = pb + __ffs(msk) - 1;
+          }
+        }
+        int layer;
+        if (host_p >= 0) {
+          layer = prioA[host_p];
+          if (lane == 0) last[host_p] = te;
+          gapc++;
+        } else {
+          int32_t *ne = nnew <= kSmemLayers ? sm_nend : nend;
+          int best_k = -1, best_e = INT_MIN;
+          for (int kb = 0; kb < nnew; kb += 32) {
+            int kk = kb + lane;
+            int e = kk < nnew ? ne[kk] : INT_MIN;
+            bool cand = kk < nnew && e < ts;
+            int mx = __reduce_max_sync(0xffffffffu, cand ? e : INT_MIN);
+            unsigned cm = __ballot_sync(0xffffffffu, cand && e == mx);
+            if (cm && (best_k < 0 || mx > best_e)) {
+              best_e = mx;
+              best_k = kb + __ffs(cm) - 1;
+            }
+          }
+          if (best_k < 0) {
+            best_k = nnew++;
+            if (nnew == kSmemLayers + 1) {  // spill the new-layer ends to global memory
+              for (int x = lane; x < kSmemLayers; x += 32) nend[x] = sm_nend[x];
+              __syncwarp();
+            }
+            if (lane == 0) newcnt[nl + best_k] = 0;
+          }
+          int32_t *ne2 = nnew <= kSmemLayers ? sm_nend : nend;
+          if (lane == 0) ne2[best_k] = te;
+          layer = nl + best_k;
+        }
+        if (lane == 0) {
+          ilayer[jj - a0] = layer;
+          irank[jj - a0] = newcnt[layer]++;
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      *out_nnew = nnew;
+      *out_gap += gapc;
+    }
+  }
+  __syncthreads();
+
 }
 
 __device__ void layers_unit(const LayerArgs &A, const int u) {
@@ -1520,10 +1746,17 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
   }
   __syncthreads();
 
+#ifdef STW_LAYERS_CLOCK
+  long long _lc = clock64();
+  if (threadIdx.x == 0) atomicAdd(&g_layers_clk[7], 1ull);
+#endif
   for (int64_t j0 = a0; j0 < a1;) {
     const int64_t j1 = A.cend[j0];
     const int m = (int)(j1 - j0);
     const int64_t S = A.it.size[j0];
+#ifdef STW_LAYERS_CLOCK
+    if (threadIdx.x == 0) atomicAdd(&g_layers_clk[6], 1ull);
+#endif
     const int nl = sh_nl;
     const int nfit = min(nl, 32 * kFitWords);
     int32_t *last = nl <= kSmemLayers ? sm_last : A.lastEnd + off;
@@ -1542,175 +1775,11 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
     }
     for (int l = tid; l < nl; l += blockDim.x) newcnt[l] = 0;
     __syncthreads();
-    // ---- 2. warp-serial resolve: gap insertion, else Alg. 1 among this class's new layers.
-    // Narrow case (<= 32 layers): the register-resident chain of k_layers_w32;
-    // if the class would open a 33rd layer it is redone by the general loop.
-    __shared__ int sh_cnt[32], sh_fast;
-    if (warp == 0) {
-      constexpr unsigned FULL = 0xffffffffu;
-      bool fast = nl <= 32;
-      int nnew = 0, gapc = 0;
-      if (fast) {
-        int lastp = INT_MIN, ne = INT_MIN;
-        sh_cnt[lane] = 0;
-        __syncwarp();
-        for (int64_t cb = j0; cb < j1 && fast; cb += 32) {
-          const int64_t mine = cb + lane;
-          const int cnt = (int)min((int64_t)32, j1 - cb);
-          int my_ts = 0, my_te = 0;
-          unsigned fm = 0;
-          if (mine < j1) {
-            my_ts = A.it.ts[mine];
-            my_te = A.it.te[mine];
-            if (gap && nl > 0) fm = fitw[(mine - a0) * kFitWords];
-          }
-          int my_code = 0;
-          for (int kg = 0; kg < cnt && fast; kg += 8) {
-#pragma unroll
-            for (int kk = 0; kk < 8; kk++) {
-              const int k = kg + kk;
-              const bool valid = k < cnt;
-              const int ts = __shfl_sync(FULL, my_ts, k & 31), te = __shfl_sync(FULL, my_te, k & 31);
-              const unsigned f = __shfl_sync(FULL, fm, k & 31);
-              const unsigned m1 = gap ? __ballot_sync(FULL, ((f >> lane) & 1u) && lastp < ts) : 0u;
-              const bool ca = lane < nnew && ne < ts;
-              const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
-              const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
-              const int host = __ffs(m1) - 1;
-              const int best = cma ? __ffs(cma) - 1 : nnew;
-              const bool newl = valid && !m1 && !cma;
-              if (newl && nl + nnew == 32) fast = false;
-              if (valid && fast) {
-                if (m1) {
-                  if (lane == host) lastp = te;
-                } else if (lane == best) {
-                  ne = te;
-                }
-              }
-              nnew += (newl && fast) ? 1 : 0;
-              if (lane == k) my_code = m1 ? host : 32 + best;
-            }
-          }
-          if (!fast) break;
-          const bool act = lane < cnt;
-          const int layer = my_code < 32 ? prioA[my_code] : nl + (my_code - 32);
-          gapc += __popc(__ballot_sync(FULL, act && my_code < 32));
-          const unsigned peers = __match_any_sync(FULL, act ? layer : -1 - lane);
-          const int r = __popc(peers & lanemask_lt());
-          const int base = act ? sh_cnt[layer] : 0;
-          __syncwarp();
-          if (act) {
-            ilayer[mine - a0] = layer;
-            irank[mine - a0] = base + r;
-            if (r == __popc(peers) - 1) sh_cnt[layer] = base + __popc(peers);
-          }
-          __syncwarp();
-        }
-        if (fast) {
-          for (int l = lane; l < nl + nnew; l += 32) newcnt[l] = sh_cnt[l];
-          if (lane == 0) {
-            sh_nnew = nnew;
-            sh_gap += gapc;
-          }
-        } else {  // restart the class on the general path
-          nnew = 0;
-          for (int p = lane; p < nl; p += 32) last[p] = INT_MIN;
-          for (int l = lane; l < nl; l += 32) newcnt[l] = 0;
-          __syncwarp();
-        }
-      }
-      if (lane == 0) sh_fast = fast;
-    }
-    __syncthreads();
-    if (!sh_fast && warp == 0) {
-      int nnew = 0;
-      long long gapc = 0;
-      int32_t *nend = A.nend + off;  // spill path when a class opens > kSmemLayers layers
-      for (int64_t cb = j0; cb < j1; cb += 32) {
-        int64_t mine = cb + lane;
-        int my_ts = 0, my_te = 0;
-        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-        if (mine < j1) {
-          my_ts = A.it.ts[mine];
-          my_te = A.it.te[mine];
-          if (gap && nl > 0) {
-            const uint32_t *f = fitw + (mine - a0) * kFitWords;
-            w0 = f[0];
-            w1 = f[1];
-            w2 = f[2];
-            w3 = f[3];
-          }
-        }
-        const int cnt = (int)min((int64_t)32, j1 - cb);
-        for (int k = 0; k < cnt; k++) {
-          const int ts = __shfl_sync(0xffffffffu, my_ts, k), te = __shfl_sync(0xffffffffu, my_te, k);
-          const uint32_t f0 = __shfl_sync(0xffffffffu, w0, k), f1 = __shfl_sync(0xffffffffu, w1, k),
-                         f2 = __shfl_sync(0xffffffffu, w2, k), f3 = __shfl_sync(0xffffffffu, w3, k);
-          const int64_t jj = cb + k;
-          int host_p = -1;
-          if (gap) {
-            for (int pb = 0; pb < nl && host_p < 0; pb += 32) {
-              int p = pb + lane;
-              bool ok = false;
-              if (p < nl) {
-                bool fit;
-                if (p < 32 * kFitWords) {
-                  uint32_t w = pb == 0 ? f0 : pb == 32 ? f1 : pb == 64 ? f2 : f3;
-                  fit = (w >> lane) & 1u;
-                } else {
-                  int l = prioA[p];
-                  fit = slot_fit(sAts, sAte, loffA[l], loffA[l + 1], ts, te);
-                }
-                ok = fit && last[p] < ts;
-              }
-              unsigned msk = __ballot_sync(0xffffffffu, ok);
-              if (msk) host_p = pb + __ffs(msk) - 1;
-            }
-          }
-          int layer;
-          if (host_p >= 0) {
-            layer = prioA[host_p];
-            if (lane == 0) last[host_p] = te;
-            gapc++;
-          } else {
-            int32_t *ne = nnew <= kSmemLayers ? sm_nend : nend;
-            int best_k = -1, best_e = INT_MIN;
-            for (int kb = 0; kb < nnew; kb += 32) {
-              int kk = kb + lane;
-              int e = kk < nnew ? ne[kk] : INT_MIN;
-              bool cand = kk < nnew && e < ts;
-              int mx = __reduce_max_sync(0xffffffffu, cand ? e : INT_MIN);
-              unsigned cm = __ballot_sync(0xffffffffu, cand && e == mx);
-              if (cm && (best_k < 0 || mx > best_e)) {
-                best_e = mx;
-                best_k = kb + __ffs(cm) - 1;
-              }
-            }
-            if (best_k < 0) {
-              best_k = nnew++;
-              if (nnew == kSmemLayers + 1) {  // spill the new-layer ends to global memory
-                for (int x = lane; x < kSmemLayers; x += 32) nend[x] = sm_nend[x];
-                __syncwarp();
-              }
-              if (lane == 0) newcnt[nl + best_k] = 0;
-            }
-            int32_t *ne2 = nnew <= kSmemLayers ? sm_nend : nend;
-            if (lane == 0) ne2[best_k] = te;
-            layer = nl + best_k;
-          }
-          if (lane == 0) {
-            ilayer[jj - a0] = layer;
-            irank[jj - a0] = newcnt[layer]++;
-          }
-          __syncwarp();
-        }
-      }
-      if (lane == 0) {
-        sh_nnew = nnew;
-        sh_gap += gapc;
-      }
-    }
-    __syncthreads();
+    LCLK(0)
+    // ---- 2. warp-serial resolve (resolve_class)
+    resolve_class(A, gap, nl, j0, j1, a0, off, fitw, prioA, sAts, sAte, loffA, last, newcnt, ilayer, irank, sm_nend,
+                  &sh_nnew, &sh_gap);
+    LCLK(1)
     // ---- 3. merge this class's slots into the per-layer sorted slot CSR
     const int nnew = sh_nnew, nl2 = nl + nnew;
     for (int x = tid; x < nnew; x += blockDim.x) lsize[nl + x] = S;
@@ -1761,6 +1830,7 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
     }
     if (tid == 0) sh_nl = nl2;
     __syncthreads();
+    LCLK(2)
     j0 = j1;
   }
   // ---- F: stacking (planner.py:441-444)
@@ -1783,6 +1853,172 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// E for the largest units (e.g. c5's single 10^6-item trace): one unit spread
+// over the whole GPU. A cooperative launch walks the unit's classes; per class
+// the fit masks (a binary search of each item in every earlier layer's sorted
+// slots) and the slot merge run on every SM, the serial resolve on one warp,
+// with grid-wide barriers between the steps (the single-CTA k_layers spent
+// 40% of c5's time in those two data-parallel steps on one SM).
+struct BigState {
+  int nl, nnew;
+  long long gap;
+};
+
+__device__ void layers_unit_big(const LayerArgs &A, const int u, BigState *st, cooperative_groups::grid_group &grid) {
+  const int c = u % A.C, t = u / A.C;
+  const int v = A.var_of[c];
+  const bool gap = (A.cand[c] & STW_CAND_GAP) != 0;
+  const int64_t a0 = A.io[(int64_t)v * A.T + t], a1 = A.io[(int64_t)v * A.T + t + 1];
+  const int64_t off = A.uo[u];
+  const int tid = threadIdx.x;
+  const bool lead = blockIdx.x == 0;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid, gs = (int64_t)gridDim.x * blockDim.x;
+  __shared__ int shi[33];
+  __shared__ int sm_nend[kSmemLayers];
+  __shared__ int sh_nnew;
+  __shared__ long long sh_gap;
+  volatile BigState *vst = st;
+
+  int32_t *sAts = A.sA_ts + off, *sAte = A.sA_te + off, *sBts = A.sB_ts + off, *sBte = A.sB_te + off;
+  int32_t *loffA = A.loffA + off + u, *loffB = A.loffB + off + u;
+  int32_t *prioA = A.prioA + off, *prioB = A.prioB + off;
+  int32_t *newcnt = A.newcnt + off, *runoff = A.runoff + off + u;
+  int32_t *run_ts = A.run_ts + off, *run_te = A.run_te + off;
+  int32_t *ilayer = A.ilayer + off, *irank = A.irank + off;
+  int32_t *last = A.lastEnd + off;
+  uint32_t *fitw = A.fitw + off * kFitWords;
+  int64_t *lsize = A.lsize + off;
+  if (lead && tid == 0) {
+    vst->nl = 0;
+    vst->gap = 0;
+    loffA[0] = 0;
+  }
+  if (lead && tid == 0) sh_gap = 0;
+  grid.sync();
+#ifdef STW_LAYERS_CLOCK
+  long long _lc = clock64();
+#define BCLK(i) if (lead && tid == 0) { long long _n = clock64(); atomicAdd(&g_layers_clk[i], (unsigned long long)(_n - _lc)); _lc = _n; }
+#else
+#define BCLK(i)
+#endif
+  for (int64_t j0 = a0; j0 < a1;) {
+    const int64_t j1 = A.cend[j0];
+    const int m = (int)(j1 - j0);
+    const int64_t S = A.it.size[j0];
+    const int nl = vst->nl;
+    const int nfit = min(nl, 32 * kFitWords);
+    // ---- 1. fit masks against the slots of earlier classes (every SM)
+    for (int64_t x = gt; x < (int64_t)m * kFitWords; x += gs) fitw[(j0 - a0) * kFitWords + x] = 0;
+    for (int64_t l = gt; l < nl; l += gs) last[l] = INT_MIN, newcnt[l] = 0;
+    grid.sync();
+    if (gap && nl > 0) {
+      for (int64_t x = gt; x < (int64_t)m * nfit; x += gs) {
+        const int jj = (int)(x / nfit), p = (int)(x % nfit);
+        const int64_t it = j0 + jj;
+        const int l = prioA[p];
+        if (slot_fit(sAts, sAte, loffA[l], loffA[l + 1], A.it.ts[it], A.it.te[it]))
+          atomicOr(fitw + (it - a0) * kFitWords + (p >> 5), 1u << (p & 31));
+      }
+    }
+    grid.sync();
+    BCLK(0)
+    // ---- 2. the serial resolve (one CTA, warp 0)
+    if (lead) {
+      resolve_class(A, gap, nl, j0, j1, a0, off, fitw, prioA, sAts, sAte, loffA, last, newcnt, ilayer, irank, sm_nend,
+                    &sh_nnew, &sh_gap);
+      __syncthreads();
+      if (tid == 0) vst->nnew = sh_nnew;
+    }
+    grid.sync();
+    BCLK(1)
+    // ---- 3. merge this class's slots into the per-layer sorted slot CSR (every SM)
+    const int nnew = vst->nnew, nl2 = nl + nnew;
+    if (lead) {
+      for (int x = tid; x < nnew; x += blockDim.x) lsize[nl + x] = S;
+      block_scan_into(nl2, [&](int l) { return (l < nl ? loffA[l + 1] - loffA[l] : 0) + newcnt[l]; }, loffB, shi);
+      block_scan_into(nl2, [&](int l) { return newcnt[l]; }, runoff, shi);
+    }
+    grid.sync();
+    for (int64_t x = gt; x < m; x += gs) {
+      const int l = ilayer[j0 - a0 + x];
+      const int pos = runoff[l] + irank[j0 - a0 + x];
+      run_ts[pos] = A.it.ts[j0 + x];
+      run_te[pos] = A.it.te[j0 + x];
+    }
+    grid.sync();
+    const int nold = nl > 0 ? loffA[nl] : 0;
+    for (int64_t s = gt; s < nold; s += gs) {
+      int a = 0, b = nl;  // layer of slot s
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (loffA[mid] <= s)
+          a = mid;
+        else
+          b = mid;
+      }
+      int l = a;
+      while (loffA[l + 1] <= s) l++;  // skip empty layers
+      const int ts = sAts[s];
+      const int k = newcnt[l] ? lower_bound_i32(run_ts, runoff[l], runoff[l] + newcnt[l], ts) - runoff[l] : 0;
+      const int dst = loffB[l] + ((int)s - loffA[l]) + k;
+      sBts[dst] = ts;
+      sBte[dst] = sAte[s];
+    }
+    for (int64_t x = gt; x < m; x += gs) {
+      const int l = ilayer[j0 - a0 + x];
+      const int ts = A.it.ts[j0 + x];
+      const int k = l < nl ? lower_bound_i32(sAts, loffA[l], loffA[l + 1], ts) - loffA[l] : 0;
+      const int dst = loffB[l] + irank[j0 - a0 + x] + k;
+      sBts[dst] = ts;
+      sBte[dst] = A.it.te[j0 + x];
+    }
+    // priority order for later classes: newest (smallest) layers first, creation order within
+    for (int64_t x = gt; x < nl2; x += gs) prioB[x] = x < nnew ? nl + (int)x : prioA[x - nnew];
+    grid.sync();
+    {
+      int32_t *tp;
+      tp = sAts, sAts = sBts, sBts = tp;
+      tp = sAte, sAte = sBte, sBte = tp;
+      tp = loffA, loffA = loffB, loffB = tp;
+      tp = prioA, prioA = prioB, prioB = tp;
+    }
+    if (lead && tid == 0) vst->nl = nl2;
+    grid.sync();
+    BCLK(2)
+    j0 = j1;
+  }
+  // ---- F: stacking (planner.py:441-444)
+  if (lead) {
+    const int nl = vst->nl;
+    int64_t *lbase = A.lbase + off;
+    long long carry = A.pers_size[t];
+    for (int c0 = 0; c0 < nl; c0 += blockDim.x) {
+      const int l = c0 + tid;
+      const long long v0 = l < nl ? lsize[l] : 0;
+      __shared__ long long shl[33];
+      long long tot;
+      const long long ex = block_excl_sum<long long>(v0, shl, &tot);
+      if (l < nl) lbase[l] = carry + ex;
+      carry += tot;
+    }
+    if (tid == 0) {
+      A.nlayers[u] = nl;
+      A.gapins[u] = sh_gap;
+      A.pool[u] = carry;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPlanThreads) k_layers_big(LayerArgs A, const int32_t *__restrict__ ulist, int nu,
+                                                             BigState *st) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  for (int i = 0; i < nu; i++) {
+    layers_unit_big(A, ulist[i], st + i, grid);
+    grid.sync();
+  }
+}
 
 __device__ __forceinline__ int warp_excl_scan(int v, int *total) {
   int inc = warp_incl_sum(v);
@@ -2739,7 +2975,28 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
       STW_LAUNCHED(ctx);
     }
     if (!bigs.empty()) {  // units too large for a warp's shared memory (runs beside the side stream)
-      STW_KL(k_layers, (unsigned)bigs.size(), kPlanThreads, ctx.stream, LA, d_bigs, (const int *)nullptr);
+      if (bigs.size() <= 4 && !getenv("STW_NO_BIG_COOP")) {
+        // a few huge units (one long trace): each spread over the whole GPU
+        int occ = 0;
+        STW_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_layers_big, kPlanThreads, 0));
+        int dev = 0, nsm = kSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        // one CTA per SM: a co-resident CTA spinning in grid.sync would compete with the resolve warp for issue slots
+        unsigned grid = (unsigned)nsm;
+        if (getenv("STW_BIG_GRID")) grid = (unsigned)atoi(getenv("STW_BIG_GRID"));  // diagnostics
+        (void)occ;
+        BigState *d_st = ar.take<BigState>(bigs.size());
+        int nb = (int)bigs.size();
+        if (!ctx.ok()) return ctx.rc;
+        void *args[] = {(void *)&LA, (void *)&d_bigs, (void *)&nb, (void *)&d_st};
+        const int slot = prof_pre(ctx.stream);
+        STW_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)k_layers_big, dim3(grid), dim3(kPlanThreads), args, 0,
+                                                  ctx.stream));
+        prof_post(ctx.stream, "k_layers_big", slot);
+      } else {
+        STW_KL(k_layers, (unsigned)bigs.size(), kPlanThreads, ctx.stream, LA, d_bigs, (const int *)nullptr);
+      }
       STW_LAUNCHED(ctx);
     }
     if (nctas) {  // gap units that overflowed 32 layers (count read on the device)
@@ -2770,6 +3027,17 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
               (long long)hs[k], hts[k], hte[k], htie[k], href[k], (long long)(hce[k] - j0), hil[k], hir[k]);
   }
 
+#ifdef STW_LAYERS_CLOCK
+  {
+    unsigned long long hc[8];
+    cudaStreamSynchronize(ctx.stream);
+    cudaMemcpyFromSymbol(hc, g_layers_clk, sizeof(hc));
+    fprintf(stderr, "k_layers phases (Mcycles, thread 0 of each CTA): fit %.1f resolve %.1f merge %.1f; item loops %.1f (%llu items); units %llu classes %llu\n",
+            hc[0] / 1e6, hc[1] / 1e6, hc[2] / 1e6, hc[3] / 1e6, hc[5], hc[7], hc[6]);
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_layers_clk, z, sizeof(z));
+  }
+#endif
   pt.mark("E layers");
   if (after_uploads) after_uploads(hook_arg);  // the unfused path: after phase E
   nv.next("F emission");
