@@ -261,6 +261,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+_SM_MAX = []
+
+
+def sm_max_mhz():
+    """The GPU's maximum SM clock (nvidia-smi, queried once; B200: 1965 MHz)."""
+    if not _SM_MAX:
+        v = None
+        try:
+            r = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits"],
+                               capture_output=True, text=True, timeout=20)
+            v = float(r.stdout.strip().splitlines()[0])
+        except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+            v = 1965.0
+        _SM_MAX.append(v)
+    return _SM_MAX[0]
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -331,6 +348,8 @@ def kernel_sweep(dev, db, hb, planned_addr, reps: int, hbm: float):
                      "ms": ms, "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                      "traffic": tr["bytes"] * launches if tr else None,
                      "traffic_source": tr["source"] if tr else None, "what": note}
+        if tr and tr.get("inst"):
+            out[name]["issue"] = issue_roofline(tr["inst"], ms / launches, sm_max_mhz())
 
     # K1: R copies of the c4 batch (static_only, as the planner's self-check)
     T, N = db.T, db.N
@@ -504,7 +523,21 @@ def ncu_traffic(key):
             e = json.load(fh).get(key)
     except (OSError, ValueError):
         return None
-    return None if e is None else {"bytes": e["dram_bytes_per_launch"], "source": e["capture"]}
+    return None if e is None else {"bytes": e["dram_bytes_per_launch"], "source": e["capture"],
+                                   "inst": e.get("warp_inst_per_launch")}
+
+
+def issue_roofline(inst_per_launch, ms, sm_mhz):
+    """Instruction-issue roofline of a kernel that is not byte-bound: warp
+    instructions per launch (ncu smsp__inst_executed of the committed capture)
+    over the CUDA-event launch time, against one warp instruction per cycle per
+    scheduler (148 SMs x 4 schedulers) at the measured SM clock."""
+    if not inst_per_launch or not ms or not sm_mhz:
+        return None
+    achieved = inst_per_launch / (ms / 1e3)
+    peak = 148 * 4 * sm_mhz * 1e6
+    return {"achieved": achieved, "peak": peak, "unit": "warp-inst/s", "frac": achieved / peak,
+            "warp_inst_per_launch": inst_per_launch}
 
 
 def main():
@@ -723,7 +756,8 @@ def main():
                 "algorithmic_bytes_per_launch": abytes, "traffic_source": tr["source"] if tr else None,
                 "avg_launch_ms": avg_ms,
                 "share_of_kernel_time": kms / prof_total if prof_total else None,
-                "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
+                "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
+                "issue": issue_roofline(tr.get("inst") if tr else None, avg_ms, sm_max_mhz())}
     if args.profile_print and rank == 0:
         for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
             print(f"{k:28s} launches {c:6d}  total {ms:9.3f} ms  avg {ms / c:8.4f} ms", file=sys.stderr)

@@ -2122,34 +2122,58 @@ __device__ __forceinline__ void layers_w32_unit(const LayerArgs &A, int32_t *__r
         }
       }
       int my_code = 0;
-      for (int kg = 0; kg < cnt; kg += 8) {
-#pragma unroll
-        for (int kk = 0; kk < 8; kk++) {
-          const int k = kg + kk;
-          const bool valid = k < cnt;  // warp-uniform
-          const int ts = __shfl_sync(FULL, my_ts, k & 31), te = __shfl_sync(FULL, my_te, k & 31);
-          // gap host (planner.py:420-431): first fitting layer in priority order whose
-          // same-class slots all end before ts
-          unsigned m1 = 0;
-          if (GAP) {
-            const unsigned f = __shfl_sync(FULL, fm, k & 31);
-            m1 = __ballot_sync(FULL, ((f >> lane) & 1u) && last < ts);
+      if (GAP) {
+        // gap host (planner.py:420-431): first fitting layer in priority order
+        // whose same-class slots all end before ts. Hot loop: consecutive
+        // gap-hosted items, one vote each; the host lane tests (m1 & le) == eq,
+        // the raw vote is decoded (ffs) after the chunk; the next item's fields
+        // are broadcast one item ahead. An item no layer hosts leaves the loop
+        // for Alg. 1.
+        const unsigned lm_eq = 1u << lane, lm_le = lm_eq | (lm_eq - 1u);
+        unsigned my_m1 = 0;
+        int k = 0;
+        int ts = __shfl_sync(FULL, my_ts, 0), te = __shfl_sync(FULL, my_te, 0);
+        unsigned f = __shfl_sync(FULL, fm, 0);
+        while (true) {
+          for (; k < cnt; k++) {
+            const int k1 = (k + 1) & 31;
+            const int nts = __shfl_sync(FULL, my_ts, k1), nte = __shfl_sync(FULL, my_te, k1);
+            const unsigned nf = __shfl_sync(FULL, fm, k1);
+            const unsigned m1 = __ballot_sync(FULL, (f & lm_eq) && last < ts);
+            if (!m1) break;
+            last = (m1 & lm_le) == lm_eq ? te : last;
+            my_m1 = lane == k ? m1 : my_m1;
+            ts = nts, te = nte, f = nf;
           }
-          // Alg. 1 (planner.py:244-252): the new layer with the largest end < ts,
-          // ties to the oldest -- one max-reduction over (end, 31 - lane) keys
-          // (ends < 2^26: the host routes longer timelines to the CTA kernel)
+          if (k >= cnt) break;
+          // Alg. 1 (planner.py:244-252) for item k: the new layer with the largest
+          // end < ts, ties to the oldest -- one max-reduction over (end, 31 - lane)
+          // keys (ends < 2^26: the host routes longer timelines to the CTA kernel)
           const int key = __reduce_max_sync(FULL, ne < ts ? (int)(((unsigned)ne << 5) | (unsigned)(31 - lane)) : -1);
           const int tgt = key >= 0 ? 31 - (key & 31) : nnew;  // nnew: open a layer
-          const int host = __ffs(m1) - 1;
-          if (valid) {
-            if (m1) {
-              if (lane == host) last = te;
-            } else if (lane == tgt) {
-              ne = te;
-            }
+          if (lane == tgt) ne = te;
+          nnew += key < 0 ? 1 : 0;
+          if (lane == k) my_m1 = 0, my_code = kWN + tgt;
+          if (++k >= cnt) break;
+          ts = __shfl_sync(FULL, my_ts, k), te = __shfl_sync(FULL, my_te, k);
+          f = __shfl_sync(FULL, fm, k);
+        }
+        if (my_m1) my_code = __ffs(my_m1) - 1;
+      } else {
+        for (int kg = 0; kg < cnt; kg += 8) {
+#pragma unroll
+          for (int kk = 0; kk < 8; kk++) {
+            const int k = kg + kk;
+            const bool valid = k < cnt;  // warp-uniform
+            const int ts = __shfl_sync(FULL, my_ts, k & 31), te = __shfl_sync(FULL, my_te, k & 31);
+            // Alg. 1 (planner.py:244-252): the new layer with the largest end < ts,
+            // ties to the oldest -- one max-reduction over (end, 31 - lane) keys
+            const int key = __reduce_max_sync(FULL, ne < ts ? (int)(((unsigned)ne << 5) | (unsigned)(31 - lane)) : -1);
+            const int tgt = key >= 0 ? 31 - (key & 31) : nnew;  // nnew: open a layer
+            if (valid && lane == tgt) ne = te;
+            nnew += (valid && key < 0) ? 1 : 0;
+            if (lane == k) my_code = kWN + tgt;
           }
-          nnew += (valid && !m1 && key < 0) ? 1 : 0;
-          if (lane == k) my_code = m1 ? host : kWN + tgt;
         }
       }
       if (nl + nnew > kWN) {  // a 33rd layer: the CTA kernel redoes the unit

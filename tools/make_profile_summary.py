@@ -31,7 +31,8 @@ CAPS = {"k_layers_w32": ("k_layers_w32", None), "k_fusion": ("k_fusion", None),
         "k_peak_warp@sweep": ("k_peak_warp_big", "k_peak_warp"),
         "k_overlap_sweep@sweep": ("k_overlap_sweep_big", "k_overlap_sweep"),
         "k_os_pass@sweep": ("k_os_pass_big", "radix_sort_pairs"), "k_os_hist@sweep": ("k_os_hist_big", None),
-        "k_scan_lb@sweep": ("k_scan_lb_big", "k_scan_lb")}
+        "k_scan_lb@sweep": ("k_scan_lb_big", "k_scan_lb"),
+        "k_replay_reg@c1": ("k_replay_reg_c1", None), "k_layers_big@c5": ("k_layers_big_c5", None)}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "ms": 1e3}
 
 
@@ -68,8 +69,9 @@ def main(tag):
                 for r in rows) / len(rows)
         us = sum(metric(hdr, units, r, "gpu__time_duration.sum") for r in rows) / len(rows)
         grid = rows[0][hdr.index("launch__grid_size")] if "launch__grid_size" in hdr else None
+        inst = sum(metric(hdr, units, r, "smsp__inst_executed.sum") for r in rows) / len(rows)
         e = {"dram_bytes_per_launch": b, "duration_us": us, "grid_size": grid, "launches_captured": len(rows),
-             "capture": f"profiles/{tag}_ncu_{name}.txt"}
+             "warp_inst_per_launch": inst, "capture": f"profiles/{tag}_ncu_{name}.txt"}
         if bench_key and bench_key in kr:
             k = kr[bench_key]
             passes = 6 if bench_key == "radix_sort_pairs" else 1  # the sort's entry spans its 6 passes
@@ -77,6 +79,9 @@ def main(tag):
             ev_us = 1e3 * k["ms"] / passes
             e["bench_launch_us"] = ev_us
             e["algorithmic_bytes_per_launch"] = algo
+            # instruction-issue roofline: warp instructions over the event-timed launch, against one
+            # warp instruction per cycle per scheduler (148 SMs x 4) at the max SM clock (1965 MHz)
+            e["issue_frac"] = inst / (ev_us * 1e-6) / (148 * 4 * 1965e6)
             ok_t = 1 / 1.6 < us / ev_us < 1.6
             ok_b = bench_key == "k_overlap_sweep" or 0.7 < b / algo < 1.3  # K7 reads shared columns once per set
             checks.append((key, ok_t, ok_b, us, ev_us, b, algo))
@@ -86,32 +91,46 @@ def main(tag):
         traffic[key] = e
     json.dump(traffic, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 
-    rows = list(csv.reader(open(os.path.join(G, f"{tag}_launches.csv"))))
-    h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
-    hdr = rows[h]
-    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-    for r in rows[h + 1:]:
-        n = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("stw::", "")
-        n = n.replace("<unnamed>::", "")
-        m, v = r[hdr.index("Metric Name")], float(r[hdr.index("Metric Value")].replace(",", ""))
-        if m == "gpu__time_duration.sum":
-            agg[n][0] += 1
-            agg[n][1] += v / 1e3
-        elif m.startswith("dram__bytes"):
-            agg[n][2] += v
+    def launches(path):
+        rows = list(csv.reader(open(path)))
+        h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+        hdr = rows[h]
+        agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+        for r in rows[h + 1:]:
+            n = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("stw::", "")
+            n = n.replace("<unnamed>::", "")
+            m, v = r[hdr.index("Metric Name")], float(r[hdr.index("Metric Value")].replace(",", ""))
+            if m == "gpu__time_duration.sum":
+                agg[n][0] += 1
+                agg[n][1] += v / 1e3
+            elif m.startswith("dram__bytes"):
+                agg[n][2] += v
+        return agg
+
+    agg = launches(os.path.join(G, f"{tag}_launches.csv"))
+    wpath = os.path.join(G, f"{tag}_launches_warm.csv")
+    warm = launches(wpath) if os.path.exists(wpath) else {}
+    if warm:
+        shutil.copy(wpath, os.path.join(P, f"{tag}_launches_c4_warm.csv"))
     calls = agg["k_fusion"][0] or 1
+    wcalls = (warm.get("k_fusion") or [0])[0] or 1
     ours = {k: v for k, v in agg.items() if not k.startswith("at::")}
     tot = sum(a[1] for a in ours.values())
     nl = sum(a[0] for a in ours.values())
-    table = "\n".join(f"| `{n[:60]}` | {a[0]} | {a[1] / calls:.1f} | {100 * a[1] / tot:.1f}% | {a[2] / calls / 1e6:.1f} |"
+    cold_mb = sum(a[2] for a in ours.values()) / calls / 1e6
+    warm_mb = sum(a[2] for k, a in warm.items() if not k.startswith("at::")) / wcalls / 1e6 if warm else float("nan")
+    table = "\n".join(f"| `{n[:60]}` | {a[0]} | {a[1] / calls:.1f} | {100 * a[1] / tot:.1f}% | {a[2] / calls / 1e6:.1f} | "
+                      + (f"{warm[n][2] / wcalls / 1e6:.1f}" if n in warm else "-") + " |"
                       for n, a in sorted(ours.items(), key=lambda x: -x[1][1])[:26])
     d = bench
     cfg = d.get("configs") or {}
     rf = d["roofline"]
     chk = "\n".join(f"| `{k}` | {ev:.1f} | {us:.1f} | {al / 1e9:.3f} | {b / 1e9:.3f} | {b / al:.2f} |"
                     for k, _, _, us, ev, b, al in checks)
+    issue = {CAPS[key][1]: e["issue_frac"] for key, e in traffic.items() if "issue_frac" in e}
     sw = "\n".join(f"| `{k}` | {v['records']:,} | {v['algorithmic_bytes_per_record']:.0f} | {v['ms']:.3f} | "
-                   f"{v['achieved']:.0f} | {100 * v['frac']:.1f}% |" for k, v in kr.items())
+                   f"{v['achieved']:.0f} | {100 * v['frac']:.1f}% | "
+                   + (f"{100 * issue[k]:.1f}%" if k in issue else "-") + " |" for k, v in kr.items())
     cf = "\n".join(
         f"| {n} | {c['events']:,} | " + " | ".join(f"{c['gpu_ms'][s]:.2f} / {c['cpu_ms'][s]:.2f}" for s in
                                                      ("plan", "reuse", "validate", "simulate", "baseline", "peak"))
@@ -152,15 +171,23 @@ over `bench.py --steps 1 --warmup 3 --no-kernel-sweep` ({calls} planner calls in
 raw CSV `{tag}_launches_c4.csv`. Per call: {nl / calls:.0f} libstw launches, {tot / calls / 1e3:.2f} ms of
 serialised kernel time.
 
-| kernel | launches ({calls} calls) | us per call | share | DRAM MB per call |
-|---|---:|---:|---:|---:|
+| kernel | launches ({calls} calls) | us per call | share | DRAM MB per call (cold) | DRAM MB per call (warm L2) |
+|---|---:|---:|---:|---:|---:|
 {table}
+
+DRAM per call, all libstw kernels: {cold_mb:.0f} MB with ncu's cache flush before every kernel (each
+kernel re-reads its inputs from HBM), {warm_mb:.0f} MB with `--cache-control none` (`{tag}_launches_c4_warm.csv`:
+the intermediates between kernels stay in the 126 MB L2, as in the real pipelined call).
 
 ## HBM roofline sweep of the data-parallel kernels (inputs >> 126 MB L2, CUDA-event timed in bench.py)
 
-| kernel | records | algorithmic B/record | ms | achieved GB/s | of measured peak |
-|---|---:|---:|---:|---:|---:|
+| kernel | records | algorithmic B/record | ms | achieved GB/s | of measured peak | of issue peak |
+|---|---:|---:|---:|---:|---:|---:|
 {sw}
+
+"Of issue peak" = warp instructions per launch (ncu `smsp__inst_executed` of the capture) over the event-timed
+launch, against one warp instruction per cycle per scheduler (148 SMs x 4) at the max SM clock: the bound of a
+kernel that is instruction-limited rather than byte-limited (K7).
 
 Capture check (the ncu launch is the timed launch): bench event time vs ncu duration per launch, and
 algorithmic vs ncu DRAM bytes per launch (K7 reads each set's shared size/t_s/t_e columns once for all
