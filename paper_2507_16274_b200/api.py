@@ -362,7 +362,7 @@ def _plan_columns(plan):
     return plan.columns() if isinstance(plan, StaticPlan) else DecisionColumns.from_decisions(tuple(plan.decisions))
 
 
-def reusable_spaces(cols, t_lo, t_hi) -> list:
+def reusable_spaces(cols, t_lo, t_hi, with_cols: bool = False):
     """K8 on the device: idle address intervals of the plan per window."""
     K = int(t_lo.shape[0])
     n = len(cols)
@@ -382,7 +382,8 @@ def reusable_spaces(cols, t_lo, t_hi) -> list:
             continue
         _lib.check(rc, err)
         break
-    return [IntervalSet.from_bounds(lo[off[k]:off[k + 1]], hi[off[k]:off[k + 1]]) for k in range(K)]
+    spaces = [IntervalSet.from_bounds(lo[off[k]:off[k + 1]], hi[off[k]:off[k + 1]]) for k in range(K)]
+    return spaces if not with_cols else (spaces, (off, lo[:off[K]].copy(), hi[:off[K]].copy()))
 
 
 def compute_reusable_space(plan, key, layer_schedule):
@@ -401,8 +402,10 @@ def derive_reuse_map(plan, trace) -> ReuseMap:
     if not keys:
         return ReuseMap({})
     t_lo, t_hi = _windows(keys, trace.layer_schedule)
-    spaces = reusable_spaces(_plan_columns(plan), t_lo, t_hi)
-    return ReuseMap({k: ReuseEntry(int(a), int(b), s) for k, a, b, s in zip(keys, t_lo, t_hi, spaces)})
+    spaces, cols = reusable_spaces(_plan_columns(plan), t_lo, t_hi, with_cols=True)
+    rm = ReuseMap({k: ReuseEntry(int(a), int(b), s) for k, a, b, s in zip(keys, t_lo, t_hi, spaces)})
+    object.__setattr__(rm, "_cols", (tuple(keys), *cols))  # the device's columns, for the replay's upload
+    return rm
 
 
 def plan_trace(trace, *, fusion=True, gap_insert=True, stats=None):
@@ -428,11 +431,18 @@ class ReplayLog(_Sequence):
     """The replay log as the reference's list of dicts, materialised on access
     from the device's columns (sim.py:164, 186, 209-229, 241-253)."""
 
-    def __init__(self, cols: dict, n: int, keys_by_id: dict):
+    def __init__(self, cols: dict, n: int, keys_by_id):
         self._c = cols
         self._n = n
-        self._keys = keys_by_id
+        self._keys_src = keys_by_id  # dict, or a callable making it on first use
+        self._keys_d = None
         self._cache = None
+
+    @property
+    def _keys(self) -> dict:
+        if self._keys_d is None:
+            self._keys_d = self._keys_src() if callable(self._keys_src) else self._keys_src
+        return self._keys_d
 
     def __len__(self) -> int:
         return self._n
@@ -509,17 +519,28 @@ def simulate(trace, plan, *, reuse: bool = True, log_path=None):
     key = np.full(len(ta), -1, np.int32)
     if len(names):
         m = kidx >= 0
-        key[m] = np.asarray([pos.get(names[k], -1) for k in kidx[m].tolist()], np.int32)
-    off = [0]
-    lo, hi = [], []
-    for k in bkeys:
-        for iv in plan.reuse[k]:
-            lo.append(iv.lo)
-            hi.append(iv.hi)
-        off.append(len(lo))
-    sp_off = np.asarray(off, np.int64)
-    sp_lo = np.asarray(lo, np.int64)
-    sp_hi = np.asarray(hi, np.int64)
+        key_of_name = np.asarray([pos.get(nm, -1) for nm in names], np.int32)  # one lookup per key, not per event
+        key[m] = key_of_name[kidx[m]]
+    rc_ = getattr(plan, "_reuse_cols", None)
+    if rc_ is not None and rc_[0] == tuple(bkeys):  # the device's reuse columns, same key order
+        sp_off, sp_lo, sp_hi = rc_[1], rc_[2], rc_[3]
+    else:
+        off = [0]
+        lo, hi = [], []
+        for k in bkeys:
+            sp = plan.reuse[k]
+            if hasattr(sp, "bounds"):
+                a, b = sp.bounds()
+                lo.extend(a.tolist())
+                hi.extend(b.tolist())
+            else:
+                for iv in sp:
+                    lo.append(iv.lo)
+                    hi.append(iv.hi)
+            off.append(len(lo))
+        sp_off = np.asarray(off, np.int64)
+        sp_lo = np.asarray(lo, np.int64)
+        sp_hi = np.asarray(hi, np.int64)
     bun = _lib.Bundle(int(plan.pool_size), int(plan.alignment), len(cols), _lib.ptr(cols.id), _lib.ptr(cols.addr),
                       _lib.ptr(cols.size), _lib.ptr(cols.t_s), _lib.ptr(cols.t_e), len(bkeys), _lib.ptr(sp_off),
                       _lib.ptr(sp_lo), _lib.ptr(sp_hi), _lib.ptr(key), int(bool(reuse)))
@@ -534,7 +555,7 @@ def simulate(trace, plan, *, reuse: bool = True, log_path=None):
         k = bkeys[eid.value]
         raise PlanError(f"reuse entry {k} outside pool")
     _lib.check(rc, err)
-    log = ReplayLog(lcols, int(lg.len), _dyn_keys_by_id(ta))
+    log = ReplayLog(lcols, int(lg.len), lambda: _dyn_keys_by_id(ta))
     if log_path is not None:
         _write_log(log, log_path)
     return _report(rep), log

@@ -242,6 +242,7 @@ class StaticPlan:
         return IntervalSet.span(int(c.addr.min()), int((c.addr + c.size).max()))
 
     def to_bundle(self, reuse=None) -> PlanBundle:
+        rcols = getattr(reuse, "_cols", None)  # the device's reuse columns (derive_reuse_map)
         if hasattr(reuse, "spaces"):
             reuse = reuse.spaces()
         c = self.columns()
@@ -251,6 +252,8 @@ class StaticPlan:
         )
         b = PlanBundle(self.pool_size, self.alignment, decs, dict(reuse or {}))
         object.__setattr__(b, "_cols", c)
+        if rcols is not None:
+            object.__setattr__(b, "_reuse_cols", rcols)
         return b
 
     def __eq__(self, other):

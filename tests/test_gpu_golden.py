@@ -102,3 +102,29 @@ def test_fuzz_fixtures_on_device():
             want = f[f"sim_reuse_{int(reuse)}"]
             assert rep.to_dict() == want["report"] and log_digest(log) == want["log_digest"]
         assert M.run_baseline(tr).to_dict() == f["baseline"]
+
+
+@pytest.mark.slow
+def test_app_b_c5_single_cta_layers(monkeypatch):
+    """c5's one huge unit through the single-CTA layer kernel (the cooperative
+    whole-GPU kernel k_layers_big switched off) gives the same plan file."""
+    monkeypatch.setenv("STW_NO_BIG_COOP", "1")
+    a = anchors()["c5_llama3_70b"]
+    tr = M.Trace.from_arrays(tracegen.synth_arrays(tracegen.config("c5_llama3_70b")))
+    plan, rmap = M.plan_trace(tr)
+    assert hashlib.sha256(planio.dumps_plan(plan.to_bundle(rmap)).encode()).hexdigest()[:16] == a["write_plan_sha16"]
+
+
+@pytest.mark.parametrize("name", ["c1_llama2_7b_1f1b", "c3_mixtral_moe", "c3b_mixtral_moe_rcp"])
+def test_app_b_replay_general_warp(name, monkeypatch):
+    """The general sequential replay warp (k_replay, forced) reproduces the
+    reference's replay report, log digest and baseline report, like the
+    register-resident warp the default path takes."""
+    monkeypatch.setenv("STW_REPLAY_GENERAL", "1")
+    a = anchors()[name]
+    tr = M.Trace.from_arrays(tracegen.synth_arrays(tracegen.config(name)))
+    plan, rmap = M.plan_trace(tr)
+    rep, log = M.simulate(tr, plan.to_bundle(rmap))
+    assert rep.to_dict() == a["sim"]
+    assert log_digest(log) == a["sim_log_digest"]
+    assert M.run_baseline(tr).to_dict() == a["baseline"]
