@@ -81,6 +81,8 @@ __device__ T block_reduce_max(T v, T *sh) {
 #define GRID_STRIDE(i, n) \
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
+__global__ void k_fill_i32(int32_t *__restrict__ p, int64_t n, int32_t v) { GRID_STRIDE(i, n) p[i] = v; }
+
 // trace index of every event: one warp per trace writes its run (coalesced)
 // Phase A in one pass, one CTA per trace: the trace index of every event
 // (coalesced runs); flags[0] = 1 unless every trace's ids increase strictly
@@ -97,13 +99,18 @@ __global__ void __launch_bounds__(128) k_trace_scan(
     const int32_t *__restrict__ te, const int64_t *__restrict__ size, const int32_t *__restrict__ ps,
     const int32_t *__restrict__ pe, const uint8_t *__restrict__ dyn, const int32_t *__restrict__ horizon,
     const int32_t *__restrict__ n_sched, long long align, int32_t *__restrict__ tr, int *__restrict__ bad_align,
-    int *__restrict__ bad_phase, int *__restrict__ flags, long long *__restrict__ mm) {
+    int *__restrict__ bad_phase, int *__restrict__ flags, long long *__restrict__ mm, int64_t chunk) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ int s_ba, s_bp;
+  // blockIdx.y: the part of a long trace (gridDim.y > 1 only when some trace
+  // has more than `chunk` events; then bad_* were filled with INT_MAX first)
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) s_ba = s_bp = INT_MAX;
   __syncthreads();
-  const int64_t e0 = ev_off[t], e1 = ev_off[t + 1];
+  const int64_t e0 = ev_off[t], te1 = ev_off[t + 1];
+  const int64_t p0 = e0 + (int64_t)blockIdx.y * chunk;
+  if (gridDim.y > 1 && p0 >= te1 && blockIdx.y > 0) return;
+  const int64_t e1 = gridDim.y > 1 ? min(te1, p0 + chunk) : te1;
   const int hz = horizon[t], ns = n_sched[t];
   bool bad = false;
   long long idmin = LLONG_MAX, idmax = LLONG_MIN;
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(128) k_trace_scan(
   const bool pow2 = (align & (align - 1)) == 0;
   // every column loaded up front and branch-free (more loads in flight per warp)
 #pragma unroll 2
-  for (int64_t i = e0 + tid; i < e1; i += blockDim.x) {
+  for (int64_t i = (gridDim.y > 1 ? p0 : e0) + tid; i < e1; i += blockDim.x) {
     const int64_t my_id = id[i], sz = size[i];
     const int my_ts = ts[i], my_te = te[i], a = ps[i], z = pe[i];
     const bool dy = dyn[i] != 0;
@@ -158,8 +165,13 @@ __global__ void __launch_bounds__(128) k_trace_scan(
   }
   __syncthreads();
   if (tid == 0) {
-    bad_align[t] = s_ba;
-    bad_phase[t] = s_bp;
+    if (gridDim.y == 1) {
+      bad_align[t] = s_ba;
+      bad_phase[t] = s_bp;
+    } else {
+      if (s_ba != INT_MAX) atomicMin(bad_align + t, s_ba);
+      if (s_bp != INT_MAX) atomicMin(bad_phase + t, s_bp);
+    }
     // batch-wide values: one CTA-level update each, and only when it changes the
     // current value (thousands of CTAs would otherwise serialise on five words)
     volatile int *vf = flags;
@@ -2620,8 +2632,17 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   int *bad_align = ar.take<int>(T), *bad_phase = ar.take<int>(T);
   if (!ctx.ok()) return ctx.rc;
   if (T > 0) {
-    STW_KL(k_trace_scan, (unsigned)T, 128, ctx.stream, b.ev_off, T, b.id, b.t_s, b.t_e, b.size,
-           b.ps, b.pe, b.dyn, b.horizon, b.n_sched, (long long)o->alignment, tr, bad_align, bad_phase, im, mm);
+    // long traces (c5: 10^6 events in one trace) are split into parts of
+    // kScanChunk events, one CTA each, combined by atomics
+    constexpr int64_t kScanChunk = 16384;
+    const int64_t parts = std::max<int64_t>(1, (b.max_trace_events + kScanChunk - 1) / kScanChunk);
+    if (parts > 1) {
+      LAUNCH(k_fill_i32, T, bad_align, (int64_t)T, INT_MAX);
+      LAUNCH(k_fill_i32, T, bad_phase, (int64_t)T, INT_MAX);
+    }
+    STW_KL(k_trace_scan, dim3((unsigned)T, (unsigned)parts), 128, ctx.stream, b.ev_off, T, b.id, b.t_s, b.t_e,
+           b.size, b.ps, b.pe, b.dyn, b.horizon, b.n_sched, (long long)o->alignment, tr, bad_align, bad_phase, im, mm,
+           kScanChunk);
     STW_LAUNCHED(ctx);
   }
   long long hmm[2] = {0, 0};

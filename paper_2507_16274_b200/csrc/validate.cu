@@ -92,9 +92,15 @@ __global__ void k_live_count(const int64_t *__restrict__ off, int S, int64_t n, 
   }
 }
 
+// a decision live into more than kLongSpan later tiles (c5's persistent
+// allocations span thousands) is handed to k_live_fill_long, where a CTA
+// spreads its tiles over the threads, instead of one thread walking them
+constexpr int64_t kLongSpan = 32;
+
 __global__ void k_live_fill(const int64_t *__restrict__ off, int S, int64_t n, const int32_t *__restrict__ te,
                             const int64_t *__restrict__ bo, const int32_t *__restrict__ T0,
-                            const int64_t *__restrict__ loff, int *__restrict__ cursor, int32_t *__restrict__ live) {
+                            const int64_t *__restrict__ loff, int *__restrict__ cursor, int32_t *__restrict__ live,
+                            int *__restrict__ nlong, int4 *__restrict__ longs) {
   GS(k, n) {
     int a = 0, z = S;
     while (z - a > 1) {
@@ -107,9 +113,25 @@ __global__ void k_live_fill(const int64_t *__restrict__ off, int S, int64_t n, c
     while (off[a + 1] <= k) a++;
     int64_t b = bo[a] + (k - off[a]) / kTile;
     int64_t last = last_tile_before(T0, b + 1, bo[a + 1], te[k]);
+    if (last - b > kLongSpan) {  // (tile indices < 2^31: the batch guard caps n)
+      longs[atomicAdd(nlong, 1)] = make_int4((int)(b + 1), (int)last, (int)(k - off[a]), 0);
+      continue;
+    }
     for (int64_t x = b + 1; x <= last; x++) {
       int slot = atomicAdd(cursor + x, 1);
       live[loff[x] + slot] = (int32_t)(k - off[a]);
+    }
+  }
+}
+
+__global__ void k_live_fill_long(const int *__restrict__ nlong, const int4 *__restrict__ longs,
+                                 const int64_t *__restrict__ loff, int *__restrict__ cursor,
+                                 int32_t *__restrict__ live) {
+  for (int i = blockIdx.x; i < *nlong; i += gridDim.x) {
+    const int4 q = longs[i];
+    for (int x = q.x + threadIdx.x; x <= q.y; x += blockDim.x) {
+      const int slot = atomicAdd(cursor + x, 1);
+      live[loff[x] + slot] = q.z;
     }
   }
 }
@@ -228,11 +250,13 @@ static void build_tiles(Ctx &ctx, Arena &ar, const RectSets &rs, Tiles *tl) {
                                   ctx.stream));
     tl->live = ar.take<int32_t>(lo[tl->NB] + 1);
   }
-  int *cursor = ar.take<int>(tl->NB + 1);
+  int *cursor = ar.take<int>(tl->NB + 2);  // [NB + 1]: the long-span count
+  int4 *longs = ar.take<int4>(rs.n + 1);
   if (!ctx.ok()) return;
-  STW_CUDA(ctx, cudaMemsetAsync(cursor, 0, (tl->NB + 1) * sizeof(int), ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(cursor, 0, (tl->NB + 2) * sizeof(int), ctx.stream));
   STW_KL(k_live_fill, grid_for(rs.n, 256), 256, ctx.stream, rs.off, rs.S, rs.n, rs.te, dbo, tl->T0, tl->loff, cursor,
-                                                          tl->live);
+         tl->live, cursor + tl->NB + 1, longs);
+  STW_KL(k_live_fill_long, 148 * 2, 256, ctx.stream, cursor + tl->NB + 1, longs, tl->loff, cursor, tl->live);
   STW_LAUNCHED(ctx);
 }
 
