@@ -1498,6 +1498,7 @@ __device__ void block_scan_into(int n, F f, int32_t *out, int *shi) {
 __device__ void layers_unit(const LayerArgs &A, const int u);
 #ifdef STW_LAYERS_CLOCK
 __device__ unsigned long long g_layers_clk[8];
+__device__ unsigned long long g_class_clk[64][3];  // per class of the big unit: cycles, items, nl
 #define LCLK(i) if (threadIdx.x == 0) { long long _n = clock64(); atomicAdd(&g_layers_clk[i], (unsigned long long)(_n - _lc)); _lc = _n; }
 #else
 #define LCLK(i)
@@ -1523,7 +1524,7 @@ __device__ void resolve_class(const LayerArgs &A, const bool gap, const int nl, 
                               const int32_t *__restrict__ prioA, const int32_t *__restrict__ sAts,
                               const int32_t *__restrict__ sAte, const int32_t *__restrict__ loffA, int32_t *last,
                               int32_t *newcnt, int32_t *ilayer, int32_t *irank, int32_t *sm_nend, int *out_nnew,
-                              long long *out_gap) {
+                              long long *out_gap, const int hz) {
   const int warp = threadIdx.x >> 5, lane = lane_id();
   // ---- 2. warp-serial resolve: gap insertion, else Alg. 1 among this class's new layers.
   // Narrow case (<= 32 layers): the register-resident chain of k_layers_w32;
@@ -1538,6 +1539,8 @@ __device__ void resolve_class(const LayerArgs &A, const bool gap, const int nl, 
       sh_cnt[lane] = 0;
       __syncwarp();
       const int my_prio = lane < nl ? prioA[lane] : 0;  // lane p: the layer at priority p
+      // Alg. 1 keys pack (end << 5 | 31 - lane) when every end is in [0, 2^26)
+      const bool packed = hz < (1 << 26);  // ends are <= horizon
       // each chunk's item fields are loaded one chunk ahead (the chain never waits on global memory)
       int nx_ts = 0, nx_te = 0;
       unsigned nx_fm = 0;
@@ -1572,7 +1575,7 @@ __device__ void resolve_class(const LayerArgs &A, const bool gap, const int nl, 
         int ts = __shfl_sync(FULL, my_ts, 0), te = __shfl_sync(FULL, my_te, 0);
         unsigned f = __shfl_sync(FULL, fm, 0);
         while (k < cnt) {
-          if (gap) {
+          if (gap && nl > 0) {
             for (; k < cnt; k++) {
               const int k1 = (k + 1) & 31;
               const int nts = __shfl_sync(FULL, my_ts, k1), nte = __shfl_sync(FULL, my_te, k1);
@@ -1586,17 +1589,28 @@ __device__ void resolve_class(const LayerArgs &A, const bool gap, const int nl, 
             if (k >= cnt) break;
           }
           // Alg. 1 for item k (planner.py:236-254): the largest end < t_s among
-          // the class's new layers, ties to the oldest; none: a new layer
-          const bool ca = lane < nnew && ne < ts;
-          const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
-          const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
-          const int best = cma ? __ffs(cma) - 1 : nnew;
-          if (!cma && nl + nnew == 32) {
+          // the class's new layers, ties to the oldest -- one max-reduction over
+          // (end << 5 | 31 - lane) keys when ends fit 26 bits; none: a new layer
+          int best;
+          bool found;
+          if (packed) {
+            const int key = __reduce_max_sync(
+                FULL, lane < nnew && ne < ts ? (int)(((unsigned)ne << 5) | (unsigned)(31 - lane)) : -1);
+            found = key >= 0;
+            best = found ? 31 - (key & 31) : nnew;
+          } else {
+            const bool ca = lane < nnew && ne < ts;
+            const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
+            const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
+            found = cma != 0;
+            best = found ? __ffs(cma) - 1 : nnew;
+          }
+          if (!found && nl + nnew == 32) {
             fast = false;
             break;
           }
           if (lane == best) ne = te;
-          nnew += cma ? 0 : 1;
+          nnew += found ? 0 : 1;
           if (lane == k) my_m1 = 0, my_code = 32 + best;
           k++;
           const int kk = k & 31;
@@ -1790,7 +1804,7 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
     LCLK(0)
     // ---- 2. warp-serial resolve (resolve_class)
     resolve_class(A, gap, nl, j0, j1, a0, off, fitw, prioA, sAts, sAte, loffA, last, newcnt, ilayer, irank, sm_nend,
-                  &sh_nnew, &sh_gap);
+                  &sh_nnew, &sh_gap, A.horizon[t]);
     LCLK(1)
     // ---- 3. merge this class's slots into the per-layer sorted slot CSR
     const int nnew = sh_nnew, nl2 = nl + nnew;
@@ -1873,10 +1887,267 @@ __device__ void layers_unit(const LayerArgs &A, const int u) {
 // slots) and the slot merge run on every SM, the serial resolve on one warp,
 // with grid-wide barriers between the steps (the single-CTA k_layers spent
 // 40% of c5's time in those two data-parallel steps on one SM).
+// Gap insertion of one class, per layer, on the whole GPU. For the layer at
+// priority p the greedy (planner.py:420-431: each item takes the first fitting
+// layer in priority order whose same-class slots all end before its start) is
+// a chain over the class's items in (t_s, tie) order: the candidates are the
+// items that fit layer p and no higher-priority layer took; the layer takes
+// the first candidate, then the first candidate starting after that item's
+// end, and so on -- so layer p's members are the chain head -> nx -> nx ...
+// with nx(i) = the first candidate at or after the first position whose t_s
+// exceeds t_e(i) (t_s is sorted, so a binary search). Layers are processed in
+// priority order (layer p's candidates exclude what layers < p took).
+// Per layer: (A) per 4096-item block a suffix-min of candidate positions,
+// (B) nx of every candidate, (C) per block each candidate's exit from the
+// block by pointer jumping in shared memory, (D) one thread walks the chain
+// over block entries (exits), (E) per block one thread walks the members
+// from the block's entry, recording their rank. Items no layer takes go
+// through Alg. 1 afterwards (few: c5 has 54 of 983,279).
+constexpr int kChainB = 4096;
+constexpr int kChainMaxL = 32;
+
+struct ChainScratch {
+  int32_t *ipri;    // [n] priority that took the item, -1: none yet
+  int32_t *nxl;     // [n] first candidate at or after x inside x's block (m: none)
+  int32_t *nx;      // [n] chain successor of a candidate (m: none)
+  int32_t *ex;      // [n] first chain node after x outside x's block (m: none)
+  int32_t *lrank;   // [n] rank of a member among its layer's members in its block
+  int32_t *bfirst;  // [nb] first candidate of the block (m: none)
+  int32_t *bsfx;    // [nb + 1] first candidate at or after the block
+  int32_t *bent;    // [nb] the chain's first node in the block (-1: none)
+  int32_t *bcnt;    // [nb * kChainMaxL] members of priority p in block b, then their exclusive prefix
+};
+
 struct BigState {
   int nl, nnew;
   long long gap;
+  int use_chain, over;
+  ChainScratch cs;
 };
+
+// thread t of a 256-thread CTA: minimum of v over threads > t (`none` if none); *total = minimum over all
+__device__ __forceinline__ int block_suffix_min_excl(int v, int none, int *sh, int *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = v;  // suffix (inclusive) inside the warp
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_down_sync(0xffffffffu, inc, o);
+    if (lane + o < 32) inc = min(inc, y);
+  }
+  if (lane == 0) sh[w] = inc;
+  __syncthreads();
+  int after = none;  // warps after w
+  for (int x = w + 1; x < (int)(blockDim.x >> 5); x++) after = min(after, sh[x]);
+  int ex = __shfl_down_sync(0xffffffffu, inc, 1);
+  if (lane == 31) ex = none;
+  ex = min(ex, after);
+  if (total) {
+    int t = none;
+    for (int x = 0; x < (int)(blockDim.x >> 5); x++) t = min(t, sh[x]);
+    *total = t;
+  }
+  __syncthreads();
+  return ex;
+}
+
+__device__ __forceinline__ int chain_nxc(const ChainScratch &cs, int y, int m) {
+  if (y >= m) return m;
+  const int v = cs.nxl[y];
+  return v < m ? v : cs.bsfx[y / kChainB + 1];
+}
+
+// returns false when the class must be redone by resolve_class (Alg. 1 would
+// need more than 32 layers in all); on success ilayer / irank / newcnt are
+// written for every item of the class, *nnew_out = new layers, *gap_out += gapped
+__device__ bool chain_class(const LayerArgs &A, const ChainScratch &cs, const int nl, const int64_t j0,
+                            const int64_t j1, const int64_t a0, const uint32_t *__restrict__ fitw,
+                            const int32_t *__restrict__ prioA, int32_t *newcnt, int32_t *ilayer, int32_t *irank,
+                            int *sh_flag, int *sh_nnew, long long *sh_gap, const bool lead, const int hz,
+                            cooperative_groups::grid_group &grid) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int m = (int)(j1 - j0);
+  const int nb = (m + kChainB - 1) / kChainB;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid, gs = (int64_t)gridDim.x * blockDim.x;
+  const int32_t *ts = A.it.ts + j0, *te = A.it.te + j0;
+  const uint32_t *fw = fitw + (j0 - a0) * kFitWords;
+  __shared__ int s_J[kChainB];
+  __shared__ int s_sh[33];
+  for (int64_t x = gt; x < m; x += gs) cs.ipri[x] = -1;
+  grid.sync();
+  for (int p = 0; p < nl; p++) {
+    // (A) per block: suffix-min of candidate positions; the block's first candidate
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+      const int base = b * kChainB, cnt = min(kChainB, m - base);
+      constexpr int IPT = kChainB / kPlanThreads;
+      int v[IPT];
+      int tmin = m;
+#pragma unroll
+      for (int k = IPT - 1; k >= 0; k--) {
+        const int x = base + tid * IPT + k;
+        const bool c = tid * IPT + k < cnt && ((fw[(int64_t)x * kFitWords + (p >> 5)] >> (p & 31)) & 1u) &&
+                       cs.ipri[x] < 0;
+        tmin = c ? x : tmin;
+        v[k] = tmin;
+      }
+      int tot;
+      const int after = block_suffix_min_excl(tmin, m, s_sh, &tot);
+#pragma unroll
+      for (int k = 0; k < IPT; k++) {
+        const int x = base + tid * IPT + k;
+        if (tid * IPT + k < cnt) cs.nxl[x] = min(v[k], after);
+      }
+      if (tid == 0) {
+        cs.bfirst[b] = tot;
+        cs.bent[b] = -1;
+      }
+    }
+    grid.sync();
+    if (lead && tid == 0) {  // suffix over the blocks
+      int r = m;
+      cs.bsfx[nb] = m;
+      for (int b = nb - 1; b >= 0; b--) r = min(r, cs.bfirst[b]), cs.bsfx[b] = r;
+    }
+    grid.sync();
+    // (B) chain successors of the candidates
+    for (int64_t x = gt; x < m; x += gs) {
+      if (cs.nxl[x] != (int)x) continue;  // not a candidate
+      const int e = te[x];
+      int lo = (int)x + 1, hi = m;  // first position with t_s > t_e(x) (> x: t_s(x) <= t_e(x))
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ts[mid] <= e)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      cs.nx[x] = chain_nxc(cs, lo, m);
+    }
+    grid.sync();
+    // (C) per block: each candidate's first chain node outside the block (pointer jumping)
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+      const int base = b * kChainB, cnt = min(kChainB, m - base);
+      for (int i = tid; i < cnt; i += blockDim.x) s_J[i] = cs.nxl[base + i] == base + i ? cs.nx[base + i] : m;
+      __syncthreads();
+      for (int round = 0; round < 14; round++) {
+        bool moved = false;
+        for (int i = tid; i < cnt; i += blockDim.x) {
+          const int j = s_J[i];
+          if (j < base + cnt) {  // still inside the block: jump (any value read is a later node of the same path)
+            s_J[i] = s_J[j - base];
+            moved = true;
+          }
+        }
+        if (!__syncthreads_or(moved)) break;
+      }
+      for (int i = tid; i < cnt; i += blockDim.x)
+        if (cs.nxl[base + i] == base + i) cs.ex[base + i] = s_J[i];
+      __syncthreads();
+    }
+    grid.sync();
+    // (D) the chain's entry into every block it visits
+    if (lead && tid == 0) {
+      for (int e = chain_nxc(cs, 0, m); e < m; e = cs.ex[e]) cs.bent[e / kChainB] = e;
+    }
+    grid.sync();
+    // (E) per block: the members from the entry, their ranks, the block's count
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+      const int base = b * kChainB, cnt = min(kChainB, m - base);
+      const int ent = cs.bent[b];
+      if (ent >= 0) {
+        for (int i = tid; i < cnt; i += blockDim.x) s_J[i] = cs.nx[base + i];  // only members are read
+        __syncthreads();
+        if (tid == 0) {
+          int r = 0;
+          for (int x = ent; x < base + cnt; x = s_J[x - base]) {
+            cs.ipri[x] = p;
+            cs.lrank[x] = r++;
+          }
+          cs.bcnt[b * kChainMaxL + p] = r;
+        }
+        __syncthreads();
+      } else if (tid == 0) {
+        cs.bcnt[b * kChainMaxL + p] = 0;
+      }
+    }
+    grid.sync();
+  }
+  // member ranks: prefix of each priority's block counts; the layers' counts
+  __shared__ unsigned long long s_gapped;
+  if (lead) {
+    if (tid == 0) s_gapped = 0;
+    __syncthreads();
+    for (int p = tid; p < nl; p += blockDim.x) {
+      int r = 0;
+      for (int b = 0; b < nb; b++) {
+        const int c = cs.bcnt[b * kChainMaxL + p];
+        cs.bcnt[b * kChainMaxL + p] = r;
+        r += c;
+      }
+      newcnt[prioA[p]] = r;
+      atomicAdd(&s_gapped, (unsigned long long)r);
+    }
+  }
+  grid.sync();
+  for (int64_t x = gt; x < m; x += gs) {
+    const int p = cs.ipri[x];
+    if (p >= 0) {
+      ilayer[j0 - a0 + x] = prioA[p];
+      irank[j0 - a0 + x] = cs.bcnt[(x / kChainB) * kChainMaxL + p] + cs.lrank[x];
+    }
+  }
+  // leftovers: Alg. 1 among the class's new layers (planner.py:236-254), in item order
+  bool ok = true;
+  if (lead) {
+    if (tid < 32) {
+      const bool packed = hz < (1 << 26);
+      int ne = INT_MIN, nnew = 0, my_cnt = 0;
+      for (int cb = 0; cb < m && ok; cb += 32) {
+        const int x = cb + lane;
+        const bool left = x < m && cs.ipri[x] < 0;
+        unsigned lm = __ballot_sync(FULL, left);
+        const int my_ts = left ? ts[x] : 0, my_te = left ? te[x] : 0;
+        while (lm) {
+          const int k = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const int t0 = __shfl_sync(FULL, my_ts, k), t1 = __shfl_sync(FULL, my_te, k);
+          int best;
+          bool found;
+          if (packed) {
+            const int key = __reduce_max_sync(
+                FULL, lane < nnew && ne < t0 ? (int)(((unsigned)ne << 5) | (unsigned)(31 - lane)) : -1);
+            found = key >= 0;
+            best = found ? 31 - (key & 31) : nnew;
+          } else {
+            const bool ca = lane < nnew && ne < t0;
+            const int mx = __reduce_max_sync(FULL, ca ? ne : INT_MIN);
+            const unsigned cma = __ballot_sync(FULL, ca && ne == mx);
+            found = cma != 0;
+            best = found ? __ffs(cma) - 1 : nnew;
+          }
+          if (!found && nl + nnew == kChainMaxL) {
+            ok = false;
+            break;
+          }
+          const int rk = __shfl_sync(FULL, my_cnt, best);
+          if (lane == best) ne = t1, my_cnt++;
+          nnew += found ? 0 : 1;
+          if (lane == k) ilayer[j0 - a0 + x] = nl + best, irank[j0 - a0 + x] = rk;
+        }
+      }
+      if (ok && lane < nnew) newcnt[nl + lane] = my_cnt;
+      if (lane == 0) {
+        *sh_nnew = nnew, *sh_flag = ok ? 1 : 0;
+        if (ok) *sh_gap += (long long)s_gapped;
+      }
+    }
+    __syncthreads();
+    ok = *sh_flag != 0;
+    if (!ok)  // resolve_class redoes the class: the gap layers' counts start from zero again
+      for (int l = tid; l < nl; l += blockDim.x) newcnt[l] = 0;
+    __syncthreads();
+  }
+  return ok;
+}
 
 __device__ void layers_unit_big(const LayerArgs &A, const int u, BigState *st, cooperative_groups::grid_group &grid) {
   const int c = u % A.C, t = u / A.C;
@@ -1937,11 +2208,28 @@ __device__ void layers_unit_big(const LayerArgs &A, const int u, BigState *st, c
     grid.sync();
     BCLK(0)
     // ---- 2. the serial resolve (one CTA, warp 0)
+#ifdef STW_LAYERS_CLOCK
+    const long long _r0 = clock64();
+#endif
+    bool done = false;
+    if (st->use_chain && gap && nl > 0 && nl <= kChainMaxL) {  // the chain resolve (grid-wide; uniform condition)
+      __shared__ int sh_flag;
+      done = chain_class(A, st->cs, nl, j0, j1, a0, fitw, prioA, newcnt, ilayer, irank, &sh_flag, &sh_nnew, &sh_gap,
+                         lead, A.horizon[t], grid);
+    }
     if (lead) {
-      resolve_class(A, gap, nl, j0, j1, a0, off, fitw, prioA, sAts, sAte, loffA, last, newcnt, ilayer, irank, sm_nend,
-                    &sh_nnew, &sh_gap);
+      if (!done)
+        resolve_class(A, gap, nl, j0, j1, a0, off, fitw, prioA, sAts, sAte, loffA, last, newcnt, ilayer, irank,
+                      sm_nend, &sh_nnew, &sh_gap, A.horizon[t]);
       __syncthreads();
       if (tid == 0) vst->nnew = sh_nnew;
+#ifdef STW_LAYERS_CLOCK
+      if (tid == 0) {
+        static __device__ int cls_i = 0;
+        const int ci = atomicAdd(&cls_i, 1) & 63;
+        g_class_clk[ci][0] = clock64() - _r0, g_class_clk[ci][1] = m, g_class_clk[ci][2] = nl;
+      }
+#endif
     }
     grid.sync();
     BCLK(1)
@@ -3031,7 +3319,16 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
         unsigned grid = (unsigned)nsm;
         if (getenv("STW_BIG_GRID")) grid = (unsigned)atoi(getenv("STW_BIG_GRID"));  // diagnostics
         (void)occ;
-        BigState *d_st = ar.take<BigState>(bigs.size());
+        // the chain resolve's scratch, shared by the big units (they run one after another)
+        int64_t maxn = 1;
+        for (int32_t u : bigs) maxn = std::max<int64_t>(maxn, uo[u + 1] - uo[u]);
+        const int64_t nbk = (maxn + kChainB - 1) / kChainB + 1;
+        ChainScratch cs{ar.take<int32_t>(maxn), ar.take<int32_t>(maxn), ar.take<int32_t>(maxn),
+                        ar.take<int32_t>(maxn), ar.take<int32_t>(maxn), ar.take<int32_t>(nbk),
+                        ar.take<int32_t>(nbk + 1), ar.take<int32_t>(nbk), ar.take<int32_t>(nbk * kChainMaxL)};
+        std::vector<BigState> hst(bigs.size());
+        for (auto &h : hst) h = BigState{0, 0, 0, getenv("STW_NO_CHAIN") ? 0 : 1, 0, cs};
+        BigState *d_st = h2d(ctx, ar, hst);
         int nb = (int)bigs.size();
         if (!ctx.ok()) return ctx.rc;
         void *args[] = {(void *)&LA, (void *)&d_bigs, (void *)&nb, (void *)&d_st};
@@ -3081,6 +3378,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
             hc[0] / 1e6, hc[1] / 1e6, hc[2] / 1e6, hc[3] / 1e6, hc[5], hc[7], hc[6]);
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_layers_clk, z, sizeof(z));
+    unsigned long long cc[64][3];
+    cudaMemcpyFromSymbol(cc, g_class_clk, sizeof(cc));
+    for (int i = 0; i < 64 && cc[i][1]; i++)
+      fprintf(stderr, "  class %d: %llu items, %llu earlier layers, %.1f Mcycles (%.0f / item)\n", i, cc[i][1],
+              cc[i][2], cc[i][0] / 1e6, (double)cc[i][0] / cc[i][1]);
   }
 #endif
   pt.mark("E layers");

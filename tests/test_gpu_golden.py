@@ -128,3 +128,18 @@ def test_app_b_replay_general_warp(name, monkeypatch):
     assert rep.to_dict() == a["sim"]
     assert log_digest(log) == a["sim_log_digest"]
     assert M.run_baseline(tr).to_dict() == a["baseline"]
+
+
+@pytest.mark.parametrize("chain", [True, False])
+def test_app_b_c2_big_unit_resolve(chain, monkeypatch):
+    """c2 is one unit too large for a warp's shared memory: the whole-GPU layer
+    kernel resolves its gap classes by the parallel per-layer chain (default)
+    or by the warp-serial resolve (STW_NO_CHAIN); both give the reference's plan."""
+    if not chain:
+        monkeypatch.setenv("STW_NO_CHAIN", "1")
+    a = anchors()["c2_llama2_7b_vpp_rcp"]
+    st = M.PlanStats()
+    tr = M.Trace.from_arrays(tracegen.synth_arrays(tracegen.config("c2_llama2_7b_vpp_rcp")))
+    plan, rmap = M.plan_trace(tr, stats=st)
+    assert st.to_dict()["gap_insertions"] == a["stats"]["gap_insertions"]
+    assert hashlib.sha256(planio.dumps_plan(plan.to_bundle(rmap)).encode()).hexdigest()[:16] == a["write_plan_sha16"]

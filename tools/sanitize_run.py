@@ -1,7 +1,8 @@
 """A small workload touching every libstw kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck): K2 radix sort and the look-back scan over
 many tiles, the batched planner (all candidates), K7, K8, K9/K10 replays, K1
-and the sub-operation kernels. Each result is checked against the oracle, so a
+the sub-operation kernels, the general replay warp, and
+c2 (the cooperative huge-unit layer kernel, the exact validator). Each result is checked against the oracle, so a
 race that changes a result fails here too.
     compute-sanitizer --tool racecheck python tools/sanitize_run.py"""
 import sys
@@ -39,6 +40,20 @@ for name in ("c1_llama2_7b_1f1b", "c3_mixtral_moe"):
     base = M.run_baseline(tr)
     assert base.to_dict() == O.baseline(ta).report, name
     assert M.validate_plan(plan) == [] and M.peak_live_bytes(ta) == O.peak_live(ta.size, ta.t_s, ta.t_e)
+# the general replay warp (forced), and c2: one unit too large for a warp's
+# shared memory -> the cooperative whole-GPU layer kernel, and > 65 K
+# rectangles -> the exact tiled validator with long-span live lists
+import os  # noqa: E402
+
+os.environ["STW_REPLAY_GENERAL"] = "1"
+ta = tracegen.synth_arrays(tracegen.config("c1_llama2_7b_1f1b"))
+assert M.run_baseline(M.Trace.from_arrays(ta)).to_dict() == O.baseline(ta).report, "general replay"
+del os.environ["STW_REPLAY_GENERAL"]
+ta = tracegen.synth_arrays(tracegen.config("c2_llama2_7b_vpp_rcp"))
+r = O.plan(ta, True, True)
+bp2 = api.plan_batch([ta], ((True, True),))
+st = ta.dyn == 0
+assert np.array_equal(bp2.addr[0][st], r.addr[st]), "c2 plan"
 ev = [M.MemoryRequestEvent(i, (1 + i % 5) * 512, i, i + 3 + i % 4, M.PhaseId.parse("F:0"), M.PhaseId.parse("B:0"))
       for i in range(300)]
 groups = planner.group_by_phase(ev)
