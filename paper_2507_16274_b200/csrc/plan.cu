@@ -2028,14 +2028,25 @@ __device__ bool chain_class(const LayerArgs &A, const ChainScratch &cs, const in
       const int base = b * kChainB, cnt = min(kChainB, m - base);
       for (int i = tid; i < cnt; i += blockDim.x) s_J[i] = cs.nxl[base + i] == base + i ? cs.nx[base + i] : m;
       __syncthreads();
-      for (int round = 0; round < 14; round++) {
+      for (int round = 0; round < 14; round++) {  // every round reads, then (after a barrier) writes
+        constexpr int IPT = kChainB / kPlanThreads;
+        int nv[IPT];
         bool moved = false;
-        for (int i = tid; i < cnt; i += blockDim.x) {
-          const int j = s_J[i];
-          if (j < base + cnt) {  // still inside the block: jump (any value read is a later node of the same path)
-            s_J[i] = s_J[j - base];
-            moved = true;
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+          const int i = tid + k * kPlanThreads;
+          nv[k] = m;
+          if (i < cnt) {
+            const int j = s_J[i];
+            nv[k] = j < base + cnt ? s_J[j - base] : j;  // inside the block: jump
+            moved |= j < base + cnt;
           }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+          const int i = tid + k * kPlanThreads;
+          if (i < cnt) s_J[i] = nv[k];
         }
         if (!__syncthreads_or(moved)) break;
       }
