@@ -61,6 +61,10 @@ struct RegArgs {
   int4 *ops;                 // per op: {size_u, flags, z, w}
   int4 *res;                 // per op: {addr_u, segment base_u, flags, 0}
   long long *out;            // see k_replay_reg
+  // resume after the cache outgrew its rows: resume[0] = op to continue at
+  // (0: start), [1] next segment base, [2] cache rows dumped; dump[r * 32 + lane]
+  long long *resume;
+  int4 *dump;
 };
 
 // the unit: OR of every size / planned address / space bound / the pool and the 2 MiB segment minimum
@@ -315,9 +319,23 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
   const uint32_t pool_u = (uint32_t)((unsigned long long)A.pool >> sh);
   if (SIM && pool_u > 0 && lane == 0) fl[0] = 0, fh[0] = pool_u;
   uint32_t next_base = SIM ? pool_u : 0u;
+  // resuming (baseline only: the cache is the whole state): the previous
+  // launch's rows, the next segment base, and the first op not yet replayed
+  const int64_t start = SIM ? 0 : A.resume[0];
+  if (start > 0) {
+    next_base = (uint32_t)A.resume[1];
+    const int rd = (int)A.resume[2];
+#pragma unroll
+    for (int r = 0; r < R; r++)
+      if (r < rd) {
+        const int4 q = A.dump[r * 32 + lane];
+        cl[r] = (uint32_t)q.x, ch[r] = (uint32_t)q.y, cs[r] = (uint32_t)q.z;
+      }
+  }
   const uint32_t minseg = (uint32_t)(kRMinSegment >> sh);
   int status = 0;
-  long long err_op = 0, err_addr = 0;
+  long long err_op = 0, err_addr = 0, done_ops = 0;
+  bool too_big = false;
 
   // caching-allocator malloc (baseline.py:49-77): best fit = min length, ties
   // to the lowest address; none fits: a fresh segment at the next base. The
@@ -350,21 +368,26 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     uint32_t ss = 1;
     while (ss < n) ss <<= 1;
     if (ss < minseg) ss = minseg;
-    if ((unsigned long long)next_base + ss >= (1ull << 31)) return false;
+    if ((unsigned long long)next_base + ss >= (1ull << 31)) {
+      too_big = true;  // values past 31 bits: the general warp
+      return false;
+    }
     const uint32_t base = next_base;
+    if (ss > n && !reg_insert<R, true>(cl, ch, cs, base + n, base + ss, base)) return false;  // state untouched
     next_base += ss;
     *grown = ss, *addr = base;
     if (lane == 0) sts32(a_sb + 4 * slot, base);
-    return !(ss > n && !reg_insert<R, true>(cl, ch, cs, base + n, base + ss, base));
+    return true;
   };
 
   // three-stage prefetch: O1/O2 = op records of the next two windows, F1 = the
   // allocation results the next window's frees release (written before this
   // window), SP1 = the next window's first two space intervals per dynamic op
   const int4 z4 = make_int4(0, 0, 0, 0);
-  int4 O1 = lane < n2 ? A.ops[lane] : z4;
-  int4 O2 = 32 + lane < n2 ? A.ops[32 + lane] : z4;
-  int4 F1 = z4;
+  int4 O1 = start + lane < n2 ? A.ops[start + lane] : z4;
+  int4 O2 = start + 32 + lane < n2 ? A.ops[start + 32 + lane] : z4;
+  int4 F1 = z4;  // a resumed run's first window: every earlier allocation is in A.res
+  if (start > 0 && start + lane < n2 && !(O1.y & 1) && O1.z < start) F1 = A.res[O1.z];
   long long SP1[4] = {0, 0, 0, 0};
   auto load_sp = [&](const int4 &o, long long *sp) {
     sp[0] = sp[1] = sp[2] = sp[3] = 0;
@@ -374,7 +397,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     }
   };
   load_sp(O1, SP1);
-  for (int64_t w0 = 0; w0 < n2; w0 += 32) {
+  for (int64_t w0 = start; w0 < n2; w0 += 32) {
     const int4 O0 = O1;
     const int4 F0 = F1;
     const uint4 SP0 = make_uint4((uint32_t)((unsigned long long)SP1[0] >> sh), (uint32_t)((unsigned long long)SP1[1] >> sh),
@@ -386,7 +409,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     load_sp(O1, SP1);
     // this window's frees: allocation of an earlier window (F0) or of the previous one (s_res, s_sb)
     int4 info = F0;
-    if (!(O0.y & 1) && O0.z >= w0 - 32 && O0.z < w0) {
+    if (w0 > start && !(O0.y & 1) && O0.z >= w0 - 32 && O0.z < w0) {
       const int j = (int)(O0.z - (w0 - 32));
       info = lds128(a_res + 16 * j);
       info.y = (int)lds32(a_sb + 4 * j);
@@ -454,6 +477,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
           uint32_t grown;
           if (!cache_malloc(n, k, &a, &grown)) {
             status = 1;
+            err_op = w0 + k;  // (resumable unless too_big: the state is untouched)
             over = 1;
             break;
           }
@@ -475,6 +499,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
           ok = reg_release<RP, false>(fl, fh, fs, (uint32_t)ai.x, (uint32_t)ai.x + n, 0);
         if (!ok) {
           status = 1;
+          err_op = w0 + k;
           over = cache ? 1 : 2;
           break;
         }
@@ -483,7 +508,23 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
       sts128(a_res + 16 * k, rec);  // every lane writes the same record (each later reads its own write)
       op = nop, fi = nfi;
     }
-    if (status) break;
+    if (status) {
+      done_ops = w0;
+      if (!SIM && status == 1 && !too_big) {  // resumable: flush this window's finished ops, dump the rows
+        const int kk = (int)(err_op - w0);
+        __syncwarp();
+        if (lane < kk) {
+          int4 r = lds128(a_res + 16 * lane);
+          r.y = (r.z & 1) ? (int)lds32(a_sb + 4 * lane) : 0;
+          A.res[w0 + lane] = r;
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) A.dump[r * 32 + lane] = make_int4((int)cl[r], (int)ch[r], (int)cs[r], 0);
+        if (lane == 0) A.resume[0] = err_op, A.resume[1] = next_base, A.resume[2] = R;
+        done_ops = err_op;
+      }
+      break;
+    }
     __syncwarp();
     if (lane < cnt) {
       int4 r = lds128(a_res + 16 * lane);
@@ -496,6 +537,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     out[1] = over;
     out[3] = err_addr;
     if (status == 2) out[2] = A.id[A.operm[err_op] >> 1];
+    out[4] = status == 1 ? done_ops : n2;  // ops replayed before an overflow (diagnostics)
   }
 }
 
@@ -604,7 +646,10 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
   A.ops = ar.take<int4>(n2 + 1);
   A.res = ar.take<int4>(n2 + 1);
   A.out = ar.take<long long>(16);
+  A.resume = ar.take<long long>(4);
+  A.dump = ar.take<int4>(16 * 32);
   if (!ctx.ok()) return 1;
+  STW_CUDA(ctx, cudaMemsetAsync(A.resume, 0, 4 * sizeof(long long), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(A.unit, 0, 2 * sizeof(unsigned long long), ctx.stream));
   STW_KL(k_reg_unit, grid_for(std::max<int64_t>(n, in.nsp), 256, 148 * 8), 256, ctx.stream, A);
   STW_KL(k_reg_ops, grid_for(n2, 256), 256, ctx.stream, A);
@@ -615,7 +660,7 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
   const bool sim = !in.baseline;
   int rc = 1, rp = 1;
   hout[0] = 1;
-  while (hout[0] == 1 && rc <= 16) {
+  while (hout[0] == 1 && rc <= 16) {  // (rc beyond 16: the general warp)
     bool launched = false;
 #define STW_RR(RC)                                                                                       \
   if (rc == RC) {                                                                                        \
@@ -624,7 +669,7 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
     else STW_KL((k_replay_reg<RC, RC, true>), 1, 32, ctx.stream, A);                                     \
     launched = true;                                                                                     \
   }
-    STW_RR(1) STW_RR(2) STW_RR(4) STW_RR(8) STW_RR(16)
+    STW_RR(1) STW_RR(2) STW_RR(3) STW_RR(5) STW_RR(8) STW_RR(16)
 #undef STW_RR
     if (!launched) break;
     STW_LAUNCHED(ctx);
@@ -632,11 +677,19 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
     STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
     if (!ctx.ok()) return 1;
 #ifdef STW_REPLAY_CLOCK
-    fprintf(stderr, "replay_reg rows=%d/%d ops=%lld: status %lld over %lld\n", rc, rp, (long long)n2, hout[0], hout[1]);
+    fprintf(stderr, "replay_reg rows=%d/%d ops=%lld: status %lld over %lld after %lld ops\n", rc, rp, (long long)n2,
+            hout[0], hout[1], hout[4]);
 #endif
     if (hout[0] != 1) break;
-    if (hout[1] == 2 && sim && rp < rc) rp = rc;  // pool outgrew its single row
-    else rc *= 2, rp = rp == 1 ? 1 : rc;
+    // the baseline resumes where the cache outgrew its rows (A.resume / A.dump
+    // were written); a simulate run restarts from the first op
+    if (hout[1] == 2 && sim && rp < rc) {  // pool outgrew its single row
+      rp = rc;
+    } else {  // 1 -> 2 -> 3 -> 5 -> 8 -> 16 rows (32 blocks each): c1 29, c3 68, c5 129 blocks
+      rc = rc == 1 ? 2 : rc == 2 ? 3 : rc == 3 ? 5 : rc == 5 ? 8 : 16 * (rc / 8 + 1);
+      rp = rp == 1 ? 1 : rc;
+    }
+    if (sim || hout[1] != 1) STW_CUDA(ctx, cudaMemsetAsync(A.resume, 0, 4 * sizeof(long long), ctx.stream));
   }
   if (hout[0] != 0) return (int)hout[0];
   // metrics
