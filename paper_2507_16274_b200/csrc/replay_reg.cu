@@ -65,7 +65,9 @@ struct RegArgs {
   // (0: start), [1] next segment base, [2] cache rows dumped; dump[r * 32 + lane]
   long long *resume;
   int4 *dump;
+  int sp_staged;  // the reuse spaces (in units) are staged in dynamic shared memory
 };
+constexpr int64_t kSpSmemMax = 16384;  // intervals staged in shared memory (128 KB)
 
 // the unit: OR of every size / planned address / space bound / the pool and the 2 MiB segment minimum
 __global__ void k_reg_unit(RegArgs A) {
@@ -294,11 +296,10 @@ __device__ __forceinline__ uint32_t rows_min(uint32_t (&v)[R]) {
 template <int R, int RP, bool SIM>
 __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
   // per window: op records, the allocations its frees release, the first space
-  // intervals of its dynamic ops, and its results ({addr, -, flags, grown}
-  // written by every lane, the cache segment base by the winning lane only)
+  // intervals of its dynamic ops, and its results ({addr, segment base, flags,
+  // grown}, uniform: every lane writes the same record and reads its own write)
   __shared__ int4 s_op[32], s_info[32], s_res[32];
   __shared__ uint4 s_sp[32];
-  __shared__ uint32_t s_sb[32];
   const int lane = threadIdx.x;
   const int sh = reg_shift(A);
   const int64_t n2 = 2 * A.n;
@@ -308,7 +309,13 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     return;
   }
   const uint32_t a_op = smem_addr(s_op), a_info = smem_addr(s_info), a_res = smem_addr(s_res),
-                 a_sp = smem_addr(s_sp), a_sb = smem_addr(s_sb);
+                 a_sp = smem_addr(s_sp);
+  extern __shared__ uint2 s_spc[];  // the whole reuse-space table, when A.sp_staged
+  if (SIM && A.sp_staged) {
+    for (int64_t j = lane; j < A.nsp; j += 32)
+      s_spc[j] = make_uint2((uint32_t)((unsigned long long)A.sp_lo[j] >> sh), (uint32_t)((unsigned long long)A.sp_hi[j] >> sh));
+    __syncwarp();
+  }
   // cache blocks {cl, ch, cs} (R rows per lane) and pool free intervals {fl, fh} (RP rows)
   uint32_t cl[R], ch[R], cs[R], fl[RP], fh[RP], fs[RP];
 #pragma unroll
@@ -339,8 +346,8 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
 
   // caching-allocator malloc (baseline.py:49-77): best fit = min length, ties
   // to the lowest address; none fits: a fresh segment at the next base. The
-  // winning lane records the block's segment base in s_sb[slot] (no collective).
-  auto cache_malloc = [&](uint32_t n, int slot, uint32_t *addr, uint32_t *grown) -> bool {
+  // block's segment base comes back uniform (one max-reduction, read late).
+  auto cache_malloc = [&](uint32_t n, uint32_t *addr, uint32_t *sbase, uint32_t *grown) -> bool {
     uint32_t key[R], t[R];
 #pragma unroll
     for (int r = 0; r < R; r++) {
@@ -353,14 +360,16 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
 #pragma unroll
       for (int r = 0; r < R; r++) t[r] = key[r] == m ? cl[r] : kRFull;
       const uint32_t a = __reduce_min_sync(kRFull, rows_min<R>(t));
+      uint32_t bs = 0;
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if (key[r] == m && cl[r] == a) {  // the one winning row of the warp
-          sts32(a_sb + 4 * slot, cs[r]);
+          bs = cs[r];
           cl[r] += n;
           if (cl[r] == ch[r]) cl[r] = ch[r] = 0, cs[r] = kNoSeg;
         }
       }
+      *sbase = __reduce_max_sync(kRFull, bs);  // (only the winner is non-zero)
       *addr = a;
       *grown = 0;
       return true;
@@ -375,8 +384,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     const uint32_t base = next_base;
     if (ss > n && !reg_insert<R, true>(cl, ch, cs, base + n, base + ss, base)) return false;  // state untouched
     next_base += ss;
-    *grown = ss, *addr = base;
-    if (lane == 0) sts32(a_sb + 4 * slot, base);
+    *grown = ss, *addr = base, *sbase = base;
     return true;
   };
 
@@ -391,7 +399,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
   long long SP1[4] = {0, 0, 0, 0};
   auto load_sp = [&](const int4 &o, long long *sp) {
     sp[0] = sp[1] = sp[2] = sp[3] = 0;
-    if (SIM && (o.y & 1) && (o.y >> 1) == RR_DYN) {
+    if (SIM && !A.sp_staged && (o.y & 1) && (o.y >> 1) == RR_DYN) {
       if (o.w > o.z) sp[0] = A.sp_lo[o.z], sp[1] = A.sp_hi[o.z];
       if (o.w > o.z + 1) sp[2] = A.sp_lo[o.z + 1], sp[3] = A.sp_hi[o.z + 1];
     }
@@ -407,13 +415,9 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     F1 = z4;
     if (w0 + 32 + lane < n2 && !(O1.y & 1) && O1.z < w0) F1 = A.res[O1.z];
     load_sp(O1, SP1);
-    // this window's frees: allocation of an earlier window (F0) or of the previous one (s_res, s_sb)
+    // this window's frees: allocation of an earlier window (F0) or of the previous one (s_res)
     int4 info = F0;
-    if (w0 > start && !(O0.y & 1) && O0.z >= w0 - 32 && O0.z < w0) {
-      const int j = (int)(O0.z - (w0 - 32));
-      info = lds128(a_res + 16 * j);
-      info.y = (int)lds32(a_sb + 4 * j);
-    }
+    if (w0 > start && !(O0.y & 1) && O0.z >= w0 - 32 && O0.z < w0) info = lds128(a_res + 16 * (int)(O0.z - (w0 - 32)));
     __syncwarp();
     sts128(a_op + 16 * lane, O0);
     sts128(a_info + 16 * lane, info);
@@ -422,7 +426,6 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     const int cnt = (int)min((int64_t)32, n2 - w0);
     int4 op = lds128(a_op), fi = lds128(a_info);
     for (int k = 0; k < cnt; k++) {
-      __syncwarp();  // s_sb of the earlier ops (written by their winning lanes) is visible
       const uint32_t nk = 16 * ((k + 1) & 31);
       const int4 nop = lds128(a_op + nk), nfi = lds128(a_info + nk);  // next op, off the chain
       const uint32_t n = (uint32_t)op.x;
@@ -451,9 +454,16 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
             uint32_t bl = kRFull, bo = kRFull;
             for (int j = op.z; j < op.w; j++) {
               uint32_t slo, shi;
-              if (j == op.z) slo = sp.x, shi = sp.y;
-              else if (j == op.z + 1) slo = sp.z, shi = sp.w;
-              else slo = (uint32_t)((unsigned long long)A.sp_lo[j] >> sh), shi = (uint32_t)((unsigned long long)A.sp_hi[j] >> sh);
+              if (A.sp_staged) {
+                const uint2 q = s_spc[j];
+                slo = q.x, shi = q.y;
+              } else if (j == op.z) {
+                slo = sp.x, shi = sp.y;
+              } else if (j == op.z + 1) {
+                slo = sp.z, shi = sp.w;
+              } else {
+                slo = (uint32_t)((unsigned long long)A.sp_lo[j] >> sh), shi = (uint32_t)((unsigned long long)A.sp_hi[j] >> sh);
+              }
 #pragma unroll
               for (int r = 0; r < RP; r++) {
                 const uint32_t lo = max(fl[r], slo), hi = min(fh[r], shi);
@@ -474,23 +484,20 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
           }
         }
         if (to_cache) {
-          uint32_t grown;
-          if (!cache_malloc(n, k, &a, &grown)) {
+          uint32_t grown, sb;
+          if (!cache_malloc(n, &a, &sb, &grown)) {
             status = 1;
             err_op = w0 + k;  // (resumable unless too_big: the state is untouched)
             over = 1;
             break;
           }
-          rec = make_int4((int)a, 0, 1 | (route << 1) | (grown ? 16 : 0), (int)grown);
+          rec = make_int4((int)a, (int)sb, 1 | (route << 1) | (grown ? 16 : 0), (int)grown);
         } else {
           rec = make_int4((int)a, 0, route << 1, 0);
         }
       } else {
         int4 ai = fi;
-        if (op.z >= w0) {  // allocation of this window: forwarded
-          ai = lds128(a_res + 16 * (op.z - w0));
-          ai.y = (int)lds32(a_sb + 4 * (op.z - w0));
-        }
+        if (op.z >= w0) ai = lds128(a_res + 16 * (op.z - w0));  // allocation of this window: forwarded
         const bool cache = !SIM || (ai.z & 1);
         bool ok;
         if (cache)
@@ -513,11 +520,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
       if (!SIM && status == 1 && !too_big) {  // resumable: flush this window's finished ops, dump the rows
         const int kk = (int)(err_op - w0);
         __syncwarp();
-        if (lane < kk) {
-          int4 r = lds128(a_res + 16 * lane);
-          r.y = (r.z & 1) ? (int)lds32(a_sb + 4 * lane) : 0;
-          A.res[w0 + lane] = r;
-        }
+        if (lane < kk) A.res[w0 + lane] = lds128(a_res + 16 * lane);
 #pragma unroll
         for (int r = 0; r < R; r++) A.dump[r * 32 + lane] = make_int4((int)cl[r], (int)ch[r], (int)cs[r], 0);
         if (lane == 0) A.resume[0] = err_op, A.resume[1] = next_base, A.resume[2] = R;
@@ -526,11 +529,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
       break;
     }
     __syncwarp();
-    if (lane < cnt) {
-      int4 r = lds128(a_res + 16 * lane);
-      r.y = (r.z & 1) ? (int)lds32(a_sb + 4 * lane) : 0;
-      A.res[w0 + lane] = r;
-    }
+    if (lane < cnt) A.res[w0 + lane] = lds128(a_res + 16 * lane);
   }
   if (lane == 0) {
     out[0] = status;
@@ -658,15 +657,23 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
   // grows early in a trace, so failed runs are short). Simulate: the pool's
   // free set has one row (c3: at most 3 intervals) or as many as the cache.
   const bool sim = !in.baseline;
+  A.sp_staged = sim && in.nsp > 0 && in.nsp <= kSpSmemMax;
+  const int sp_smem = A.sp_staged ? (int)(in.nsp * sizeof(uint2)) : 0;
   int rc = 1, rp = 1;
   hout[0] = 1;
   while (hout[0] == 1 && rc <= 16) {  // (rc beyond 16: the general warp)
     bool launched = false;
 #define STW_RR(RC)                                                                                       \
   if (rc == RC) {                                                                                        \
-    if (!sim) STW_KL((k_replay_reg<RC, 1, false>), 1, 32, ctx.stream, A);                                \
-    else if (rp == 1) STW_KL((k_replay_reg<RC, 1, true>), 1, 32, ctx.stream, A);                         \
-    else STW_KL((k_replay_reg<RC, RC, true>), 1, 32, ctx.stream, A);                                     \
+    if (!sim) {                                                                                          \
+      STW_KL((k_replay_reg<RC, 1, false>), 1, 32, ctx.stream, A);                                        \
+    } else if (rp == 1) {                                                                                \
+      cudaFuncSetAttribute(k_replay_reg<RC, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp_smem); \
+      STW_KLS((k_replay_reg<RC, 1, true>), 1, 32, sp_smem, ctx.stream, A);                               \
+    } else {                                                                                             \
+      cudaFuncSetAttribute(k_replay_reg<RC, RC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp_smem); \
+      STW_KLS((k_replay_reg<RC, RC, true>), 1, 32, sp_smem, ctx.stream, A);                              \
+    }                                                                                                    \
     launched = true;                                                                                     \
   }
     STW_RR(1) STW_RR(2) STW_RR(3) STW_RR(5) STW_RR(8) STW_RR(16)
