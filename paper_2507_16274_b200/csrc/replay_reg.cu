@@ -141,6 +141,12 @@ __global__ void k_reg_ops(RegArgs A) {
 // {0, 0, kNoSeg} (length 0, no segment), a pool row {kRFull, kRFull}.
 constexpr uint32_t kNoSeg = kRFull;
 
+// this lane is the lowest set bit of m (lanemask compare: no variable-latency ffs on the chain)
+__device__ __forceinline__ bool lowest_lane(unsigned m) {
+  const unsigned eq = 1u << (threadIdx.x & 31);
+  return (m & (eq | (eq - 1u))) == eq;
+}
+
 // first empty row of the first lane that has one; false if the state is full
 template <int R, bool CACHE>
 __device__ __forceinline__ bool reg_insert(uint32_t (&lo)[R], uint32_t (&hi)[R], uint32_t (&sg)[R], uint32_t a,
@@ -150,7 +156,7 @@ __device__ __forceinline__ bool reg_insert(uint32_t (&lo)[R], uint32_t (&hi)[R],
   for (int r = 0; r < R; r++) has |= CACHE ? sg[r] == kNoSeg : hi[r] == kRFull;
   const unsigned m = __ballot_sync(kRFull, has);
   if (!m) return false;
-  if ((int)(threadIdx.x & 31) == __ffs(m) - 1) {
+  if (lowest_lane(m)) {
     bool done = false;
 #pragma unroll
     for (int r = 0; r < R; r++) {
@@ -169,7 +175,7 @@ __device__ __forceinline__ bool reg_insert(uint32_t (&lo)[R], uint32_t (&hi)[R],
 template <int R, bool CACHE>
 __device__ __forceinline__ void reg_put(uint32_t (&lo)[R], uint32_t (&hi)[R], uint32_t (&sg)[R], unsigned me,
                                         uint32_t a, uint32_t b, uint32_t s) {
-  if ((int)(threadIdx.x & 31) == __ffs(me) - 1) {
+  if (lowest_lane(me)) {
     bool done = false;
 #pragma unroll
     for (int r = 0; r < R; r++) {
