@@ -58,11 +58,20 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
   const int C = o->n_cand;
   const int64_t maxU = maxT * C;
   const stw_plan_out &want = out[0];
-  cudaStream_t cs;
+  // uploads on one copy stream, downloads on another: the two DMA directions
+  // run at the same time
+  cudaStream_t cs, ds;
   STW_CUDA(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  STW_CUDA(ctx, cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
   if (!ctx.ok()) return ctx.rc;
   Ctx cctx = ctx;  // copy-stream context (shares the error buffer)
   cctx.stream = cs;
+  Ctx dctx = ctx;
+  dctx.stream = ds;
+  // upload batch k+1 when batch k starts (STW_PIPE_EARLY) or at its phase D
+  // (default: measured faster -- the big upload then does not contend with
+  // batch k's host round trips over the link)
+  const bool early = getenv("STW_PIPE_EARLY") != nullptr;
   {
     Arena ar(&ctx);
     Slot sl[2];
@@ -100,9 +109,11 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
     cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
     STW_CUDA(ctx, cudaEventRecord(ready, ctx.stream));
     STW_CUDA(ctx, cudaStreamWaitEvent(cs, ready, 0));
+    STW_CUDA(ctx, cudaStreamWaitEvent(ds, ready, 0));
     auto stage = [&](int k) {
       Slot &s = sl[k & 1];
       const stw_batch &b = in[k];
+      if (k >= 2) STW_CUDA(cctx, cudaStreamWaitEvent(cs, s.planned, 0));  // batch k-2 has read its inputs
       const int64_t N = b.n_events, T = b.n_traces;
       h2d(cctx, s.ev_off, b.ev_off, T + 1, cs);
       h2d(cctx, s.id, b.id, N, cs);
@@ -118,23 +129,23 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
     };
     auto download = [&](int k) {  // batch k's results, once it is planned
       Slot &s = sl[k & 1];
-      STW_CUDA(cctx, cudaStreamWaitEvent(cs, s.planned, 0));
+      STW_CUDA(dctx, cudaStreamWaitEvent(ds, s.planned, 0));
       const int64_t N = in[k].n_events, T = in[k].n_traces, U = T * C;
       const stw_plan_out &h = out[k];
-      d2h(cctx, h.rc, s.dout.rc, U, cs);
-      d2h(cctx, h.err_ids, s.dout.err_ids, 2 * U, cs);
-      d2h(cctx, h.stats, s.dout.stats, U * STW_NSTATS, cs);
-      d2h(cctx, h.addr, s.dout.addr, C * N, cs);
-      d2h(cctx, h.layer_of, s.dout.layer_of, C * N, cs);
-      d2h(cctx, h.layer_base, s.dout.layer_base, C * N, cs);
-      d2h(cctx, h.layer_size, s.dout.layer_size, C * N, cs);
-      d2h(cctx, h.fus_tmp, s.dout.fus_tmp, C * N, cs);
-      d2h(cctx, h.fus_avg, s.dout.fus_avg, C * N, cs);
-      d2h(cctx, h.order, s.dout.order, N, cs);
-      d2h(cctx, h.best_cand, s.dout.best_cand, T, cs);
-      d2h(cctx, h.addr_best, s.dout.addr_best, N, cs);
-      d2h(cctx, h.best_pool, s.dout.best_pool, T, cs);
-      STW_CUDA(cctx, cudaEventRecord(s.d2h, cs));
+      d2h(dctx, h.rc, s.dout.rc, U, ds);
+      d2h(dctx, h.err_ids, s.dout.err_ids, 2 * U, ds);
+      d2h(dctx, h.stats, s.dout.stats, U * STW_NSTATS, ds);
+      d2h(dctx, h.addr, s.dout.addr, C * N, ds);
+      d2h(dctx, h.layer_of, s.dout.layer_of, C * N, ds);
+      d2h(dctx, h.layer_base, s.dout.layer_base, C * N, ds);
+      d2h(dctx, h.layer_size, s.dout.layer_size, C * N, ds);
+      d2h(dctx, h.fus_tmp, s.dout.fus_tmp, C * N, ds);
+      d2h(dctx, h.fus_avg, s.dout.fus_avg, C * N, ds);
+      d2h(dctx, h.order, s.dout.order, N, ds);
+      d2h(dctx, h.best_cand, s.dout.best_cand, T, ds);
+      d2h(dctx, h.addr_best, s.dout.addr_best, N, ds);
+      d2h(dctx, h.best_pool, s.dout.best_pool, T, ds);
+      STW_CUDA(dctx, cudaEventRecord(s.d2h, ds));
     };
     // Batch k+1's upload and batch k-1's download are issued from inside batch
     // k's planning once its host round trips are done (at the phase D launch):
@@ -171,7 +182,12 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
       db.horizon = s.horizon;
       db.n_sched = s.n_sched;
       Hook hk{k, n, &stage, &download, false};
-      plan_batch(ctx, &db, o, &s.dout, &in[k], &Hook::run, &hk);
+      if (early) {  // both transfers start with batch k's planning
+        Hook::run(&hk);
+        plan_batch(ctx, &db, o, &s.dout, &in[k], nullptr, nullptr);
+      } else {
+        plan_batch(ctx, &db, o, &s.dout, &in[k], &Hook::run, &hk);
+      }
       if (!ctx.ok()) break;
       if (!hk.ran) Hook::run(&hk);  // a batch that returned before phase E (no traces)
       STW_CUDA(ctx, cudaEventRecord(s.planned, ctx.stream));
@@ -180,8 +196,11 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
     if (ctx.ok() && cctx.ok())
       for (int k = done; k < n; k++) download(k);
     STW_CUDA(cctx, cudaStreamSynchronize(cs));
-    // the arena frees on the compute stream: order it after the copy stream's last use
+    STW_CUDA(dctx, cudaStreamSynchronize(ds));
+    // the arena frees on the compute stream: order it after the copy streams' last use
     STW_CUDA(ctx, cudaEventRecord(ready, cs));
+    STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, ready, 0));
+    STW_CUDA(ctx, cudaEventRecord(ready, ds));
     STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, ready, 0));
     for (Slot &s : sl) {
       cudaEventDestroy(s.h2d);
@@ -191,7 +210,9 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
     cudaEventDestroy(ready);
   }
   if (!cctx.ok() && ctx.ok()) ctx.rc = cctx.rc;
+  if (!dctx.ok() && ctx.ok()) ctx.rc = dctx.rc;
   cudaStreamDestroy(cs);
+  cudaStreamDestroy(ds);
   return ctx.rc;
 }
 
