@@ -51,6 +51,14 @@ typedef struct {
   const uint8_t *dyn;
   const int32_t *horizon;
   const int32_t *n_sched;
+  /* optional compact host columns, read by stw_plan_batches only (which then
+   * uploads 8 bytes less per event): id[i] = id_base + id32[i], size[i] =
+   * (int64_t)size32[i] << size_shift. NULL: upload id / size as they are. */
+  const int32_t *id32;
+  const uint32_t *size32;
+  int64_t id_base;
+  int32_t size_shift;
+  int32_t reserved;
 } stw_batch;
 
 /* ---- K1: peak live bytes (model.py:261-281) ----------------------------

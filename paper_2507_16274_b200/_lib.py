@@ -32,6 +32,8 @@ class Batch(C.Structure):
         ("ev_off", C.c_void_p), ("id", C.c_void_p), ("size", C.c_void_p), ("t_s", C.c_void_p),
         ("t_e", C.c_void_p), ("ps", C.c_void_p), ("pe", C.c_void_p), ("dyn", C.c_void_p),
         ("horizon", C.c_void_p), ("n_sched", C.c_void_p),
+        ("id32", C.c_void_p), ("size32", C.c_void_p), ("id_base", C.c_int64), ("size_shift", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -55,11 +55,50 @@ class HostBatch:
     def nbytes(self) -> int:
         return sum(a.nbytes for a in self.cols.values()) + self.ev_off.nbytes + self.horizon.nbytes + self.n_sched.nbytes
 
+    def pack(self) -> bool:
+        """Compact copies of id (int32 offsets from the smallest id) and size
+        (uint32 multiples of the largest power of two dividing every size) for
+        stw_plan_batches, which then uploads 25 instead of 33 bytes per event.
+        False (nothing changes) when the values do not fit."""
+        self._packed = None
+        if self.N == 0:
+            return False
+        ids, sizes = self.cols["id"], self.cols["size"]
+        base = int(ids.min())
+        if int(ids.max()) - base >= (1 << 31) or int(sizes.min()) <= 0:
+            return False
+        o = int(np.bitwise_or.reduce(sizes))
+        shift = (o & -o).bit_length() - 1
+        s32 = sizes >> shift
+        if int(s32.max()) >= (1 << 32):
+            return False
+        id32 = (ids - base).astype(np.int32)
+        s32 = s32.astype(np.uint32)
+        if getattr(self, "_pins", None) is not None:
+            import torch
+
+            id32 = torch.from_numpy(id32).pin_memory().numpy()
+            s32 = torch.from_numpy(s32).pin_memory().numpy()
+        self._packed = (id32, s32, base, shift)
+        return True
+
+    @property
+    def upload_nbytes(self) -> int:
+        """Bytes stw_plan_batches moves host -> device per batch."""
+        p = getattr(self, "_packed", None)
+        if p is None:
+            return self.nbytes
+        return self.nbytes - self.cols["id"].nbytes - self.cols["size"].nbytes + p[0].nbytes + p[1].nbytes
+
     def struct(self) -> _lib.Batch:
         c = self.cols
-        return _lib.Batch(self.T, 0, self.N, _lib.ptr(self.ev_off), _lib.ptr(c["id"]), _lib.ptr(c["size"]),
-                          _lib.ptr(c["t_s"]), _lib.ptr(c["t_e"]), _lib.ptr(c["ps"]), _lib.ptr(c["pe"]),
-                          _lib.ptr(c["dyn"]), _lib.ptr(self.horizon), _lib.ptr(self.n_sched))
+        b = _lib.Batch(self.T, 0, self.N, _lib.ptr(self.ev_off), _lib.ptr(c["id"]), _lib.ptr(c["size"]),
+                       _lib.ptr(c["t_s"]), _lib.ptr(c["t_e"]), _lib.ptr(c["ps"]), _lib.ptr(c["pe"]),
+                       _lib.ptr(c["dyn"]), _lib.ptr(self.horizon), _lib.ptr(self.n_sched))
+        p = getattr(self, "_packed", None)
+        if p is not None:
+            b.id32, b.size32, b.id_base, b.size_shift = _lib.ptr(p[0]), _lib.ptr(p[1]), p[2], p[3]
+        return b
 
     def to_device(self, device="cuda"):
         return DeviceBatch(self, device)

@@ -126,6 +126,24 @@ def test_plan_batches_pipeline_matches_single_calls():
         assert np.array_equal(got.fus_tmp.view(np.int64), want.fus_tmp.view(np.int64))
 
 
+def test_plan_batches_compact_upload():
+    """Host batches with compact columns (HostBatch.pack: int32 id offsets,
+    sizes in power-of-two units, widened on the device) plan exactly like the
+    full-width upload; mixed packed / unpacked batches in one call."""
+    from paper_2507_16274_b200.batching import HostBatch
+
+    groups = [[tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(a, b)] for a, b in
+              ((0, 24), (24, 31), (50, 90))]
+    hbs = [HostBatch(g, pinned=True) for g in groups]
+    assert hbs[0].pack() and hbs[2].pack()
+    assert hbs[0].upload_nbytes < hbs[0].nbytes
+    many = api.plan_batches(hbs, tracegen.C4_CANDIDATES, select_best=True)
+    for g, got in zip(groups, many):
+        want = api.plan_batch(g, tracegen.C4_CANDIDATES, select_best=True)
+        for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
+            assert np.array_equal(getattr(got, f), getattr(want, f)), f
+
+
 def test_plan_invariant_to_event_listing_order():
     """Shuffled event listings take the sorting path of the canonical ranks (the
     recorded order takes the identity fast path); plans must match by id."""
