@@ -486,6 +486,14 @@ def config_sweep(names, reps: int = 3, cpu: bool = True):
         g["simulate"], (rep, _log) = best(lambda: M.simulate(tr, bundle))
         g["baseline"], base = best(lambda: M.run_baseline(tr))
         g["peak"], peak = best(lambda: M.peak_live_bytes(ta))
+        # the same plan from a trace of event objects, as the reference's
+        # parse_trace / synth_trace hand it over: the tensorising walk is timed too
+        from paper_2507_16274_b200.domain import Trace as _ObjTrace
+
+        objs = _ObjTrace(tuple(tr.events), tr.phase_schedule, tr.layer_schedule)
+        t_obj, plan_obj = best(lambda: M.synthesize_static_plan(objs), 1)
+        assert plan_obj.pool_size == plan.pool_size
+        del objs, plan_obj
         n = len(ta)
         row = {"events": n, "pool_size": int(plan.pool_size),
                "planned_allocs_per_s": int((ta.dyn == 0).sum()) / g["plan"],
@@ -493,7 +501,8 @@ def config_sweep(names, reps: int = 3, cpu: bool = True):
                "fragmentation": rep.fragmentation, "efficiency": rep.efficiency,
                "baseline_fragmentation": base.fragmentation,
                "fallbacks": int(rep.fallback_count), "reuse_hits": int(rep.reuse_hits),
-               "gpu_ms": {k: 1e3 * v for k, v in g.items()}}
+               "gpu_ms": {k: 1e3 * v for k, v in g.items()},
+               "plan_from_event_objects_ms": 1e3 * t_obj}
         if cpu:
             keys, kidx = ta.dynamic_keys()
             t_lo = np.asarray([rmap.entries[k].t_lo for k in keys], np.int64)

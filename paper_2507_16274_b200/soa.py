@@ -134,16 +134,8 @@ def from_events(events, phase_schedule=(), layer_schedule=()) -> TraceArrays:
     lindex = {}
     for i, n in enumerate(names):
         lindex.setdefault(n, i)
-    n = len(events)
-    ids = np.empty(n, dtype=object)
-    sizes = np.empty(n, dtype=object)
-    ts = np.empty(n, dtype=np.int64)
-    te = np.empty(n, dtype=np.int64)
-    ps = np.empty(n, dtype=np.int32)
-    pe = np.empty(n, dtype=np.int32)
-    dyn = np.zeros(n, dtype=np.uint8)
-    ls = np.full(n, -1, dtype=np.int32)
-    le = np.full(n, -1, dtype=np.int32)
+    evs = events if isinstance(events, (list, tuple)) else list(events)
+    n = len(evs)
 
     def pidx(p):
         i = index.get(p)
@@ -159,20 +151,34 @@ def from_events(events, phase_schedule=(), layer_schedule=()) -> TraceArrays:
             names.append(name)
         return i
 
-    for k, ev in enumerate(events):
-        ids[k] = ev.id
-        sizes[k] = ev.size
-        ts[k] = ev.t_s
-        te[k] = ev.t_e
-        ps[k] = pidx(ev.p_s)
-        pe[k] = pidx(ev.p_e)
-        if ev.dynamic:
-            dyn[k] = 1
-            ls[k] = lidx(ev.l_s)
-            le[k] = lidx(ev.l_e)
+    # one comprehension per attribute (no per-element numpy stores); phase
+    # objects are looked up by identity first (a trace reuses a few hundred
+    # PhaseId objects), then by value
+    by_obj = {}
+
+    def pix(p):
+        i = by_obj.get(id(p))
+        if i is None:
+            i = by_obj[id(p)] = (pidx(p), p)  # (keeps p alive: ids stay unique)
+        return i[0]
+
+    ids = [e.id for e in evs]
+    sizes = [e.size for e in evs]
+    ts = np.fromiter((e.t_s for e in evs), dtype=np.int64, count=n)
+    te = np.fromiter((e.t_e for e in evs), dtype=np.int64, count=n)
+    # p_s then p_e of each event in turn: phases missing from the schedule get
+    # their indices in the reference's order of first appearance
+    pp = np.fromiter((pix(x) for e in evs for x in (e.p_s, e.p_e)), dtype=np.int32, count=2 * n)
+    ps, pe = np.ascontiguousarray(pp[0::2]), np.ascontiguousarray(pp[1::2])
+    dyn = np.fromiter((1 if e.dynamic else 0 for e in evs), dtype=np.uint8, count=n)
+    ls = np.full(n, -1, dtype=np.int32)
+    le = np.full(n, -1, dtype=np.int32)
+    for k in np.flatnonzero(dyn).tolist():
+        ls[k] = lidx(evs[k].l_s)
+        le[k] = lidx(evs[k].l_e)
     try:
-        id_arr = ids.astype(np.int64)
-        size_arr = sizes.astype(np.int64)
+        id_arr = np.asarray(ids, dtype=np.int64)
+        size_arr = np.asarray(sizes, dtype=np.int64)
     except OverflowError:
         raise TraceError("event id or size outside the supported int64 range") from None
     nl = len(layer_schedule)
