@@ -51,7 +51,7 @@ typedef struct {
   const uint8_t *dyn;
   const int32_t *horizon;
   const int32_t *n_sched;
-  /* optional compact host columns, read by stw_plan_batches only (which then
+  /* optional compact host columns, read by stw_plan_batch(es) when the batch is on the host (which then
    * uploads 8 bytes less per event): id[i] = id_base + id32[i], size[i] =
    * (int64_t)size32[i] << size_shift. NULL: upload id / size as they are. */
   const int32_t *id32;

@@ -58,7 +58,7 @@ class HostBatch:
     def pack(self) -> bool:
         """Compact copies of id (int32 offsets from the smallest id) and size
         (uint32 multiples of the largest power of two dividing every size) for
-        stw_plan_batches, which then uploads 25 instead of 33 bytes per event.
+        stw_plan_batch(es), which then uploads 25 instead of 33 bytes per event.
         False (nothing changes) when the values do not fit."""
         self._packed = None
         if self.N == 0:
@@ -84,7 +84,7 @@ class HostBatch:
 
     @property
     def upload_nbytes(self) -> int:
-        """Bytes stw_plan_batches moves host -> device per batch."""
+        """Bytes stw_plan_batch(es) move host -> device per batch."""
         p = getattr(self, "_packed", None)
         if p is None:
             return self.nbytes

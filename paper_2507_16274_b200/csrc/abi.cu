@@ -9,7 +9,8 @@ using namespace stw;
   ctx.stream = (cudaStream_t)(stream_ptr);  \
   ctx.err = (err);                          \
   ctx.errlen = (errlen);                    \
-  if ((err) && (errlen)) (err)[0] = 0;
+  if ((err) && (errlen)) (err)[0] = 0;      \
+  bind_stream_device(ctx.stream);
 
 static int finish(Ctx &ctx) {
   cudaError_t e = cudaStreamSynchronize(ctx.stream);

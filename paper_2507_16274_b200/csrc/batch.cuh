@@ -42,6 +42,10 @@ static void fetch_small(Ctx &ctx, std::vector<T> &dst, const T *src, int64_t n, 
   }
 }
 
+// a compact upload widened on the device: id = base + id32, size = size32 << shift (pipeline.cu)
+__global__ void k_widen(const int32_t *__restrict__ id32, const uint32_t *__restrict__ s32, int64_t base, int shift,
+                        int64_t n, int64_t *__restrict__ id, int64_t *__restrict__ size);
+
 // `mirror` (optional): the same batch in host memory, read for the small
 // per-trace arrays instead of a device round trip (stw_plan_batches stages its
 // batches itself and keeps the host originals).
@@ -78,8 +82,20 @@ inline bool stage_batch(Ctx &ctx, Arena &ar, const stw_batch *b, DevBatch *d, co
   }
   int64_t *by = &d->h2d_bytes;
   d->ev_off = stage(ctx, ar, b->ev_off, (int64_t)d->T + 1, dev, by);
-  d->id = stage(ctx, ar, b->id, d->N, dev, by);
-  d->size = stage(ctx, ar, b->size, d->N, dev, by);
+  if (!dev && b->id32 && b->size32) {  // compact host columns: 8 bytes less per event, widened on the device
+    const int32_t *i32 = stage(ctx, ar, b->id32, d->N, dev, by);
+    const uint32_t *s32 = stage(ctx, ar, b->size32, d->N, dev, by);
+    int64_t *id = ar.take<int64_t>(d->N + 1), *size = ar.take<int64_t>(d->N + 1);
+    if (ctx.ok() && d->N > 0) {
+      STW_KL(k_widen, grid_for(d->N, 256), 256, ctx.stream, i32, s32, b->id_base, b->size_shift, d->N, id, size);
+      STW_LAUNCHED(ctx);
+    }
+    d->id = id;
+    d->size = size;
+  } else {
+    d->id = stage(ctx, ar, b->id, d->N, dev, by);
+    d->size = stage(ctx, ar, b->size, d->N, dev, by);
+  }
   d->t_s = stage(ctx, ar, b->t_s, d->N, dev, by);
   d->t_e = stage(ctx, ar, b->t_e, d->N, dev, by);
   d->ps = stage(ctx, ar, b->ps, d->N, dev, by);

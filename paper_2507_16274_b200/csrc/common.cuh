@@ -43,6 +43,20 @@ struct Ctx {
 
 #define STW_LAUNCHED(ctx) STW_CUDA(ctx, cudaGetLastError())
 
+// libstw links its own (static) CUDA runtime: an entry point given a stream
+// binds that runtime to the stream's device, so a caller on device k (one
+// process per GPU, torch.cuda.set_device(k)) is served on device k. Without a
+// stream the runtime uses the thread's current context, as any CUDA library.
+inline void bind_stream_device(cudaStream_t s) {
+  if (!s || s == cudaStreamLegacy || s == cudaStreamPerThread) return;
+  int dev = -1, cur = -1;
+  if (cudaStreamGetDevice(s, &dev) != cudaSuccess) {
+    cudaGetLastError();  // (not a stream of this process: the launch reports it)
+    return;
+  }
+  if (cudaGetDevice(&cur) == cudaSuccess && cur != dev) cudaSetDevice(dev);
+}
+
 // Every kernel launch goes through STW_KL: it counts launches and, when the
 // opt-in profiler is on (stw_prof_enable), brackets the launch with CUDA
 // events recorded on the launching stream.

@@ -27,6 +27,7 @@ void d2h(Ctx &ctx, T *dst, const T *src, int64_t n, cudaStream_t s) {
 }
 
 // a compact upload widened on the device: id = base + id32, size = size32 << shift
+}  // namespace
 __global__ void k_widen(const int32_t *__restrict__ id32, const uint32_t *__restrict__ s32, int64_t base, int shift,
                         int64_t n, int64_t *__restrict__ id, int64_t *__restrict__ size) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -34,6 +35,7 @@ __global__ void k_widen(const int32_t *__restrict__ id32, const uint32_t *__rest
     size[i] = (int64_t)s32[i] << shift;
   }
 }
+namespace {
 
 struct Slot {
   // device copies of one batch

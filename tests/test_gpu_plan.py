@@ -142,6 +142,10 @@ def test_plan_batches_compact_upload():
         want = api.plan_batch(g, tracegen.C4_CANDIDATES, select_best=True)
         for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
             assert np.array_equal(getattr(got, f), getattr(want, f)), f
+    one = api.plan_batch(hbs[2], tracegen.C4_CANDIDATES, select_best=True)  # the single call stages compact too
+    want = api.plan_batch(groups[2], tracegen.C4_CANDIDATES, select_best=True)
+    for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
+        assert np.array_equal(getattr(one, f), getattr(want, f)), f
 
 
 def test_plan_invariant_to_event_listing_order():
