@@ -517,30 +517,42 @@ struct Groups {
   int64_t *height;
 };
 
+struct TraceCounts {
+  int *n_static, *n_pers, *n_groups, *n_plans, *n_res;
+  int64_t *pers_size;
+};
+
 // Phase B fused (traces of <= 4096 events): one CTA per trace sorts the
 // trace's events by (class, p_s, p_e, r) in shared memory (k_key_group + the
-// segmented sort), then marks group heads and makes the trace-local group ids
-// (inclusive count of heads) and size prefix sums S (exclusive; only
-// differences inside a group are used) by chunked block scans -- k_group_heads
-// and the two global scans. Group ids become global in k_group_table (+ the
-// trace's offset from the group counts written here).
+// segmented sort) and builds the whole group table from the sorted order --
+// the work of k_group_heads, the two global scans, k_group_table, k_group_rel
+// and k_trace_counts -- without a round trip through HBM. Group ids are sparse:
+// trace t's groups take [ev_off[t], ev_off[t] + groups of t) (a trace has no
+// more groups than events), so no cross-trace offset is needed; the gaps read
+// as non-plan groups (is_plan is zeroed). pidx gets each plan group's rank
+// among the trace's plan groups (the global plan index is pl_off[t] + that).
 template <int IPT>
 __global__ void __launch_bounds__(256, IPT == 8 ? 4 : 1) k_groups_fused(Ev e, const int64_t *__restrict__ ev_off,
                                                       const int32_t *__restrict__ r, int pb, int qb, int bit0,
-                                                      uint32_t *__restrict__ gperm, uint32_t *__restrict__ head,
-                                                      uint32_t *__restrict__ lgid, int64_t *__restrict__ szs,
-                                                      int64_t *__restrict__ S, uint32_t *__restrict__ ngroups) {
+                                                      uint32_t *__restrict__ gperm, Groups g,
+                                                      int64_t *__restrict__ rel, int32_t *__restrict__ gof,
+                                                      TraceCounts tc, uint32_t *__restrict__ is_plan,
+                                                      uint32_t *__restrict__ pidx) {
   constexpr int CAP = 256 * IPT;
   extern __shared__ __align__(16) unsigned char sgs[];
   uint64_t *kA = (uint64_t *)sgs;
   uint32_t *vA = (uint32_t *)(kA + CAP);
   uint32_t *wh = vA + CAP;
+  long long *gS = (long long *)(wh + 8 * 256);  // [CAP + 1] group start offsets (prefix of sizes)
+  uint8_t *gc = (uint8_t *)(gS + CAP + 1);      // [CAP] class | plan << 2
   __shared__ uint32_t sh[33];
   __shared__ long long shl[33];
+  __shared__ int cnt[4];  // static events, persistent events, residual events, class-1 groups
   const int t = blockIdx.x, tid = threadIdx.x;
   const int64_t g0 = ev_off[t];
   const int n = (int)(ev_off[t + 1] - g0);
   const int hz = e.horizon[t];
+  if (tid < 4) cnt[tid] = 0;
   for (int j = tid; j < n; j += blockDim.x) {
     const int64_t i = g0 + j;
     const int c = ev_class(e.dyn[i], e.te[i], hz);
@@ -550,34 +562,89 @@ __global__ void __launch_bounds__(256, IPT == 8 ? 4 : 1) k_groups_fused(Ev e, co
   }
   __syncthreads();
   cta_radix<IPT>(kA, vA, wh, sh, n, bit0, qb + 2 + 2 * pb);
+  const uint64_t pmask = (1ull << pb) - 1;
   // chunked scans: thread tid owns sorted positions [c0, c1)
   const int per = (n + 255) >> 8, c0 = min(n, tid * per), c1 = min(n, c0 + per);
-  uint32_t hm = 0, nh = 0;  // head bits of the chunk (per <= 16)
+  uint32_t hm = 0, nh = 0, np = 0;  // head bits of the chunk (per <= 16), heads, plan heads
   long long ssum = 0;
   for (int k = c0; k < c1; k++) {
-    const bool h = k == 0 || (kA[k] >> qb) != (kA[k - 1] >> qb);
+    const uint64_t key = kA[k] >> qb;
+    const bool h = k == 0 || key != (kA[k - 1] >> qb);
     hm |= (h ? 1u : 0u) << (k - c0);
     nh += h;
+    np += h && (key >> (2 * pb)) == 1 && ((key >> pb) & pmask) != (key & pmask);
     const int64_t i = g0 + vA[k];
-    const long long sz = e.size[i];
-    szs[g0 + k] = sz;
     gperm[g0 + k] = (uint32_t)i;
-    ssum += sz;
+    ssum += e.size[i];
   }
   uint32_t htot;
   const uint32_t hex = block_excl_sum<uint32_t>(nh, sh, &htot);
-  const long long sex = block_excl_sum<long long>(ssum, shl, nullptr);
-  uint32_t gcount = hex;
+  uint32_t ptot;
+  const uint32_t pex = block_excl_sum<uint32_t>(np, sh, &ptot);
+  long long stot;
+  const long long sex = block_excl_sum<long long>(ssum, shl, &stot);
+  // heads: the group table; every position: its offset (kept in kA)
+  uint32_t gcount = hex, pcount = pex;
   long long run = sex;
   for (int k = c0; k < c1; k++) {
-    const bool h = (hm >> (k - c0)) & 1u;
-    gcount += h;
-    head[g0 + k] = h;
-    lgid[g0 + k] = gcount;
-    S[g0 + k] = run;
-    run += szs[g0 + k];
+    const uint64_t key = kA[k] >> qb;
+    const long long sz = e.size[g0 + vA[k]];
+    if ((hm >> (k - c0)) & 1u) {
+      const int lg = (int)gcount++;
+      const int c = (int)(key >> (2 * pb));
+      const int a = (int)((key >> pb) & pmask), b = (int)(key & pmask);
+      const bool plan = c == 1 && a != b;
+      const int64_t gi = g0 + lg;
+      g.start[gi] = g0 + k;
+      g.tr[gi] = t;
+      g.cls[gi] = c;
+      g.ps[gi] = a;
+      g.pe[gi] = b;
+      is_plan[gi] = plan;
+      if (plan) pidx[gi] = pcount++;
+      gS[lg] = run;
+      gc[lg] = (uint8_t)(c | (plan ? 4 : 0));
+    }
+    kA[k] = (uint64_t)run;
+    run += sz;
   }
-  if (tid == 0) ngroups[t] = htot;
+  if (tid == 0) gS[htot] = stot;
+  __syncthreads();
+  // every event: its offset inside its group, its group; the event counts
+  gcount = hex;
+  int nst = 0, npe = 0, nre = 0;
+  for (int k = c0; k < c1; k++) {
+    gcount += (hm >> (k - c0)) & 1u;
+    const int lg = (int)gcount - 1;
+    const int64_t i = g0 + vA[k];
+    rel[i] = (long long)kA[k] - gS[lg];
+    gof[i] = (int32_t)(g0 + lg);
+    const int m = gc[lg];
+    nst += (m & 3) <= 1;
+    npe += (m & 3) == 0;
+    nre += m == 1;
+  }
+  // every group: its height; the group counts
+  int ngr = 0;
+  for (int lg = tid; lg < (int)htot; lg += blockDim.x) {
+    const long long h = gS[lg + 1] - gS[lg];
+    g.height[g0 + lg] = h;
+    const int m = gc[lg];
+    if ((m & 3) == 0) tc.pers_size[t] = h;
+    ngr += (m & 3) == 1;
+  }
+  if (nst) atomicAdd(&cnt[0], nst);
+  if (npe) atomicAdd(&cnt[1], npe);
+  if (nre) atomicAdd(&cnt[2], nre);
+  if (ngr) atomicAdd(&cnt[3], ngr);
+  __syncthreads();
+  if (tid == 0) {
+    tc.n_static[t] = cnt[0];
+    tc.n_pers[t] = cnt[1];
+    tc.n_res[t] = cnt[2];
+    tc.n_groups[t] = cnt[3];
+    tc.n_plans[t] = (int)ptot;
+  }
 }
 
 // goff (optional): per-trace group offsets when gid holds trace-local ids
@@ -615,11 +682,6 @@ __global__ void k_group_rel(const uint32_t *__restrict__ gperm, const uint32_t *
   }
 }
 
-struct TraceCounts {
-  int *n_static, *n_pers, *n_groups, *n_plans, *n_res;
-  int64_t *pers_size;
-};
-
 __global__ void k_trace_counts(Groups g, const uint32_t *__restrict__ Gp, int64_t n, TraceCounts tc,
                                uint32_t *__restrict__ is_plan) {
   const int G = (int)*Gp;  // launched over an upper bound (n); groups past G idle
@@ -656,13 +718,15 @@ struct Plans {
   uint8_t *alive;
 };
 
-__global__ void k_plan_init(Groups g, const uint32_t *__restrict__ Gp, const uint32_t *__restrict__ is_plan,
-                            const uint32_t *__restrict__ pidx_excl, const uint32_t *__restrict__ gperm, Ev e,
-                            Plans p) {
-  const int G = (int)*Gp;
-  GRID_STRIDE(gi, (int64_t)G) {
+// pl_off: pidx holds trace-local plan ranks (k_groups_fused), else global ones;
+// Gp: the group count (nullptr: sparse ids below gcap)
+__global__ void k_plan_init(Groups g, const uint32_t *__restrict__ Gp, int64_t gcap, const uint32_t *__restrict__ is_plan,
+                            const uint32_t *__restrict__ pidx, const int64_t *__restrict__ pl_off,
+                            const uint32_t *__restrict__ gperm, Ev e, Plans p) {
+  const int64_t G = Gp ? (int64_t)*Gp : gcap;
+  GRID_STRIDE(gi, G) {
     if (!is_plan[gi]) continue;
-    uint32_t k = pidx_excl[gi];
+    const int64_t k = pidx[gi] + (pl_off ? pl_off[g.tr[gi]] : 0);
     p.grp[k] = (int)gi;
     p.tr[k] = g.tr[gi];
     p.h[k] = g.height[gi];
@@ -678,8 +742,9 @@ __global__ void k_plan_init(Groups g, const uint32_t *__restrict__ Gp, const uin
 }
 
 __global__ void k_plan_members(const uint32_t *__restrict__ gperm, const int32_t *__restrict__ gof,
-                               const uint32_t *__restrict__ is_plan, const uint32_t *__restrict__ pidx_excl, Ev e,
-                               int64_t n, Plans p, int32_t *__restrict__ pid) {
+                               const uint32_t *__restrict__ is_plan, const uint32_t *__restrict__ pidx,
+                               const int64_t *__restrict__ pl_off, Ev e, int64_t n, Plans p,
+                               int32_t *__restrict__ pid) {
   GRID_STRIDE(k, n) {
     uint32_t i = gperm[k];
     int gi = gof[i];
@@ -687,7 +752,7 @@ __global__ void k_plan_members(const uint32_t *__restrict__ gperm, const int32_t
       pid[i] = -1;
       continue;
     }
-    uint32_t pk = pidx_excl[gi];
+    const int64_t pk = pidx[gi] + (pl_off ? pl_off[e.tr[i]] : 0);
     pid[i] = (int)pk;
     atomicMax(p.te + pk, e.te[i]);
     atomicMin(p.minq + pk, e.q[i]);
@@ -2590,19 +2655,35 @@ struct EmitArgs {
   const int64_t *io, *uo;
   const int32_t *ilayer;
   const int64_t *lbase;
-  int64_t *addr;    // [C * N]
-  int32_t *layer;   // [C * N]
+  const uint32_t *rperm;  // events in sweep order (trace, t_s, id)
+  const uint32_t *sflag, *spos;  // per sweep position: static event, its rectangle slot
+  int64_t NS;
+  int64_t *addr;    // [C * N] event order, or nullptr (not requested)
+  int32_t *layer;   // [C * N] event order, or nullptr
+  int32_t *rts, *rte;  // [NS] sweep-order rectangles of the static events (validate_plan)
+  int64_t *rsz, *raddr;  // [NS], [C * NS]
 };
 
-// thread per event, every candidate in turn: the event's columns are read once
-// and the candidates' dependent lookups (item -> layer -> base) overlap
+// emission (planner.py:446-455) straight into the self-check's sweep order:
+// thread per sweep position, every candidate in turn (the event's columns are
+// read once and the candidates' dependent lookups item -> layer -> base
+// overlap). The static events' rectangles are written in sweep order, the
+// event-order address / layer tables only when the caller asked for them.
 __global__ void k_emit(EmitArgs A) {
-  GRID_STRIDE(i, A.N) {
+  GRID_STRIDE(k, A.N) {
+    const uint32_t i = A.rperm[k];
     const int t = A.e.tr[i];
     const int cl = ev_class(A.e.dyn[i], A.e.te[i], A.e.horizon[t]);
     const int64_t rel = cl == 2 ? 0 : A.rel[i];
     const int p0 = cl == 1 ? A.pid0[i] : -1;
     const int p1 = cl == 1 && A.pid1 ? A.pid1[i] : -1;
+    const bool st = A.sflag[k] != 0;
+    const int64_t o = st ? (int64_t)A.spos[k] : 0;
+    if (st) {
+      A.rts[o] = A.e.ts[i];
+      A.rte[o] = A.e.te[i];
+      A.rsz[o] = A.e.size[i];
+    }
     for (int c = 0; c < A.C; c++) {
       const int64_t u = (int64_t)t * A.C + c;
       const int v = A.var_of[c];
@@ -2624,8 +2705,9 @@ __global__ void k_emit(EmitArgs A) {
         ly = A.ilayer[A.uo[u] + local];
         ad = A.lbase[A.uo[u] + ly] + fr;
       }
-      A.addr[(int64_t)c * A.N + i] = ad;
-      A.layer[(int64_t)c * A.N + i] = ly;
+      if (st) A.raddr[(int64_t)c * A.NS + o] = ad;
+      if (A.addr) A.addr[(int64_t)c * A.N + i] = ad;
+      if (A.layer) A.layer[(int64_t)c * A.N + i] = ly;
     }
   }
 }
@@ -2636,19 +2718,11 @@ __global__ void k_static_flag(const uint32_t *__restrict__ rperm, const uint8_t 
   GRID_STRIDE(k, n) f[k] = dyn[rperm[k]] ? 0u : 1u;
 }
 
-__global__ void k_rect_fill(const uint32_t *__restrict__ rperm, const uint32_t *__restrict__ f,
-                            const uint32_t *__restrict__ pos, Ev e, int64_t n, int C, const int64_t *__restrict__ addr,
-                            int32_t *__restrict__ rs_ev, int32_t *__restrict__ rts, int32_t *__restrict__ rte,
-                            int64_t *__restrict__ rsz, int64_t *__restrict__ raddr, int64_t nstat) {
+// the event behind each rectangle (only the conflict report needs it)
+__global__ void k_rect_events(const uint32_t *__restrict__ rperm, const uint32_t *__restrict__ f,
+                              const uint32_t *__restrict__ pos, int64_t n, int32_t *__restrict__ rs_ev) {
   GRID_STRIDE(k, n) {
-    if (!f[k]) continue;
-    uint32_t i = rperm[k];
-    uint32_t o = pos[k];
-    rs_ev[o] = (int32_t)i;
-    rts[o] = e.ts[i];
-    rte[o] = e.te[i];
-    rsz[o] = e.size[i];
-    for (int c = 0; c < C; c++) raddr[(int64_t)c * nstat + o] = addr[(int64_t)c * n + i];
+    if (f[k]) rs_ev[pos[k]] = (int32_t)rperm[k];
   }
 }
 
@@ -2725,11 +2799,16 @@ __global__ void k_select_best(const int32_t *__restrict__ rc, const int64_t *__r
   }
 }
 
+// the best candidate's addresses, event order, from the sweep-order rectangles
+// (dynamic events: -1, as emitted)
 __global__ void k_gather_best(const int32_t *__restrict__ tr, const int32_t *__restrict__ best,
-                              const int64_t *__restrict__ addr, int64_t N, int64_t *__restrict__ out) {
-  GRID_STRIDE(i, N) {
-    int b = best[tr[i]];
-    out[i] = b >= 0 ? addr[(int64_t)b * N + i] : -1;
+                              const uint32_t *__restrict__ rperm, const uint32_t *__restrict__ f,
+                              const uint32_t *__restrict__ pos, const int64_t *__restrict__ raddr, int64_t NS,
+                              int64_t N, int64_t *__restrict__ out) {
+  GRID_STRIDE(k, N) {
+    const uint32_t i = rperm[k];
+    const int b = best[tr[i]];
+    out[i] = b >= 0 && f[k] ? raddr[(int64_t)b * NS + pos[k]] : -1;
   }
 }
 
@@ -2817,7 +2896,7 @@ static void sync(Ctx &ctx) { host_sync(ctx); }
 
 template <class T>
 static void out_copy(Ctx &ctx, T *dst, const T *src, int64_t n, bool dst_dev) {
-  if (!dst || n <= 0 || !ctx.ok()) return;
+  if (!dst || dst == src || n <= 0 || !ctx.ok()) return;
   STW_CUDA(ctx, cudaMemcpyAsync(dst, src, n * sizeof(T), dst_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                 ctx.stream));
 }
@@ -2974,47 +3053,11 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   nv.next("B groups");
   // ---- B: phase groups
   Ev e{tr, b.t_s, b.t_e, b.ps, b.pe, q, b.size, b.dyn, b.horizon};
-  uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
-  int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
   int64_t *rel = ar.take<int64_t>(N + 1);
   int32_t *gof = ar.take<int32_t>(N + 1);
-  uint32_t *ngroups = ar.take<uint32_t>(T + 1), *goff = ar.take<uint32_t>(T + 1);
-  if (!ctx.ok()) return ctx.rc;
-  // the group count stays on the device (G <= N): tables are sized by N and
-  // the group kernels read G themselves
-  const uint32_t *d_G = nullptr;
-  const bool fused_groups = T > 0 && b.max_trace_events <= kSegSortMax && qb + 2 + 2 * pb <= 64;
-  if (fused_groups) {
-    const int gbit0 = him[0] == 0 ? qb : 0;  // recorded order: r is the position, already in order
-    if (b.max_trace_events <= 2048) {
-      constexpr int smem = 2048 * 12 + 8 * 256 * 4;
-      STW_KLS(k_groups_fused<8>, (unsigned)T, 256, smem, ctx.stream, e, b.ev_off, r, pb, qb, gbit0, gperm, head,
-              gid, szs, S, ngroups);
-    } else {
-      constexpr int smem = 4096 * 12 + 8 * 256 * 4;
-      STW_CUDA(ctx, cudaFuncSetAttribute(k_groups_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      STW_KLS(k_groups_fused<16>, (unsigned)T, 256, smem, ctx.stream, e, b.ev_off, r, pb, qb, gbit0, gperm, head,
-              gid, szs, S, ngroups);
-    }
-    STW_LAUNCHED(ctx);
-    STW_KL(k_offsets_u32, 1, 1024, ctx.stream, ngroups, T, goff);
-    STW_LAUNCHED(ctx);
-    d_G = goff + T;
-  } else {
-    LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
-    seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events,
-             /*lo_in_order=*/him[0] == 0);
-    LAUNCH(k_group_heads, N, e, gperm, b.ev_off, N, head, szs);
-    device_scan<uint32_t>(ctx, ar, head, gid, N, true);
-    device_scan<int64_t>(ctx, ar, szs, S, N, false);
-    d_G = gid + (N > 0 ? N - 1 : 0);
-  }
-  const int G = (int)N;  // capacity
+  const int G = (int)N;  // capacity (a trace has no more groups than events)
   Groups g{ar.take<int64_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1), ar.take<int32_t>(G + 1),
            ar.take<int32_t>(G + 1), ar.take<int64_t>(G + 1)};
-  if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_group_table, N, e, gperm, head, gid, fused_groups ? goff : nullptr, N, g);
-  LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, N, d_G, rel, gof);
   // per-trace counters and the plan flags in one zeroed block
   const size_t tc_bytes = (size_t)T * (5 * sizeof(int) + sizeof(int64_t)) + (size_t)(G + 1) * sizeof(uint32_t);
   char *tcb = ar.take<char>(tc_bytes + 64);
@@ -3025,8 +3068,40 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   TraceCounts tc{tc_ints, tc_ints + T, tc_ints + 2 * T, tc_ints + 3 * T, tc_ints + 4 * T, tc_pers};
   uint32_t *is_plan = (uint32_t *)(tc_ints + 5 * T);
   STW_CUDA(ctx, cudaMemsetAsync(tcb, 0, tc_bytes, ctx.stream));
-  LAUNCH(k_trace_counts, G, g, d_G, N, tc, is_plan);
-  device_scan<uint32_t>(ctx, ar, is_plan, pidx, G, false);
+  // the group count stays on the device (G <= N): tables are sized by N and
+  // the group kernels read G themselves (fused: sparse ids, no count)
+  const uint32_t *d_G = nullptr;
+  const bool fused_groups = T > 0 && b.max_trace_events <= kSegSortMax && qb + 2 + 2 * pb <= 64;
+  if (fused_groups) {
+    const int gbit0 = him[0] == 0 ? qb : 0;  // recorded order: r is the position, already in order
+    if (b.max_trace_events <= 2048) {
+      constexpr int smem = 2048 * 12 + 8 * 256 * 4 + 2049 * 8 + 2048;
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_groups_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      STW_KLS(k_groups_fused<8>, (unsigned)T, 256, smem, ctx.stream, e, b.ev_off, r, pb, qb, gbit0, gperm, g, rel,
+              gof, tc, is_plan, pidx);
+    } else {
+      constexpr int smem = 4096 * 12 + 8 * 256 * 4 + 4097 * 8 + 4096;
+      STW_CUDA(ctx, cudaFuncSetAttribute(k_groups_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      STW_KLS(k_groups_fused<16>, (unsigned)T, 256, smem, ctx.stream, e, b.ev_off, r, pb, qb, gbit0, gperm, g, rel,
+              gof, tc, is_plan, pidx);
+    }
+    STW_LAUNCHED(ctx);
+  } else {
+    uint32_t *head = ar.take<uint32_t>(N + 1), *gid = ar.take<uint32_t>(N + 1);
+    int64_t *szs = ar.take<int64_t>(N + 1), *S = ar.take<int64_t>(N + 1);
+    if (!ctx.ok()) return ctx.rc;
+    LAUNCH(k_key_group, N, tr, b.t_e, b.ps, b.pe, b.dyn, b.horizon, r, N, pb, khi, klo);
+    seg_sort(ctx, ar, khi, tb + 2 + 2 * pb, tb, klo, qb, gperm, N, b.ev_off, T, b.max_trace_events,
+             /*lo_in_order=*/him[0] == 0);
+    LAUNCH(k_group_heads, N, e, gperm, b.ev_off, N, head, szs);
+    device_scan<uint32_t>(ctx, ar, head, gid, N, true);
+    device_scan<int64_t>(ctx, ar, szs, S, N, false);
+    d_G = gid + (N > 0 ? N - 1 : 0);
+    LAUNCH(k_group_table, N, e, gperm, head, gid, (const uint32_t *)nullptr, N, g);
+    LAUNCH(k_group_rel, N, gperm, gid, S, szs, g, N, d_G, rel, gof);
+    LAUNCH(k_trace_counts, G, g, d_G, N, tc, is_plan);
+    device_scan<uint32_t>(ctx, ar, is_plan, pidx, G, false);
+  }
   std::vector<int> h_nplans, h_nstatic, h_nres;
   d2h(ctx, h_nplans, tc.n_plans, T);
   d2h(ctx, h_nstatic, tc.n_static, T);
@@ -3046,8 +3121,9 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   Plans p0 = mk_plans();
   int32_t *pid0 = ar.take<int32_t>(N + 1);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_plan_init, G, g, d_G, is_plan, pidx, gperm, e, p0);
-  LAUNCH(k_plan_members, N, gperm, gof, is_plan, pidx, e, N, p0, pid0);
+  const int64_t *pl_local = fused_groups ? d_pl_off : nullptr;  // fused: trace-local plan ranks
+  LAUNCH(k_plan_init, G, g, d_G, (int64_t)G, is_plan, pidx, pl_local, gperm, e, p0);
+  LAUNCH(k_plan_members, N, gperm, gof, is_plan, pidx, pl_local, e, N, p0, pid0);
   LAUNCH(k_plan_tmp, P, p0, P);
 
   pt.mark("B groups");
@@ -3399,17 +3475,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   pt.mark("E layers");
   if (after_uploads) after_uploads(hook_arg);  // the unfused path: after phase E
   nv.next("F emission");
-  // ---- F: emission
-  int64_t *addr = ar.take<int64_t>((int64_t)C * N + 1);
-  int32_t *layer = ar.take<int32_t>((int64_t)C * N + 1);
-  if (!ctx.ok()) return ctx.rc;
-  EmitArgs EA{C, T, N, P, d_var, e, rel, frel1, pid0, pid1, item_of_plan, item_of_res, d_io, d_uo,
-              LA.ilayer, LA.lbase, addr, layer};
-  LAUNCH(k_emit, N, EA);
-
-  pt.mark("F emit");
-  nv.next("G self-check");
-  // ---- G: self-check -- static peak (K1) and the sweep validator (K7)
+  // ---- F + G: emission in sweep order, the self-check's rectangles with it;
+  // static peak (K1) and the sweep validator (K7)
   int64_t *peak = ar.take<int64_t>(T);
   if (!ctx.ok()) return ctx.rc;
   // finished at the finalize round trip
@@ -3426,12 +3493,19 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   if (!ctx.ok()) return ctx.rc;
   STW_KL(k_offsets_i32, 1, 1024, ctx.stream, tc.n_static, T, d_so);
   STW_LAUNCHED(ctx);
-  int32_t *rs_ev = ar.take<int32_t>(NS + 1), *rts = ar.take<int32_t>(NS + 1), *rte = ar.take<int32_t>(NS + 1);
+  int32_t *rts = ar.take<int32_t>(NS + 1), *rte = ar.take<int32_t>(NS + 1);
   int64_t *rsz = ar.take<int64_t>(NS + 1), *raddr = ar.take<int64_t>((int64_t)C * NS + 1);
+  // device outputs are emitted in place; host outputs are staged
+  int64_t *addr = !out->addr ? nullptr : out->on_device ? out->addr : ar.take<int64_t>((int64_t)C * N + 1);
+  int32_t *layer = !out->layer_of ? nullptr : out->on_device ? out->layer_of : ar.take<int32_t>((int64_t)C * N + 1);
   long long *vcount = ar.take<long long>(U);
   int *vfirst = ar.take<int>(U);
   if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_rect_fill, N, rperm, sflag, spos, e, N, C, addr, rs_ev, rts, rte, rsz, raddr, NS);
+  EmitArgs EA{C, T, N, P, d_var, e, rel, frel1, pid0, pid1, item_of_plan, item_of_res, d_io, d_uo,
+              LA.ilayer, LA.lbase, rperm, sflag, spos, NS, addr, layer, rts, rte, rsz, raddr};
+  LAUNCH(k_emit, N, EA);
+  pt.mark("F emit");
+  nv.next("G self-check");
   RectSets rs{T, NS, d_so, rts, rte, rsz, C, raddr};
   // fast validity test now; its verdict is read at the finalize round trip
   STW_CUDA(ctx, cudaMemsetAsync(vcount, 0, U * sizeof(long long), ctx.stream));
@@ -3454,7 +3528,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     STW_CUDA(ctx, cudaMemsetAsync(d_nconf, 0, sizeof(int), ctx.stream));
     LAUNCH(k_unit_finalize, U, FA);
     LAUNCH(k_select_best, T, d_rc, LA.pool, T, C, d_best, d_bpool);
-    LAUNCH(k_gather_best, N, tr, d_best, addr, N, d_abest);
+    LAUNCH(k_gather_best, N, tr, d_best, rperm, sflag, spos, raddr, NS, N, d_abest);
   };
   finalize();
   // one host round trip for the deferred checks: conflicts, units the fast
@@ -3483,6 +3557,8 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
     d2h(ctx, h_vf, vfirst, U);
     d2h(ctx, h_rc2, d_rc, U);
     d2h(ctx, h_err2, d_err, 2 * U);
+    int32_t *rs_ev = ar.take<int32_t>(NS + 1);
+    if (ctx.ok()) LAUNCH(k_rect_events, N, rperm, sflag, spos, N, rs_ev);
     sync(ctx);
     for (int64_t u = 0; u < U && ctx.ok(); u++) {
       if (h_vc[u] <= 0 || h_err2[2 * u] >= 0) continue;
