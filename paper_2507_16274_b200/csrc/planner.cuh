@@ -64,7 +64,15 @@ struct RegIn {
   int64_t nsp;
   int reuse, baseline;
   long long pool;
+  // simulate only: planned static allocations off the sequential chain (see
+  // offchain_check): full op -> kept op index, and the kept op count; nullptr:
+  // every op is replayed
+  const uint32_t *ridx;
+  int64_t nkept;
 };
 int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log);
+// true when the planned static allocations of a simulate call can leave the
+// sequential chain; then in.ridx / in.nkept are set
+bool offchain_check(Ctx &ctx, Arena &ar, RegIn &in, int64_t nkeys);
 
 }  // namespace stw

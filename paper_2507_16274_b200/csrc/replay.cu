@@ -980,10 +980,23 @@ int replay(Ctx &ctx, const stw_batch *in, const stw_bundle *bun, stw_report *rep
   if (n > 0 && nu == n && !getenv("STW_REPLAY_GENERAL")) {
     nv.next("sequential replay (registers)");
     RegIn ri{n, operm, apos, b.id, b.size, b.t_s, b.t_e, b.dyn, route, paddr, key, sp_off, sp_lo, sp_hi,
-             baseline ? 0 : (K ? bun->sp_off[K] : 0), baseline ? 0 : bun->reuse, baseline ? 1 : 0, pool};
-    long long ho[16] = {0};
-    const int st = replay_reg(ctx, ar, ri, ho, log);
+             baseline ? 0 : (K ? bun->sp_off[K] : 0), baseline ? 0 : bun->reuse, baseline ? 1 : 0, pool,
+             nullptr, 2 * n};
+    // simulate: the planned static allocations leave the chain when that is exact
+    const bool off = !baseline && !getenv("STW_REPLAY_FULL_CHAIN") && offchain_check(ctx, ar, ri, K);
     if (!ctx.ok()) return ctx.rc;
+    if (getenv("STW_REPLAY_STATS"))
+      fprintf(stderr, "replay: %s chain, %lld of %lld ops\n", off ? "off-planned" : "full", (long long)ri.nkept,
+              (long long)(2 * n));
+    long long ho[16] = {0};
+    int st = replay_reg(ctx, ar, ri, ho, log);
+    if (!ctx.ok()) return ctx.rc;
+    if (off && st == 2) {  // (cannot happen when the conditions hold) the full chain decides
+      ri.ridx = nullptr;
+      ri.nkept = 2 * n;
+      st = replay_reg(ctx, ar, ri, ho, log);
+      if (!ctx.ok()) return ctx.rc;
+    }
     if (st == 2) {
       *err_id = ho[2];
       ctx.fail(STW_ESIM, "planned address %lld for event %lld is occupied", ho[3], ho[2]);

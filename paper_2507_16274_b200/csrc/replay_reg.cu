@@ -66,7 +66,16 @@ struct RegArgs {
   long long *resume;
   int4 *dump;
   int sp_staged;  // the reuse spaces (in units) are staged in dynamic shared memory
+  // off-chain mode (simulate): the planned static allocations and their frees
+  // are not replayed; ridx maps a full op index to its replayed index
+  const uint32_t *ridx;
+  int64_t nops;  // ops replayed (2n, or the kept ops)
 };
+
+// a static event whose allocation got a planned address (sim.py:189-203)
+__device__ __forceinline__ bool reg_planned(const RegArgs &A, int e) {
+  return !A.baseline && !A.dyn[e] && A.route0[e] == RR_PLANNED;
+}
 constexpr int64_t kSpSmemMax = 16384;  // intervals staged in shared memory (128 KB)
 
 // the unit: OR of every size / planned address / space bound / the pool and the 2 MiB segment minimum
@@ -109,6 +118,8 @@ __global__ void k_reg_ops(RegArgs A) {
   GS4(k, 2 * A.n) {
     const uint32_t o = A.operm[k];
     const int e = (int)(o >> 1);
+    if (A.ridx && reg_planned(A, e)) continue;  // off the chain
+    const int64_t j = A.ridx ? (int64_t)A.ridx[k] : k;
     const bool alloc = !(o & 1);
     int4 r;
     r.x = (int)((unsigned long long)A.size[e] >> sh);
@@ -131,9 +142,9 @@ __global__ void k_reg_ops(RegArgs A) {
       r.y = 1 | (route << 1);
     } else {
       r.y = 0;
-      r.z = A.apos[e];
+      r.z = A.ridx ? (int)A.ridx[A.apos[e]] : A.apos[e];
     }
-    A.ops[k] = r;
+    A.ops[j] = r;
   }
 }
 
@@ -141,22 +152,20 @@ __global__ void k_reg_ops(RegArgs A) {
 // {0, 0, kNoSeg} (length 0, no segment), a pool row {kRFull, kRFull}.
 constexpr uint32_t kNoSeg = kRFull;
 
-// this lane is the lowest set bit of m (lanemask compare: no variable-latency ffs on the chain)
-__device__ __forceinline__ bool lowest_lane(unsigned m) {
-  const unsigned eq = 1u << (threadIdx.x & 31);
-  return (m & (eq | (eq - 1u))) == eq;
-}
+// this lane (eq = 1 << lane, computed once per kernel: no S2R on the chain) is
+// the lowest set bit of m (lanemask compare: no variable-latency ffs either)
+__device__ __forceinline__ bool lowest_lane(unsigned m, unsigned eq) { return (m & (eq | (eq - 1u))) == eq; }
 
 // first empty row of the first lane that has one; false if the state is full
 template <int R, bool CACHE>
 __device__ __forceinline__ bool reg_insert(uint32_t (&lo)[R], uint32_t (&hi)[R], uint32_t (&sg)[R], uint32_t a,
-                                           uint32_t b, uint32_t s) {
+                                           uint32_t b, uint32_t s, unsigned eq) {
   bool has = false;
 #pragma unroll
   for (int r = 0; r < R; r++) has |= CACHE ? sg[r] == kNoSeg : hi[r] == kRFull;
   const unsigned m = __ballot_sync(kRFull, has);
   if (!m) return false;
-  if (lowest_lane(m)) {
+  if (lowest_lane(m, eq)) {
     bool done = false;
 #pragma unroll
     for (int r = 0; r < R; r++) {
@@ -174,8 +183,8 @@ __device__ __forceinline__ bool reg_insert(uint32_t (&lo)[R], uint32_t (&hi)[R],
 // the first empty row of lane ffs(me) - 1 takes [a, b) (segment s)
 template <int R, bool CACHE>
 __device__ __forceinline__ void reg_put(uint32_t (&lo)[R], uint32_t (&hi)[R], uint32_t (&sg)[R], unsigned me,
-                                        uint32_t a, uint32_t b, uint32_t s) {
-  if (lowest_lane(me)) {
+                                        uint32_t a, uint32_t b, uint32_t s, unsigned eq) {
+  if (lowest_lane(me, eq)) {
     bool done = false;
 #pragma unroll
     for (int r = 0; r < R; r++) {
@@ -195,7 +204,7 @@ __device__ __forceinline__ void reg_put(uint32_t (&lo)[R], uint32_t (&hi)[R], ui
 // independent and issued together; the updates are predicated.
 template <int R, bool CACHE>
 __device__ __forceinline__ bool reg_release(uint32_t (&lo)[R], uint32_t (&hi)[R], uint32_t (&sg)[R], uint32_t a,
-                                            uint32_t b, uint32_t s) {
+                                            uint32_t b, uint32_t s, unsigned eq) {
   unsigned lm = 0, rm = 0;
   uint32_t rhi = 0;
   bool has_e = false;
@@ -226,7 +235,7 @@ __device__ __forceinline__ bool reg_release(uint32_t (&lo)[R], uint32_t (&hi)[R]
   }
   if (ml | mr) return true;
   if (!me) return false;
-  reg_put<R, CACHE>(lo, hi, sg, me, a, b, s);
+  reg_put<R, CACHE>(lo, hi, sg, me, a, b, s, eq);
   return true;
 }
 
@@ -235,7 +244,7 @@ __device__ __forceinline__ bool reg_release(uint32_t (&lo)[R], uint32_t (&hi)[R]
 // The votes (owner, split, empty row) and the owner's end are issued together.
 template <int R>
 __device__ __forceinline__ int reg_pool_take(uint32_t (&fl)[R], uint32_t (&fh)[R], uint32_t (&dummy)[R], uint32_t a,
-                                             uint32_t n) {
+                                             uint32_t n, unsigned eq) {
   const uint32_t e = a + n;
   bool own = false, split = false, has_e = false;
   uint32_t oh = 0;
@@ -257,7 +266,7 @@ __device__ __forceinline__ int reg_pool_take(uint32_t (&fl)[R], uint32_t (&fh)[R
   if (!mo) return 1;
   if (ms) {
     if (!me) return 2;
-    reg_put<R, false>(fl, fh, dummy, me, e, nh, 0);
+    reg_put<R, false>(fl, fh, dummy, me, e, nh, 0, eq);
   }
   return 0;
 }
@@ -297,6 +306,10 @@ __device__ __forceinline__ uint32_t rows_min(uint32_t (&v)[R]) {
   return v[0];
 }
 
+#ifdef STW_REPLAY_PROF
+__device__ unsigned long long g_rr_prof[4][2];
+#endif
+
 // out: [0] status (0 done, 1 outside the preconditions: more rows / k_replay,
 // 2 replay error), [2] error id, [3] error address
 template <int R, int RP, bool SIM>
@@ -307,8 +320,9 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
   __shared__ int4 s_op[32], s_info[32], s_res[32];
   __shared__ uint4 s_sp[32];
   const int lane = threadIdx.x;
+  const unsigned leq = 1u << lane;
   const int sh = reg_shift(A);
-  const int64_t n2 = 2 * A.n;
+  const int64_t n2 = A.nops;
   long long *out = A.out;
   if (A.unit[1] >> sh >= (1ull << 31) || ((unsigned long long)A.pool >> sh) >= (1ull << 31)) {
     if (lane == 0) out[0] = 1;  // values must fit 31 bits in units
@@ -388,7 +402,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
       return false;
     }
     const uint32_t base = next_base;
-    if (ss > n && !reg_insert<R, true>(cl, ch, cs, base + n, base + ss, base)) return false;  // state untouched
+    if (ss > n && !reg_insert<R, true>(cl, ch, cs, base + n, base + ss, base, leq)) return false;  // state untouched
     next_base += ss;
     *grown = ss, *addr = base, *sbase = base;
     return true;
@@ -432,6 +446,9 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     const int cnt = (int)min((int64_t)32, n2 - w0);
     int4 op = lds128(a_op), fi = lds128(a_info);
     for (int k = 0; k < cnt; k++) {
+#ifdef STW_REPLAY_PROF
+      const long long c0 = clock64();
+#endif
       const uint32_t nk = 16 * ((k + 1) & 31);
       const int4 nop = lds128(a_op + nk), nfi = lds128(a_info + nk);  // next op, off the chain
       const uint32_t n = (uint32_t)op.x;
@@ -442,7 +459,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
         uint32_t a = 0;
         if (SIM && route == RR_PLANNED) {
           a = (uint32_t)op.z;
-          const int st = reg_pool_take<RP>(fl, fh, fs, a, n);
+          const int st = reg_pool_take<RP>(fl, fh, fs, a, n, leq);
           if (st) {
             status = st == 1 ? 2 : 1;
             over = 2;
@@ -457,7 +474,9 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
           if (op.w > op.z) {
             const int4 sp4 = lds128(a_sp + 16 * k);
             const uint4 sp = make_uint4((uint32_t)sp4.x, (uint32_t)sp4.y, (uint32_t)sp4.z, (uint32_t)sp4.w);
-            uint32_t bl = kRFull, bo = kRFull;
+            // per lane: its best piece as (length << 32 | address), min over the
+            // spaces and rows without branches (ties to the lowest address)
+            unsigned long long best = ~0ull;
             for (int j = op.z; j < op.w; j++) {
               uint32_t slo, shi;
               if (A.sp_staged) {
@@ -473,13 +492,15 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
 #pragma unroll
               for (int r = 0; r < RP; r++) {
                 const uint32_t lo = max(fl[r], slo), hi = min(fh[r], shi);
-                if (hi > lo && hi - lo >= n && (hi - lo < bl || (hi - lo == bl && lo < bo))) bl = hi - lo, bo = lo;
+                const unsigned long long k = ((unsigned long long)(hi - lo) << 32) | lo;
+                best = hi > lo && hi - lo >= n && k < best ? k : best;
               }
             }
+            const uint32_t bl = (uint32_t)(best >> 32), bo = (uint32_t)best;
             const uint32_t m = __reduce_min_sync(kRFull, bl);
             if (m != kRFull) {
               a = __reduce_min_sync(kRFull, bl == m ? bo : kRFull);
-              if (reg_pool_take<RP>(fl, fh, fs, a, n)) {  // inside a free interval: only a full state fails
+              if (reg_pool_take<RP>(fl, fh, fs, a, n, leq)) {  // inside a free interval: only a full state fails
                 status = 1;
                 over = 2;
                 break;
@@ -507,9 +528,9 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
         const bool cache = !SIM || (ai.z & 1);
         bool ok;
         if (cache)
-          ok = reg_release<R, true>(cl, ch, cs, (uint32_t)ai.x, (uint32_t)ai.x + n, (uint32_t)ai.y);
+          ok = reg_release<R, true>(cl, ch, cs, (uint32_t)ai.x, (uint32_t)ai.x + n, (uint32_t)ai.y, leq);
         else
-          ok = reg_release<RP, false>(fl, fh, fs, (uint32_t)ai.x, (uint32_t)ai.x + n, 0);
+          ok = reg_release<RP, false>(fl, fh, fs, (uint32_t)ai.x, (uint32_t)ai.x + n, 0, leq);
         if (!ok) {
           status = 1;
           err_op = w0 + k;
@@ -519,6 +540,16 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
         rec = make_int4(ai.x, 0, ai.z & 1, 0);
       }
       sts128(a_res + 16 * k, rec);  // every lane writes the same record (each later reads its own write)
+#ifdef STW_REPLAY_PROF
+      {  // cycles per op kind: [0] alloc pool, [1] alloc cache, [2] free pool, [3] free cache
+        const int kind = (op.y & 1) ? ((rec.z & 1) ? 1 : 0) : ((rec.z & 1) ? 3 : 2);
+        __syncwarp();
+        if (lane == 0) {
+          atomicAdd(&g_rr_prof[kind][0], (unsigned long long)(clock64() - c0));
+          atomicAdd(&g_rr_prof[kind][1], 1ull);
+        }
+      }
+#endif
       op = nop, fi = nfi;
     }
     if (status) {
@@ -541,7 +572,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
     out[0] = status;
     out[1] = over;
     out[3] = err_addr;
-    if (status == 2) out[2] = A.id[A.operm[err_op] >> 1];
+    if (status == 2) out[2] = A.ridx ? -1 : A.id[A.operm[err_op] >> 1];  // (off-chain: no planned op replayed)
     out[4] = status == 1 ? done_ops : n2;  // ops replayed before an overflow (diagnostics)
   }
 }
@@ -621,6 +652,182 @@ __global__ void k_reg_log(RegArgs A, const uint32_t *__restrict__ gex, int8_t *l
   }
 }
 
+// off-chain mode: every op's result in full op order -- a planned allocation
+// and its free land at the planned address in the pool (route PLANNED)
+__global__ void k_reg_expand(RegArgs A, const int4 *__restrict__ rres, int4 *__restrict__ res) {
+  const int sh = reg_shift(A);
+  GS4(k, 2 * A.n) {
+    const int e = (int)(A.operm[k] >> 1);
+    res[k] = reg_planned(A, e) ? make_int4((int)((unsigned long long)A.paddr[e] >> sh), 0, 0, 0) : rres[A.ridx[k]];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Planned static allocations off the sequential chain (simulate).
+//
+// A planned allocation's outcome is fixed (its planned address, or the
+// "occupied" SimulationError); it feeds the chain only through the pool's
+// free set, i.e. through (a) the error test of later planned allocations and
+// (b) the free-set pieces a dynamic request sees inside its reuse space
+// (sim.py:120-140). Both vanish when
+//   1. the planned rectangles (event lifespan x planned interval) are pairwise
+//      disjoint -- no planned allocation fails against another (the K7 test);
+//   2. no planned rectangle meets (space x [t_s, t_e)) for any reuse space of
+//      any dynamic request that may take the reuse route -- so no planned
+//      interval is live inside a space while a dynamic request of that space
+//      is placed or alive (then a dynamic placement never collides with a
+//      planned one either, and free ∩ space is the same with or without the
+//      planned intervals).
+// derive_reuse_map builds spaces that hold this (reuse.py:54-80: the spaces
+// avoid every decision live in the key's window). When both hold, the chain
+// replays only the dynamic and mismatched requests with the pool's free set
+// taken as [0, pool) minus the live dynamic placements, which gives every op
+// the result the full replay gives; otherwise the full chain runs (and
+// reports the reference's exact error, if any).
+
+struct OffArgs {
+  int64_t n;
+  const uint32_t *operm;
+  const uint8_t *dyn;
+  const int8_t *route0;
+  const int32_t *ts, *te, *key;
+  const int64_t *size, *paddr, *sp_off, *sp_lo, *sp_hi;
+  int reuse;
+  uint32_t *af, *rank, *keep;
+  int32_t *rts, *rte;
+  int64_t *rsz, *raddr, *roff;
+  int *bad;
+};
+
+__device__ __forceinline__ bool off_planned(const OffArgs &A, int e) { return !A.dyn[e] && A.route0[e] == RR_PLANNED; }
+
+__global__ void k_off_flags(OffArgs A) {
+  GS4(k, 2 * A.n) {
+    const uint32_t o = A.operm[k];
+    const bool p = off_planned(A, (int)(o >> 1));
+    A.af[k] = p && !(o & 1) ? 1u : 0u;  // planned allocations, in op order
+    A.keep[k] = p ? 0u : 1u;            // ops that stay on the chain
+  }
+}
+
+// the planned rectangles in op order of their allocations ((t_s, id) order)
+__global__ void k_off_rects(OffArgs A) {
+  GS4(k, 2 * A.n) {
+    if (k == 2 * A.n - 1) A.roff[1] = (int64_t)A.rank[k] + A.af[k];
+    if (!A.af[k]) continue;
+    const int e = (int)(A.operm[k] >> 1);
+    const uint32_t r = A.rank[k];
+    A.rts[r] = A.ts[e];
+    A.rte[r] = A.te[e];
+    A.rsz[r] = A.size[e];
+    A.raddr[r] = A.paddr[e];
+  }
+}
+
+// per reuse key: the hull [min t_s, max t_e) of its dynamic requests
+__global__ void k_off_hull(OffArgs A, int32_t *__restrict__ hlo, int32_t *__restrict__ hhi) {
+  GS4(e, A.n) {
+    if (!A.dyn[e] || !A.reuse) continue;
+    const int kk = A.key[e];
+    if (kk < 0 || A.sp_off[kk + 1] <= A.sp_off[kk]) continue;
+    atomicMin(hlo + kk, A.ts[e]);
+    atomicMax(hhi + kk, A.te[e]);
+  }
+}
+
+// condition 2 on the key's hull (it covers every request of the key, so it
+// is sufficient), one CTA per key
+__global__ void __launch_bounds__(256) k_off_spaces(OffArgs A, const int32_t *__restrict__ hlo,
+                                                    const int32_t *__restrict__ hhi) {
+  const int kk = blockIdx.x;
+  const int32_t ets = hlo[kk], ete = hhi[kk];
+  if (ets >= ete) return;  // no request of this key can take the reuse route
+  const int64_t s0 = A.sp_off[kk], s1 = A.sp_off[kk + 1];
+  const int ns = s1 - s0 < 4 ? (int)(s1 - s0) : 4;
+  long long sl[4], sh[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    sl[q] = q < ns ? A.sp_lo[s0 + q] : 0;
+    sh[q] = q < ns ? A.sp_hi[s0 + q] : 0;
+  }
+  const int64_t np = A.roff[1];
+  // rectangles are in t_s order: only those starting before the hull's end can meet it
+  int64_t lo = 0, hi = np;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (A.rts[m] < ete)
+      lo = m + 1;
+    else
+      hi = m;
+  }
+  bool hit = false;
+  for (int64_t j = threadIdx.x; j < lo; j += blockDim.x) {
+    if (A.rte[j] <= ets) continue;
+    const long long a = A.raddr[j], b = a + A.rsz[j];
+#pragma unroll
+    for (int q = 0; q < 4; q++) hit |= q < ns && a < sh[q] && sl[q] < b;
+    for (int64_t s = s0 + 4; s < s1; s++) hit |= a < A.sp_hi[s] && A.sp_lo[s] < b;  // (keys of > 4 spaces)
+  }
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicOr(A.bad, 1);
+}
+
+bool offchain_check(Ctx &ctx, Arena &ar, RegIn &in, int64_t nkeys) {
+  in.ridx = nullptr;
+  in.nkept = 2 * in.n;
+  const int64_t n = in.n, n2 = 2 * n;
+  if (!ctx.ok() || in.baseline || n <= 0 || n > (1 << 20)) return false;
+  OffArgs A{n, in.operm, in.dyn, in.route0, in.ts, in.te, in.key, in.size, in.paddr, in.sp_off, in.sp_lo, in.sp_hi,
+            in.reuse};
+  A.af = ar.take<uint32_t>(n2);
+  A.rank = ar.take<uint32_t>(n2);
+  A.keep = ar.take<uint32_t>(n2);
+  A.rts = ar.take<int32_t>(n + 1);
+  A.rte = ar.take<int32_t>(n + 1);
+  A.rsz = ar.take<int64_t>(n + 1);
+  A.raddr = ar.take<int64_t>(n + 1);
+  A.roff = ar.take<int64_t>(2);
+  A.bad = ar.take<int>(1);
+  uint32_t *ridx = ar.take<uint32_t>(n2);
+  if (!ctx.ok()) return false;
+  STW_CUDA(ctx, cudaMemsetAsync(A.roff, 0, 2 * sizeof(int64_t), ctx.stream));
+  STW_CUDA(ctx, cudaMemsetAsync(A.bad, 0, sizeof(int), ctx.stream));
+  STW_KL(k_off_flags, grid_for(n2, 256), 256, ctx.stream, A);
+  device_scan<uint32_t>(ctx, ar, A.af, A.rank, n2, false);
+  device_scan<uint32_t>(ctx, ar, A.keep, ridx, n2, false);
+  STW_KL(k_off_rects, grid_for(n2, 256), 256, ctx.stream, A);
+  STW_LAUNCHED(ctx);
+  if (in.reuse && nkeys > 0) {
+    int32_t *hlo = ar.take<int32_t>(nkeys), *hhi = ar.take<int32_t>(nkeys);
+    if (!ctx.ok()) return false;
+    STW_CUDA(ctx, cudaMemsetAsync(hlo, 0x7f, nkeys * sizeof(int32_t), ctx.stream));
+    STW_CUDA(ctx, cudaMemsetAsync(hhi, 0, nkeys * sizeof(int32_t), ctx.stream));
+    STW_KL(k_off_hull, grid_for(n, 256), 256, ctx.stream, A, hlo, hhi);
+    STW_KL(k_off_spaces, (unsigned)nkeys, 256, ctx.stream, A, hlo, hhi);
+    STW_LAUNCHED(ctx);
+  }
+  // condition 1: the exact tiled reporter (the whole GPU on one trace) over the
+  // np planned rectangles
+  long long np = 0;
+  STW_CUDA(ctx, cudaMemcpyAsync(&np, A.roff + 1, sizeof(long long), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (!ctx.ok() || np == 0) return false;
+  RectSets rs{1, np, A.roff, A.rts, A.rte, A.rsz, 1, A.raddr};
+  long long *cnt = ar.take<long long>(1);
+  int *first = ar.take<int>(1);
+  if (!ctx.ok()) return false;
+  validate_exact(ctx, ar, rs, cnt, first);
+  if (!ctx.ok()) return false;
+  long long hf = 1;
+  int hb = 1;
+  STW_CUDA(ctx, cudaMemcpyAsync(&hf, cnt, sizeof(long long), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaMemcpyAsync(&hb, A.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
+  if (!ctx.ok() || hf != 0 || hb != 0) return false;
+  in.ridx = ridx;
+  in.nkept = n2 - 2 * np;
+  return true;
+}
+
 // Runs the register-resident replay; returns 0 when it produced the result
 // (hout[4..10] = metrics, log written when asked), 1 when the call must fall
 // back to k_replay (state or values outside the preconditions), 2 on a replay
@@ -647,9 +854,11 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
   A.reuse = in.reuse;
   A.baseline = in.baseline;
   A.pool = in.pool;
+  A.ridx = in.ridx;
+  A.nops = in.ridx ? in.nkept : n2;
   A.unit = ar.take<unsigned long long>(2);
-  A.ops = ar.take<int4>(n2 + 1);
-  A.res = ar.take<int4>(n2 + 1);
+  A.ops = ar.take<int4>(A.nops + 1);
+  A.res = ar.take<int4>(A.nops + 1);
   A.out = ar.take<long long>(16);
   A.resume = ar.take<long long>(4);
   A.dump = ar.take<int4>(16 * 32);
@@ -693,6 +902,17 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
     fprintf(stderr, "replay_reg rows=%d/%d ops=%lld: status %lld over %lld after %lld ops\n", rc, rp, (long long)n2,
             hout[0], hout[1], hout[4]);
 #endif
+#ifdef STW_REPLAY_PROF
+    {
+      unsigned long long hp[4][2];
+      cudaMemcpyFromSymbol(hp, g_rr_prof, sizeof(hp));
+      const char *nm[4] = {"alloc pool", "alloc cache", "free pool", "free cache"};
+      for (int q = 0; q < 4; q++)
+        if (hp[q][1]) fprintf(stderr, "  %s: %llu ops, %.0f cycles/op\n", nm[q], hp[q][1], (double)hp[q][0] / hp[q][1]);
+      unsigned long long z[4][2] = {};
+      cudaMemcpyToSymbol(g_rr_prof, z, sizeof(z));
+    }
+#endif
     if (hout[0] != 1) break;
     // the baseline resumes where the cache outgrew its rows (A.resume / A.dump
     // were written); a simulate run restarts from the first op
@@ -705,6 +925,15 @@ int replay_reg(Ctx &ctx, Arena &ar, RegIn &in, long long *hout, stw_log *log) {
     if (sim || hout[1] != 1) STW_CUDA(ctx, cudaMemsetAsync(A.resume, 0, 4 * sizeof(long long), ctx.stream));
   }
   if (hout[0] != 0) return (int)hout[0];
+  if (A.ridx) {  // every op's result in full op order
+    int4 *full = ar.take<int4>(n2 + 1);
+    if (!ctx.ok()) return 1;
+    STW_KL(k_reg_expand, grid_for(n2, 256), 256, ctx.stream, A, A.res, full);
+    STW_LAUNCHED(ctx);
+    A.res = full;
+    A.ridx = nullptr;
+    A.nops = n2;
+  }
   // metrics
   int64_t *dl = ar.take<int64_t>(n2), *dc = ar.take<int64_t>(n2);
   unsigned long long *cnt = ar.take<unsigned long long>(8);

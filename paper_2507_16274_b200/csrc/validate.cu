@@ -471,7 +471,9 @@ void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, 
   int64_t U = (int64_t)rs.S * rs.n_cand;
   STW_CUDA(ctx, cudaMemsetAsync(d_count, 0, U * sizeof(long long), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(d_first, 0x7f, U * sizeof(int), ctx.stream));  // 0x7f7f7f7f: no report
-  if (overlap_flags(ctx, ar, rs, shift) == 0) return;  // every unit valid: nothing reported
+  // one warp per unit: with few units the serial sweep leaves the GPU idle, and
+  // the tiled reporter (CTA per 128-decision tile) is faster outright
+  if (U >= 148 && overlap_flags(ctx, ar, rs, shift) == 0) return;  // every unit valid: nothing reported
   validate_exact(ctx, ar, rs, d_count, d_first);
 }
 

@@ -130,6 +130,25 @@ def test_app_b_replay_general_warp(name, monkeypatch):
     assert M.run_baseline(tr).to_dict() == a["baseline"]
 
 
+@pytest.mark.parametrize("name", ["c3_mixtral_moe", "c3b_mixtral_moe_rcp"])
+def test_app_b_simulate_full_chain(name, monkeypatch, capfd):
+    """simulate takes the planned static allocations off the sequential chain
+    when that is exact (replay_reg.cu: offchain_check); the full chain (forced)
+    and the default give the reference's report and log digest."""
+    a = anchors()[name]
+    tr = M.Trace.from_arrays(tracegen.synth_arrays(tracegen.config(name)))
+    plan, rmap = M.plan_trace(tr)
+    bundle = plan.to_bundle(rmap)
+    monkeypatch.setenv("STW_REPLAY_STATS", "1")
+    rep, log = M.simulate(tr, bundle)
+    assert "off-planned chain" in capfd.readouterr().err  # the default took the short chain here
+    assert rep.to_dict() == a["sim"] and log_digest(log) == a["sim_log_digest"]
+    monkeypatch.setenv("STW_REPLAY_FULL_CHAIN", "1")
+    rep, log = M.simulate(tr, bundle)
+    assert "full chain" in capfd.readouterr().err
+    assert rep.to_dict() == a["sim"] and log_digest(log) == a["sim_log_digest"]
+
+
 @pytest.mark.parametrize("chain", [True, False])
 def test_app_b_c2_big_unit_resolve(chain, monkeypatch):
     """c2 is one unit too large for a warp's shared memory: the whole-GPU layer

@@ -175,3 +175,54 @@ def test_replay_register_capacity(k):
     tr = Trace(evs, sched)
     b = api.run_baseline(tr)
     assert b.to_dict() == O.baseline(api._arrays_of(tr)).report
+
+
+def test_replay_offchain_adversarial_spaces(monkeypatch, capfd):
+    """Reuse spaces that overlap planned rectangles (the whole pool, or random
+    windows of it) break the off-chain conditions: the call must notice and
+    replay the full chain, matching the oracle (reports, logs, or the exact
+    SimulationError). Unmodified bundles take the short chain."""
+    from paper_2507_16274_b200.domain import SimulationError, Trace
+    from paper_2507_16274_b200.ivset import Interval, IntervalSet
+    from paper_2507_16274_b200.plan_types import PlanBundle
+
+    monkeypatch.setenv("STW_REPLAY_STATS", "1")
+    rng = np.random.default_rng(3)
+    seen = {"off-planned": 0, "full": 0}
+    for s in range(4, 40, 6):  # MoE presets (dynamic requests)
+        ta = tracegen.synth_arrays(fuzz_cfg(s))
+        tr = Trace.from_arrays(ta)
+        plan, rmap = api.plan_trace(tr)
+        good = plan.to_bundle(rmap)
+        variants = [good]
+        P, U = good.pool_size, good.alignment
+
+        def bundle_with(spaces):
+            nb = PlanBundle(P, U, good.decisions, spaces)
+            object.__setattr__(nb, "_cols", good._cols)
+            return nb
+
+        whole = {k: IntervalSet([Interval(0, P)]) for k in good.reuse}
+        variants.append(bundle_with(whole))
+        rnd = {}
+        for k in good.reuse:
+            a = int(rng.integers(0, P // U)) * U
+            b = min(P, a + int(rng.integers(1, 64)) * U * 256)
+            rnd[k] = IntervalSet([Interval(a, b)])
+        variants.append(bundle_with(rnd))
+        for bundle in variants:
+            key, dcols, off, lo, hi = oracle_inputs(ta, bundle)
+            o = O.simulate(ta, key, bundle.pool_size, bundle.alignment, *dcols, off, lo, hi, True)
+            capfd.readouterr()
+            if o.rc == 0:
+                rep, log = api.simulate(tr, bundle)
+                assert rep.to_dict() == o.report, s
+                assert list(log) == oracle_log_dicts(o.log, ta), s
+            else:
+                with pytest.raises(SimulationError) as ei:
+                    api.simulate(tr, bundle)
+                assert str(o.err_id) in str(ei.value), (str(ei.value), o.err)
+            err = capfd.readouterr().err
+            for k in seen:
+                seen[k] += f"{k} chain" in err
+    assert seen["off-planned"] > 0 and seen["full"] > 0, seen
