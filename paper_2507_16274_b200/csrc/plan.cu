@@ -3510,7 +3510,14 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // fast validity test now; its verdict is read at the finalize round trip
   STW_CUDA(ctx, cudaMemsetAsync(vcount, 0, U * sizeof(long long), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(vfirst, 0x7f, U * sizeof(int), ctx.stream));
-  int *d_nflag = overlap_launch(ctx, ar, rs, __builtin_ctzll((unsigned long long)o->alignment));
+  const int32_t *d_vorder = nullptr;  // traces by static event count, largest first
+  if (T > 1 && !getenv("STW_K7_NATURAL")) {
+    std::vector<int32_t> ord(T);
+    for (int t = 0; t < T; t++) ord[t] = t;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int c) { return h_nstatic[a] > h_nstatic[c]; });
+    d_vorder = h2d(ctx, ar, ord);
+  }
+  int *d_nflag = overlap_launch(ctx, ar, rs, __builtin_ctzll((unsigned long long)o->alignment), d_vorder);
   if (!ctx.ok()) return ctx.rc;
 
   pt.mark("G check");

@@ -36,7 +36,9 @@ void validate_sets(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, 
 // on a CUDA error.
 int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift);
 // the same test without the host round trip: returns the device counter
-int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift);
+// order (optional, device): the sets in launch order (largest first evens out the
+// tail of the one-warp-per-unit sweep)
+int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift, const int32_t *order = nullptr);
 // the exact reporter for every unit (fills d_count / d_first)
 void validate_exact(Ctx &ctx, Arena &ar, const RectSets &rs, long long *d_count, int *d_first);
 

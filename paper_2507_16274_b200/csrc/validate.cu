@@ -284,14 +284,15 @@ constexpr int kOvWarps = 8;
 constexpr int kOvCap = 320;
 constexpr int64_t kOvMaxSerial = 1 << 16;
 
-__global__ void __launch_bounds__(kOvWarps * 32, 5) k_overlap_sweep(RectSets rs, int shift, int *__restrict__ nflag) {
+__global__ void __launch_bounds__(kOvWarps * 32, 5) k_overlap_sweep(RectSets rs, int shift, int *__restrict__ nflag,
+                                                                    const int32_t *__restrict__ order) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ int4 act[kOvWarps][kOvCap];
   __shared__ int4 tile[kOvWarps][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t u = (int64_t)blockIdx.x * kOvWarps + w;
   if (u >= (int64_t)rs.S * rs.n_cand) return;
-  const int s = (int)(u / rs.n_cand), c = (int)(u % rs.n_cand);
+  const int s = order ? order[u / rs.n_cand] : (int)(u / rs.n_cand), c = (int)(u % rs.n_cand);
   const int64_t s0 = rs.off[s], n = rs.off[s + 1] - s0;
   if (n > kOvMaxSerial) {
     if (lane == 0) atomicAdd(nflag, 1);
@@ -444,14 +445,15 @@ __global__ void __launch_bounds__(kOvWarps * 32, 5) k_overlap_sweep(RectSets rs,
 
 // launches the fast test; returns the device counter of units that need the
 // exact reporter (valid after the stream reaches it)
-int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift) {
+int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift, const int32_t *order) {
   if (!ctx.ok()) return nullptr;
   const int64_t U = (int64_t)rs.S * rs.n_cand;
   int *nflag = ar.take<int>(1);
   if (!ctx.ok()) return nullptr;
   STW_CUDA(ctx, cudaMemsetAsync(nflag, 0, sizeof(int), ctx.stream));
   if (U > 0) {
-    STW_KL(k_overlap_sweep, (unsigned)((U + kOvWarps - 1) / kOvWarps), kOvWarps * 32, ctx.stream, rs, shift, nflag);
+    STW_KL(k_overlap_sweep, (unsigned)((U + kOvWarps - 1) / kOvWarps), kOvWarps * 32, ctx.stream, rs, shift, nflag,
+           order);
     STW_LAUNCHED(ctx);
   }
   return nflag;
