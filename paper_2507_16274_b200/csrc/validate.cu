@@ -280,6 +280,9 @@ static void build_tiles(Ctx &ctx, Arena &ar, const RectSets &rs, Tiles *tl) {
 // conflicts, does not scale to 32 bits, overflows the active list, or is too
 // long for a serial sweep is flagged and the exact tiled reporter above runs
 // instead.
+#ifdef STW_K7_STATS
+__device__ unsigned long long g_k7_stats[4];  // max active, sum active, tiles, sum survivors
+#endif
 constexpr int kOvWarps = 8;
 constexpr int kOvCap = 320;
 constexpr int64_t kOvMaxSerial = 1 << 16;
@@ -439,6 +442,14 @@ __global__ void __launch_bounds__(kOvWarps * 32, 5) k_overlap_sweep(RectSets rs,
       if (keep) A[pos] = mine;
     }
     na = nn + ns;
+#ifdef STW_K7_STATS
+    if (lane == 0) {
+      atomicMax(&g_k7_stats[0], (unsigned long long)na);
+      atomicAdd(&g_k7_stats[1], (unsigned long long)na);
+      atomicAdd(&g_k7_stats[2], 1ull);
+      atomicAdd(&g_k7_stats[3], (unsigned long long)ns);
+    }
+#endif
     __syncwarp();
   }
 }
@@ -462,6 +473,17 @@ int *overlap_launch(Ctx &ctx, Arena &ar, const RectSets &rs, int shift, const in
 int overlap_flags(Ctx &ctx, Arena &ar, const RectSets &rs, int shift) {
   int *nflag = overlap_launch(ctx, ar, rs, shift);
   if (!nflag) return -1;
+#ifdef STW_K7_STATS
+  {
+    unsigned long long h[4];
+    cudaStreamSynchronize(ctx.stream);
+    cudaMemcpyFromSymbol(h, g_k7_stats, sizeof(h));
+    fprintf(stderr, "K7: max active %llu, mean active %.1f, mean survivors %.1f over %llu tiles\n", h[0],
+            (double)h[1] / h[2], (double)h[3] / h[2], h[2]);
+    unsigned long long z[4] = {};
+    cudaMemcpyToSymbol(g_k7_stats, z, sizeof(z));
+  }
+#endif
   int h = 0;
   STW_CUDA(ctx, cudaMemcpyAsync(&h, nflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   STW_CUDA(ctx, cudaStreamSynchronize(ctx.stream));
