@@ -21,6 +21,7 @@ static int finish(Ctx &ctx) {
 namespace stw {
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror,
                void (*after_uploads)(void *), void *hook_arg);
+bool plan_batch_split(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
                         const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap);
@@ -84,7 +85,7 @@ int stw_plan_batch(const stw_batch *b, const stw_plan_opts *opts, stw_plan_out *
     ctx.fail(STW_EARG, "null argument");
     return ctx.rc;
   }
-  plan_batch(ctx, b, opts, out, nullptr, nullptr, nullptr);
+  if (!plan_batch_split(ctx, b, opts, out)) plan_batch(ctx, b, opts, out, nullptr, nullptr, nullptr);
   return finish(ctx);
 }
 

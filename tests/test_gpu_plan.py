@@ -211,3 +211,56 @@ def test_failed_call_leaves_no_state_behind():
     with pytest.raises(Exception, match="64 bits"):
         api.plan_batch(tas, CANDS)
     check_batch(tas[:8])
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_plan_split_call_matches_unsplit(on_device, monkeypatch):
+    """Large host batches run as two concurrent halves (split.cu; device batches
+    stay whole); every output field equals the unsplit call's (STW_NO_SPLIT),
+    including the rebased event indices of erroring units in the second half,
+    for host outputs and for device outputs of a host batch."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2507_16274_b200 import _lib
+
+    tas = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(2048)]
+    bad = _manual_trace([(1, 100, 0, 2, "F:0", "F:0"), (2, 512, 1, 3, "F:0", "F:0")], [("F:0", 0, 4)])
+    tas[10] = bad
+    tas[1900] = bad  # (the cut is near half of the events: both halves get one)
+    hb = HostBatch(tas, pinned=True)
+    T, N, Cn = hb.T, hb.N, len(CANDS)
+
+    def run():
+        if not on_device:
+            return api.plan_batch(hb, CANDS, select_best=True)
+        f = {"rc": (T * Cn, torch.int32), "err_ids": (2 * T * Cn, torch.int64), "stats": (T * Cn * _lib.NSTATS, torch.int64),
+             "addr": (Cn * N, torch.int64), "layer_of": (Cn * N, torch.int32), "layer_base": (Cn * N, torch.int64),
+             "layer_size": (Cn * N, torch.int64), "fus_tmp": (Cn * N, torch.float64), "fus_avg": (Cn * N, torch.float64),
+             "order": (N, torch.int32), "best_cand": (T, torch.int32), "addr_best": (N, torch.int64),
+             "best_pool": (T, torch.int64)}
+        bufs = {k: torch.full((n,), -7, dtype=dt, device="cuda") for k, (n, dt) in f.items()}
+        out = _lib.PlanOut(1, *[_lib.ptr(bufs[k]) for k in ("rc", "err_ids", "stats", "addr", "layer_of", "layer_base",
+                                                             "layer_size", "fus_tmp", "fus_avg", "order", "best_cand",
+                                                             "addr_best", "best_pool")])
+        opts = _lib.PlanOpts(Cn, 1, _lib.ptr(api._cand_bits(CANDS)), 512, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        b = hb.struct()
+        err = _lib.errbuf()
+        _lib.check(_lib.load().stw_plan_batch(C.byref(b), C.byref(opts), C.byref(out), err, 1024), err)
+        torch.cuda.synchronize()
+        return {k: v.cpu().numpy() for k, v in bufs.items()}
+
+    got = run()
+    monkeypatch.setenv("STW_NO_SPLIT", "1")
+    want = run()
+    for k in ("rc", "err_ids", "stats", "addr", "layer_of", "layer_base", "layer_size", "fus_tmp", "fus_avg", "order",
+              "best_cand", "addr_best", "best_pool"):
+        a, b = (got[k], want[k]) if on_device else (getattr(got, k), getattr(want, k))
+        if a.dtype == np.float64:
+            a, b = a.view(np.int64), b.view(np.int64)
+        assert np.array_equal(a, b), k
+    rc = (got["rc"] if on_device else got.rc).reshape(T, Cn)
+    err = (got["err_ids"] if on_device else got.err_ids).reshape(T, Cn, 2)
+    assert (rc[10] != 0).all() and (rc[1900] != 0).all() and (rc[:10] == 0).all()
+    assert (err[1900] >= 0).any() and int(err[1900].max()) >= int(hb.ev_off[1900])  # rebased into the batch
