@@ -22,6 +22,7 @@ namespace stw {
 int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out, const stw_batch *mirror,
                void (*after_uploads)(void *), void *hook_arg);
 bool plan_batch_split(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
+bool plan_batches_2lane(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 int validate_plan_pairs(Ctx &ctx, int64_t n, const int64_t *id, const int64_t *addr, const int64_t *size,
                         const int32_t *t_s, const int32_t *t_e, int64_t *n_pairs, int32_t *pairs, int64_t cap);
@@ -96,7 +97,7 @@ int stw_plan_batches(int32_t n, const stw_batch *b, const stw_plan_opts *opts, s
     ctx.fail(STW_EARG, "null argument");
     return ctx.rc;
   }
-  plan_batches(ctx, n, b, opts, out);
+  if (!plan_batches_2lane(ctx, n, b, opts, out)) plan_batches(ctx, n, b, opts, out);
   return finish(ctx);
 }
 

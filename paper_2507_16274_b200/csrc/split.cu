@@ -257,4 +257,55 @@ bool plan_batch_split(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw
   return true;
 }
 
+int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
+
+// stw_plan_batches as two concurrent lanes: even batches on the caller's stream
+// (this thread), odd batches on the worker's stream (the worker thread), each
+// lane the ordinary pipeline over its own subsequence (own staging slots and
+// copy streams). The lanes' kernels fill each other's host round trips; every
+// batch's outputs are what stw_plan_batch gives for it.
+bool plan_batches_2lane(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out) {
+  if (n < 2 || getenv("STW_NO_SPLIT")) return false;
+  Worker &wk = Worker::get();
+  std::unique_lock<std::mutex> lk(wk.busy, std::try_to_lock);
+  if (!lk.owns_lock()) return false;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaStream_t s1 = worker_stream(dev);
+  if (!s1) return false;
+  std::vector<stw_batch> bi[2];
+  std::vector<stw_plan_out> oi[2];
+  for (int k = 0; k < n; k++) {
+    bi[k & 1].push_back(in[k]);
+    oi[k & 1].push_back(out[k]);
+  }
+  // the second lane starts after whatever the caller queued before this call
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  STW_CUDA(ctx, cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  STW_CUDA(ctx, cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  STW_CUDA(ctx, cudaEventRecord(ev_fork, ctx.stream));
+  if (!ctx.ok()) return true;
+  Ctx c1;
+  c1.stream = s1;
+  std::vector<char> err1(ctx.errlen ? ctx.errlen : 256, 0);
+  c1.err = err1.data();
+  c1.errlen = err1.size();
+  stw_plan_opts o1 = *o;
+  o1.stream = s1;
+  wk.run([&] {
+    cudaSetDevice(dev);
+    STW_CUDA(c1, cudaStreamWaitEvent(s1, ev_fork, 0));
+    if (c1.ok()) plan_batches(c1, (int)bi[1].size(), bi[1].data(), &o1, oi[1].data());
+    STW_CUDA(c1, cudaEventRecord(ev_join, s1));
+    STW_CUDA(c1, cudaStreamSynchronize(s1));
+  });
+  plan_batches(ctx, (int)bi[0].size(), bi[0].data(), o, oi[0].data());
+  wk.wait();
+  STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, ev_join, 0));
+  if (!c1.ok() && ctx.ok()) ctx.fail(c1.rc, "%s", c1.err);
+  cudaEventDestroy(ev_fork);
+  cudaEventDestroy(ev_join);
+  return true;
+}
+
 }  // namespace stw

@@ -264,3 +264,18 @@ def test_plan_split_call_matches_unsplit(on_device, monkeypatch):
     err = (got["err_ids"] if on_device else got.err_ids).reshape(T, Cn, 2)
     assert (rc[10] != 0).all() and (rc[1900] != 0).all() and (rc[:10] == 0).all()
     assert (err[1900] >= 0).any() and int(err[1900].max()) >= int(hb.ev_off[1900])  # rebased into the batch
+
+
+def test_plan_batches_two_lanes_error_in_second_lane():
+    """stw_plan_batches runs even and odd batches in two concurrent lanes
+    (split.cu); a batch failing in the worker's lane raises like the
+    sequential pipeline, and the next call is exact."""
+    good = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(4095)]
+    bad = good + [_manual_trace([(1, 1 << 61, 0, 2, "F:0", "F:0")], [("F:0", 0, 4)])]  # (as the test above)
+    with pytest.raises(Exception, match="64 bits"):
+        api.plan_batches([good[:4], bad, good[4:8]], CANDS, select_best=True)
+    many = api.plan_batches([good[:4], good[4:8], good[8:]], CANDS, select_best=True)
+    for g, got in zip((good[:4], good[4:8], good[8:]), many):
+        want = api.plan_batch(g, CANDS, select_best=True)
+        for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
+            assert np.array_equal(getattr(got, f), getattr(want, f)), f
