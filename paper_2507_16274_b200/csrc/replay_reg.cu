@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(32) k_replay_reg(RegArgs A) {
         rec = make_int4(ai.x, 0, ai.z & 1, 0);
       }
       sts128(a_res + 16 * k, rec);  // every lane writes the same record (each later reads its own write)
+      __syncwarp();  // later reads of the record by other lanes are ordered after every lane's write (racecheck-clean; no measurable cost)
 #ifdef STW_REPLAY_PROF
       {  // cycles per op kind: [0] alloc pool, [1] alloc cache, [2] free pool, [3] free cache
         const int kind = (op.y & 1) ? ((rec.z & 1) ? 1 : 0) : ((rec.z & 1) ? 3 : 2);

@@ -60,4 +60,17 @@ groups = planner.group_by_phase(ev)
 plans = planner.pack_groups(groups)
 items = [planner._Item(512, e.t_s, e.t_e, e.id, e) for e in ev]
 assert len(planner.build_layers_for_size(items)) >= 1
+# the concurrent paths (split.cu): a host batch of >= 1024 traces runs as two
+# halves on two threads / streams, and stw_plan_batches as two lanes
+if os.environ.get("STW_SAN_CONCURRENT"):
+    big = [tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(1024)]
+    bpa = api.plan_batch(big, tracegen.C4_CANDIDATES, select_best=True)
+    os.environ["STW_NO_SPLIT"] = "1"
+    bpb = api.plan_batch(big, tracegen.C4_CANDIDATES, select_best=True)
+    del os.environ["STW_NO_SPLIT"]
+    assert np.array_equal(bpa.addr, bpb.addr) and np.array_equal(bpa.stats, bpb.stats), "split call"
+    many = api.plan_batches([tas[:16], tas[16:32], tas[32:]], tracegen.C4_CANDIDATES, select_best=True)
+    for k, g in enumerate((tas[:16], tas[16:32], tas[32:])):
+        w = api.plan_batch(g, tracegen.C4_CANDIDATES, select_best=True)
+        assert np.array_equal(many[k].addr, w.addr) and np.array_equal(many[k].addr_best, w.addr_best), "two lanes"
 print("sanitize workload ok")
