@@ -49,7 +49,7 @@ CANDS = ((True, True), (True, False), (False, True), (False, False))
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="stw", choices=["stw", "reference"])
     ap.add_argument("--traces", type=int, default=4096,
@@ -648,6 +648,11 @@ def main():
     h_abest = torch.empty(N, dtype=torch.int64).pin_memory()
     host_out = _lib.PlanOut(0, _lib.ptr(h_rc), _lib.ptr(h_err), _lib.ptr(h_stats), None, None, None, None, None,
                             None, None, _lib.ptr(h_best), _lib.ptr(h_abest), _lib.ptr(h_bpool))
+    # a second host output set: stw_plan_batches runs odd steps concurrently with
+    # even ones, so consecutive steps must not share result buffers
+    h2 = [torch.empty_like(x).pin_memory() for x in (h_rc, h_err, h_stats, h_best, h_abest, h_bpool)]
+    host_out_b = _lib.PlanOut(0, _lib.ptr(h2[0]), _lib.ptr(h2[1]), _lib.ptr(h2[2]), None, None, None, None, None,
+                              None, None, _lib.ptr(h2[3]), _lib.ptr(h2[4]), _lib.ptr(h2[5]))
     hstruct = hb.struct()
 
     def step_e2e():
@@ -661,15 +666,15 @@ def main():
         on the launching stream around the whole call, which joins its copy
         stream before returning); the L2 is flushed before the call."""
         bs = (_lib.Batch * k)(*([hstruct] * k))
-        os_ = (_lib.PlanOut * k)(*([host_out] * k))
+        os_ = (_lib.PlanOut * k)(*[host_out if i % 2 == 0 else host_out_b for i in range(k)])
         flush.zero_()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         ev0.record(stream)
         _lib.check(L.stw_plan_batches(k, bs, C.byref(opts), os_, err, 1024), err)
-        for _ in range(k):  # every step's results go through the exchange
-            combine(h_bpool, h_best, h_rc)
+        for i in range(k):  # every step's results go through the exchange
+            combine(*((h_bpool, h_best, h_rc) if i % 2 == 0 else (h2[5], h2[3], h2[0])))
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         return ev0.elapsed_time(ev1) / 1e3
@@ -812,7 +817,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": hb.upload_nbytes, "compact_upload": packed,
                     "d2h_bytes_per_step": int(N * 8 + T * (4 + 8) + T * Cn * (4 + 16 + 8 * _lib.NSTATS)),
                     "how": "stw_plan_batches over the K steps: pinned host batch in, host results out every step, "
-                           "double-buffered staging (copies overlap the neighbouring steps' planning)",
+                           "double-buffered staging (copies overlap the neighbouring steps' planning); even and odd steps "
+                           "in two concurrent lanes (threads/streams) that fill each other's host round trips",
                     "serial_value": total_planned / t_e2e_serial_max,
                     "serial_how": "one synchronous stw_plan_batch call per step with host buffers"},
             "gpu_launches": int(launches),
