@@ -279,3 +279,32 @@ def test_plan_batches_two_lanes_error_in_second_lane():
         want = api.plan_batch(g, CANDS, select_best=True)
         for f in ("rc", "stats", "addr", "best_cand", "best_pool", "addr_best"):
             assert np.array_equal(getattr(got, f), getattr(want, f)), f
+
+
+def test_plan_batches_shared_outputs_keep_sequential_semantics():
+    """Batches whose output structs share buffers run in one lane: the buffers
+    end with the last batch's results, as with sequential calls."""
+    import ctypes as C
+
+    from paper_2507_16274_b200 import _lib
+
+    groups = [[tracegen.synth_arrays(tracegen.c4_config(s)) for s in range(a, a + 6)] for a in (0, 30, 60, 90)]
+    hbs = [HostBatch(g, pinned=True) for g in groups]
+    Cn = len(CANDS)
+    maxU, maxN = max(h.T for h in hbs) * Cn, max(h.N for h in hbs)
+    rc = np.full(maxU, -1, np.int32)
+    stats = np.zeros(maxU * _lib.NSTATS, np.int64)
+    abest = np.zeros(maxN, np.int64)
+    bpool = np.zeros(max(h.T for h in hbs), np.int64)
+    best = np.zeros(max(h.T for h in hbs), np.int32)
+    out = _lib.PlanOut(0, _lib.ptr(rc), None, _lib.ptr(stats), None, None, None, None, None, None, None,
+                       _lib.ptr(best), _lib.ptr(abest), _lib.ptr(bpool))
+    opts = _lib.PlanOpts(Cn, 1, _lib.ptr(api._cand_bits(CANDS)), 512, None)
+    bs = (_lib.Batch * 4)(*[h.struct() for h in hbs])
+    outs = (_lib.PlanOut * 4)(*([out] * 4))
+    err = _lib.errbuf()
+    _lib.check(_lib.load().stw_plan_batches(4, bs, C.byref(opts), outs, err, 1024), err)
+    want = api.plan_batch(groups[-1], CANDS, select_best=True)
+    U, N = hbs[-1].T * Cn, hbs[-1].N
+    assert np.array_equal(stats[:U * _lib.NSTATS].reshape(U, -1), want.stats)
+    assert np.array_equal(abest[:N], want.addr_best) and np.array_equal(bpool[:hbs[-1].T], want.best_pool)
