@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <iterator>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -266,18 +267,21 @@ int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, s
 // batch's outputs are what stw_plan_batch gives for it.
 bool plan_batches_2lane(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out) {
   if (n < 2 || getenv("STW_NO_SPLIT")) return false;
-  {  // outputs shared between batches keep the sequential semantics (the last batch's results win)
-    std::vector<const void *> p;
+  {  // outputs shared by an even and an odd batch keep the sequential semantics
+     // (the last batch's results win): one lane. (Sharing inside a lane is sequential anyway.)
+    std::vector<const void *> p[2];
     for (int k = 0; k < n; k++) {
       const stw_plan_out &q = out[k];
       for (const void *x : {(const void *)q.rc, (const void *)q.err_ids, (const void *)q.stats, (const void *)q.addr,
                             (const void *)q.layer_of, (const void *)q.layer_base, (const void *)q.layer_size,
                             (const void *)q.fus_tmp, (const void *)q.fus_avg, (const void *)q.order,
                             (const void *)q.best_cand, (const void *)q.addr_best, (const void *)q.best_pool})
-        if (x) p.push_back(x);
+        if (x) p[k & 1].push_back(x);
     }
-    std::sort(p.begin(), p.end());
-    if (std::adjacent_find(p.begin(), p.end()) != p.end()) return false;
+    for (auto &v : p) std::sort(v.begin(), v.end());
+    std::vector<const void *> both;
+    std::set_intersection(p[0].begin(), p[0].end(), p[1].begin(), p[1].end(), std::back_inserter(both));
+    if (!both.empty()) return false;
   }
   Worker &wk = Worker::get();
   std::unique_lock<std::mutex> lk(wk.busy, std::try_to_lock);
