@@ -648,11 +648,15 @@ def main():
     h_abest = torch.empty(N, dtype=torch.int64).pin_memory()
     host_out = _lib.PlanOut(0, _lib.ptr(h_rc), _lib.ptr(h_err), _lib.ptr(h_stats), None, None, None, None, None,
                             None, None, _lib.ptr(h_best), _lib.ptr(h_abest), _lib.ptr(h_bpool))
-    # a second host output set: stw_plan_batches runs odd steps concurrently with
-    # even ones, so consecutive steps must not share result buffers
-    h2 = [torch.empty_like(x).pin_memory() for x in (h_rc, h_err, h_stats, h_best, h_abest, h_bpool)]
-    host_out_b = _lib.PlanOut(0, _lib.ptr(h2[0]), _lib.ptr(h2[1]), _lib.ptr(h2[2]), None, None, None, None, None,
-                              None, None, _lib.ptr(h2[3]), _lib.ptr(h2[4]), _lib.ptr(h2[5]))
+    # one host output set per lane: stw_plan_batches plans step k in lane
+    # k % lanes, concurrently with the other lanes, so steps of different lanes
+    # must not share result buffers
+    lanes = int(os.environ.get("STW_LANES", "2"))
+    hsets = [(h_rc, h_err, h_stats, h_best, h_abest, h_bpool)]
+    for _ in range(1, max(lanes, 1)):
+        hsets.append(tuple(torch.empty_like(x).pin_memory() for x in hsets[0]))
+    houts = [_lib.PlanOut(0, _lib.ptr(a), _lib.ptr(b_), _lib.ptr(c), None, None, None, None, None, None, None,
+                          _lib.ptr(d), _lib.ptr(e), _lib.ptr(f)) for a, b_, c, d, e, f in hsets]
     hstruct = hb.struct()
 
     def step_e2e():
@@ -666,7 +670,7 @@ def main():
         on the launching stream around the whole call, which joins its copy
         stream before returning); the L2 is flushed before the call."""
         bs = (_lib.Batch * k)(*([hstruct] * k))
-        os_ = (_lib.PlanOut * k)(*[host_out if i % 2 == 0 else host_out_b for i in range(k)])
+        os_ = (_lib.PlanOut * k)(*[houts[i % len(houts)] for i in range(k)])
         flush.zero_()
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -674,7 +678,8 @@ def main():
         ev0.record(stream)
         _lib.check(L.stw_plan_batches(k, bs, C.byref(opts), os_, err, 1024), err)
         for i in range(k):  # every step's results go through the exchange
-            combine(*((h_bpool, h_best, h_rc) if i % 2 == 0 else (h2[5], h2[3], h2[0])))
+            hs = hsets[i % len(hsets)]
+            combine(hs[5], hs[3], hs[0])
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         return ev0.elapsed_time(ev1) / 1e3

@@ -29,12 +29,17 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
 
 namespace {
 
-// one persistent worker thread (never joined: it outlives every call)
+constexpr int kMaxWorkers = 3;
+
+// persistent worker threads (never joined: they outlive every call)
 class Worker {
  public:
-  static Worker &get() {
-    static Worker *w = new Worker();
-    return *w;
+  static Worker &get(int i = 0) {  // workers 0 .. kMaxWorkers-1
+    static Worker *w[kMaxWorkers] = {};
+    static std::mutex mk;
+    std::lock_guard<std::mutex> g(mk);
+    if (!w[i]) w[i] = new Worker();
+    return *w[i];
   }
   std::mutex busy;  // one split call at a time (others run unsplit)
   void run(std::function<void()> f) {
@@ -260,68 +265,85 @@ bool plan_batch_split(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw
 
 int plan_batches(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out);
 
-// stw_plan_batches as two concurrent lanes: even batches on the caller's stream
-// (this thread), odd batches on the worker's stream (the worker thread), each
-// lane the ordinary pipeline over its own subsequence (own staging slots and
-// copy streams). The lanes' kernels fill each other's host round trips; every
-// batch's outputs are what stw_plan_batch gives for it.
+// stw_plan_batches as L concurrent lanes (default 2, STW_LANES; measured on the
+// c4 e2e run: 2 lanes 4.1e9 allocs/s, 3 lanes 0.7-2.6e9, 4 lanes 0.9-2.0e9 --
+// beyond two the lanes' host threads, uploads and arena growth contend): batch k on
+// lane k % L; lane 0 is the caller's thread and stream, lane j a persistent
+// worker thread with its own stream. Each lane is the ordinary pipeline over
+// its own subsequence (own staging slots and copy streams). The lanes' kernels
+// fill each other's host round trips; every batch's outputs are what
+// stw_plan_batch gives for it.
 bool plan_batches_2lane(Ctx &ctx, int n, const stw_batch *in, const stw_plan_opts *o, stw_plan_out *out) {
-  if (n < 2 || getenv("STW_NO_SPLIT")) return false;
-  {  // outputs shared by an even and an odd batch keep the sequential semantics
+  int L = 2;
+  if (const char *e = getenv("STW_LANES")) L = atoi(e);
+  L = std::min(std::min(L, n), kMaxWorkers + 1);
+  if (L < 2 || getenv("STW_NO_SPLIT")) return false;
+  {  // outputs shared by batches of different lanes keep the sequential semantics
      // (the last batch's results win): one lane. (Sharing inside a lane is sequential anyway.)
-    std::vector<const void *> p[2];
+    std::vector<std::pair<const void *, int>> p;
     for (int k = 0; k < n; k++) {
       const stw_plan_out &q = out[k];
       for (const void *x : {(const void *)q.rc, (const void *)q.err_ids, (const void *)q.stats, (const void *)q.addr,
                             (const void *)q.layer_of, (const void *)q.layer_base, (const void *)q.layer_size,
                             (const void *)q.fus_tmp, (const void *)q.fus_avg, (const void *)q.order,
                             (const void *)q.best_cand, (const void *)q.addr_best, (const void *)q.best_pool})
-        if (x) p[k & 1].push_back(x);
+        if (x) p.push_back({x, k % L});
     }
-    for (auto &v : p) std::sort(v.begin(), v.end());
-    std::vector<const void *> both;
-    std::set_intersection(p[0].begin(), p[0].end(), p[1].begin(), p[1].end(), std::back_inserter(both));
-    if (!both.empty()) return false;
+    std::sort(p.begin(), p.end());
+    for (size_t i = 1; i < p.size(); i++)
+      if (p[i].first == p[i - 1].first && p[i].second != p[i - 1].second) return false;
   }
-  Worker &wk = Worker::get();
-  std::unique_lock<std::mutex> lk(wk.busy, std::try_to_lock);
-  if (!lk.owns_lock()) return false;
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int j = 1; j < L; j++) {
+    locks.emplace_back(Worker::get(j - 1).busy, std::try_to_lock);
+    if (!locks.back().owns_lock()) return false;
+  }
   int dev = -1;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
-  cudaStream_t s1 = worker_stream(dev);
-  if (!s1) return false;
-  std::vector<stw_batch> bi[2];
-  std::vector<stw_plan_out> oi[2];
+  std::vector<std::vector<stw_batch>> bi(L);
+  std::vector<std::vector<stw_plan_out>> oi(L);
   for (int k = 0; k < n; k++) {
-    bi[k & 1].push_back(in[k]);
-    oi[k & 1].push_back(out[k]);
+    bi[k % L].push_back(in[k]);
+    oi[k % L].push_back(out[k]);
   }
-  // the second lane starts after whatever the caller queued before this call
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the other lanes start after whatever the caller queued before this call
+  cudaEvent_t ev_fork = nullptr;
+  std::vector<cudaEvent_t> ev_join(L, nullptr);
   STW_CUDA(ctx, cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-  STW_CUDA(ctx, cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  for (int j = 1; j < L; j++) STW_CUDA(ctx, cudaEventCreateWithFlags(&ev_join[j], cudaEventDisableTiming));
   STW_CUDA(ctx, cudaEventRecord(ev_fork, ctx.stream));
   if (!ctx.ok()) return true;
-  Ctx c1;
-  c1.stream = s1;
-  std::vector<char> err1(ctx.errlen ? ctx.errlen : 256, 0);
-  c1.err = err1.data();
-  c1.errlen = err1.size();
-  stw_plan_opts o1 = *o;
-  o1.stream = s1;
-  wk.run([&] {
-    cudaSetDevice(dev);
-    STW_CUDA(c1, cudaStreamWaitEvent(s1, ev_fork, 0));
-    if (c1.ok()) plan_batches(c1, (int)bi[1].size(), bi[1].data(), &o1, oi[1].data());
-    STW_CUDA(c1, cudaEventRecord(ev_join, s1));
-    STW_CUDA(c1, cudaStreamSynchronize(s1));
-  });
+  std::vector<Ctx> cj(L);
+  std::vector<std::vector<char>> errs(L, std::vector<char>(ctx.errlen ? ctx.errlen : 256, 0));
+  std::vector<stw_plan_opts> oj(L, *o);
+  for (int j = 1; j < L; j++) {
+    Ctx &c = cj[j];
+    c.stream = nullptr;
+    c.err = errs[j].data();
+    c.errlen = errs[j].size();
+    Worker::get(j - 1).run([&, j] {
+      Ctx &c = cj[j];
+      cudaSetDevice(dev);
+      c.stream = worker_stream(dev);
+      if (!c.stream) {
+        c.fail(STW_ECUDA, "no worker stream");
+        return;
+      }
+      oj[j].stream = c.stream;
+      STW_CUDA(c, cudaStreamWaitEvent(c.stream, ev_fork, 0));
+      if (c.ok()) plan_batches(c, (int)bi[j].size(), bi[j].data(), &oj[j], oi[j].data());
+      STW_CUDA(c, cudaEventRecord(ev_join[j], c.stream));
+      STW_CUDA(c, cudaStreamSynchronize(c.stream));
+    });
+  }
   plan_batches(ctx, (int)bi[0].size(), bi[0].data(), o, oi[0].data());
-  wk.wait();
-  STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, ev_join, 0));
-  if (!c1.ok() && ctx.ok()) ctx.fail(c1.rc, "%s", c1.err);
+  for (int j = 1; j < L; j++) {
+    Worker::get(j - 1).wait();
+    if (ev_join[j]) STW_CUDA(ctx, cudaStreamWaitEvent(ctx.stream, ev_join[j], 0));
+    if (!cj[j].ok() && ctx.ok()) ctx.fail(cj[j].rc, "%s", cj[j].err);
+  }
   cudaEventDestroy(ev_fork);
-  cudaEventDestroy(ev_join);
+  for (int j = 1; j < L; j++) cudaEventDestroy(ev_join[j]);
   return true;
 }
 
