@@ -1384,9 +1384,13 @@ __global__ void __launch_bounds__(256, IPT == 8 ? 5 : 1) k_items_sorted(Plans p0
     }
     pos += tot;
   }
+  // residual events: scoped static events of a single-phase group (class 1,
+  // p_s == p_e: no cross-phase plan, so pid0 < 0) -- from the event's own
+  // columns (coalesced) rather than the pid0 -> gof -> group-class gathers
+  const int ehz = e.horizon[t];
   for (int64_t i0 = ev_off[t]; i0 < ev_off[t + 1]; i0 += blockDim.x) {
     const int64_t i = i0 + tid;
-    const bool res = i < ev_off[t + 1] && !e.dyn[i] && pid0[i] < 0 && g.cls[gof[i]] == 1;
+    const bool res = i < ev_off[t + 1] && ev_class(e.dyn[i], e.te[i], ehz) == 1 && e.ps[i] == e.pe[i];
     uint32_t tot;
     const uint32_t ex = block_excl_sum<uint32_t>(res ? 1u : 0u, sh, &tot);
     if (res) {
