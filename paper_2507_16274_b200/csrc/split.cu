@@ -100,7 +100,8 @@ bool plan_batch_split(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw
   // the host (one more round trip), and measured slower split (1.52 vs 1.42 ms
   // per c4 call with device outputs) than whole; a host batch gains 6% (its
   // uploads and downloads overlap the other half's planning too)
-  if (in->on_device || T < 1024 || N < (1 << 16) || getenv("STW_NO_SPLIT")) return false;
+  if ((in->on_device && !getenv("STW_SPLIT_DEVICE")) || T < 1024 || N < (1 << 16) || getenv("STW_NO_SPLIT"))
+    return false;
   Worker &wk = Worker::get();
   std::unique_lock<std::mutex> lk(wk.busy, std::try_to_lock);
   if (!lk.owns_lock()) return false;
