@@ -2681,9 +2681,11 @@ __global__ void k_emit(EmitArgs A) {
     const int64_t rel = cl == 2 ? 0 : A.rel[i];
     const int p0 = cl == 1 ? A.pid0[i] : -1;
     const int p1 = cl == 1 && A.pid1 ? A.pid1[i] : -1;
-    const bool st = A.sflag[k] != 0;
-    const int64_t o = st ? (int64_t)A.spos[k] : 0;
-    if (st) {
+    // (sflag == nullptr: every event static and listed in sweep order -- the
+    // rectangles are the batch's own columns and the event-order addresses)
+    const bool st = A.sflag ? A.sflag[k] != 0 : true;
+    const int64_t o = !st ? 0 : A.spos ? (int64_t)A.spos[k] : k;
+    if (st && A.rts) {
       A.rts[o] = A.e.ts[i];
       A.rte[o] = A.e.te[i];
       A.rsz[o] = A.e.size[i];
@@ -2709,7 +2711,7 @@ __global__ void k_emit(EmitArgs A) {
         ly = A.ilayer[A.uo[u] + local];
         ad = A.lbase[A.uo[u] + ly] + fr;
       }
-      if (st) A.raddr[(int64_t)c * A.NS + o] = ad;
+      if (st && A.raddr != A.addr) A.raddr[(int64_t)c * A.NS + o] = ad;
       if (A.addr) A.addr[(int64_t)c * A.N + i] = ad;
       if (A.layer) A.layer[(int64_t)c * A.N + i] = ly;
     }
@@ -2726,7 +2728,7 @@ __global__ void k_static_flag(const uint32_t *__restrict__ rperm, const uint8_t 
 __global__ void k_rect_events(const uint32_t *__restrict__ rperm, const uint32_t *__restrict__ f,
                               const uint32_t *__restrict__ pos, int64_t n, int32_t *__restrict__ rs_ev) {
   GRID_STRIDE(k, n) {
-    if (f[k]) rs_ev[pos[k]] = (int32_t)rperm[k];
+    if (!f || f[k]) rs_ev[pos ? pos[k] : k] = (int32_t)rperm[k];
   }
 }
 
@@ -2812,7 +2814,7 @@ __global__ void k_gather_best(const int32_t *__restrict__ tr, const int32_t *__r
   GRID_STRIDE(k, N) {
     const uint32_t i = rperm[k];
     const int b = best[tr[i]];
-    out[i] = b >= 0 && f[k] ? raddr[(int64_t)b * NS + pos[k]] : -1;
+    out[i] = b >= 0 && (!f || f[k]) ? raddr[(int64_t)b * NS + (pos ? (int64_t)pos[k] : k)] : -1;
   }
 }
 
@@ -3486,22 +3488,32 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   // finished at the finalize round trip
   const PeakPending ppk =
       peak_live_launch(ctx, ar, b, true, peak, __builtin_ctzll((unsigned long long)o->alignment), /*pinned=*/true);
-  uint32_t *sflag = ar.take<uint32_t>(N + 1), *spos = ar.take<uint32_t>(N + 1);
-  if (!ctx.ok()) return ctx.rc;
-  LAUNCH(k_static_flag, N, rperm, b.dyn, N, sflag);
-  device_scan<uint32_t>(ctx, ar, sflag, spos, N, false);
   std::vector<int64_t> so(T + 1, 0);
   for (int t = 0; t < T; t++) so[t + 1] = so[t] + h_nstatic[t];
   const int64_t NS = so[T];
-  int64_t *d_so = ar.take<int64_t>(T + 1);  // the same offsets, made on the device (no upload)
-  if (!ctx.ok()) return ctx.rc;
-  STW_KL(k_offsets_i32, 1, 1024, ctx.stream, tc.n_static, T, d_so);
-  STW_LAUNCHED(ctx);
-  int32_t *rts = ar.take<int32_t>(NS + 1), *rte = ar.take<int32_t>(NS + 1);
-  int64_t *rsz = ar.take<int64_t>(NS + 1), *raddr = ar.take<int64_t>((int64_t)C * NS + 1);
+  // every event static and every trace in recorded order: the sweep order is the
+  // event order, so the self-check's rectangles are the batch's own columns and
+  // the event-order addresses (no flags, positions, or copies)
+  const bool ident = NS == N && him[0] == 0;
+  uint32_t *sflag = nullptr, *spos = nullptr;
+  const int64_t *d_so = b.ev_off;
+  int32_t *rts = nullptr, *rte = nullptr;
+  int64_t *rsz = nullptr;
+  if (!ident) {
+    sflag = ar.take<uint32_t>(N + 1), spos = ar.take<uint32_t>(N + 1);
+    int64_t *so_dev = ar.take<int64_t>(T + 1);  // the same offsets, made on the device (no upload)
+    rts = ar.take<int32_t>(NS + 1), rte = ar.take<int32_t>(NS + 1), rsz = ar.take<int64_t>(NS + 1);
+    if (!ctx.ok()) return ctx.rc;
+    LAUNCH(k_static_flag, N, rperm, b.dyn, N, sflag);
+    device_scan<uint32_t>(ctx, ar, sflag, spos, N, false);
+    STW_KL(k_offsets_i32, 1, 1024, ctx.stream, tc.n_static, T, so_dev);
+    STW_LAUNCHED(ctx);
+    d_so = so_dev;
+  }
   // device outputs are emitted in place; host outputs are staged
   int64_t *addr = !out->addr ? nullptr : out->on_device ? out->addr : ar.take<int64_t>((int64_t)C * N + 1);
   int32_t *layer = !out->layer_of ? nullptr : out->on_device ? out->layer_of : ar.take<int32_t>((int64_t)C * N + 1);
+  int64_t *raddr = ident && addr ? addr : ar.take<int64_t>((int64_t)C * NS + 1);
   long long *vcount = ar.take<long long>(U);
   int *vfirst = ar.take<int>(U);
   if (!ctx.ok()) return ctx.rc;
@@ -3510,7 +3522,7 @@ int plan_batch(Ctx &ctx, const stw_batch *in, const stw_plan_opts *o, stw_plan_o
   LAUNCH(k_emit, N, EA);
   pt.mark("F emit");
   nv.next("G self-check");
-  RectSets rs{T, NS, d_so, rts, rte, rsz, C, raddr};
+  RectSets rs{T, NS, d_so, ident ? b.t_s : rts, ident ? b.t_e : rte, ident ? b.size : rsz, C, raddr};
   // fast validity test now; its verdict is read at the finalize round trip
   STW_CUDA(ctx, cudaMemsetAsync(vcount, 0, U * sizeof(long long), ctx.stream));
   STW_CUDA(ctx, cudaMemsetAsync(vfirst, 0x7f, U * sizeof(int), ctx.stream));
