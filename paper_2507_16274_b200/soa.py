@@ -164,13 +164,26 @@ def from_events(events, phase_schedule=(), layer_schedule=()) -> TraceArrays:
 
     ids = [e.id for e in evs]
     sizes = [e.size for e in evs]
-    ts = np.fromiter((e.t_s for e in evs), dtype=np.int64, count=n)
-    te = np.fromiter((e.t_e for e in evs), dtype=np.int64, count=n)
-    # p_s then p_e of each event in turn: phases missing from the schedule get
-    # their indices in the reference's order of first appearance
-    pp = np.fromiter((pix(x) for e in evs for x in (e.p_s, e.p_e)), dtype=np.int32, count=2 * n)
-    ps, pe = np.ascontiguousarray(pp[0::2]), np.ascontiguousarray(pp[1::2])
-    dyn = np.fromiter((1 if e.dynamic else 0 for e in evs), dtype=np.uint8, count=n)
+    ts = np.array([e.t_s for e in evs], dtype=np.int64)  # (list comprehensions beat generator fromiter ~4x)
+    te = np.array([e.t_e for e in evs], dtype=np.int64)
+    # phase indices: the distinct phase objects (a trace reuses a few hundred)
+    # are collected by identity with C-level maps; when all of them are in the
+    # schedule each event's index is one dict lookup, also C-level
+    ps_obj = [e.p_s for e in evs]
+    pe_obj = [e.p_e for e in evs]
+    uniq = dict(zip(map(id, ps_obj), ps_obj))
+    uniq.update(zip(map(id, pe_obj), pe_obj))
+    if all(p in index for p in uniq.values()):
+        idmap = {k: index[p] for k, p in uniq.items()}
+        ps = np.array(list(map(idmap.__getitem__, map(id, ps_obj))), dtype=np.int32)
+        pe = np.array(list(map(idmap.__getitem__, map(id, pe_obj))), dtype=np.int32)
+    else:
+        # p_s then p_e of each event in turn: phases missing from the schedule
+        # get their indices in the reference's order of first appearance
+        pp = np.fromiter((pix(x) for e in evs for x in (e.p_s, e.p_e)), dtype=np.int32, count=2 * n)
+        ps, pe = np.ascontiguousarray(pp[0::2]), np.ascontiguousarray(pp[1::2])
+    del ps_obj, pe_obj, uniq
+    dyn = np.array([e.dynamic for e in evs], dtype=bool).view(np.uint8)
     ls = np.full(n, -1, dtype=np.int32)
     le = np.full(n, -1, dtype=np.int32)
     for k in np.flatnonzero(dyn).tolist():
