@@ -226,3 +226,19 @@ def test_replay_offchain_adversarial_spaces(monkeypatch, capfd):
             for k in seen:
                 seen[k] += f"{k} chain" in err
     assert seen["off-planned"] > 0 and seen["full"] > 0, seen
+
+
+def test_replay_shuffled_listing_takes_the_general_id_path():
+    """Replay preprocessing skips the id sorts when ids increase along the
+    listing (the usual trace); a shuffled listing takes the sorting path.
+    Both match the oracle (reports and every log record)."""
+    import dataclasses
+
+    rng = np.random.default_rng(17)
+    for s in (4, 5, 10, 11):
+        ta = tracegen.synth_arrays(fuzz_cfg(s))
+        p = rng.permutation(len(ta))
+        sh = dataclasses.replace(ta, **{k: getattr(ta, k)[p] for k in
+                                        ("id", "size", "t_s", "t_e", "ps", "pe", "dyn", "ls", "le")})
+        check_trace(ta, (True,))
+        check_trace(sh, (True,))
