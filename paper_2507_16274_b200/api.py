@@ -480,11 +480,26 @@ class ReplayLog(_Sequence):
         return list(self) == list(other)
 
 
+_LOG_FIELDS = (("t", np.int64), ("id", np.int64), ("size", np.int64), ("addr", np.int64), ("kind", np.int8),
+               ("space", np.int8), ("route", np.int8))
+
+
 def _log_buffers(n: int):
     cap = 1 + 3 * n
-    cols = dict(kind=np.empty(cap, np.int8), t=np.empty(cap, np.int64), id=np.empty(cap, np.int64),
-                size=np.empty(cap, np.int64), addr=np.empty(cap, np.int64), space=np.empty(cap, np.int8),
-                route=np.empty(cap, np.int8))
+    if n >= (1 << 15):
+        # a large log comes back over PCIe at page-locked speed: one pinned block
+        # (torch's host allocator caches it between calls) carved into the columns
+        import torch
+
+        total = sum(cap * np.dtype(dt).itemsize for _, dt in _LOG_FIELDS)
+        raw = torch.empty(total, dtype=torch.uint8, pin_memory=True).numpy()
+        cols, off = {}, 0
+        for name, dt in _LOG_FIELDS:
+            nb = cap * np.dtype(dt).itemsize
+            cols[name] = raw[off:off + nb].view(dt)
+            off += nb
+    else:
+        cols = {name: np.empty(cap, dt) for name, dt in _LOG_FIELDS}
     lg = _lib.Log(cap, 0, *(_lib.ptr(cols[k]) for k in ("kind", "t", "id", "size", "addr", "space", "route")))
     return lg, cols
 
