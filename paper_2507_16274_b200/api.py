@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import os as _os
+
 import numpy as np
 
 from . import _lib
@@ -117,30 +119,47 @@ def _cand_bits(cands) -> np.ndarray:
                       dtype=np.uint8)
 
 
+def _host_arrays(spec, pinned_from: int = 8 << 20) -> dict:
+    """Uninitialised host arrays for the given (name, shape, dtype) fields: one
+    page-locked block when they total at least `pinned_from` bytes (device ->
+    host copies then run at full link speed), else plain numpy arrays."""
+    sizes = [int(np.prod(shape)) * np.dtype(dt).itemsize for _, shape, dt in spec]
+    total = sum((z + 63) // 64 * 64 for z in sizes)
+    out = {}
+    if total >= pinned_from and not _os.environ.get("STW_PAGEABLE_OUT"):
+        import torch
+
+        if torch.cuda.is_available():
+            raw = torch.empty(total, dtype=torch.uint8, pin_memory=True).numpy()
+            off = 0
+            for (name, shape, dt), z in zip(spec, sizes):
+                out[name] = raw[off:off + z].view(dt).reshape(shape)
+                off += (z + 63) // 64 * 64
+            return out
+    for name, shape, dt in spec:
+        out[name] = np.empty(shape, dt)
+    return out
+
+
 def _plan_buffers(hb, cands, alignment, select_best, detail, stream):
     """Host output buffers + the stw_plan_opts/stw_plan_out structs for one batch."""
     C_ = len(cands)
     T, N = hb.T, hb.N
     U = T * C_
     cb = _cand_bits(cands)
-    rc = np.zeros(U, np.int32)
-    err_ids = np.full((U, 2), -1, np.int64)
-    stats = np.zeros((U, _lib.NSTATS), np.int64)
-    addr = np.empty((C_, N), np.int64)
-    order = np.empty(N, np.int32)
+    # every field is written in full by the library; large outputs land in one
+    # pinned host block (page-locked copies, torch's host allocator caches it)
+    spec = [("rc", (U,), np.int32), ("err_ids", (U, 2), np.int64), ("stats", (U, _lib.NSTATS), np.int64),
+            ("addr", (C_, N), np.int64), ("order", (N,), np.int32)]
     if detail:
-        layer_of = np.empty((C_, N), np.int32)
-        lbase = np.zeros((C_, N), np.int64)
-        lsize = np.zeros((C_, N), np.int64)
-        ftmp = np.zeros((C_, N), np.float64)
-        favg = np.zeros((C_, N), np.float64)
-    else:
-        layer_of = lbase = lsize = ftmp = favg = None
-    best = bpool = abest = None
+        spec += [("layer_of", (C_, N), np.int32), ("lbase", (C_, N), np.int64), ("lsize", (C_, N), np.int64),
+                 ("ftmp", (C_, N), np.float64), ("favg", (C_, N), np.float64)]
     if select_best:
-        best = np.empty(T, np.int32)
-        bpool = np.empty(T, np.int64)
-        abest = np.empty(N, np.int64)
+        spec += [("best", (T,), np.int32), ("bpool", (T,), np.int64), ("abest", (N,), np.int64)]
+    a = _host_arrays(spec)
+    rc, err_ids, stats, addr, order = a["rc"], a["err_ids"], a["stats"], a["addr"], a["order"]
+    layer_of, lbase, lsize, ftmp, favg = (a.get(k) for k in ("layer_of", "lbase", "lsize", "ftmp", "favg"))
+    best, bpool, abest = (a.get(k) for k in ("best", "bpool", "abest"))
     opts = _lib.PlanOpts(C_, int(select_best), _lib.ptr(cb), alignment,
                          _lib.stream_handle(stream) if stream is not None else None)
     out = _lib.PlanOut(0, _lib.ptr(rc), _lib.ptr(err_ids), _lib.ptr(stats), _lib.ptr(addr), _lib.ptr(layer_of),
